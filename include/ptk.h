@@ -1,0 +1,114 @@
+/*
+ * ptk.h — the C ABI between the pipetune host layer (C++ / Python ctypes)
+ * and the sm_100a stage runtime.  Plain pointers, sizes and ints only; no
+ * torch or C++ types cross this boundary.  Every function returns an int
+ * status (PTK_OK == 0) and never throws; ptk_last_error() describes the
+ * most recent failure on the calling thread.
+ *
+ * Reference interfaces these entry points stand in for (paths relative to
+ * /root/reference):
+ *   - proj/src/model.cpp:43-47 compute_duration(): the reference models a
+ *     stage's forward/backward as an affine duration.  ptk_stage_forward /
+ *     ptk_stage_backward execute the real GPT stage for one micro-batch.
+ *   - proj/src/taskgraph.cpp:68-76 Send/Recv node pairs: realised by the
+ *     executor's P2P engine (ptk_exec_*), one copy stream per link.
+ *   - proj/src/plan.cpp:75-81 plan_kfkb(): ptk_plan_* expose the planner over
+ *     the ABI for FFI callers; the C++ API in include/pipetune/ is the
+ *     source-compatible drop-in.
+ *   - SPEC.md:342 simulate / :453 run_adaptive: ptk_sim_* and ptk_tuner_*.
+ */
+#ifndef PTK_H_
+#define PTK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status */
+enum {
+    PTK_OK = 0,
+    PTK_ERR_ARG = 1,       /* invalid argument (maps to pipetune::ConfigError) */
+    PTK_ERR_PLAN = 2,      /* plan parameters out of range (pipetune::PlanError) */
+    PTK_ERR_CUDA = 3,      /* CUDA runtime / driver failure (pipetune::CudaError) */
+    PTK_ERR_ALIGN = 4,     /* pointer or stride not 16-byte aligned */
+    PTK_ERR_DEADLOCK = 5,  /* pipetune::DeadlockDetected */
+    PTK_ERR_NOPROFILE = 6, /* pipetune::NoProfileData */
+    PTK_ERR_INFEASIBLE = 7,/* pipetune::InfeasibleModel */
+    PTK_ERR_UNKNOWN_CANDIDATE = 8,
+    PTK_ERR_INTERNAL = 9,
+    PTK_ERR_NOMEM = 10
+};
+
+const char* ptk_last_error(void);
+const char* ptk_version(void);
+
+/* ------------------------------------------------------------ GEMM */
+enum { PTK_EPI_BF16 = 0, PTK_EPI_F32 = 1, PTK_EPI_ACC_F32 = 2, PTK_EPI_BIAS_GELU = 3, PTK_EPI_DGELU = 4 };
+enum { PTK_CAUSAL_NONE = 0, PTK_CAUSAL_TILES = 1, PTK_CAUSAL_KHEAD = 2, PTK_CAUSAL_KTAIL = 3 };
+
+/* A strided (optionally batched) matrix in device memory.  For operands,
+ * mn_major = 0 means the reduction index k is contiguous: element (r, k) at
+ * ptr[r*ld + k]; mn_major = 1 means element (r, k) at ptr[k*ld + r].
+ * Batch index z = z1 + batch[0]*z2 adds z1*batch_stride[0] + z2*batch_stride[1]
+ * (elements). */
+typedef struct ptk_matrix {
+    void* ptr;
+    int mn_major;
+    int64_t ld;
+    int64_t batch_stride[2];
+} ptk_matrix;
+
+/* D[z] = A[z] (m x k) * B[z]^T (B is n x k), bf16 operands, fp32 accumulation,
+ * epilogue selected by `epilogue` (see gemm_sm100.cu). */
+typedef struct ptk_gemm_desc {
+    int m, n, k;
+    int batch[2];
+    ptk_matrix a, b, c;
+    void* c2;          /* PTK_EPI_BIAS_GELU: pre-activation output (same strides as c) */
+    ptk_matrix aux;    /* residual (EPI_BF16) or pre-activation (EPI_DGELU) input */
+    const void* bias;  /* bf16 [n] or NULL */
+    int epilogue;
+    int causal;
+    int bn_hint;       /* 0 = auto, else 64 / 128 / 256 */
+} ptk_gemm_desc;
+
+int ptk_gemm(const ptk_gemm_desc* desc, void* stream);
+
+/* ------------------------------------------------------------ planner
+ * Mirrors pipetune::StageProfile / ModelSpec (proj/include/pipetune/model.hpp:30-51). */
+typedef struct ptk_stage_profile {
+    int stage_id;
+    double forward_fixed, forward_per_sample;
+    double backward_fixed, backward_per_sample;
+    int64_t weight_bytes;
+    int64_t activation_bytes_per_sample;
+    int64_t output_bytes_per_sample_fwd;
+    int64_t output_bytes_per_sample_bwd;
+} ptk_stage_profile;
+
+typedef struct ptk_model {
+    const ptk_stage_profile* stages;
+    int stage_count;
+    int global_batch;
+} ptk_model;
+
+enum { PTK_PLAN_1F1B = 0, PTK_PLAN_KFKB = 1, PTK_PLAN_GPIPE = 2 };
+
+/* build_task_graph(model, b) + plan_1f1b / plan_kfkb(k) / plan_gpipe
+ * (proj/src/taskgraph.cpp:35, proj/src/plan.cpp:70-104), dumped as JSON:
+ * nodes, edges, lookup tables, per-device orders, units, sequences,
+ * validate() violations, check_plan() count and topological_order().
+ * On a pipetune::Error the JSON is {"error": "<type name>"} and the status
+ * is the matching PTK_ERR_*.  *written receives the bytes needed (incl. NUL);
+ * PTK_ERR_NOMEM if cap is too small. */
+int ptk_plan_json(const ptk_model* model, int micro_batch_size, int plan_kind, int k, char* buf, size_t cap,
+                  size_t* written);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PTK_H_ */

@@ -1,0 +1,522 @@
+// Persistent, warp-specialised bf16 GEMM for sm_100a (tcgen05 + TMEM + TMA).
+//
+//   D[z][m][n] = sum_k A[z][m][k] * B[z][n][k]      (fp32 accumulate in TMEM)
+//
+// A and B are each either K-major (k contiguous) or MN-major (m / n
+// contiguous); the operand layout is folded into the TMA box and the UMMA
+// smem descriptor, so the dense-layer forward (X·Wᵀ), dgrad (dY·W) and wgrad
+// (dYᵀ·X) and every attention product are the same kernel without a
+// transpose pass.  One CTA per SM, 6 warps:
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      TMEM allocator + tcgen05.mma issuer (one elected lane)
+//   warps 2..5  epilogue: tcgen05.ld → fused epilogue → st.global
+// The accumulator is double-buffered in TMEM (2 x BN fp32 columns) so the
+// epilogue of tile i overlaps the main loop of tile i+1.
+//
+// Epilogues (runtime switch, warp-uniform):
+//   EPI_BF16      C = acc (+bias[n]) (+aux[m][n])          bf16 out
+//   EPI_F32       C = acc                                   fp32 out
+//   EPI_ACC_F32   C += acc                                  fp32 in/out (wgrad accumulation, β=1)
+//   EPI_BIAS_GELU C2 = acc+bias (pre-activation), C = gelu(C2)   bf16 out
+//   EPI_DGELU     C = acc * gelu'(aux[m][n])                bf16 out
+// Causal modes (attention):
+//   CAUSAL_TILES  only tiles with n0 <= m0 (+BM-1) are computed (lower-triangular output, BM == BN)
+//   CAUSAL_KHEAD  k range clipped to [0, m0+BM)   (P·V, dS·K: P/dS are zero above the diagonal)
+//   CAUSAL_KTAIL  k range clipped to [m0, K)      (dSᵀ·Q, Pᵀ·dO)
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "../../../include/ptk.h"
+#include "gemm_sm100.h"
+#include "sm100_ptx.cuh"
+
+namespace ptk {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int kThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps
+constexpr int kSmemBudget = 226 * 1024;
+
+template <int BN>
+struct Cfg {
+    static constexpr int kABytes = kBM * kBK * 2;
+    static constexpr int kBBytes = BN * kBK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kEpiBytes = 8 * 32 * 32 * 4;
+    static constexpr int kStagesRaw = (kSmemBudget - 2048 - kEpiBytes) / kStageBytes;
+    static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+    static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 512 /*barriers*/ + kEpiBytes;
+};
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const float u = k0 * (x + k1 * x * x * x);
+    return 0.5f * x * (1.f + tanhf(u));
+}
+
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const float x2 = x * x;
+    const float t = tanhf(k0 * (x + k1 * x * x2));
+    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x2);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+
+__device__ __forceinline__ void unpack_bf16x8(const uint4& u, float (&f)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 p = __bfloat1622float2(h[i]);
+        f[2 * i] = p.x;
+        f[2 * i + 1] = p.y;
+    }
+}
+
+__device__ __forceinline__ uint4 pack_bf16x8(const float* f) {
+    uint4 u;
+    u.x = pack_bf16(f[0], f[1]);
+    u.y = pack_bf16(f[2], f[3]);
+    u.z = pack_bf16(f[4], f[5]);
+    u.w = pack_bf16(f[6], f[7]);
+    return u;
+}
+
+struct TileCoord {
+    int z1, z2, m0, n0, kb0, kb1;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t) {
+    TileCoord c;
+    const int z = t / a.tiles_per_batch;
+    int r = t - z * a.tiles_per_batch;
+    int mb, nb;
+    if (a.causal == PTK_CAUSAL_TILES) {
+        // r enumerates the lower triangle row by row: row i holds i+1 tiles.
+        mb = static_cast<int>((sqrtf(8.f * r + 1.f) - 1.f) * 0.5f);
+        while ((mb + 1) * (mb + 2) / 2 <= r) ++mb;
+        while (mb * (mb + 1) / 2 > r) --mb;
+        nb = r - mb * (mb + 1) / 2;
+    } else {
+        nb = r / a.tiles_m;
+        mb = r - nb * a.tiles_m;
+    }
+    c.z1 = z % a.batch1;
+    c.z2 = z / a.batch1;
+    c.m0 = mb * kBM;
+    c.n0 = nb * a.bn;
+    const int kbs = (a.K + kBK - 1) / kBK;
+    c.kb0 = 0;
+    c.kb1 = kbs;
+    if (a.causal == PTK_CAUSAL_KHEAD) {
+        const int kend = min(a.K, c.m0 + kBM);
+        c.kb1 = (kend + kBK - 1) / kBK;
+    } else if (a.causal == PTK_CAUSAL_KTAIL) {
+        c.kb0 = min(c.m0 / kBK, kbs - 1);
+    }
+    return c;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ GemmArgs args) {
+    using C = Cfg<BN>;
+    constexpr int S = C::kStages;
+    constexpr uint32_t kIdesc = make_idesc_bf16(kBM, BN, A_MN, B_MN);
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint8_t* epi_smem = smem + S * C::kStageBytes + 512;  // 8 warps x 4 KB transpose buffers
+
+    const int warp = threadIdx.x / 32;
+    const uint32_t lane = lane_id();
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 8);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
+                const TileCoord tc = decode_tile(args, t);
+                for (int kb = tc.kb0; kb < tc.kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                    uint8_t* sa = smem + stage * C::kStageBytes;
+                    uint8_t* sb = sa + C::kABytes;
+                    const int k0 = kb * kBK;
+                    if (!A_MN) {
+                        tma_load_4d(&tmA, &full[stage], sa, k0, tc.m0, tc.z1, tc.z2);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < kBM / 64; ++j)
+                            tma_load_4d(&tmA, &full[stage], sa + j * 64 * kBK * 2, tc.m0 + 64 * j, k0, tc.z1, tc.z2);
+                    }
+                    if (!B_MN) {
+                        tma_load_4d(&tmB, &full[stage], sb, k0, tc.n0, tc.z1, tc.z2);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j)
+                            tma_load_4d(&tmB, &full[stage], sb + j * 64 * kBK * 2, tc.n0 + 64 * j, k0, tc.z1, tc.z2);
+                    }
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
+                const TileCoord tc = decode_tile(args, t);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                for (int kb = tc.kb0; kb < tc.kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(smem + stage * C::kStageBytes);
+                    const uint32_t b_base = a_base + C::kABytes;
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        // K-major: advance 32 B inside the swizzled 128 B row.
+                        // MN-major: advance two 8-row core groups (2 x 1024 B).
+                        const uint64_t da = A_MN ? make_sw128_desc(a_base + k * 2048, 64 * kBK * 2, 1024)
+                                                 : make_sw128_desc(a_base + k * 32, 16, 1024);
+                        const uint64_t db = B_MN ? make_sw128_desc(b_base + k * 2048, 64 * kBK * 2, 1024)
+                                                 : make_sw128_desc(b_base + k * 32, 16, 1024);
+                        mma_bf16_ss(d_tmem, da, db, kIdesc, (kb > tc.kb0 || k > 0) ? 1u : 0u);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ---------------- epilogue warps: 8 warps, two per TMEM lane quadrant
+        // (warp % 4); the pair splits the 32-column chunks of a tile.
+        const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;  // 0 or 1
+        float4* stage_buf = reinterpret_cast<float4*>(epi_smem) + (warp - 2) * 256;  // 32 rows x 8 float4
+        const int q = static_cast<int>(lane & 7);
+        const int r0 = static_cast<int>(lane >> 3);
+        const bool f32_out = args.epi == PTK_EPI_F32 || args.epi == PTK_EPI_ACC_F32;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
+            const TileCoord tc = decode_tile(args, t);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t zoff_c = tc.z1 * args.c_bs1 + tc.z2 * args.c_bs2;
+            const int64_t zoff_x = tc.z1 * args.aux_bs1 + tc.z2 * args.aux_bs2;
+            const int row_base = tc.m0 + quad * 32;
+#pragma unroll 1
+            for (int c = half; c < BN / 32; c += 2) {
+                float v[32];
+                __syncwarp();
+                tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                                       static_cast<uint32_t>(acc * BN + c * 32),
+                                   v);
+                if (f32_out) {
+                    // fp32 output: transpose through smem so each warp store covers
+                    // 4 rows x 128 contiguous bytes; all loads issued before stores.
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        stage_buf[lane * 8 + (j ^ (lane & 7))] =
+                            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    __syncwarp();
+                    const int gn = tc.n0 + c * 32 + q * 4;
+                    if (gn < args.N) {
+                        float* cbase = static_cast<float*>(args.C) + zoff_c + gn;
+                        float4 prev[8];
+                        if (args.epi == PTK_EPI_ACC_F32) {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const int gm = row_base + r0 + 4 * i;
+                                prev[i] = gm < args.M ? *reinterpret_cast<const float4*>(cbase + static_cast<int64_t>(gm) * args.ldc)
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) prev[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int r = r0 + 4 * i;
+                            const int gm = row_base + r;
+                            const float4 a4 = stage_buf[r * 8 + (q ^ (r & 7))];
+                            if (gm < args.M)
+                                *reinterpret_cast<float4*>(cbase + static_cast<int64_t>(gm) * args.ldc) =
+                                    make_float4(prev[i].x + a4.x, prev[i].y + a4.y, prev[i].z + a4.z, prev[i].w + a4.w);
+                        }
+                    }
+                    continue;
+                }
+                // bf16 output: thread = row, 16-byte stores of 8 columns
+                const int gm = row_base + static_cast<int>(lane);
+                const int gn0 = tc.n0 + c * 32;
+                if (gm >= args.M) continue;
+                const int64_t rowoff = zoff_c + static_cast<int64_t>(gm) * args.ldc;
+                const int64_t xrowoff = zoff_x + static_cast<int64_t>(gm) * args.ld_aux;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int gn = gn0 + 8 * j;
+                    if (gn >= args.N) continue;
+                    float* f = v + 8 * j;
+                    if (args.bias != nullptr) {
+                        float b[8];
+                        unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.bias) + gn), b);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[i] += b[i];
+                    }
+                    if (args.epi == PTK_EPI_BF16 && args.aux != nullptr) {
+                        float r[8];
+                        unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.aux) + xrowoff + gn), r);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[i] += r[i];
+                    } else if (args.epi == PTK_EPI_BIAS_GELU) {
+                        const uint4 pre = pack_bf16x8(f);
+                        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C2) + rowoff + gn) = pre;
+                        float p[8];
+                        unpack_bf16x8(pre, p);  // gelu of the rounded pre-activation, as stored
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[i] = gelu_tanh(p[i]);
+                    } else if (args.epi == PTK_EPI_DGELU) {
+                        float p[8];
+                        unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.aux) + xrowoff + gn), p);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[i] *= gelu_tanh_grad(p[i]);
+                    }
+                    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + rowoff + gn) = pack_bf16x8(f);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<C::kTmemCols>(tmem_base);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// Operand map: dims = {contiguous, strided, batch1, batch2}; box = {64, rows}.
+int encode_operand(CUtensorMap* map, const ptk_matrix& m, int contig_extent, int strided_extent, int box_rows,
+                   int batch1, int batch2) {
+    EncodeTiledFn enc = encode_fn();
+    if (enc == nullptr) return PTK_ERR_CUDA;
+    if ((reinterpret_cast<uintptr_t>(m.ptr) & 15) != 0 || (m.ld * 2) % 16 != 0) return PTK_ERR_ALIGN;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(contig_extent), static_cast<cuuint64_t>(strided_extent),
+                          static_cast<cuuint64_t>(batch1), static_cast<cuuint64_t>(batch2)};
+    const int64_t row_bytes = m.ld * 2;
+    int64_t s1 = m.batch_stride[0] * 2, s2 = m.batch_stride[1] * 2;
+    if (batch1 <= 1) s1 = row_bytes * strided_extent;
+    if (batch2 <= 1) s2 = s1 * (batch1 > 0 ? batch1 : 1);
+    if (s1 % 16 != 0 || s2 % 16 != 0 || s1 <= 0 || s2 <= 0) return PTK_ERR_ALIGN;
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(row_bytes), static_cast<cuuint64_t>(s1),
+                             static_cast<cuuint64_t>(s2)};
+    cuuint32_t box[4] = {64, static_cast<cuuint32_t>(box_rows), 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, m.ptr, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? PTK_OK : PTK_ERR_CUDA;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+int launch_impl(const GemmPlan& p, cudaStream_t stream) {
+    using C = Cfg<BN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(gemm_bf16_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::kSmemBytes) != cudaSuccess)
+            return PTK_ERR_CUDA;
+        attr_set = true;
+    }
+    gemm_bf16_kernel<BN, A_MN, B_MN><<<p.grid, kThreads, C::kSmemBytes, stream>>>(p.tmA, p.tmB, p.args);
+    return cudaPeekAtLastError() == cudaSuccess ? PTK_OK : PTK_ERR_CUDA;
+}
+
+template <int BN>
+GemmPlan::Launcher pick(bool a_mn, bool b_mn) {
+    if (!a_mn && !b_mn) return &launch_impl<BN, false, false>;
+    if (!a_mn && b_mn) return &launch_impl<BN, false, true>;
+    if (a_mn && !b_mn) return &launch_impl<BN, true, false>;
+    return &launch_impl<BN, true, true>;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+}  // namespace
+
+int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
+    if (d.m <= 0 || d.n <= 0 || d.k <= 0) return PTK_ERR_ARG;
+    if (d.n % 8 != 0) return PTK_ERR_ARG;
+    const int b1 = d.batch[0] > 0 ? d.batch[0] : 1;
+    const int b2 = d.batch[1] > 0 ? d.batch[1] : 1;
+    const int tiles_m = (d.m + kBM - 1) / kBM;
+
+    int bn;
+    if (d.bn_hint == 64 || d.bn_hint == 128 || d.bn_hint == 256) {
+        bn = d.bn_hint;
+    } else if (d.causal == PTK_CAUSAL_TILES) {
+        bn = 128;
+    } else if (d.n <= 64) {
+        bn = 64;
+    } else if (d.n <= 128) {
+        bn = 128;
+    } else {
+        // Prefer the wide tile unless the narrow one fills the machine clearly better.
+        const int sms = num_sms();
+        auto eff = [&](int w) {
+            const long tiles = static_cast<long>(tiles_m) * ((d.n + w - 1) / w) * b1 * b2;
+            const long waves = (tiles + sms - 1) / sms;
+            return static_cast<double>(tiles) / static_cast<double>(waves * sms);
+        };
+        bn = eff(128) > eff(256) + 0.15 ? 128 : 256;
+    }
+    if (d.causal == PTK_CAUSAL_TILES && (bn != kBM || d.m != d.n)) return PTK_ERR_ARG;
+
+    GemmPlan p{};
+    int rc;
+    // A: logical [M][K]
+    if (!d.a.mn_major)
+        rc = encode_operand(&p.tmA, d.a, d.k, d.m, kBM, b1, b2);
+    else
+        rc = encode_operand(&p.tmA, d.a, d.m, d.k, kBK, b1, b2);
+    if (rc != PTK_OK) return rc;
+    // B: logical [N][K]
+    if (!d.b.mn_major)
+        rc = encode_operand(&p.tmB, d.b, d.k, d.n, bn, b1, b2);
+    else
+        rc = encode_operand(&p.tmB, d.b, d.n, d.k, kBK, b1, b2);
+    if (rc != PTK_OK) return rc;
+
+    GemmArgs& a = p.args;
+    a.M = d.m;
+    a.N = d.n;
+    a.K = d.k;
+    a.batch1 = b1;
+    a.bn = bn;
+    a.tiles_m = tiles_m;
+    a.tiles_n = (d.n + bn - 1) / bn;
+    a.tiles_per_batch = d.causal == PTK_CAUSAL_TILES ? tiles_m * (tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
+    a.num_tiles = a.tiles_per_batch * b1 * b2;
+    a.causal = d.causal;
+    a.epi = d.epilogue;
+    a.C = d.c.ptr;
+    a.ldc = d.c.ld;
+    a.c_bs1 = d.c.batch_stride[0];
+    a.c_bs2 = d.c.batch_stride[1];
+    a.C2 = d.c2;
+    a.aux = d.aux.ptr;
+    a.ld_aux = d.aux.ld;
+    a.aux_bs1 = d.aux.batch_stride[0];
+    a.aux_bs2 = d.aux.batch_stride[1];
+    a.bias = d.bias;
+    if ((a.epi == PTK_EPI_DGELU && a.aux == nullptr) || (a.epi == PTK_EPI_BIAS_GELU && (a.C2 == nullptr)))
+        return PTK_ERR_ARG;
+
+    const int sms = num_sms();
+    p.grid = a.num_tiles < sms ? a.num_tiles : sms;
+    p.flops = 2.0 * d.m * static_cast<double>(d.n) * d.k * b1 * b2;
+    if (d.causal != PTK_CAUSAL_NONE) p.flops *= 0.5;
+    switch (bn) {
+        case 64: p.launch = pick<64>(d.a.mn_major, d.b.mn_major); break;
+        case 128: p.launch = pick<128>(d.a.mn_major, d.b.mn_major); break;
+        default: p.launch = pick<256>(d.a.mn_major, d.b.mn_major); break;
+    }
+    *out = p;
+    return PTK_OK;
+}
+
+int gemm_run(const GemmPlan& p, cudaStream_t stream) { return p.launch(p, stream); }
+
+}  // namespace ptk

@@ -1,0 +1,38 @@
+// Host-side handle for one prepared GEMM launch (tensor maps encoded once).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../../include/ptk.h"
+
+namespace ptk {
+
+struct GemmArgs {
+    int M, N, K;
+    int batch1;
+    int bn;
+    int tiles_m, tiles_n, tiles_per_batch, num_tiles;
+    int causal, epi;
+    void* C;
+    int64_t ldc, c_bs1, c_bs2;
+    void* C2;
+    const void* aux;
+    int64_t ld_aux, aux_bs1, aux_bs2;
+    const void* bias;
+};
+
+struct GemmPlan {
+    using Launcher = int (*)(const GemmPlan&, cudaStream_t);
+    alignas(64) CUtensorMap tmA;
+    alignas(64) CUtensorMap tmB;
+    GemmArgs args;
+    int grid = 0;
+    double flops = 0.0;  // algorithmic FLOPs of one launch
+    Launcher launch = nullptr;
+};
+
+int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out);
+int gemm_run(const GemmPlan& p, cudaStream_t stream);
+
+}  // namespace ptk

@@ -1,0 +1,173 @@
+"""tcgen05 GEMM parity against a plain PyTorch fp32 reference (CPU, fp64 accumulate).
+
+Covers every operand-major combination the GPT stage uses, batched strided
+operands (the attention head layout), all epilogues and the causal modes.
+Tolerance: bf16 output rounding (rel 1e-2 of the row scale) on top of fp32
+accumulation order differences.
+"""
+import math
+
+import pytest
+import torch
+
+from paper_2303_01675_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref_mm(a, b):
+    return (a.double() @ b.double().T).float()
+
+
+def _run(desc):
+    L.check(L.lib().ptk_gemm(desc, torch.cuda.current_stream().cuda_stream))
+
+
+def _desc(m, n, k, a, b, c, epi=L.EPI_BF16, bias=None, aux=None, c2=None, causal=0, batch=(1, 1), bn=0):
+    d = L.GemmDesc()
+    d.m, d.n, d.k = m, n, k
+    d.batch[0], d.batch[1] = batch
+    d.a, d.b, d.c = a, b, c
+    d.aux = aux if aux is not None else L.matrix(0, 0)
+    d.c2 = c2 or 0
+    d.bias = bias or 0
+    d.epilogue, d.causal, d.bn_hint = epi, causal, bn
+    return d
+
+
+def _close(out, ref, tol=1.5e-2):
+    scale = ref.abs().max().item() + 1e-6
+    err = (out.float().cpu() - ref).abs().max().item()
+    assert err <= tol * scale, f"max err {err} vs scale {scale}"
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("shape", [(128, 64, 64), (300, 520, 200), (256, 384, 1024)])
+@pytest.mark.parametrize("bn", [0, 64, 128, 256])
+def test_gemm_majors(cuda, a_mn, b_mn, shape, bn):
+    m, n, k = shape
+    if a_mn and m % 8:
+        m += 8 - m % 8
+    torch.manual_seed(m * 7 + n * 3 + k + a_mn * 2 + b_mn)
+    A = torch.randn(m, k).bfloat16()
+    B = torch.randn(n, k).bfloat16()
+    ref = _ref_mm(A.float(), B.float())
+    As = (A.T.contiguous() if a_mn else A).to(cuda)
+    Bs = (B.T.contiguous() if b_mn else B).to(cuda)
+    Cd = torch.zeros(m, n, dtype=torch.bfloat16, device=cuda)
+    d = _desc(m, n, k, L.matrix(As.data_ptr(), m if a_mn else k, a_mn),
+              L.matrix(Bs.data_ptr(), n if b_mn else k, b_mn), L.matrix(Cd.data_ptr(), n), bn=bn)
+    _run(d)
+    torch.cuda.synchronize()
+    _close(Cd, ref)
+
+
+def test_gemm_epilogues(cuda):
+    m, n, k = 256, 512, 384
+    torch.manual_seed(0)
+    A = torch.randn(m, k).bfloat16()
+    B = (torch.randn(n, k) * 0.05).bfloat16()
+    bias = torch.randn(n).bfloat16()
+    res = torch.randn(m, n).bfloat16()
+    acc = A.double() @ B.double().T
+    Ad, Bd = A.to(cuda), B.to(cuda)
+    bd, rd = bias.to(cuda), res.to(cuda)
+    a, b = L.matrix(Ad.data_ptr(), k), L.matrix(Bd.data_ptr(), k)
+
+    # bias + residual
+    C = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    _run(_desc(m, n, k, a, b, L.matrix(C.data_ptr(), n), bias=bd.data_ptr(), aux=L.matrix(rd.data_ptr(), n)))
+    _close(C, (acc + bias.double() + res.double()).float())
+
+    # fp32 store and fp32 accumulate
+    F = torch.ones(m, n, dtype=torch.float32, device=cuda)
+    _run(_desc(m, n, k, a, b, L.matrix(F.data_ptr(), n), epi=L.EPI_F32))
+    _close(F, acc.float(), tol=1e-4)
+    _run(_desc(m, n, k, a, b, L.matrix(F.data_ptr(), n), epi=L.EPI_ACC_F32))
+    _close(F, (2 * acc).float(), tol=1e-4)
+
+    # bias + gelu (tanh form) with pre-activation side output
+    G = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    P = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    _run(_desc(m, n, k, a, b, L.matrix(G.data_ptr(), n), epi=L.EPI_BIAS_GELU, bias=bd.data_ptr(),
+               c2=P.data_ptr()))
+    pre = (acc + bias.double()).float()
+    _close(P, pre)
+    _close(G, torch.nn.functional.gelu(P.float().cpu(), approximate="tanh"))
+
+    # dgelu: C = acc * gelu'(pre)
+    D = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    _run(_desc(m, n, k, a, b, L.matrix(D.data_ptr(), n), epi=L.EPI_DGELU, aux=L.matrix(rd.data_ptr(), n)))
+    x = res.float().requires_grad_(True)
+    torch.nn.functional.gelu(x, approximate="tanh").backward(torch.ones_like(x))
+    _close(D, acc.float() * x.grad)
+
+
+def _attn_layout(cuda, b, s, h, d, seed):
+    """qkv [b, s, 3, h, d] as one [b*s, 3*h*d] buffer, like the QKV projection output."""
+    torch.manual_seed(seed)
+    qkv = torch.randn(b, s, 3, h, d).bfloat16()
+    return qkv, qkv.to(cuda)
+
+
+def test_gemm_batched_attention_scores(cuda):
+    b, s, h, d = 2, 256, 4, 64
+    qkv, qkvd = _attn_layout(cuda, b, s, h, d, 1)
+    row = 3 * h * d
+    S = torch.full((b, h, s, s), float("nan"), dtype=torch.float32, device=cuda)
+    # batch z1 = head, z2 = sample
+    qa = L.matrix(qkvd.data_ptr(), row, 0, d, s * row)
+    kb = L.matrix(qkvd.data_ptr() + h * d * 2, row, 0, d, s * row)
+    c = L.matrix(S.data_ptr(), s, 0, s * s, h * s * s)
+    _run(_desc(s, s, d, qa, kb, c, epi=L.EPI_F32, causal=L.CAUSAL_TILES, batch=(h, b)))
+    torch.cuda.synchronize()
+    q = qkv[:, :, 0].permute(0, 2, 1, 3).double()
+    k = qkv[:, :, 1].permute(0, 2, 1, 3).double()
+    ref = (q @ k.transpose(-1, -2)).float()
+    mask = torch.tril(torch.ones(s, s, dtype=torch.bool))
+    out = S.cpu()
+    assert torch.allclose(out[..., mask], ref[..., mask], atol=1e-3, rtol=1e-3)
+
+
+def test_gemm_batched_pv_and_grads(cuda):
+    """P·V (K-head), dSᵀ·Q style (K-tail, both operands MN-major) on a causal P."""
+    b, s, h, d = 2, 256, 4, 64
+    qkv, qkvd = _attn_layout(cuda, b, s, h, d, 2)
+    row = 3 * h * d
+    torch.manual_seed(3)
+    P = torch.rand(b, h, s, s).tril().bfloat16()
+    Pd = P.to(cuda)
+    v = qkv[:, :, 2].permute(0, 2, 1, 3).double()
+    # O[z] = P[z] · V[z]: A = P (K-major), B[n=d][k=kv] = V stored [kv][d] → MN-major
+    O = torch.empty(b, s, h, d, dtype=torch.bfloat16, device=cuda)
+    pa = L.matrix(Pd.data_ptr(), s, 0, s * s, h * s * s)
+    vb = L.matrix(qkvd.data_ptr() + 2 * h * d * 2, row, 1, d, s * row)
+    oc = L.matrix(O.data_ptr(), h * d, 0, d, s * h * d)
+    _run(_desc(s, d, s, pa, vb, oc, causal=L.CAUSAL_KHEAD, batch=(h, b)))
+    ref = (P.double() @ v).float().permute(0, 2, 1, 3)
+    _close(O, ref)
+
+    # dV[z] = P[z]^T · dO[z]: A[m=kv][k=q] = P stored [q][kv] → MN-major; B[n=d][k=q] = dO [q][d] → MN-major
+    torch.manual_seed(4)
+    dO = torch.randn(b, s, h, d).bfloat16()
+    dOd = dO.to(cuda)
+    dV = torch.empty(b, s, h, d, dtype=torch.bfloat16, device=cuda)
+    pa_t = L.matrix(Pd.data_ptr(), s, 1, s * s, h * s * s)
+    dob = L.matrix(dOd.data_ptr(), h * d, 1, d, s * h * d)
+    dvc = L.matrix(dV.data_ptr(), h * d, 0, d, s * h * d)
+    _run(_desc(s, d, s, pa_t, dob, dvc, causal=L.CAUSAL_KTAIL, batch=(h, b)))
+    ref = (P.double().transpose(-1, -2) @ dO.permute(0, 2, 1, 3).double()).float().permute(0, 2, 1, 3)
+    _close(dV, ref)
+
+
+def test_gemm_large_dense(cuda):
+    m, n, k = 2048, 6144, 2048
+    torch.manual_seed(5)
+    A = (torch.randn(m, k) * 0.5).bfloat16().to(cuda)
+    B = (torch.randn(n, k) * 0.02).bfloat16().to(cuda)
+    C = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    _run(_desc(m, n, k, L.matrix(A.data_ptr(), k), L.matrix(B.data_ptr(), k), L.matrix(C.data_ptr(), n)))
+    ref = (A.float() @ B.float().T)  # fp32 on the GPU (TF32 disabled by default for matmul)
+    torch.cuda.synchronize()
+    err = (C.float() - ref).abs().max().item()
+    assert err <= 1e-2 * ref.abs().max().item()
