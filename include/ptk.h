@@ -107,6 +107,14 @@ enum { PTK_PLAN_1F1B = 0, PTK_PLAN_KFKB = 1, PTK_PLAN_GPIPE = 2 };
 int ptk_plan_json(const ptk_model* model, int micro_batch_size, int plan_kind, int k, char* buf, size_t cap,
                   size_t* written);
 
+/* ------------------------------------------------------------ spec modules
+ * One JSON scenario in (schema_version 1, unknown keys rejected), one JSON
+ * result out.  "op" selects: transfer | estimate | peak_memory | simulate |
+ * enumerate | profile | compare | decide | tune — the memory, network,
+ * simulator, costmodel and tuner operations of SPEC.md:203-491.  Errors:
+ * {"error": "<pipetune type>", "message": ...} and the matching status. */
+int ptk_scenario_json(const char* request, char* buf, size_t cap, size_t* written);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,8 @@ def _declare(L: C.CDLL) -> None:
     L.ptk_plan_json.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t,
                                 C.POINTER(C.c_size_t)]
     L.ptk_plan_json.restype = C.c_int
+    L.ptk_scenario_json.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
+    L.ptk_scenario_json.restype = C.c_int
 
 
 def check(rc: int) -> None:

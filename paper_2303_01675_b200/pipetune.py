@@ -119,3 +119,24 @@ def uniform_model(stage_count: int, global_batch: int, fwd_base: int = 10, bwd_b
                                    output_bytes_per_sample_fwd=fwd_base * (s + 1),
                                    output_bytes_per_sample_bwd=bwd_base * (s + 1))
                       for s in range(stage_count)], global_batch)
+
+
+def scenario(request: dict) -> dict:
+    """Run one JSON scenario through the C++ spec modules (ptk_scenario_json)."""
+    lib = L.lib()
+    req = json.dumps(request).encode()
+    size = C.c_size_t(0)
+    buf = C.create_string_buffer(1 << 20)
+    rc = lib.ptk_scenario_json(req, buf, len(buf), C.byref(size))
+    if size.value > len(buf):
+        buf = C.create_string_buffer(size.value)
+        rc = lib.ptk_scenario_json(req, buf, len(buf), C.byref(size))
+    out = json.loads(buf.value.decode())
+    if rc != 0:
+        raise PipetuneError(out.get("error", str(rc)), out.get("message", ""))
+    return out
+
+
+def model_dict(model: ModelSpec) -> dict:
+    return {"global_batch": model.global_batch,
+            "stages": [{k: getattr(s, k) for k in StageProfile.__dataclass_fields__} for s in model.stages]}
