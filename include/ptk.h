@@ -115,6 +115,46 @@ int ptk_plan_json(const ptk_model* model, int micro_batch_size, int plan_kind, i
  * {"error": "<pipetune type>", "message": ...} and the matching status. */
 int ptk_scenario_json(const char* request, char* buf, size_t cap, size_t* written);
 
+/* ------------------------------------------------------------ GPT stage
+ * One pipeline stage of a GPT model on the current CUDA device: the real
+ * compute behind compute_duration() (proj/src/model.cpp:43-47).  Layers
+ * [layer_begin, layer_end) of an n_layer model; the embedding lives on the
+ * stage with has_embedding, final LayerNorm + LM head + loss on has_head.
+ * Weights are initialised on the device from `seed` per global tensor, so any
+ * stage partition of the same model starts from identical weights. */
+typedef struct ptk_gpt_config {
+    int n_layer, hidden, heads, ffn, seq, vocab;
+    int layer_begin, layer_end;
+    int has_embedding, has_head;
+    int micro_batch_size;  /* b */
+    int slots;             /* activation-stash slots = max in-flight micro-batches */
+    int micro_batches;     /* M: loss and gradients are the mean over M*b*seq tokens */
+    uint64_t seed;
+} ptk_gpt_config;
+
+typedef struct ptk_stage ptk_stage;
+
+int ptk_stage_create(const ptk_gpt_config* cfg, ptk_stage** out);
+int ptk_stage_destroy(ptk_stage* st);
+/* F(m) into stash slot `slot`: tok (int32 [b*seq], embedding stage), x_in (bf16
+ * [b*seq, hidden], other stages), labels (int32, head stage), x_out (bf16, non-head). */
+int ptk_stage_forward(ptk_stage* st, int slot, const int32_t* tok, const void* x_in, const int32_t* labels,
+                      void* x_out, void* stream);
+/* B(m) of stash slot `slot`: dy (bf16, non-head stages), dx (bf16, non-embedding). */
+int ptk_stage_backward(ptk_stage* st, int slot, const int32_t* tok, const void* dy, void* dx, void* stream);
+/* GradAccum finalisation: AdamW on the accumulated gradients, then zero them. */
+int ptk_stage_optimizer_step(ptk_stage* st, float lr, float weight_decay, void* stream);
+int ptk_stage_zero_grads(ptk_stage* st, void* stream);
+/* Flat device buffers (elements): fp32 master weights, bf16 weights, fp32 grads;
+ * loss: device float accumulating the mean loss of the current iteration. */
+int ptk_stage_buffers(ptk_stage* st, float** master, void** weights_bf16, float** grads, float** loss,
+                      int64_t* numel);
+/* Parameter i: name (copied into name_buf), element offset and shape; PTK_ERR_ARG past the end. */
+int ptk_stage_param(ptk_stage* st, int i, char* name_buf, size_t cap, int64_t* offset, int64_t* rows, int64_t* cols);
+/* GEMM event timing inside the stage's launches (roofline evidence). */
+int ptk_stage_gemm_timing(ptk_stage* st, int enable, double* total_flops, double* total_ms, long* launches);
+size_t ptk_stage_stash_bytes(ptk_stage* st);
+
 #ifdef __cplusplus
 }
 #endif

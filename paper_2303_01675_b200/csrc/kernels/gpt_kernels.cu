@@ -1,0 +1,606 @@
+// Memory-bound GPT stage kernels for sm_100a: LayerNorm fwd/bwd, causal
+// softmax fwd/bwd, fused softmax-cross-entropy (loss + dlogits), embedding
+// fwd/bwd, deterministic column reductions (bias / LN-affine grads), AdamW,
+// parameter init.  All reductions use fixed orders (no float atomics), so
+// gradients are bit-reproducible and independent of the schedule's k.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gpt_kernels.h"
+
+namespace ptk {
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 x = __bfloat1622float2(h[i]);
+        f[2 * i] = x.x;
+        f[2 * i + 1] = x.y;
+    }
+}
+
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+}
+
+// --------------------------------------------------------------- LayerNorm
+// One warp per row; lane owns columns {j*256 + lane*8 .. +7}.  V = h / 256.
+template <int V>
+__global__ void __launch_bounds__(128) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                     const __nv_bfloat16* __restrict__ g,
+                                                     const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y,
+                                                     float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                     int rows, float eps) {
+    constexpr int H = V * 256;
+    const int row = blockIdx.x * 4 + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    float v[V][8];
+    const __nv_bfloat16* xr = x + static_cast<int64_t>(row) * H;
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        load8(xr + j * 256 + lane * 8, v[j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += v[j][i];
+    }
+    const float mean = warp_sum(s) * (1.f / H);
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float d = v[j][i] - mean;
+            q += d * d;
+        }
+    const float rstd = rsqrtf(warp_sum(q) * (1.f / H) + eps);
+    __nv_bfloat16* yr = y + static_cast<int64_t>(row) * H;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        float gg[8], bb[8], o[8];
+        load8(g + j * 256 + lane * 8, gg);
+        load8(b + j * 256 + lane * 8, bb);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = (v[j][i] - mean) * rstd * gg[i] + bb[i];
+        store8(yr + j * 256 + lane * 8, o);
+    }
+    if (lane == 0) {
+        mean_out[row] = mean;
+        rstd_out[row] = rstd;
+    }
+}
+
+// dx = rstd * (dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)) + resid.  One warp
+// per row, two passes over the row (the second hits L1), so registers stay
+// bounded for any h.  The affine grads are a separate column reduction.
+template <int V>
+__global__ void __launch_bounds__(128) ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                     const __nv_bfloat16* __restrict__ x,
+                                                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                                                     const __nv_bfloat16* __restrict__ g,
+                                                     const __nv_bfloat16* __restrict__ resid,
+                                                     __nv_bfloat16* __restrict__ dx, int rows) {
+    constexpr int H = V * 256;
+    const int row = blockIdx.x * 4 + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const float mean = mean_in[row], rstd = rstd_in[row];
+    const __nv_bfloat16* xr = x + static_cast<int64_t>(row) * H;
+    const __nv_bfloat16* dr = dy + static_cast<int64_t>(row) * H;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll 4
+    for (int j = 0; j < V; ++j) {
+        float xv[8], dv[8], gv[8];
+        load8(xr + j * 256 + lane * 8, xv);
+        load8(dr + j * 256 + lane * 8, dv);
+        load8(g + j * 256 + lane * 8, gv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float dg = dv[i] * gv[i];
+            s1 += dg;
+            s2 += dg * (xv[i] - mean) * rstd;
+        }
+    }
+    s1 = warp_sum(s1) * (1.f / H);
+    s2 = warp_sum(s2) * (1.f / H);
+#pragma unroll 4
+    for (int j = 0; j < V; ++j) {
+        float xv[8], dv[8], gv[8], o[8];
+        load8(xr + j * 256 + lane * 8, xv);
+        load8(dr + j * 256 + lane * 8, dv);
+        load8(g + j * 256 + lane * 8, gv);
+        float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (resid != nullptr) load8(resid + static_cast<int64_t>(row) * H + j * 256 + lane * 8, rv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = rstd * (dv[i] * gv[i] - s1 - (xv[i] - mean) * rstd * s2) + rv[i];
+        store8(dx + static_cast<int64_t>(row) * H + j * 256 + lane * 8, o);
+    }
+}
+
+// Per-chunk column partials of dgamma = sum dy*xhat and dbeta = sum dy.
+constexpr int kColRows = 64;
+__global__ void ln_affine_partial_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                                         const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                                         float* __restrict__ part_g, float* __restrict__ part_b, int rows, int cols) {
+    const int c2 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (c2 >= cols) return;
+    const int r0 = blockIdx.y * kColRows;
+    float g0 = 0.f, g1 = 0.f, b0 = 0.f, b1 = 0.f;
+    for (int r = r0; r < min(rows, r0 + kColRows); ++r) {
+        const int64_t o = static_cast<int64_t>(r) * cols + c2;
+        const float2 d = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy + o));
+        const float2 xv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + o));
+        const float mean = mean_in[r], rstd = rstd_in[r];
+        g0 += d.x * ((xv.x - mean) * rstd);
+        g1 += d.y * ((xv.y - mean) * rstd);
+        b0 += d.x;
+        b1 += d.y;
+    }
+    part_g[static_cast<int64_t>(blockIdx.y) * cols + c2] = g0;
+    part_g[static_cast<int64_t>(blockIdx.y) * cols + c2 + 1] = g1;
+    part_b[static_cast<int64_t>(blockIdx.y) * cols + c2] = b0;
+    part_b[static_cast<int64_t>(blockIdx.y) * cols + c2 + 1] = b1;
+}
+
+// out[c] += sum_{p < nparts} part[p][c]   (ascending p)
+__global__ void reduce_partials_kernel(const float* __restrict__ part, float* __restrict__ out, int nparts, int cols) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    float s = 0.f;
+    for (int p = 0; p < nparts; ++p) s += part[static_cast<int64_t>(p) * cols + c];
+    out[c] += s;
+}
+
+// Column sums of a bf16 [rows][cols] matrix into per-chunk partials.
+__global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ m, float* __restrict__ part, int rows,
+                                      int cols) {
+    const int c2 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (c2 >= cols) return;
+    const int r0 = blockIdx.y * kColRows;
+    float s0 = 0.f, s1 = 0.f;
+    for (int r = r0; r < min(rows, r0 + kColRows); ++r) {
+        const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(m + static_cast<int64_t>(r) * cols + c2));
+        s0 += v.x;
+        s1 += v.y;
+    }
+    part[static_cast<int64_t>(blockIdx.y) * cols + c2] = s0;
+    part[static_cast<int64_t>(blockIdx.y) * cols + c2 + 1] = s1;
+}
+
+// --------------------------------------------------------------- softmax (causal)
+// S: fp32 [rows][n] (row r of a head covers query q = r % n); P: bf16.
+// Writes P for columns < round_up(q+1, 128): exp for k <= q, exact 0 above.
+__global__ void __launch_bounds__(128) softmax_causal_fwd_kernel(const float* __restrict__ S,
+                                                                 __nv_bfloat16* __restrict__ P, int rows, int n,
+                                                                 float scale_log2) {
+    const int row = blockIdx.x * 4 + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int q = row % n;
+    const int tile_end = min(n, (q / 128 + 1) * 128);
+    const float* s = S + static_cast<int64_t>(row) * n;
+    __nv_bfloat16* p = P + static_cast<int64_t>(row) * n;
+    float mx = -INFINITY;
+    for (int c = lane * 4; c <= q; c += 128) {
+        const float4 v = *reinterpret_cast<const float4*>(s + c);
+        mx = fmaxf(mx, v.x);
+        if (c + 1 <= q) mx = fmaxf(mx, v.y);
+        if (c + 2 <= q) mx = fmaxf(mx, v.z);
+        if (c + 3 <= q) mx = fmaxf(mx, v.w);
+    }
+    mx = warp_max(mx) * scale_log2;
+    float sum = 0.f;
+    for (int c = lane * 4; c <= q; c += 128) {
+        const float4 v = *reinterpret_cast<const float4*>(s + c);
+        sum += exp2f(v.x * scale_log2 - mx);
+        if (c + 1 <= q) sum += exp2f(v.y * scale_log2 - mx);
+        if (c + 2 <= q) sum += exp2f(v.z * scale_log2 - mx);
+        if (c + 3 <= q) sum += exp2f(v.w * scale_log2 - mx);
+    }
+    const float inv = 1.f / warp_sum(sum);
+    for (int c = lane * 4; c < tile_end; c += 128) {
+        const float4 v = *reinterpret_cast<const float4*>(s + c);
+        const float e0 = c <= q ? exp2f(v.x * scale_log2 - mx) * inv : 0.f;
+        const float e1 = c + 1 <= q ? exp2f(v.y * scale_log2 - mx) * inv : 0.f;
+        const float e2 = c + 2 <= q ? exp2f(v.z * scale_log2 - mx) * inv : 0.f;
+        const float e3 = c + 3 <= q ? exp2f(v.w * scale_log2 - mx) * inv : 0.f;
+        __nv_bfloat162 a = __floats2bfloat162_rn(e0, e1), b = __floats2bfloat162_rn(e2, e3);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&a);
+        u.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(p + c) = u;
+    }
+}
+
+// dS = scale * P * (dP - sum_k P dP), written like P (zeros above the diagonal).
+__global__ void __launch_bounds__(128) softmax_causal_bwd_kernel(const __nv_bfloat16* __restrict__ P,
+                                                                 const float* __restrict__ dP,
+                                                                 __nv_bfloat16* __restrict__ dS, int rows, int n,
+                                                                 float scale) {
+    const int row = blockIdx.x * 4 + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int q = row % n;
+    const int tile_end = min(n, (q / 128 + 1) * 128);
+    const __nv_bfloat16* p = P + static_cast<int64_t>(row) * n;
+    const float* d = dP + static_cast<int64_t>(row) * n;
+    float dot = 0.f;
+    for (int c = lane * 4; c <= q; c += 128) {
+        const uint2 u = *reinterpret_cast<const uint2*>(p + c);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        const float4 v = *reinterpret_cast<const float4*>(d + c);
+        dot += a.x * v.x + (c + 1 <= q ? a.y * v.y : 0.f) + (c + 2 <= q ? b.x * v.z : 0.f) +
+               (c + 3 <= q ? b.y * v.w : 0.f);
+    }
+    dot = warp_sum(dot);
+    __nv_bfloat16* o = dS + static_cast<int64_t>(row) * n;
+    for (int c = lane * 4; c < tile_end; c += 128) {
+        const uint2 u = *reinterpret_cast<const uint2*>(p + c);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        const float4 v = *reinterpret_cast<const float4*>(d + c);
+        const float e0 = c <= q ? scale * a.x * (v.x - dot) : 0.f;
+        const float e1 = c + 1 <= q ? scale * a.y * (v.y - dot) : 0.f;
+        const float e2 = c + 2 <= q ? scale * b.x * (v.z - dot) : 0.f;
+        const float e3 = c + 3 <= q ? scale * b.y * (v.w - dot) : 0.f;
+        __nv_bfloat162 x = __floats2bfloat162_rn(e0, e1), y = __floats2bfloat162_rn(e2, e3);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&x);
+        w.y = *reinterpret_cast<uint32_t*>(&y);
+        *reinterpret_cast<uint2*>(o + c) = w;
+    }
+}
+
+// --------------------------------------------------------------- cross-entropy
+// One 512-thread block per row of bf16 logits [rows][V]: loss[row] and, in
+// place, dlogits = (softmax - onehot(label)) * grad_scale.
+__global__ void __launch_bounds__(512) xent_kernel(__nv_bfloat16* __restrict__ logits,
+                                                   const int32_t* __restrict__ labels, float* __restrict__ loss_rows,
+                                                   int V, float grad_scale) {
+    __shared__ float red[32];
+    const int row = blockIdx.x;
+    __nv_bfloat16* z = logits + static_cast<int64_t>(row) * V;
+    const int nvec = V / 8;  // V % 8 == 0
+    // pass 1: online max / sum
+    float mx = -INFINITY, sm = 0.f;
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+        float f[8];
+        load8(z + i * 8, f);
+        float lm = f[0];
+#pragma unroll
+        for (int k = 1; k < 8; ++k) lm = fmaxf(lm, f[k]);
+        const float nm = fmaxf(mx, lm);
+        float add = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) add += __expf(f[k] - nm);
+        sm = sm * __expf(mx - nm) + add;
+        mx = nm;
+    }
+    // block reduce (max, sum)
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    float wm = warp_max(mx);
+    float ws = mx == -INFINITY ? 0.f : sm * __expf(mx - wm);  // idle lanes: avoid (-inf) - (-inf)
+    ws = warp_sum(ws);
+    if (lane == 0) red[warp] = wm;
+    __syncthreads();
+    float gm = -INFINITY;
+    for (int w = 0; w < blockDim.x / 32; ++w) gm = fmaxf(gm, red[w]);
+    __syncthreads();
+    if (lane == 0) red[warp] = wm == -INFINITY ? 0.f : ws * __expf(wm - gm);
+    __syncthreads();
+    float gs = 0.f;
+    for (int w = 0; w < blockDim.x / 32; ++w) gs += red[w];
+    const int lab = labels[row];
+    const float zl = __bfloat162float(z[lab]);
+    __syncthreads();  // everyone has read z[lab] before it is overwritten
+    if (threadIdx.x == 0) loss_rows[row] = __logf(gs) + gm - zl;
+    const float inv = 1.f / gs;
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+        float f[8];
+        load8(z + i * 8, f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float pk = __expf(f[k] - gm) * inv;
+            f[k] = (pk - (i * 8 + k == lab ? 1.f : 0.f)) * grad_scale;
+        }
+        store8(z + i * 8, f);
+    }
+}
+
+// loss_out[0] += sum(loss_rows) * scale  (single block, fixed order)
+__global__ void loss_sum_kernel(const float* __restrict__ loss_rows, float* __restrict__ loss_out, int rows,
+                                float scale) {
+    __shared__ float red[32];
+    float s = 0.f;
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) s += loss_rows[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < blockDim.x / 32; ++w) t += red[w];
+        loss_out[0] += t * scale;
+    }
+}
+
+// --------------------------------------------------------------- embedding
+template <int V>
+__global__ void __launch_bounds__(128) embed_fwd_kernel(const int32_t* __restrict__ tok,
+                                                        const __nv_bfloat16* __restrict__ wte,
+                                                        const __nv_bfloat16* __restrict__ wpe,
+                                                        __nv_bfloat16* __restrict__ x, int rows, int seq) {
+    constexpr int H = V * 256;
+    const int row = blockIdx.x * 4 + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int64_t t = tok[row];
+    const int pos = row % seq;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        float a[8], b[8];
+        load8(wte + t * H + j * 256 + lane * 8, a);
+        load8(wpe + static_cast<int64_t>(pos) * H + j * 256 + lane * 8, b);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] += b[i];
+        store8(x + static_cast<int64_t>(row) * H + j * 256 + lane * 8, a);
+    }
+}
+
+// Owner-computes token-embedding gradient: each warp owns vocabulary rows,
+// scans the micro-batch's tokens (in smem) in position order and accumulates
+// matching dX rows; dwte[v] += sum.  Deterministic, no atomics.
+template <int V>
+__global__ void __launch_bounds__(256) embed_bwd_wte_kernel(const int32_t* __restrict__ tok,
+                                                            const __nv_bfloat16* __restrict__ dx,
+                                                            float* __restrict__ dwte, int rows, int vocab) {
+    constexpr int H = V * 256;
+    extern __shared__ int32_t stok[];
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) stok[i] = tok[i];
+    __syncthreads();
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x / 32;
+    for (int v = blockIdx.x * nwarps + warp; v < vocab; v += gridDim.x * nwarps) {
+        float acc[V][8];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
+        for (int base = 0; base < rows; base += 32) {
+            const int idx = base + lane;
+            unsigned mask = __ballot_sync(0xffffffffu, idx < rows && stok[idx] == v);
+            while (mask) {
+                const int r = base + __ffs(mask) - 1;
+                mask &= mask - 1;
+                any = true;
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    float f[8];
+                    load8(dx + static_cast<int64_t>(r) * H + j * 256 + lane * 8, f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[j][i] += f[i];
+                }
+            }
+        }
+        if (!any) continue;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            float4* d = reinterpret_cast<float4*>(dwte + static_cast<int64_t>(v) * H + j * 256 + lane * 8);
+            float4 a = d[0], b = d[1];
+            a.x += acc[j][0];
+            a.y += acc[j][1];
+            a.z += acc[j][2];
+            a.w += acc[j][3];
+            b.x += acc[j][4];
+            b.y += acc[j][5];
+            b.z += acc[j][6];
+            b.w += acc[j][7];
+            d[0] = a;
+            d[1] = b;
+        }
+    }
+}
+
+// dwpe[p] += sum over samples (ascending) of dx[sample*seq + p]
+__global__ void embed_bwd_wpe_kernel(const __nv_bfloat16* __restrict__ dx, float* __restrict__ dwpe, int seq,
+                                     int samples, int h) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    if (c >= h) return;
+    float s = 0.f;
+    for (int b = 0; b < samples; ++b) s += __bfloat162float(dx[(static_cast<int64_t>(b) * seq + p) * h + c]);
+    dwpe[static_cast<int64_t>(p) * h + c] += s;
+}
+
+// --------------------------------------------------------------- optimizer / init
+__global__ void adamw_kernel(float* __restrict__ w, float* __restrict__ g, float* __restrict__ m,
+                             float* __restrict__ v, __nv_bfloat16* __restrict__ wb, int64_t n, float lr, float b1,
+                             float b2, float eps, float wd, float bc1, float bc2) {
+    for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 4; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x * 4) {
+        float4 ww = *reinterpret_cast<float4*>(w + i), gg = *reinterpret_cast<float4*>(g + i);
+        float4 mm = *reinterpret_cast<float4*>(m + i), vv = *reinterpret_cast<float4*>(v + i);
+        float* pw = &ww.x;
+        float* pg = &gg.x;
+        float* pm = &mm.x;
+        float* pv = &vv.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            pm[k] = b1 * pm[k] + (1.f - b1) * pg[k];
+            pv[k] = b2 * pv[k] + (1.f - b2) * pg[k] * pg[k];
+            const float mh = pm[k] / bc1, vh = pv[k] / bc2;
+            pw[k] = pw[k] - lr * (mh / (sqrtf(vh) + eps) + wd * pw[k]);
+        }
+        *reinterpret_cast<float4*>(w + i) = ww;
+        *reinterpret_cast<float4*>(m + i) = mm;
+        *reinterpret_cast<float4*>(v + i) = vv;
+        *reinterpret_cast<float4*>(g + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        __nv_bfloat162 a = __floats2bfloat162_rn(ww.x, ww.y), b = __floats2bfloat162_rn(ww.z, ww.w);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&a);
+        u.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(wb + i) = u;
+    }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// Counter-based normal init: element i of stream `seed` -> N(0, std) (+ mean for LN gamma).
+__global__ void init_normal_kernel(float* __restrict__ w, int64_t n, uint64_t seed, float std, float mean) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (std == 0.f) {
+            w[i] = mean;
+            continue;
+        }
+        const uint64_t r = splitmix64(seed * 0x100000001B3ull + static_cast<uint64_t>(i));
+        const float u1 = (static_cast<float>(r >> 40) + 1.f) * (1.f / 16777217.f);  // (0,1]
+        const float u2 = static_cast<float>((r >> 16) & 0xFFFFFF) * (1.f / 16777216.f);
+        w[i] = mean + std * sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+    }
+}
+
+__global__ void cast_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+int grid_for(int64_t n, int per_block) {
+    const int64_t g = (n + per_block - 1) / per_block;
+    return static_cast<int>(g < 148 * 32 ? (g < 1 ? 1 : g) : 148 * 32);
+}
+
+}  // namespace
+
+#define PTK_DISPATCH_V(h, CALL)                    \
+    switch ((h) / 256) {                           \
+        case 1: { constexpr int V = 1; CALL; break; } \
+        case 2: { constexpr int V = 2; CALL; break; } \
+        case 4: { constexpr int V = 4; CALL; break; } \
+        case 8: { constexpr int V = 8; CALL; break; } \
+        case 16: { constexpr int V = 16; CALL; break; } \
+        default: return cudaErrorInvalidValue;     \
+    }
+
+cudaError_t layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const __nv_bfloat16* b, __nv_bfloat16* y,
+                          float* mean, float* rstd, int rows, int h, float eps, cudaStream_t st) {
+    if (h % 256) return cudaErrorInvalidValue;
+    const int grid = (rows + 3) / 4;
+    PTK_DISPATCH_V(h, (ln_fwd_kernel<V><<<grid, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps)));
+    return cudaPeekAtLastError();
+}
+
+int layernorm_bwd_parts(int rows) { return (rows + kColRows - 1) / kColRows; }
+
+cudaError_t layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* mean, const float* rstd,
+                          const __nv_bfloat16* g, const __nv_bfloat16* resid, __nv_bfloat16* dx, float* dgamma,
+                          float* dbeta, float* scratch, int rows, int h, cudaStream_t st) {
+    if (h % 256) return cudaErrorInvalidValue;
+    PTK_DISPATCH_V(h, (ln_bwd_kernel<V><<<(rows + 3) / 4, 128, 0, st>>>(dy, x, mean, rstd, g, resid, dx, rows)));
+    const int parts = layernorm_bwd_parts(rows);
+    float* pg = scratch;
+    float* pb = scratch + static_cast<int64_t>(parts) * h;
+    dim3 grid((h / 2 + 127) / 128, parts);
+    ln_affine_partial_kernel<<<grid, 128, 0, st>>>(dy, x, mean, rstd, pg, pb, rows, h);
+    reduce_partials_kernel<<<(h + 255) / 256, 256, 0, st>>>(pg, dgamma, parts, h);
+    reduce_partials_kernel<<<(h + 255) / 256, 256, 0, st>>>(pb, dbeta, parts, h);
+    return cudaPeekAtLastError();
+}
+
+int colsum_parts(int rows) { return (rows + kColRows - 1) / kColRows; }
+
+cudaError_t colsum_accumulate(const __nv_bfloat16* m, float* out, float* scratch, int rows, int cols, cudaStream_t st) {
+    if (cols % 2) return cudaErrorInvalidValue;
+    const int parts = colsum_parts(rows);
+    dim3 grid((cols / 2 + 127) / 128, parts);
+    colsum_partial_kernel<<<grid, 128, 0, st>>>(m, scratch, rows, cols);
+    reduce_partials_kernel<<<(cols + 255) / 256, 256, 0, st>>>(scratch, out, parts, cols);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t softmax_causal_fwd(const float* S, __nv_bfloat16* P, int rows, int n, float scale, cudaStream_t st) {
+    if (n % 128) return cudaErrorInvalidValue;
+    softmax_causal_fwd_kernel<<<(rows + 3) / 4, 128, 0, st>>>(S, P, rows, n, scale * 1.4426950408889634f);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t softmax_causal_bwd(const __nv_bfloat16* P, const float* dP, __nv_bfloat16* dS, int rows, int n,
+                               float scale, cudaStream_t st) {
+    if (n % 128) return cudaErrorInvalidValue;
+    softmax_causal_bwd_kernel<<<(rows + 3) / 4, 128, 0, st>>>(P, dP, dS, rows, n, scale);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss_rows, float* loss_out, int rows,
+                          int vocab, float grad_scale, float loss_scale, cudaStream_t st) {
+    if (vocab % 8) return cudaErrorInvalidValue;
+    xent_kernel<<<rows, 512, 0, st>>>(logits, labels, loss_rows, vocab, grad_scale);
+    loss_sum_kernel<<<1, 1024, 0, st>>>(loss_rows, loss_out, rows, loss_scale);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t embedding_fwd(const int32_t* tok, const __nv_bfloat16* wte, const __nv_bfloat16* wpe, __nv_bfloat16* x,
+                          int rows, int seq, int h, cudaStream_t st) {
+    if (h % 256) return cudaErrorInvalidValue;
+    PTK_DISPATCH_V(h, (embed_fwd_kernel<V><<<(rows + 3) / 4, 128, 0, st>>>(tok, wte, wpe, x, rows, seq)));
+    return cudaPeekAtLastError();
+}
+
+cudaError_t embedding_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* dwte, float* dwpe, int rows, int seq,
+                          int h, int vocab, cudaStream_t st) {
+    if (h % 256 || h > 2048) return cudaErrorInvalidValue;
+    const size_t smem = static_cast<size_t>(rows) * sizeof(int32_t);
+    PTK_DISPATCH_V(h, (embed_bwd_wte_kernel<V><<<148 * 4, 256, smem, st>>>(tok, dx, dwte, rows, vocab)));
+    dim3 grid((h + 255) / 256, seq);
+    embed_bwd_wpe_kernel<<<grid, 256, 0, st>>>(dx, dwpe, seq, rows / seq, h);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t adamw_step(float* w, float* g, float* m, float* v, __nv_bfloat16* wb, int64_t n, float lr, float b1,
+                       float b2, float eps, float wd, int step, cudaStream_t st) {
+    if (n % 4) return cudaErrorInvalidValue;
+    const float bc1 = 1.f - powf(b1, static_cast<float>(step));
+    const float bc2 = 1.f - powf(b2, static_cast<float>(step));
+    adamw_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(w, g, m, v, wb, n, lr, b1, b2, eps, wd, bc1, bc2);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t init_normal(float* w, int64_t n, uint64_t seed, float std, float mean, cudaStream_t st) {
+    init_normal_kernel<<<grid_for(n, 256), 256, 0, st>>>(w, n, seed, std, mean);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t cast_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t st) {
+    cast_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, dst, n);
+    return cudaPeekAtLastError();
+}
+
+}  // namespace ptk

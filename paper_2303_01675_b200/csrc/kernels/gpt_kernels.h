@@ -1,0 +1,36 @@
+// Host launchers for the memory-bound GPT stage kernels (gpt_kernels.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ptk {
+
+cudaError_t layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const __nv_bfloat16* b, __nv_bfloat16* y,
+                          float* mean, float* rstd, int rows, int h, float eps, cudaStream_t st);
+// scratch: 2 * layernorm_bwd_parts(rows) * h floats.  dgamma/dbeta accumulate (+=).
+int layernorm_bwd_parts(int rows);
+cudaError_t layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* mean, const float* rstd,
+                          const __nv_bfloat16* g, const __nv_bfloat16* resid, __nv_bfloat16* dx, float* dgamma,
+                          float* dbeta, float* scratch, int rows, int h, cudaStream_t st);
+// out[c] += sum_r m[r][c]; scratch: colsum_parts(rows) * cols floats.
+int colsum_parts(int rows);
+cudaError_t colsum_accumulate(const __nv_bfloat16* m, float* out, float* scratch, int rows, int cols, cudaStream_t st);
+cudaError_t softmax_causal_fwd(const float* S, __nv_bfloat16* P, int rows, int n, float scale, cudaStream_t st);
+cudaError_t softmax_causal_bwd(const __nv_bfloat16* P, const float* dP, __nv_bfloat16* dS, int rows, int n,
+                               float scale, cudaStream_t st);
+// logits overwritten by dlogits * grad_scale; loss_out[0] += sum(row losses) * loss_scale.
+cudaError_t cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss_rows, float* loss_out, int rows,
+                          int vocab, float grad_scale, float loss_scale, cudaStream_t st);
+cudaError_t embedding_fwd(const int32_t* tok, const __nv_bfloat16* wte, const __nv_bfloat16* wpe, __nv_bfloat16* x,
+                          int rows, int seq, int h, cudaStream_t st);
+cudaError_t embedding_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* dwte, float* dwpe, int rows, int seq,
+                          int h, int vocab, cudaStream_t st);
+cudaError_t adamw_step(float* w, float* g, float* m, float* v, __nv_bfloat16* wb, int64_t n, float lr, float b1,
+                       float b2, float eps, float wd, int step, cudaStream_t st);
+cudaError_t init_normal(float* w, int64_t n, uint64_t seed, float std, float mean, cudaStream_t st);
+cudaError_t cast_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t st);
+
+}  // namespace ptk

@@ -1,0 +1,132 @@
+// kFkB stage executor: the hardware twin of the spec simulator.
+//
+// One Executor per process / GPU / pipeline stage.  run_iteration() walks
+// plan.per_device[stage] (pipetune::plan_kfkb) and enqueues, in plan order:
+//   F(m): [compute stream waits act_flag[m] >= iter+1]  stage.forward
+//         -> send stream: waits F(m) done, copies the output into the next
+//            stage's receive slot m over NVLink (peer copy engine), then
+//            writes the peer's act_flag[m] = iter+1 (stream memory op)
+//   B(m): same with grad_flag / the previous stage
+//   GA:   AdamW step on the accumulated gradients
+// Compute and transfers sit on separate streams and synchronise only through
+// per-micro-batch flags, so a stage whose inputs have arrived keeps computing
+// while a (possibly preempted) transfer drains — the overlap kFkB exploits.
+// The preemption emulator paces every transfer against a LinkTrace on the
+// device (globaltimer-gated chunks), and contender kernels add real competing
+// NVLink traffic (emulator.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../../include/ptk.h"
+#include "emulator.h"
+#include "gpt_stage.h"
+#include "pipetune/plan.hpp"
+
+namespace ptk {
+
+struct CompRecord {
+    int node;   // plan node id
+    int kind;   // 0 F, 1 B, 2 GA
+    int mb;
+    cudaEvent_t start, end;
+};
+
+struct XferRecord {
+    int link;
+    int mb;
+    int64_t bytes;
+    cudaEvent_t start, end;
+};
+
+class Executor {
+  public:
+    explicit Executor(const ptk_exec_config& cfg);
+    ~Executor();
+
+    const ptk_exec_config& cfg() const { return cfg_; }
+    GptStage& stage() { return *stage_; }
+
+    // IPC: this stage's receive blocks and flags, and the peers' in return.
+    std::vector<uint8_t> export_handles() const;
+    void import_peer(int peer_stage, const uint8_t* handles, size_t n);
+    // Same-process peers (tests): raw device pointers instead of IPC.
+    void connect_local(int peer_stage, Executor& peer);
+
+    void set_plan(int k, int micro_batch_size);
+    int plan_k() const { return k_; }
+    int plan_b() const { return b_; }
+
+    void set_trace(int link, const EmuTrace& trace);  // outgoing link pacing
+    void set_contender(bool on) { contender_on_ = on; }
+
+    // Enqueue one training iteration (non-blocking); host_tokens: pinned or
+    // pageable int32 [global_batch][seq+1] (NULL -> built-in synthetic data).
+    void run_iteration(int iter, const int32_t* host_tokens);
+    // Block until the iteration finished; fills records; returns device ms
+    // from iteration start to the GA completion on this stage.
+    double finish_iteration();
+    float read_loss();  // D2H of the iteration's loss (last stage only)
+
+    // Timed probes on an outgoing link with the pipeline suspended.
+    std::vector<int64_t> probe_link(int link, int64_t bytes, int repeats);
+    // Measured compute durations (ns) of F and B at micro-batch size b.
+    void profile_compute(int b, int repeats, int64_t* fwd_ns, int64_t* bwd_ns);
+
+    const std::vector<CompRecord>& comp_records() const { return comp_; }
+    const std::vector<XferRecord>& xfer_records() const { return xfer_; }
+    cudaEvent_t iteration_start() const { return it_start_; }
+    int64_t h2d_bytes() const { return h2d_bytes_; }
+    int64_t d2h_bytes() const { return 4; }
+    int64_t kernel_launches() const { return launches_; }
+
+  private:
+    void alloc_comm();
+    void send(bool forward, int mb, const __nv_bfloat16* src, int64_t bytes, cudaEvent_t ready);
+    cudaEvent_t ev();
+    void synth_tokens(int iter, int32_t* dst) const;
+
+    ptk_exec_config cfg_;
+    std::unique_ptr<GptStage> stage_;
+    std::shared_ptr<const pipetune::TaskGraph> graph_;
+    pipetune::SchedulePlan plan_;
+    int k_ = 1, b_ = 1, M_ = 1;
+    int iter_ = 0;
+
+    cudaStream_t comp_ = nullptr, sendst_ = nullptr, contend_ = nullptr;
+    // receive blocks (owned; written by peers) and flags
+    __nv_bfloat16 *act_recv_ = nullptr, *grad_recv_ = nullptr;
+    uint32_t *act_flag_ = nullptr, *grad_flag_ = nullptr;
+    // peers' blocks (IPC-mapped or same-process)
+    __nv_bfloat16 *peer_act_recv_ = nullptr, *peer_grad_recv_ = nullptr;
+    uint32_t *peer_act_flag_ = nullptr, *peer_grad_flag_ = nullptr;
+    std::vector<void*> ipc_opened_;
+    // send staging, one per stash slot, with WAR events
+    std::vector<__nv_bfloat16*> act_send_, grad_send_;
+    std::vector<cudaEvent_t> act_sent_, grad_sent_;
+    // data
+    int32_t *tok_dev_ = nullptr, *lab_dev_ = nullptr;
+    int32_t* host_stage_ = nullptr;  // pinned [gb][seq+1]
+    int64_t h2d_bytes_ = 0;
+    long launches_ = 0;
+
+    // event pools and records
+    std::vector<cudaEvent_t> pool_;
+    size_t pool_used_ = 0;
+    cudaEvent_t it_start_ = nullptr, it_end_ = nullptr;
+    std::vector<CompRecord> comp_;
+    std::vector<XferRecord> xfer_;
+
+    // emulator
+    Emulator emu_;
+    bool contender_on_ = false;
+
+    std::vector<void*> allocs_;
+};
+
+}  // namespace ptk

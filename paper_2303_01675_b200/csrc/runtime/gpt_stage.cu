@@ -1,0 +1,441 @@
+// GPT stage forward/backward on sm_100a.  See gpt_stage.h and DESIGN.md §4.
+//
+// Per layer forward (T = b*s tokens, h hidden, H heads, d = h/H):
+//   ln1 = LN(x)                          qkv = ln1·Wqkvᵀ + b           (tcgen05 GEMM)
+//   S = Q·Kᵀ (fp32, causal tiles)        P = softmax(S/√d) (bf16)
+//   o = P·V                              x_mid = o·Woᵀ + b + x        (residual in epilogue)
+//   ln2 = LN(x_mid)                      pre = ln2·W1ᵀ + b, a = gelu(pre) (one epilogue)
+//   x_out = a·W2ᵀ + b + x_mid
+// Backward mirrors it; every weight gradient is a K = T GEMM accumulated in
+// place (fp32, β = 1) in the order micro-batches are run — ascending on every
+// device for every k, so gradients are bit-identical across k at fixed b.
+#include "gpt_stage.h"
+
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "../kernels/gpt_kernels.h"
+#include "errors.h"
+
+namespace ptk {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+ptk_matrix mat(const void* p, int64_t ld, int mn = 0, int64_t bs0 = 0, int64_t bs1 = 0) {
+    ptk_matrix m;
+    std::memset(&m, 0, sizeof m);
+    m.ptr = const_cast<void*>(p);
+    m.ld = ld;
+    m.mn_major = mn;
+    m.batch_stride[0] = bs0;
+    m.batch_stride[1] = bs1;
+    return m;
+}
+
+ptk_gemm_desc desc(int m, int n, int k, ptk_matrix a, ptk_matrix b, ptk_matrix c, int epi) {
+    ptk_gemm_desc d;
+    std::memset(&d, 0, sizeof d);
+    d.m = m;
+    d.n = n;
+    d.k = k;
+    d.batch[0] = d.batch[1] = 1;
+    d.a = a;
+    d.b = b;
+    d.c = c;
+    d.epilogue = epi;
+    return d;
+}
+
+}  // namespace
+
+const GemmPlan& GemmCache::get(const ptk_gemm_desc& d) {
+    std::string key(reinterpret_cast<const char*>(&d), sizeof d);
+    auto it = plans_.find(key);
+    if (it != plans_.end()) return *it->second;
+    auto p = std::make_unique<GemmPlan>();
+    const int rc = gemm_prepare(d, p.get());
+    if (rc != PTK_OK)
+        throw std::runtime_error("gemm_prepare failed (" + std::to_string(rc) + ") m=" + std::to_string(d.m) +
+                                 " n=" + std::to_string(d.n) + " k=" + std::to_string(d.k));
+    return *plans_.emplace(std::move(key), std::move(p)).first->second;
+}
+
+void* GptStage::alloc(size_t bytes) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, bytes < 256 ? 256 : bytes), "cudaMalloc");
+    allocs_.push_back(p);
+    return p;
+}
+
+int64_t GptStage::add_param(const std::string& name, int64_t rows, int64_t cols, float std, float mean, uint64_t seed) {
+    ParamInfo p;
+    p.name = name;
+    p.offset = total_;
+    p.rows = rows;
+    p.cols = cols;
+    p.numel = rows * cols;
+    total_ += (p.numel + 63) / 64 * 64;  // keep every tensor 128-byte aligned in bf16
+    params_.push_back(p);
+    init_.push_back({p.offset, p.numel, seed, std, mean});
+    return p.offset;
+}
+
+GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
+    const int h = c.hidden, f = c.ffn, V = c.vocab;
+    if (h % 256 || c.heads <= 0 || h % c.heads || (h / c.heads) % 64 || c.seq % 128 || f % 64 || V % 64)
+        throw std::invalid_argument("GptStage: unsupported shape (h%256, d%64, seq%128, ffn%64, vocab%64)");
+    if (c.layer_begin < 0 || c.layer_end < c.layer_begin || c.layer_end > c.n_layer || c.slots < 1 ||
+        c.micro_batch_size < 1 || c.micro_batches < 1)
+        throw std::invalid_argument("GptStage: bad layer range / slots / batch");
+    L_ = c.layer_end - c.layer_begin;
+    const float proj_std = 0.02f / std::sqrt(2.f * c.n_layer);
+    const uint64_t base = c.seed * 1000003ull;
+
+    // ---- parameters (seeded per global tensor identity: any partition of the
+    //      model into stages initialises identical weights)
+    if (c.has_embedding) {
+        wte_ = add_param("wte", V, h, 0.02f, 0.f, base + 1);
+        wpe_ = add_param("wpe", c.seq, h, 0.02f, 0.f, base + 2);
+    }
+    for (int i = 0; i < L_; ++i) {
+        const int l = c.layer_begin + i;
+        const uint64_t s = base + 100 + 16ull * l;
+        const std::string p = "h" + std::to_string(l) + ".";
+        LayerW w;
+        w.ln1_g = add_param(p + "ln1_g", 1, h, 0.f, 1.f, s + 0);
+        w.ln1_b = add_param(p + "ln1_b", 1, h, 0.f, 0.f, s + 1);
+        w.w_qkv = add_param(p + "w_qkv", 3 * h, h, 0.02f, 0.f, s + 2);
+        w.b_qkv = add_param(p + "b_qkv", 1, 3 * h, 0.f, 0.f, s + 3);
+        w.w_o = add_param(p + "w_o", h, h, proj_std, 0.f, s + 4);
+        w.b_o = add_param(p + "b_o", 1, h, 0.f, 0.f, s + 5);
+        w.ln2_g = add_param(p + "ln2_g", 1, h, 0.f, 1.f, s + 6);
+        w.ln2_b = add_param(p + "ln2_b", 1, h, 0.f, 0.f, s + 7);
+        w.w_fc1 = add_param(p + "w_fc1", f, h, 0.02f, 0.f, s + 8);
+        w.b_fc1 = add_param(p + "b_fc1", 1, f, 0.f, 0.f, s + 9);
+        w.w_fc2 = add_param(p + "w_fc2", h, f, proj_std, 0.f, s + 10);
+        w.b_fc2 = add_param(p + "b_fc2", 1, h, 0.f, 0.f, s + 11);
+        lw_.push_back(w);
+    }
+    if (c.has_head) {
+        lnf_g_ = add_param("lnf_g", 1, h, 0.f, 1.f, base + 3);
+        lnf_b_ = add_param("lnf_b", 1, h, 0.f, 0.f, base + 4);
+        w_head_ = add_param("w_head", V, h, 0.02f, 0.f, base + 5);
+    }
+    master_ = static_cast<float*>(alloc(total_ * 4));
+    grad_ = static_cast<float*>(alloc(total_ * 4));
+    adam_m_ = static_cast<float*>(alloc(total_ * 4));
+    adam_v_ = static_cast<float*>(alloc(total_ * 4));
+    wbf_ = static_cast<__nv_bfloat16*>(alloc(total_ * 2));
+    ck(cudaMemset(master_, 0, total_ * 4), "memset");
+    ck(cudaMemset(grad_, 0, total_ * 4), "memset");
+    ck(cudaMemset(adam_m_, 0, total_ * 4), "memset");
+    ck(cudaMemset(adam_v_, 0, total_ * 4), "memset");
+    for (const InitSpec& in : init_) ck(init_normal(master_ + in.offset, in.numel, in.seed, in.std, in.mean, 0), "init");
+    ck(cast_to_bf16(master_, wbf_, total_, 0), "cast");
+
+    // ---- activation stash
+    const int64_t T = tokens();
+    const int64_t att = static_cast<int64_t>(c.micro_batch_size) * c.heads * c.seq * c.seq;
+    stash_.assign(c.slots, std::vector<LayerStash>(L_));
+    head_.resize(c.slots);
+    const size_t before = 0;
+    (void)before;
+    for (int sl = 0; sl < c.slots; ++sl) {
+        size_t bytes = 0;
+        for (int i = 0; i < L_; ++i) {
+            LayerStash& s = stash_[sl][i];
+            auto bf = [&](int64_t n) {
+                bytes += n * 2;
+                return static_cast<__nv_bfloat16*>(alloc(n * 2));
+            };
+            auto fl = [&](int64_t n) {
+                bytes += n * 4;
+                return static_cast<float*>(alloc(n * 4));
+            };
+            s.x_in = (i == 0 && !c.has_embedding) ? nullptr : bf(T * h);  // layer 0 reads the stage input
+            s.ln1 = bf(T * h);
+            s.qkv = bf(T * 3 * h);
+            s.P = bf(att);
+            s.attn_o = bf(T * h);
+            s.x_mid = bf(T * h);
+            s.ln2 = bf(T * h);
+            s.fc1_pre = bf(T * f);
+            s.fc1_act = bf(T * f);
+            s.mean1 = fl(T);
+            s.rstd1 = fl(T);
+            s.mean2 = fl(T);
+            s.rstd2 = fl(T);
+        }
+        if (c.has_head) {
+            HeadStash& hs = head_[sl];
+            hs.x_fin = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+            hs.xf = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+            hs.dlogits = static_cast<__nv_bfloat16*>(alloc(T * V * 2));
+            hs.meanf = static_cast<float*>(alloc(T * 4));
+            hs.rstdf = static_cast<float*>(alloc(T * 4));
+            bytes += T * h * 4 + T * V * 2 + T * 8;
+        }
+        stash_per_slot_ = bytes;
+    }
+    // x_in of layer i>0 is layer i-1's output: point the stash there.
+    // (layer_forward writes x_out of layer i into stash[i+1].x_in)
+
+    // ---- scratch
+    S_ = static_cast<float*>(alloc(att * 4));
+    dS_ = static_cast<__nv_bfloat16*>(alloc(att * 2));
+    const int64_t wide = std::max<int64_t>(std::max<int64_t>(3 * h, f), h);
+    g_a_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+    g_b_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+    d_pre_ = static_cast<__nv_bfloat16*>(alloc(T * f * 2));
+    d_ln_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+    d_attn_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+    dqkv_ = static_cast<__nv_bfloat16*>(alloc(T * 3 * h * 2));
+    dx_mid_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+    const int64_t parts = std::max(colsum_parts(static_cast<int>(T)), layernorm_bwd_parts(static_cast<int>(T)));
+    red_ = static_cast<float*>(alloc(2 * parts * std::max<int64_t>(wide, V) * 4));
+    loss_rows_ = static_cast<float*>(alloc(T * 4));
+    loss_acc_ = static_cast<float*>(alloc(64));
+    ck(cudaMemset(loss_acc_, 0, 64), "memset");
+    ck(cudaDeviceSynchronize(), "stage init");
+}
+
+GptStage::~GptStage() {
+    for (cudaEvent_t e : timing_.pool) cudaEventDestroy(e);
+    for (void* p : allocs_) cudaFree(p);
+}
+
+void GptStage::gemm(ptk_gemm_desc d, cudaStream_t st) {
+    const GemmPlan& p = cache_.get(d);
+    if (timing_.enabled) {
+        if (timing_.used + 2 > timing_.pool.size()) {
+            for (int i = 0; i < 256; ++i) {
+                cudaEvent_t e;
+                ck(cudaEventCreate(&e), "event");
+                timing_.pool.push_back(e);
+            }
+        }
+        ck(cudaEventRecord(timing_.pool[timing_.used], st), "event");
+        const int rc = gemm_run(p, st);
+        ck(cudaEventRecord(timing_.pool[timing_.used + 1], st), "event");
+        timing_.used += 2;
+        timing_.flops.push_back(p.flops);
+        if (rc != PTK_OK) throw std::runtime_error("gemm launch failed");
+        return;
+    }
+    if (gemm_run(p, st) != PTK_OK) throw std::runtime_error("gemm launch failed");
+}
+
+void GptStage::layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, __nv_bfloat16* x_out,
+                             cudaStream_t st) {
+    const ptk_gpt_config& c = cfg_;
+    const LayerW& w = lw_[li];
+    const int T = tokens(), h = c.hidden, f = c.ffn, H = c.heads, d = h / H, n = c.seq, b = c.micro_batch_size;
+    const __nv_bfloat16* W = wbf_;
+    const int64_t ss = static_cast<int64_t>(n) * n;
+
+    ck(layernorm_fwd(x_in, W + w.ln1_g, W + w.ln1_b, s.ln1, s.mean1, s.rstd1, T, h, 1e-5f, st), "ln1");
+    {
+        ptk_gemm_desc g = desc(T, 3 * h, h, mat(s.ln1, h), mat(W + w.w_qkv, h), mat(s.qkv, 3 * h), PTK_EPI_BF16);
+        g.bias = W + w.b_qkv;
+        gemm(g, st);
+    }
+    {  // S = Q Kᵀ per (head, sample), lower-triangular tiles only
+        ptk_gemm_desc g = desc(n, n, d, mat(s.qkv, 3 * h, 0, d, static_cast<int64_t>(n) * 3 * h),
+                               mat(s.qkv + h, 3 * h, 0, d, static_cast<int64_t>(n) * 3 * h),
+                               mat(S_, n, 0, ss, ss * H), PTK_EPI_F32);
+        g.batch[0] = H;
+        g.batch[1] = b;
+        g.causal = PTK_CAUSAL_TILES;
+        gemm(g, st);
+    }
+    ck(softmax_causal_fwd(S_, s.P, b * H * n, n, 1.f / std::sqrt(static_cast<float>(d)), st), "softmax");
+    {  // O = P V
+        ptk_gemm_desc g = desc(n, d, n, mat(s.P, n, 0, ss, ss * H),
+                               mat(s.qkv + 2 * h, 3 * h, 1, d, static_cast<int64_t>(n) * 3 * h),
+                               mat(s.attn_o, h, 0, d, static_cast<int64_t>(n) * h), PTK_EPI_BF16);
+        g.batch[0] = H;
+        g.batch[1] = b;
+        g.causal = PTK_CAUSAL_KHEAD;
+        gemm(g, st);
+    }
+    {  // x_mid = o Woᵀ + b + x
+        ptk_gemm_desc g = desc(T, h, h, mat(s.attn_o, h), mat(W + w.w_o, h), mat(s.x_mid, h), PTK_EPI_BF16);
+        g.bias = W + w.b_o;
+        g.aux = mat(x_in, h);
+        gemm(g, st);
+    }
+    ck(layernorm_fwd(s.x_mid, W + w.ln2_g, W + w.ln2_b, s.ln2, s.mean2, s.rstd2, T, h, 1e-5f, st), "ln2");
+    {
+        ptk_gemm_desc g = desc(T, f, h, mat(s.ln2, h), mat(W + w.w_fc1, h), mat(s.fc1_act, f), PTK_EPI_BIAS_GELU);
+        g.bias = W + w.b_fc1;
+        g.c2 = s.fc1_pre;
+        gemm(g, st);
+    }
+    {
+        ptk_gemm_desc g = desc(T, h, f, mat(s.fc1_act, f), mat(W + w.w_fc2, f), mat(x_out, h), PTK_EPI_BF16);
+        g.bias = W + w.b_fc2;
+        g.aux = mat(s.x_mid, h);
+        gemm(g, st);
+    }
+}
+
+void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st) {
+    const ptk_gpt_config& c = cfg_;
+    const LayerW& w = lw_[li];
+    const int T = tokens(), h = c.hidden, f = c.ffn, H = c.heads, d = h / H, n = c.seq, b = c.micro_batch_size;
+    const __nv_bfloat16* W = wbf_;
+    float* G = grad_;
+    const int64_t ss = static_cast<int64_t>(n) * n;
+    const int64_t qkv_bs = static_cast<int64_t>(n) * 3 * h;
+    const int64_t o_bs = static_cast<int64_t>(n) * h;
+
+    // FC2: d_pre = (dy W2) * gelu'(pre); dW2 += dyᵀ a; db2 += Σ dy
+    {
+        ptk_gemm_desc g = desc(T, f, h, mat(dy, h), mat(W + w.w_fc2, f, 1), mat(d_pre_, f), PTK_EPI_DGELU);
+        g.aux = mat(s.fc1_pre, f);
+        gemm(g, st);
+    }
+    gemm(desc(h, f, T, mat(dy, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
+    ck(colsum_accumulate(dy, G + w.b_fc2, red_, T, h, st), "db2");
+    // FC1: d_ln2 = d_pre W1; dW1 += d_preᵀ ln2; db1 += Σ d_pre
+    gemm(desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
+    gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.ln2, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
+    ck(colsum_accumulate(d_pre_, G + w.b_fc1, red_, T, f, st), "db1");
+    // LN2 backward + residual: dx_mid = LN2'(d_ln2) + dy
+    ck(layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, G + w.ln2_g, G + w.ln2_b, red_, T, h,
+                     st),
+       "ln2 bwd");
+    // out-proj: d_attn = dx_mid Wo; dWo += dx_midᵀ o; dbo += Σ dx_mid
+    gemm(desc(T, h, h, mat(dx_mid_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
+    gemm(desc(h, h, T, mat(dx_mid_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
+    ck(colsum_accumulate(dx_mid_, G + w.b_o, red_, T, h, st), "dbo");
+    // attention
+    {  // dP = dO Vᵀ
+        ptk_gemm_desc g = desc(n, n, d, mat(d_attn_, h, 0, d, o_bs), mat(s.qkv + 2 * h, 3 * h, 0, d, qkv_bs),
+                               mat(S_, n, 0, ss, ss * H), PTK_EPI_F32);
+        g.batch[0] = H;
+        g.batch[1] = b;
+        g.causal = PTK_CAUSAL_TILES;
+        gemm(g, st);
+    }
+    ck(softmax_causal_bwd(s.P, S_, dS_, b * H * n, n, 1.f / std::sqrt(static_cast<float>(d)), st), "softmax bwd");
+    {  // dQ = dS K
+        ptk_gemm_desc g = desc(n, d, n, mat(dS_, n, 0, ss, ss * H), mat(s.qkv + h, 3 * h, 1, d, qkv_bs),
+                               mat(dqkv_, 3 * h, 0, d, qkv_bs), PTK_EPI_BF16);
+        g.batch[0] = H;
+        g.batch[1] = b;
+        g.causal = PTK_CAUSAL_KHEAD;
+        gemm(g, st);
+    }
+    {  // dK = dSᵀ Q
+        ptk_gemm_desc g = desc(n, d, n, mat(dS_, n, 1, ss, ss * H), mat(s.qkv, 3 * h, 1, d, qkv_bs),
+                               mat(dqkv_ + h, 3 * h, 0, d, qkv_bs), PTK_EPI_BF16);
+        g.batch[0] = H;
+        g.batch[1] = b;
+        g.causal = PTK_CAUSAL_KTAIL;
+        gemm(g, st);
+    }
+    {  // dV = Pᵀ dO
+        ptk_gemm_desc g = desc(n, d, n, mat(s.P, n, 1, ss, ss * H), mat(d_attn_, h, 1, d, o_bs),
+                               mat(dqkv_ + 2 * h, 3 * h, 0, d, qkv_bs), PTK_EPI_BF16);
+        g.batch[0] = H;
+        g.batch[1] = b;
+        g.causal = PTK_CAUSAL_KTAIL;
+        gemm(g, st);
+    }
+    // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv += Σ dqkv
+    gemm(desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
+    gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
+    ck(colsum_accumulate(dqkv_, G + w.b_qkv, red_, T, 3 * h, st), "dbqkv");
+    // LN1 backward + residual: dx = LN1'(d_ln1) + dx_mid
+    ck(layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, dx_mid_, dx, G + w.ln1_g, G + w.ln1_b, red_, T, h,
+                     st),
+       "ln1 bwd");
+}
+
+void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, const int32_t* labels,
+                       __nv_bfloat16* x_out, cudaStream_t st) {
+    const ptk_gpt_config& c = cfg_;
+    const int T = tokens(), h = c.hidden;
+    auto& S = stash_.at(static_cast<size_t>(slot));
+    const __nv_bfloat16* W = wbf_;
+    const __nv_bfloat16* cur = x_in;
+    if (c.has_embedding) {
+        ck(embedding_fwd(tok, W + wte_, W + wpe_, S[0].x_in, T, c.seq, h, st), "embedding");
+        cur = S[0].x_in;
+    } else if (L_ > 0) {
+        S[0].x_in = const_cast<__nv_bfloat16*>(x_in);  // stage input stays live until this slot's backward
+    }
+    for (int i = 0; i < L_; ++i) {
+        __nv_bfloat16* out = (i + 1 < L_) ? S[i + 1].x_in : (c.has_head ? head_[slot].x_fin : x_out);
+        layer_forward(i, S[i], cur, out, st);
+        cur = out;
+    }
+    if (c.has_head) {
+        HeadStash& hs = head_[slot];
+        if (L_ == 0) ck(cudaMemcpyAsync(hs.x_fin, cur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, st), "copy");
+        ck(layernorm_fwd(hs.x_fin, W + lnf_g_, W + lnf_b_, hs.xf, hs.meanf, hs.rstdf, T, h, 1e-5f, st), "lnf");
+        gemm(desc(T, c.vocab, h, mat(hs.xf, h), mat(W + w_head_, h), mat(hs.dlogits, c.vocab), PTK_EPI_BF16), st);
+        const float scale = 1.f / (static_cast<float>(T) * c.micro_batches);
+        ck(cross_entropy(hs.dlogits, labels, loss_rows_, loss_acc_, T, c.vocab, scale, scale, st), "xent");
+    } else if (L_ == 0) {
+        ck(cudaMemcpyAsync(x_out, cur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, st), "copy");
+    }
+}
+
+void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st) {
+    const ptk_gpt_config& c = cfg_;
+    const int T = tokens(), h = c.hidden;
+    auto& S = stash_.at(static_cast<size_t>(slot));
+    const __nv_bfloat16* W = wbf_;
+    float* G = grad_;
+    const __nv_bfloat16* g = dy;
+    if (c.has_head) {
+        HeadStash& hs = head_[slot];
+        // dxf = dlogits W_head ; dW_head += dlogitsᵀ xf
+        gemm(desc(T, h, c.vocab, mat(hs.dlogits, c.vocab), mat(W + w_head_, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
+        gemm(desc(c.vocab, h, T, mat(hs.dlogits, c.vocab, 1), mat(hs.xf, h, 1), mat(G + w_head_, h), PTK_EPI_ACC_F32),
+             st);
+        ck(layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, G + lnf_g_, G + lnf_b_, red_, T,
+                         h, st),
+           "lnf bwd");
+        g = g_a_;
+    }
+    for (int i = L_ - 1; i >= 0; --i) {
+        __nv_bfloat16* out = (i == 0 && !c.has_embedding) ? dx : (g == g_a_ ? g_b_ : g_a_);
+        layer_backward(i, S[i], g, out, st);
+        g = out;
+    }
+    if (c.has_embedding) {
+        ck(embedding_bwd(tok, g, G + wte_, G + wpe_, T, c.seq, h, c.vocab, st), "embedding bwd");
+    } else if (L_ == 0) {
+        ck(cudaMemcpyAsync(dx, g, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, st), "copy");
+    }
+}
+
+void GptStage::optimizer_step(float lr, float wd, cudaStream_t st) {
+    ++step_;
+    ck(adamw_step(master_, grad_, adam_m_, adam_v_, wbf_, total_, lr, 0.9f, 0.95f, 1e-8f, wd, step_, st), "adamw");
+}
+
+void GptStage::collect_timing() {
+    for (size_t i = 0; i + 1 < timing_.used; i += 2) {
+        ck(cudaEventSynchronize(timing_.pool[i + 1]), "event sync");
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, timing_.pool[i], timing_.pool[i + 1]), "elapsed");
+        timing_.total_ms += ms;
+        timing_.total_flops += timing_.flops[i / 2];
+        ++timing_.launches;
+    }
+    timing_.used = 0;
+    timing_.flops.clear();
+}
+
+void GptStage::zero_grads(cudaStream_t st) { ck(cudaMemsetAsync(grad_, 0, total_ * 4, st), "zero grads"); }
+
+}  // namespace ptk

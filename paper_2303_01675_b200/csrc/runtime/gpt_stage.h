@@ -1,0 +1,129 @@
+// One GPT pipeline stage on one B200: parameters (fp32 master + bf16 compute
+// copy + fp32 grads + AdamW moments, each one flat buffer), the activation
+// stash (one slot per in-flight micro-batch), scratch, and the fwd/bwd
+// sequences of sm_100a kernels.  This is the real compute behind the
+// reference's compute_duration() (proj/src/model.cpp:43-47).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../../include/ptk.h"
+#include "../kernels/gemm_sm100.h"
+
+namespace ptk {
+
+struct ParamInfo {
+    std::string name;
+    int64_t offset = 0;  // elements into the flat buffers
+    int64_t numel = 0;
+    int64_t rows = 0, cols = 0;
+};
+
+// Prepared-GEMM cache keyed by the descriptor bytes (tensor maps are bound
+// to buffer addresses; every address the stage uses is stable).
+class GemmCache {
+  public:
+    const GemmPlan& get(const ptk_gemm_desc& d);
+
+  private:
+    std::unordered_map<std::string, std::unique_ptr<GemmPlan>> plans_;
+};
+
+struct GemmTiming {
+    bool enabled = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<double> flops;  // per recorded launch pair
+    double total_flops = 0.0;
+    double total_ms = 0.0;
+    long launches = 0;
+};
+
+class GptStage {
+  public:
+    explicit GptStage(const ptk_gpt_config& cfg);
+    ~GptStage();
+
+    const ptk_gpt_config& cfg() const { return cfg_; }
+    int tokens() const { return cfg_.micro_batch_size * cfg_.seq; }
+
+    // x_in: device bf16 [T, h] activations (ignored on the embedding stage,
+    // which reads `tok`); x_out: where the stage output goes (ignored on the
+    // head stage, which computes the loss from `labels`).
+    void forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, const int32_t* labels,
+                 __nv_bfloat16* x_out, cudaStream_t st);
+    // dy: device bf16 [T, h] gradient of this stage's output (ignored on the
+    // head stage); dx: gradient of the input (ignored on the embedding stage).
+    void backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st);
+    void optimizer_step(float lr, float wd, cudaStream_t st);
+    void zero_grads(cudaStream_t st);
+
+    float* loss_accumulator() { return loss_acc_; }
+    const std::vector<ParamInfo>& params() const { return params_; }
+    float* master() { return master_; }
+    __nv_bfloat16* weights() { return wbf_; }
+    float* grads() { return grad_; }
+    int64_t param_count() const { return total_; }
+    size_t stash_bytes_per_slot() const { return stash_per_slot_; }
+
+    GemmTiming& gemm_timing() { return timing_; }
+    // Synchronises the recorded GEMM event pairs into totals and recycles them.
+    void collect_timing();
+
+  private:
+    struct LayerW {  // element offsets
+        int64_t ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_fc1, b_fc1, w_fc2, b_fc2;
+    };
+    struct LayerStash {
+        __nv_bfloat16 *x_in, *ln1, *qkv, *P, *attn_o, *x_mid, *ln2, *fc1_pre, *fc1_act;
+        float *mean1, *rstd1, *mean2, *rstd2;
+    };
+    struct HeadStash {
+        __nv_bfloat16 *x_fin, *xf, *dlogits;
+        float *meanf, *rstdf;
+    };
+
+    struct InitSpec {
+        int64_t offset, numel;
+        uint64_t seed;
+        float std, mean;
+    };
+    std::vector<InitSpec> init_;
+
+    int64_t add_param(const std::string& name, int64_t rows, int64_t cols, float std, float mean, uint64_t seed);
+    void gemm(ptk_gemm_desc d, cudaStream_t st);
+    void layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, __nv_bfloat16* x_out, cudaStream_t st);
+    void layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st);
+    void* alloc(size_t bytes);
+
+    ptk_gpt_config cfg_;
+    int L_ = 0;  // layers on this stage
+    std::vector<ParamInfo> params_;
+    std::vector<LayerW> lw_;
+    int64_t wte_ = -1, wpe_ = -1, lnf_g_ = -1, lnf_b_ = -1, w_head_ = -1;
+    int64_t total_ = 0;
+    float *master_ = nullptr, *grad_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
+    __nv_bfloat16* wbf_ = nullptr;
+    int step_ = 0;
+
+    std::vector<std::vector<LayerStash>> stash_;  // [slot][layer]
+    std::vector<HeadStash> head_;                 // [slot]
+    size_t stash_per_slot_ = 0;
+
+    // scratch (one micro-batch in flight on the compute stream at a time)
+    float *S_ = nullptr, *red_ = nullptr, *loss_rows_ = nullptr, *loss_acc_ = nullptr;
+    __nv_bfloat16 *dS_ = nullptr, *g_a_ = nullptr, *g_b_ = nullptr, *d_pre_ = nullptr, *d_ln_ = nullptr,
+                  *d_attn_ = nullptr, *dqkv_ = nullptr, *dx_mid_ = nullptr;
+
+    std::vector<void*> allocs_;
+    GemmCache cache_;
+    GemmTiming timing_;
+};
+
+}  // namespace ptk

@@ -1,0 +1,162 @@
+"""Python handle over one GPT pipeline stage (ptk_stage_* in include/ptk.h).
+
+Device buffers owned by the C++ stage are exposed to torch zero-copy through
+__cuda_array_interface__, so tests can read weights/grads without a copy and
+feed torch-allocated activations in by pointer.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+
+
+class GptConfig(C.Structure):
+    _fields_ = [
+        ("n_layer", C.c_int), ("hidden", C.c_int), ("heads", C.c_int), ("ffn", C.c_int), ("seq", C.c_int),
+        ("vocab", C.c_int), ("layer_begin", C.c_int), ("layer_end", C.c_int), ("has_embedding", C.c_int),
+        ("has_head", C.c_int), ("micro_batch_size", C.c_int), ("slots", C.c_int), ("micro_batches", C.c_int),
+        ("seed", C.c_uint64),
+    ]
+
+
+@dataclass(frozen=True)
+class ModelShape:
+    n_layer: int
+    hidden: int
+    heads: int
+    ffn: int
+    seq: int
+    vocab: int
+
+    def params_per_layer(self) -> int:
+        h, f = self.hidden, self.ffn
+        return 3 * h * h + 3 * h + h * h + h + 2 * h * f + f + h + 4 * h
+
+    def flops_per_sample(self) -> float:
+        """Training FLOPs per sample (fwd + bwd = 3x fwd), causal attention at half."""
+        h, f, s, l, V = self.hidden, self.ffn, self.seq, self.n_layer, self.vocab
+        per_tok_layer = 2 * (3 * h * h + h * h + 2 * h * f) + 2 * s * h  # GEMMs + QKᵀ/PV at causal half
+        return 3.0 * s * (l * per_tok_layer + 2 * h * V)
+
+
+GPT_1_3B = ModelShape(24, 2048, 32, 8192, 1024, 50304)
+GPT_6_7B = ModelShape(32, 4096, 32, 16384, 1024, 50304)
+TOY = ModelShape(4, 256, 4, 1024, 128, 512)
+
+
+class _CAI:
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def device_view(ptr: int, numel: int, dtype: torch.dtype) -> torch.Tensor:
+    if dtype == torch.float32:
+        return torch.as_tensor(_CAI(ptr, (numel,), "<f4"), device="cuda")
+    if dtype == torch.bfloat16:
+        return torch.as_tensor(_CAI(ptr, (numel,), "<i2"), device="cuda").view(torch.bfloat16)
+    raise TypeError(dtype)
+
+
+def _declare(lib):
+    if getattr(lib, "_stage_declared", False):
+        return
+    lib.ptk_stage_create.argtypes = [C.POINTER(GptConfig), C.POINTER(C.c_void_p)]
+    lib.ptk_stage_destroy.argtypes = [C.c_void_p]
+    lib.ptk_stage_forward.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.ptk_stage_backward.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.ptk_stage_optimizer_step.argtypes = [C.c_void_p, C.c_float, C.c_float, C.c_void_p]
+    lib.ptk_stage_zero_grads.argtypes = [C.c_void_p, C.c_void_p]
+    lib.ptk_stage_buffers.argtypes = [C.c_void_p] + [C.c_void_p] * 5
+    lib.ptk_stage_param.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_size_t] + [C.POINTER(C.c_int64)] * 3
+    lib.ptk_stage_gemm_timing.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                          C.POINTER(C.c_long)]
+    lib.ptk_stage_stash_bytes.argtypes = [C.c_void_p]
+    lib.ptk_stage_stash_bytes.restype = C.c_size_t
+    lib._stage_declared = True
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return 0
+    return t if isinstance(t, int) else t.data_ptr()
+
+
+class GptStage:
+    def __init__(self, shape: ModelShape, layer_begin: int, layer_end: int, has_embedding: bool, has_head: bool,
+                 micro_batch_size: int, slots: int, micro_batches: int, seed: int = 42):
+        self.lib = L.lib()
+        _declare(self.lib)
+        self.shape = shape
+        self.cfg = GptConfig(shape.n_layer, shape.hidden, shape.heads, shape.ffn, shape.seq, shape.vocab,
+                             layer_begin, layer_end, int(has_embedding), int(has_head), micro_batch_size, slots,
+                             micro_batches, seed)
+        h = C.c_void_p()
+        L.check(self.lib.ptk_stage_create(C.byref(self.cfg), C.byref(h)))
+        self.h = h
+        m, w, g, loss = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        n = C.c_int64()
+        L.check(self.lib.ptk_stage_buffers(self.h, C.byref(m), C.byref(w), C.byref(g), C.byref(loss), C.byref(n)))
+        self.numel = n.value
+        self.master = device_view(m.value, n.value, torch.float32)
+        self.weights = device_view(w.value, n.value, torch.bfloat16)
+        self.grads = device_view(g.value, n.value, torch.float32)
+        self.loss = device_view(loss.value, 1, torch.float32)
+        self.params = {}
+        i = 0
+        buf = C.create_string_buffer(128)
+        while True:
+            off, r, c = C.c_int64(), C.c_int64(), C.c_int64()
+            if self.lib.ptk_stage_param(self.h, i, buf, 128, C.byref(off), C.byref(r), C.byref(c)) != 0:
+                break
+            self.params[buf.value.decode()] = (off.value, r.value, c.value)
+            i += 1
+
+    @property
+    def tokens(self) -> int:
+        return self.cfg.micro_batch_size * self.shape.seq
+
+    def param(self, name: str, which: str = "weights") -> torch.Tensor:
+        off, r, c = self.params[name]
+        flat = {"weights": self.weights, "master": self.master, "grads": self.grads}[which]
+        t = flat[off:off + r * c]
+        return t.view(c) if r == 1 else t.view(r, c)
+
+    def forward(self, slot, tok=None, x_in=None, labels=None, x_out=None, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        L.check(self.lib.ptk_stage_forward(self.h, slot, _ptr(tok), _ptr(x_in), _ptr(labels), _ptr(x_out), s))
+
+    def backward(self, slot, tok=None, dy=None, dx=None, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        L.check(self.lib.ptk_stage_backward(self.h, slot, _ptr(tok), _ptr(dy), _ptr(dx), s))
+
+    def optimizer_step(self, lr=1e-4, wd=0.0, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        L.check(self.lib.ptk_stage_optimizer_step(self.h, lr, wd, s))
+
+    def zero_grads(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        L.check(self.lib.ptk_stage_zero_grads(self.h, s))
+
+    def gemm_timing(self, enable: int = -1):
+        fl, ms, n = C.c_double(), C.c_double(), C.c_long()
+        L.check(self.lib.ptk_stage_gemm_timing(self.h, enable, C.byref(fl), C.byref(ms), C.byref(n)))
+        return fl.value, ms.value, n.value
+
+    def stash_bytes(self) -> int:
+        return self.lib.ptk_stage_stash_bytes(self.h)
+
+    def close(self):
+        if self.h:
+            self.lib.ptk_stage_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
