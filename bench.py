@@ -1,0 +1,296 @@
+"""bench.py — samples/s of the B200 kFkB pipeline executor (GPT-1.3B, bf16).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1: one GPU runs the whole model as a single stage (no pipeline), 32
+micro-batches of b = 2 (global batch 64, seq 1024) — BASELINE.json configs[1]
+at one GPU.  N > 1 (torchrun, one rank per GPU = one pipeline stage): the same
+model split into N stages with emulated NVLink preemption on every link; the
+timed steps run the Ada-Grouper plan (k chosen online by the C++ tuner from
+live link/compute profiles), and 1F1B is timed beside it on the same kernels.
+One JSON line on rank 0.  `--impl reference` times the CPU path (reference
+planner from oracle/_ref + fp32 oracle model on the host cores).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "samples/sec under emulated preemption: Ada-Grouper kFkB vs 1F1B, 2/4/8 B200"
+GLOBAL_BATCH, MICRO_B = 64, 2
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--link-gbps", type=float, default=100.0, help="emulated link bandwidth (Gb/s)")
+    p.add_argument("--availability", type=float, default=0.5, help="constant preempted availability")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--timeline", type=str, default="")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.stop = gpu, [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.cpu_baseline import time_cpu_training
+    from paper_2303_01675_b200.stage import GPT_1_3B
+    vals = []
+    cb = None
+    for i in range(max(1, args.steps)):
+        cb = time_cpu_training(GPT_1_3B, 1, 1)
+        vals.append(cb["value"])
+    v = statistics.median(vals)
+    cb["value"] = v
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "GPT-1.3B (24L, h2048, s1024, V50304) training step, CPU fp32, bounded sample",
+                   "global_batch": GLOBAL_BATCH, "seq_len": 1024, "parallelism": "none (host cores)"},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_01675_b200.executor import StageExecutor, max_inflight, partition_layers
+    from paper_2303_01675_b200.stage import GPT_1_3B
+    from paper_2303_01675_b200.tuning import OnlineTuner, outgoing_links
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.new_group(backend="gloo")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(group=group)
+
+    shape = GPT_1_3B
+    S, M, b = world, GLOBAL_BATCH // MICRO_B, MICRO_B
+    layers = partition_layers(shape.n_layer, S)
+    ks = [1, 2, 4, 8] if S > 1 else [1]
+    slots = max(max_inflight(rank, S, M, k) for k in ks)
+    ex = StageExecutor(shape, rank, S, GLOBAL_BATCH, b_max=b, slots=slots, layers=layers[rank])
+    act_bytes = b * shape.seq * shape.hidden * 2
+    trace_desc = None
+    if S > 1:
+        ex.connect_dist(group)
+        base = args.link_gbps * 1e9 / 8 / 1e9  # bytes per ns
+        horizon = 10**15
+        seg = [(0, horizon, args.availability)] if args.availability < 1.0 else []
+        for link in outgoing_links(rank, S):
+            ex.set_trace(link, base, 0, seg)
+        barrier()
+        ex.set_epoch(ex.globaltimer())
+        trace_desc = {"emulated_link_gbps": args.link_gbps, "availability": args.availability,
+                      "kind": "constant duty cycle" if args.availability < 1 else "no contention"}
+
+    it = 0
+
+    def run(n, k):
+        nonlocal it
+        ex.set_plan(k, b)
+        ms = []
+        for _ in range(n):
+            ex.run_iteration(it)
+            ms.append(ex.finish_iteration())
+            it += 1
+        return ms
+
+    run(args.warmup, 1)
+
+    # ---- Ada-Grouper tuning round (pipeline suspended): live profiles -> C++ decision
+    chosen_k, decision = 1, None
+    if S > 1:
+        tuner = OnlineTuner(ex, rank, S, GLOBAL_BATCH, [(k, b) for k in ks], act_bytes // b, group=group)
+        decision = tuner.round([1, b, M])
+        chosen_k = decision["chosen"][0]
+        barrier()
+        run(1, chosen_k)  # warm the chosen plan
+
+    # ---- timed region: K steps of the chosen plan
+    barrier()
+    with ClockSampler(local) as clk:
+        ex.gemm_timing(1)
+        t0 = time.perf_counter()
+        ms = run(args.steps, chosen_k)
+        barrier()
+        wall = time.perf_counter() - t0
+        gemm_flops, gemm_ms, gemm_n = ex.gemm_timing(0)
+    tl = ex.timeline()
+    loss = ex.read_loss() if rank == S - 1 else None
+    step_ms = sum(ms) / len(ms)
+
+    # ---- 1F1B on the same kernels (reported beside the adaptive plan)
+    ms_1f1b = run(args.steps, 1) if S > 1 else ms
+
+    # ---- e2e: host token buffers through the C ABI, H2D + loss D2H inside the timed steps
+    import numpy as np
+    rng = np.random.default_rng(7)
+    host = rng.integers(0, shape.vocab, size=(2, GLOBAL_BATCH * shape.seq), dtype=np.int32)
+    ex.set_plan(chosen_k, b)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ex.run_iteration(it, host.ctypes.data)
+        ex.finish_iteration()
+        if rank == S - 1:
+            ex.read_loss()
+        it += 1
+    barrier()
+    e2e_s = time.perf_counter() - t0
+
+    def gather(x):
+        if world == 1:
+            return [x]
+        out = [None] * world
+        dist.all_gather_object(out, x, group=group)
+        return out
+
+    all_ms = gather(sum(ms))
+    all_1f1b = gather(sum(ms_1f1b))
+    all_e2e = gather(e2e_s)
+    all_launch = gather(tl["launches"] * args.steps)
+    all_h2d = gather(tl["h2d_bytes"])
+    all_gemm = gather((gemm_flops, gemm_ms, gemm_n))
+    all_clk = gather(clk.summary())
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    T = max(all_ms) / 1e3
+    value = GLOBAL_BATCH * args.steps / T
+    v1f1b = GLOBAL_BATCH * args.steps / (max(all_1f1b) / 1e3)
+    pk, pk_kind = peaks()
+    peak_sus = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    gf = sum(g[0] for g in all_gemm)
+    gt = sum(g[1] for g in all_gemm) / 1e3
+    achieved = gf / gt / 1e12 if gt > 0 else 0.0
+    flops_sample = shape.flops_per_sample()
+    # ideal pipeline roofline: T* = sum_s T_s + (M-1) max_s T_s, T_s = b*FLOPs_s/P
+    per_layer = flops_sample / (shape.n_layer + 2.0)  # head ≈ 2 layer-equivalents (H7) for the split
+    Ts = [b * per_layer * ((e - s_) + (2.0 if i == S - 1 else 0.0)) / (peak_sus * 1e12) for i, (s_, e) in
+          enumerate(layers)]
+    t_star = sum(Ts) + (M - 1) * max(Ts)
+    ideal = M * b / t_star
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(T * 1e3 / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "GPT-1.3B training step (configs[1]: 24L h2048 32 heads s1024 V50304)",
+                   "global_batch": GLOBAL_BATCH, "micro_batch": b, "micro_batches": M, "seq_len": 1024,
+                   "stages": S, "layers_per_stage": [e - s_ for s_, e in layers],
+                   "parallelism": f"pp{S}" if S > 1 else "single stage (no pipeline)",
+                   "schedule": f"Ada-Grouper kFkB (chosen k={chosen_k})" if S > 1 else "1F1B (S=1)",
+                   "emulated_preemption": trace_desc, "l2": "working set (weights + activations) >> 126 MB L2"},
+        "schedules": {"ada_grouper": {"k": chosen_k, "samples_per_s": round(value, 3)},
+                      "1f1b": {"k": 1, "samples_per_s": round(v1f1b, 3)},
+                      "speedup_vs_1f1b": round(value / v1f1b, 4)},
+        "tuner_decision": decision,
+        "pipeline_roofline": {"ideal_samples_per_s": round(ideal, 2), "frac": round(value / ideal, 4),
+                              "peak_tflops": peak_sus, "peak_kind": f"sustained bf16, {pk_kind}"},
+        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_kernel (tcgen05 + TMA, all stage GEMMs)",
+                     "achieved": round(achieved, 1), "peak": peak_sus, "unit": "TFLOP/s",
+                     "frac": round(achieved / peak_sus, 4), "traffic": None,
+                     "launches": sum(g[2] for g in all_gemm),
+                     "note": f"algorithmic GEMM FLOPs / summed CUDA-event GEMM durations over the timed steps; "
+                             f"peak = sustained bf16 of {pk_kind} MEASURED_PEAKS.json"},
+        "e2e": {"value": round(GLOBAL_BATCH * args.steps / max(all_e2e), 3), "unit": "samples/s",
+                "h2d_bytes_per_step": int(sum(all_h2d)), "d2h_bytes_per_step": 4},
+        "gpu_launches": int(sum(all_launch)),
+        "loss": loss,
+        "clocks": all_clk[0],
+        "wall_s_timed": round(wall, 3),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        from oracle.cpu_baseline import time_cpu_training
+        torch.cuda.empty_cache()
+        out["cpu_baseline"] = time_cpu_training(shape, 1, 1)
+    if args.timeline:
+        Path(args.timeline).write_text(json.dumps(tl))
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -155,6 +155,48 @@ int ptk_stage_param(ptk_stage* st, int i, char* name_buf, size_t cap, int64_t* o
 int ptk_stage_gemm_timing(ptk_stage* st, int enable, double* total_flops, double* total_ms, long* launches);
 size_t ptk_stage_stash_bytes(ptk_stage* st);
 
+/* ------------------------------------------------------------ executor
+ * One pipeline stage per process/GPU walking plan_kfkb() orders
+ * (proj/src/plan.cpp:20-59) with Send/Recv pairs (proj/src/taskgraph.cpp:68-76)
+ * realised as NVLink peer copies on a dedicated copy stream plus
+ * per-micro-batch arrival flags (stream memory ops).  gpt.micro_batch_size is
+ * the largest b any plan will use; gpt.slots the largest in-flight count. */
+typedef struct ptk_exec_config {
+    ptk_gpt_config gpt;
+    int stage, stages;
+    int global_batch;
+    float lr, weight_decay;
+    uint64_t data_seed;
+} ptk_exec_config;
+
+typedef struct ptk_exec ptk_exec;
+
+int ptk_exec_create(const ptk_exec_config* cfg, ptk_exec** out);
+int ptk_exec_destroy(ptk_exec* ex);
+/* IPC handles of this stage's receive blocks + arrival flags (opaque bytes). */
+int ptk_exec_export(ptk_exec* ex, void* buf, size_t cap, size_t* written);
+int ptk_exec_import(ptk_exec* ex, int peer_stage, const void* buf, size_t n);
+int ptk_exec_connect_local(ptk_exec* ex, int peer_stage, ptk_exec* peer);
+int ptk_exec_set_plan(ptk_exec* ex, int k, int micro_batch_size);
+/* Emulated-preemption trace for an outgoing link (times relative to the epoch). */
+int ptk_exec_set_trace(ptk_exec* ex, int link, double base_bytes_per_ns, int64_t latency_ns, int nseg,
+                       const int64_t* start_ns, const int64_t* end_ns, const double* availability);
+int ptk_exec_set_epoch(ptk_exec* ex, int64_t epoch_ns);
+int64_t ptk_globaltimer(void);
+/* Enqueue iteration `iter` (host_tokens: int32 [2][global_batch*seq] tokens then
+ * labels, or NULL for the built-in synthetic corpus); finish blocks and
+ * returns the stage's device milliseconds for it. */
+int ptk_exec_run_iteration(ptk_exec* ex, int iter, const int32_t* host_tokens);
+int ptk_exec_finish_iteration(ptk_exec* ex, double* ms);
+int ptk_exec_read_loss(ptk_exec* ex, float* loss);
+/* Records of the last finished iteration, ns from its start:
+ * {"compute": [[node, kind(0F/1B/2GA), mb, start, end]...], "xfer": [[link, mb, bytes, start, end]...],
+ *  "launches": n, "h2d_bytes": n} */
+int ptk_exec_timeline_json(ptk_exec* ex, char* buf, size_t cap, size_t* written);
+int ptk_exec_probe_link(ptk_exec* ex, int link, int64_t bytes, int repeats, int64_t* out_ns);
+int ptk_exec_profile_compute(ptk_exec* ex, int micro_batch_size, int repeats, int64_t* fwd_ns, int64_t* bwd_ns);
+int ptk_exec_gemm_timing(ptk_exec* ex, int enable, double* total_flops, double* total_ms, long* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,81 @@
+"""ORACLE TEST INFRASTRUCTURE — the CPU path timed as bench.py's baseline.
+
+"The reference's CPU path" for this hot path:
+  (i)   the reference planner, compiled unmodified from /root/reference into
+        oracle/_ref/ref_dump (travels to the GPU box with the snapshot), gives
+        the per-device kFkB order;
+  (ii)  that order is executed on the host cores by the fp32 oracle model
+        (oracle/gpt_oracle.py) — one fwd+bwd per scheduled micro-batch —
+        over a BOUNDED sample of the workload.
+Only bench.py's cpu_baseline leg and `--impl reference` call this.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import time
+from pathlib import Path
+
+import torch
+
+from . import gpt_oracle as G
+
+ROOT = Path(__file__).resolve().parents[1]
+REF_BIN = ROOT / "oracle" / "_ref" / "ref_dump"
+
+
+def reference_order(stages: int, micro_batches: int, b: int, k: int) -> tuple[list[str], str]:
+    """Stage-0 order from the compiled reference planner, else the oracle restatement."""
+    if REF_BIN.exists():
+        out = subprocess.run([str(REF_BIN)], input=f"{stages} {micro_batches} {b} 1 {k} 1 1\n",
+                             capture_output=True, text=True, check=True).stdout
+        import json
+        seq = json.loads(out)["sequences"][0].split()
+        return seq, "reference"
+    from . import spec_oracle as O
+    g = O.Graph([{"output_bytes_per_sample_fwd": 1, "output_bytes_per_sample_bwd": 1}] * stages, b, micro_batches)
+    orders = O.kfkb_orders(g, k)
+    names = {0: "F", 1: "B", 4: "GA"}
+    seq = [names[g.nodes[i][0]] + (str(g.nodes[i][2]) if g.nodes[i][0] != 4 else "") for i in orders[0]]
+    return seq, "port"
+
+
+def time_cpu_training(shape, b: int, micro_batches_to_run: int, k: int = 1, threads: int | None = None,
+                      seed: int = 1234) -> dict:
+    """fwd+bwd of `micro_batches_to_run` micro-batches of size b of the full model
+    (single stage, S=1) on the host cores, in the reference planner's order."""
+    threads = threads or os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    seq, kind = reference_order(1, micro_batches_to_run, b, k)
+    g = torch.Generator().manual_seed(42)
+    h, f, V, s = shape.hidden, shape.ffn, shape.vocab, shape.seq
+    w = {"wte": torch.randn(V, h, generator=g) * 0.02, "wpe": torch.randn(s, h, generator=g) * 0.02,
+         "lnf_g": torch.ones(h), "lnf_b": torch.zeros(h), "w_head": torch.randn(V, h, generator=g) * 0.02}
+    for l in range(shape.n_layer):
+        p = f"h{l}."
+        w.update({p + "ln1_g": torch.ones(h), p + "ln1_b": torch.zeros(h),
+                  p + "w_qkv": torch.randn(3 * h, h, generator=g) * 0.02, p + "b_qkv": torch.zeros(3 * h),
+                  p + "w_o": torch.randn(h, h, generator=g) * 0.02, p + "b_o": torch.zeros(h),
+                  p + "ln2_g": torch.ones(h), p + "ln2_b": torch.zeros(h),
+                  p + "w_fc1": torch.randn(f, h, generator=g) * 0.02, p + "b_fc1": torch.zeros(f),
+                  p + "w_fc2": torch.randn(h, f, generator=g) * 0.02, p + "b_fc2": torch.zeros(h)})
+    for t in w.values():
+        t.requires_grad_(True)
+    stash = {}
+    t0 = time.perf_counter()
+    for tok_name in seq:
+        if tok_name == "GA":
+            continue
+        m = int(tok_name[1:])
+        if tok_name[0] == "F":
+            tok, lab = G.synthetic_batch(seed, m, b, s, V)
+            _, loss = G.stage_forward(w, shape, 0, shape.n_layer, True, True, tok=tok, labels=lab,
+                                      micro_batches=micro_batches_to_run)
+            stash[m] = loss
+        else:
+            stash.pop(m).backward()
+    dt = time.perf_counter() - t0
+    samples = b * micro_batches_to_run
+    return {"value": samples / dt, "unit": "samples/s", "cores": threads, "kind": kind,
+            "sample": f"{shape.n_layer}-layer h={h} s={s} GPT fp32 fwd+bwd of {samples} sample(s) "
+                      f"(b={b}) on the host cores in the reference planner's order; {dt:.1f} s"}

@@ -1,0 +1,181 @@
+// C-ABI over the kFkB stage executor (include/ptk.h ptk_exec_*).
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "../../../include/ptk.h"
+#include "../host/json_out.h"
+#include "errors.h"
+#include "executor.h"
+#include "pipetune/errors.hpp"
+
+struct ptk_exec {
+    ptk::Executor impl;
+    explicit ptk_exec(const ptk_exec_config& c) : impl(c) {}
+};
+
+namespace {
+
+template <class F>
+int guarded(const char* what, F&& f) {
+    try {
+        f();
+        return PTK_OK;
+    } catch (const pipetune::ConfigError& e) {
+        return ptk::set_error(PTK_ERR_ARG, std::string(what) + ": " + e.what());
+    } catch (const pipetune::PlanError& e) {
+        return ptk::set_error(PTK_ERR_PLAN, std::string(what) + ": " + e.what());
+    } catch (const pipetune::InfeasibleModel& e) {
+        return ptk::set_error(PTK_ERR_INFEASIBLE, std::string(what) + ": " + e.what());
+    } catch (const std::invalid_argument& e) {
+        return ptk::set_error(PTK_ERR_ARG, std::string(what) + ": " + e.what());
+    } catch (const std::exception& e) {
+        return ptk::set_error(PTK_ERR_CUDA, std::string(what) + ": " + e.what());
+    }
+}
+
+float ms_between(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+}  // namespace
+
+#define EX_CHECK(ex) \
+    if (!(ex)) return ptk::set_error(PTK_ERR_ARG, "null executor")
+
+extern "C" int ptk_exec_create(const ptk_exec_config* cfg, ptk_exec** out) {
+    if (!cfg || !out) return ptk::set_error(PTK_ERR_ARG, "ptk_exec_create: null argument");
+    return guarded("ptk_exec_create", [&] { *out = new ptk_exec(*cfg); });
+}
+
+extern "C" int ptk_exec_destroy(ptk_exec* ex) {
+    delete ex;
+    return PTK_OK;
+}
+
+extern "C" int ptk_exec_export(ptk_exec* ex, void* buf, size_t cap, size_t* written) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_export", [&] {
+        const auto h = ex->impl.export_handles();
+        if (written) *written = h.size();
+        if (!buf || cap < h.size()) throw std::invalid_argument("buffer too small");
+        std::memcpy(buf, h.data(), h.size());
+    });
+}
+
+extern "C" int ptk_exec_import(ptk_exec* ex, int peer, const void* buf, size_t n) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_import",
+                   [&] { ex->impl.import_peer(peer, static_cast<const uint8_t*>(buf), n); });
+}
+
+extern "C" int ptk_exec_connect_local(ptk_exec* ex, int peer, ptk_exec* other) {
+    EX_CHECK(ex);
+    if (!other) return ptk::set_error(PTK_ERR_ARG, "null peer");
+    return guarded("ptk_exec_connect_local", [&] { ex->impl.connect_local(peer, other->impl); });
+}
+
+extern "C" int ptk_exec_set_plan(ptk_exec* ex, int k, int b) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_set_plan", [&] { ex->impl.set_plan(k, b); });
+}
+
+extern "C" int ptk_exec_set_trace(ptk_exec* ex, int link, double base, int64_t latency, int nseg, const int64_t* s,
+                                  const int64_t* e, const double* a) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_set_trace", [&] {
+        ptk::EmuTrace t;
+        t.active = base > 0.0;
+        t.base_bytes_per_ns = base;
+        t.latency_ns = latency;
+        for (int i = 0; i < nseg; ++i) t.segments.push_back({s[i], e[i], a[i]});
+        ex->impl.set_trace(link, t);
+    });
+}
+
+extern "C" int ptk_exec_set_epoch(ptk_exec* ex, int64_t epoch) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_set_epoch", [&] { ex->impl.set_epoch(epoch); });
+}
+
+extern "C" int64_t ptk_globaltimer(void) {
+    try {
+        return ptk::device_globaltimer(0);
+    } catch (...) {
+        return -1;
+    }
+}
+
+extern "C" int ptk_exec_run_iteration(ptk_exec* ex, int iter, const int32_t* host_tokens) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_run_iteration", [&] { ex->impl.run_iteration(iter, host_tokens); });
+}
+
+extern "C" int ptk_exec_finish_iteration(ptk_exec* ex, double* ms) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_finish_iteration", [&] {
+        const double v = ex->impl.finish_iteration();
+        if (ms) *ms = v;
+    });
+}
+
+extern "C" int ptk_exec_read_loss(ptk_exec* ex, float* loss) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_read_loss", [&] { *loss = ex->impl.read_loss(); });
+}
+
+extern "C" int ptk_exec_timeline_json(ptk_exec* ex, char* buf, size_t cap, size_t* written) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_timeline_json", [&] {
+        pipetune::json::Writer w;
+        cudaEvent_t t0 = ex->impl.iteration_start();
+        auto ns = [&](cudaEvent_t e) { return static_cast<long long>(ms_between(t0, e) * 1e6 + 0.5); };
+        w.begin_obj().key("compute").begin_arr();
+        for (const auto& r : ex->impl.comp_records())
+            w.begin_arr().v(r.node).v(r.kind).v(r.mb).v(ns(r.start)).v(ns(r.end)).end_arr();
+        w.end_arr().key("xfer").begin_arr();
+        for (const auto& r : ex->impl.xfer_records())
+            w.begin_arr().v(r.link).v(r.mb).v(r.bytes).v(ns(r.start)).v(ns(r.end)).end_arr();
+        w.end_arr();
+        w.key("launches").num(ex->impl.kernel_launches());
+        w.key("h2d_bytes").num(ex->impl.h2d_bytes());
+        w.key("k").num(ex->impl.plan_k());
+        w.key("b").num(ex->impl.plan_b());
+        w.end_obj();
+        if (written) *written = w.out.size() + 1;
+        if (!buf || cap < w.out.size() + 1) throw std::invalid_argument("buffer too small");
+        std::memcpy(buf, w.out.c_str(), w.out.size() + 1);
+    });
+}
+
+extern "C" int ptk_exec_probe_link(ptk_exec* ex, int link, int64_t bytes, int repeats, int64_t* out_ns) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_probe_link", [&] {
+        const auto v = ex->impl.probe_link(link, bytes, repeats);
+        for (size_t i = 0; i < v.size(); ++i) out_ns[i] = v[i];
+    });
+}
+
+extern "C" int ptk_exec_profile_compute(ptk_exec* ex, int b, int repeats, int64_t* f, int64_t* bw) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_profile_compute", [&] { ex->impl.profile_compute(b, repeats, f, bw); });
+}
+
+extern "C" int ptk_exec_gemm_timing(ptk_exec* ex, int enable, double* total_flops, double* total_ms,
+                                    long* launches) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_gemm_timing", [&] {
+        ptk::GemmTiming& t = ex->impl.stage().gemm_timing();
+        ex->impl.stage().collect_timing();
+        if (total_flops) *total_flops = t.total_flops;
+        if (total_ms) *total_ms = t.total_ms;
+        if (launches) *launches = t.launches;
+        if (enable >= 0) {
+            t.enabled = enable != 0;
+            t.total_flops = t.total_ms = 0.0;
+            t.launches = 0;
+        }
+    });
+}

@@ -1,0 +1,438 @@
+// kFkB stage executor — see executor.h.
+#include "executor.h"
+
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+
+#include "pipetune/errors.hpp"
+
+namespace ptk {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct StreamOps {
+    WaitValueFn wait = nullptr;
+    WriteValueFn write = nullptr;
+};
+
+const StreamOps& stream_ops() {
+    static StreamOps ops;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            ops.wait = reinterpret_cast<WaitValueFn>(p);
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            ops.write = reinterpret_cast<WriteValueFn>(p);
+    });
+    if (!ops.wait || !ops.write) throw std::runtime_error("cuStreamWaitValue32/WriteValue32 unavailable");
+    return ops;
+}
+
+void wait_flag(cudaStream_t st, const uint32_t* flag, uint32_t value) {
+    const CUresult r = stream_ops().wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flag), value,
+                                         CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuStreamWaitValue32 failed: " + std::to_string(r));
+}
+
+void write_flag(cudaStream_t st, uint32_t* flag, uint32_t value) {
+    const CUresult r = stream_ops().write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flag), value,
+                                          CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuStreamWriteValue32 failed: " + std::to_string(r));
+}
+
+uint64_t mix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+constexpr size_t kHandle = sizeof(cudaIpcMemHandle_t);
+
+}  // namespace
+
+Executor::Executor(const ptk_exec_config& c) : cfg_(c) {
+    if (c.stages < 1 || c.stage < 0 || c.stage >= c.stages || c.global_batch < 1)
+        throw std::invalid_argument("Executor: bad stage / global batch");
+    int lo = 0, hi = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priorities");
+    ck(cudaStreamCreateWithPriority(&comp_, cudaStreamNonBlocking, hi), "stream");
+    ck(cudaStreamCreateWithPriority(&sendst_, cudaStreamNonBlocking, lo), "stream");
+    ck(cudaStreamCreateWithPriority(&contend_, cudaStreamNonBlocking, lo), "stream");
+    stage_ = std::make_unique<GptStage>(c.gpt);
+    ck(cudaEventCreate(&it_start_), "event");
+    ck(cudaEventCreate(&it_end_), "event");
+    ck(cudaEventCreateWithFlags(&h2d_done_, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(h2d_done_, comp_), "event");
+    alloc_comm();
+    set_plan(1, c.gpt.micro_batch_size);
+}
+
+Executor::~Executor() {
+    emu_.stop_contender();
+    cudaDeviceSynchronize();
+    for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+    for (cudaEvent_t e : pool_) cudaEventDestroy(e);
+    for (cudaEvent_t e : act_sent_) cudaEventDestroy(e);
+    for (cudaEvent_t e : grad_sent_) cudaEventDestroy(e);
+    cudaEventDestroy(it_start_);
+    cudaEventDestroy(it_end_);
+    cudaEventDestroy(h2d_done_);
+    for (void* p : allocs_) cudaFree(p);
+    if (host_stage_) cudaFreeHost(host_stage_);
+    cudaStreamDestroy(comp_);
+    cudaStreamDestroy(sendst_);
+    cudaStreamDestroy(contend_);
+}
+
+void Executor::alloc_comm() {
+    const ptk_gpt_config& g = cfg_.gpt;
+    const int64_t block = static_cast<int64_t>(cfg_.global_batch) * g.seq * g.hidden * 2;
+    const int64_t tmax = static_cast<int64_t>(g.micro_batch_size) * g.seq;
+    auto dalloc = [this](size_t n) {
+        void* p = nullptr;
+        ck(cudaMalloc(&p, n), "cudaMalloc comm");
+        ck(cudaMemset(p, 0, n), "memset");
+        allocs_.push_back(p);
+        return p;
+    };
+    if (cfg_.stage > 0) {
+        act_recv_ = static_cast<__nv_bfloat16*>(dalloc(block));
+        act_flag_ = static_cast<uint32_t*>(dalloc(cfg_.global_batch * 4 + 256));
+        for (int s = 0; s < g.slots; ++s) {
+            grad_send_.push_back(static_cast<__nv_bfloat16*>(dalloc(tmax * g.hidden * 2)));
+            cudaEvent_t e;
+            ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(e, sendst_), "event");
+            grad_sent_.push_back(e);
+        }
+    }
+    if (cfg_.stage + 1 < cfg_.stages) {
+        grad_recv_ = static_cast<__nv_bfloat16*>(dalloc(block));
+        grad_flag_ = static_cast<uint32_t*>(dalloc(cfg_.global_batch * 4 + 256));
+        for (int s = 0; s < g.slots; ++s) {
+            act_send_.push_back(static_cast<__nv_bfloat16*>(dalloc(tmax * g.hidden * 2)));
+            cudaEvent_t e;
+            ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(e, sendst_), "event");
+            act_sent_.push_back(e);
+        }
+    }
+    const int64_t toks = static_cast<int64_t>(cfg_.global_batch) * g.seq;
+    tok_dev_ = static_cast<int32_t*>(dalloc(toks * 4));
+    lab_dev_ = static_cast<int32_t*>(dalloc(toks * 4));
+    ck(cudaHostAlloc(&host_stage_, toks * 2 * 4, cudaHostAllocDefault), "pinned");
+}
+
+std::vector<uint8_t> Executor::export_handles() const {
+    std::vector<uint8_t> out(4 * (1 + kHandle), 0);
+    const void* ptrs[4] = {act_recv_, act_flag_, grad_recv_, grad_flag_};
+    for (int i = 0; i < 4; ++i) {
+        if (!ptrs[i]) continue;
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, const_cast<void*>(ptrs[i])), "ipc get");
+        out[i * (1 + kHandle)] = 1;
+        std::memcpy(&out[i * (1 + kHandle) + 1], &h, kHandle);
+    }
+    return out;
+}
+
+void Executor::import_peer(int peer, const uint8_t* bytes, size_t n) {
+    if (n < 4 * (1 + kHandle)) throw std::invalid_argument("import_peer: short handle blob");
+    auto open = [&](int i) -> void* {
+        if (!bytes[i * (1 + kHandle)]) throw std::invalid_argument("import_peer: peer lacks the needed buffer");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, bytes + i * (1 + kHandle) + 1, kHandle);
+        void* p = nullptr;
+        ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+        ipc_opened_.push_back(p);
+        return p;
+    };
+    if (peer == cfg_.stage + 1) {
+        peer_act_recv_ = static_cast<__nv_bfloat16*>(open(0));
+        peer_act_flag_ = static_cast<uint32_t*>(open(1));
+    } else if (peer == cfg_.stage - 1) {
+        peer_grad_recv_ = static_cast<__nv_bfloat16*>(open(2));
+        peer_grad_flag_ = static_cast<uint32_t*>(open(3));
+    } else {
+        throw std::invalid_argument("import_peer: not an adjacent stage");
+    }
+}
+
+void Executor::connect_local(int peer, Executor& p) {
+    if (peer == cfg_.stage + 1) {
+        peer_act_recv_ = p.act_recv_;
+        peer_act_flag_ = p.act_flag_;
+    } else if (peer == cfg_.stage - 1) {
+        peer_grad_recv_ = p.grad_recv_;
+        peer_grad_flag_ = p.grad_flag_;
+    } else {
+        throw std::invalid_argument("connect_local: not an adjacent stage");
+    }
+}
+
+void Executor::set_plan(int k, int b) {
+    const ptk_gpt_config& g = cfg_.gpt;
+    if (b < 1 || b > g.micro_batch_size || cfg_.global_batch % b)
+        throw pipetune::ConfigError("set_plan: micro-batch size must divide the global batch and be <= b_max");
+    pipetune::ModelSpec spec;
+    spec.global_batch = cfg_.global_batch;
+    for (int s = 0; s < cfg_.stages; ++s) {
+        pipetune::StageProfile p;
+        p.stage_id = s;
+        p.output_bytes_per_sample_fwd = static_cast<pipetune::Bytes>(g.seq) * g.hidden * 2;
+        p.output_bytes_per_sample_bwd = p.output_bytes_per_sample_fwd;
+        spec.stages.push_back(p);
+    }
+    pipetune::PlanConfig pc{1, b, cfg_.global_batch / b};
+    graph_ = std::make_shared<const pipetune::TaskGraph>(pipetune::build_task_graph(spec, pc));
+    plan_ = pipetune::plan_kfkb(graph_, k);
+    // the stash must hold this stage's peak number of in-flight micro-batches
+    int live = 0, peak = 0;
+    for (int id : plan_.per_device[static_cast<size_t>(cfg_.stage)]) {
+        const auto kind = graph_->node(id).kind;
+        if (kind == pipetune::TaskKind::ForwardCompute) peak = std::max(peak, ++live);
+        if (kind == pipetune::TaskKind::BackwardCompute) --live;
+    }
+    if (peak > g.slots)
+        throw pipetune::InfeasibleModel("set_plan: k=" + std::to_string(k) + " needs " + std::to_string(peak) +
+                                        " stash slots, stage has " + std::to_string(g.slots));
+    k_ = k;
+    b_ = b;
+    M_ = cfg_.global_batch / b;
+    stage_->set_micro_batch(b, M_);
+}
+
+void Executor::set_trace(int link, const EmuTrace& t) {
+    const int slot = (link == 2 * cfg_.stage) ? 0 : (link == 2 * cfg_.stage - 1 ? 1 : -1);
+    if (slot < 0) throw std::invalid_argument("set_trace: link is not outgoing from this stage");
+    emu_.set_trace(slot, t);
+}
+
+void Executor::set_epoch(int64_t epoch_ns) { emu_.set_epoch(epoch_ns); }
+
+cudaEvent_t Executor::ev() {
+    if (pool_used_ == pool_.size()) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "event");
+        pool_.push_back(e);
+    }
+    return pool_[pool_used_++];
+}
+
+void Executor::synth_tokens(int iter, int32_t* dst) const {
+    // Synthetic corpus: tokens uniform in [0, V) from a counter-based hash of
+    // (seed, iteration, sample, position); labels are the next token.
+    const ptk_gpt_config& g = cfg_.gpt;
+    const int64_t gb = cfg_.global_batch, s = g.seq;
+    int32_t* tok = dst;
+    int32_t* lab = dst + gb * s;
+    for (int64_t i = 0; i < gb; ++i) {
+        uint64_t base = mix64(cfg_.data_seed ^ mix64(static_cast<uint64_t>(iter) * 0x10001ull + static_cast<uint64_t>(i)));
+        int32_t prev = static_cast<int32_t>(mix64(base) % static_cast<uint64_t>(g.vocab));
+        for (int64_t p = 0; p < s; ++p) {
+            const int32_t next = static_cast<int32_t>(mix64(base + static_cast<uint64_t>(p) + 1) % static_cast<uint64_t>(g.vocab));
+            tok[i * s + p] = prev;
+            lab[i * s + p] = next;
+            prev = next;
+        }
+    }
+}
+
+void Executor::send(bool fwd, int mb, const __nv_bfloat16* src, int64_t bytes, cudaEvent_t ready) {
+    const ptk_gpt_config& g = cfg_.gpt;
+    __nv_bfloat16* dst_block = fwd ? peer_act_recv_ : peer_grad_recv_;
+    uint32_t* flag = fwd ? peer_act_flag_ : peer_grad_flag_;
+    if (!dst_block || !flag) throw std::runtime_error("send: peer not connected");
+    const int64_t off = static_cast<int64_t>(mb) * b_ * g.seq * g.hidden;
+    ck(cudaStreamWaitEvent(sendst_, ready, 0), "wait");
+    XferRecord r{fwd ? 2 * cfg_.stage : 2 * cfg_.stage - 1, mb, bytes, ev(), ev()};
+    ck(cudaEventRecord(r.start, sendst_), "event");
+    ck(emu_.paced_copy(fwd ? 0 : 1, dst_block + off, src, bytes, sendst_), "peer copy");
+    if (emu_.active(fwd ? 0 : 1)) emu_launches_ += Emulator::kChunks + 1;
+    write_flag(sendst_, flag + mb, static_cast<uint32_t>(iter_ + 1));
+    ck(cudaEventRecord(r.end, sendst_), "event");
+    xrec_.push_back(r);
+}
+
+void Executor::run_iteration(int iter, const int32_t* host_tokens) {
+    const ptk_gpt_config& g = cfg_.gpt;
+    const int S = cfg_.stages, s = cfg_.stage;
+    const bool first = s == 0, last = s == S - 1;
+    const int64_t T = static_cast<int64_t>(b_) * g.seq;
+    const int64_t act_bytes = T * g.hidden * 2;
+    const int64_t toks = static_cast<int64_t>(cfg_.global_batch) * g.seq;
+    iter_ = iter;
+    pool_used_ = 0;
+    crec_.clear();
+    xrec_.clear();
+    stage_->reset_launches();
+
+    // data for this iteration (host -> device inside the iteration, e2e);
+    // the pinned staging buffer is free once the previous iteration's H2D ran
+    ck(cudaEventSynchronize(h2d_done_), "h2d wait");
+    if (host_tokens)
+        std::memcpy(host_stage_, host_tokens, static_cast<size_t>(toks) * 2 * 4);
+    else
+        synth_tokens(iter, host_stage_);
+    ck(cudaEventRecord(it_start_, comp_), "event");
+    ck(cudaStreamWaitEvent(sendst_, it_start_, 0), "wait");
+    h2d_bytes_ = 0;
+    if (first) {
+        ck(cudaMemcpyAsync(tok_dev_, host_stage_, toks * 4, cudaMemcpyHostToDevice, comp_), "h2d");
+        h2d_bytes_ += toks * 4;
+    }
+    if (last) {
+        ck(cudaMemcpyAsync(lab_dev_, host_stage_ + toks, toks * 4, cudaMemcpyHostToDevice, comp_), "h2d");
+        h2d_bytes_ += toks * 4;
+    }
+    ck(cudaEventRecord(h2d_done_, comp_), "event");
+    if (last) ck(cudaMemsetAsync(stage_->loss_accumulator(), 0, 4, comp_), "memset");
+    emu_launches_ = 0;
+
+    for (int id : plan_.per_device[static_cast<size_t>(s)]) {
+        const pipetune::TaskNode& n = graph_->node(id);
+        const int m = n.micro_batch;
+        const int slot = m >= 0 ? m % g.slots : 0;
+        if (n.kind == pipetune::TaskKind::ForwardCompute) {
+            if (!first) wait_flag(comp_, act_flag_ + m, static_cast<uint32_t>(iter + 1));
+            __nv_bfloat16* out = last ? nullptr : act_send_[static_cast<size_t>(slot)];
+            if (!last) ck(cudaStreamWaitEvent(comp_, act_sent_[static_cast<size_t>(slot)], 0), "wait");
+            CompRecord r{id, 0, m, ev(), ev()};
+            ck(cudaEventRecord(r.start, comp_), "event");
+            stage_->forward(slot, tok_dev_ + m * T, first ? nullptr : act_recv_ + m * T * g.hidden, lab_dev_ + m * T,
+                            out, comp_);
+            ck(cudaEventRecord(r.end, comp_), "event");
+            crec_.push_back(r);
+            if (!last) {
+                send(true, m, out, act_bytes, r.end);
+                ck(cudaEventRecord(act_sent_[static_cast<size_t>(slot)], sendst_), "event");
+            }
+        } else if (n.kind == pipetune::TaskKind::BackwardCompute) {
+            if (!last) wait_flag(comp_, grad_flag_ + m, static_cast<uint32_t>(iter + 1));
+            __nv_bfloat16* dx = first ? nullptr : grad_send_[static_cast<size_t>(slot)];
+            if (!first) ck(cudaStreamWaitEvent(comp_, grad_sent_[static_cast<size_t>(slot)], 0), "wait");
+            CompRecord r{id, 1, m, ev(), ev()};
+            ck(cudaEventRecord(r.start, comp_), "event");
+            stage_->backward(slot, tok_dev_ + m * T, last ? nullptr : grad_recv_ + m * T * g.hidden, dx, comp_);
+            ck(cudaEventRecord(r.end, comp_), "event");
+            crec_.push_back(r);
+            if (!first) {
+                send(false, m, dx, act_bytes, r.end);
+                ck(cudaEventRecord(grad_sent_[static_cast<size_t>(slot)], sendst_), "event");
+            }
+        } else if (n.kind == pipetune::TaskKind::GradAccum) {
+            CompRecord r{id, 2, -1, ev(), ev()};
+            ck(cudaEventRecord(r.start, comp_), "event");
+            stage_->optimizer_step(cfg_.lr, cfg_.weight_decay, comp_);
+            ck(cudaEventRecord(r.end, comp_), "event");
+            crec_.push_back(r);
+        }
+    }
+    ck(cudaEventRecord(it_end_, comp_), "event");
+}
+
+double Executor::finish_iteration() {
+    ck(cudaStreamSynchronize(comp_), "sync compute");
+    ck(cudaStreamSynchronize(sendst_), "sync send");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, it_start_, it_end_), "elapsed");
+    return ms;
+}
+
+float Executor::read_loss() {
+    float v = 0.f;
+    ck(cudaMemcpyAsync(&v, stage_->loss_accumulator(), 4, cudaMemcpyDeviceToHost, comp_), "d2h");
+    ck(cudaStreamSynchronize(comp_), "sync");
+    return v;
+}
+
+std::vector<int64_t> Executor::probe_link(int link, int64_t bytes, int repeats) {
+    const bool fwd = link == 2 * cfg_.stage;
+    if (!fwd && link != 2 * cfg_.stage - 1) throw std::invalid_argument("probe_link: not an outgoing link");
+    __nv_bfloat16* dst = fwd ? peer_act_recv_ : peer_grad_recv_;
+    const __nv_bfloat16* src = fwd ? act_send_.at(0) : grad_send_.at(0);
+    const int64_t cap = static_cast<int64_t>(cfg_.gpt.micro_batch_size) * cfg_.gpt.seq * cfg_.gpt.hidden * 2;
+    if (!dst || bytes > cap) throw std::invalid_argument("probe_link: peer not connected or payload too large");
+    std::vector<int64_t> out;
+    cudaEvent_t a, b;
+    ck(cudaEventCreate(&a), "event");
+    ck(cudaEventCreate(&b), "event");
+    for (int r = 0; r < repeats; ++r) {
+        ck(cudaEventRecord(a, sendst_), "event");
+        ck(emu_.paced_copy(fwd ? 0 : 1, dst, src, bytes, sendst_), "probe copy");
+        ck(cudaEventRecord(b, sendst_), "event");
+        ck(cudaEventSynchronize(b), "sync");
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+        out.push_back(static_cast<int64_t>(static_cast<double>(ms) * 1e6 + 0.5));
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return out;
+}
+
+void Executor::profile_compute(int b, int repeats, int64_t* fwd_ns, int64_t* bwd_ns) {
+    const ptk_gpt_config& g = cfg_.gpt;
+    const int keep_b = b_, keep_k = k_;
+    set_plan(1, b);
+    const bool first = cfg_.stage == 0, last = cfg_.stage == cfg_.stages - 1;
+    const int64_t T = static_cast<int64_t>(b) * g.seq;
+    __nv_bfloat16* xin = first ? nullptr : act_recv_;
+    __nv_bfloat16* xout = last ? nullptr : act_send_.at(0);
+    __nv_bfloat16* dy = last ? nullptr : grad_recv_;
+    __nv_bfloat16* dx = first ? nullptr : grad_send_.at(0);
+    if (first || last) {  // deterministic data for the profile runs
+        synth_tokens(0, host_stage_);
+        const int64_t toks = static_cast<int64_t>(cfg_.global_batch) * g.seq;
+        ck(cudaMemcpyAsync(tok_dev_, host_stage_, toks * 4, cudaMemcpyHostToDevice, comp_), "h2d");
+        ck(cudaMemcpyAsync(lab_dev_, host_stage_ + toks, toks * 4, cudaMemcpyHostToDevice, comp_), "h2d");
+    }
+    cudaEvent_t e0, e1, e2;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    ck(cudaEventCreate(&e2), "event");
+    double f = 0, bw = 0;
+    for (int r = 0; r < repeats + 1; ++r) {  // first round is warm-up
+        ck(cudaEventRecord(e0, comp_), "event");
+        stage_->forward(0, tok_dev_, xin, lab_dev_, xout, comp_);
+        ck(cudaEventRecord(e1, comp_), "event");
+        stage_->backward(0, tok_dev_, dy, dx, comp_);
+        ck(cudaEventRecord(e2, comp_), "event");
+        ck(cudaEventSynchronize(e2), "sync");
+        float a = 0, c = 0;
+        ck(cudaEventElapsedTime(&a, e0, e1), "elapsed");
+        ck(cudaEventElapsedTime(&c, e1, e2), "elapsed");
+        if (r > 0) {
+            f += a;
+            bw += c;
+        }
+    }
+    (void)T;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    stage_->zero_grads(comp_);
+    ck(cudaMemsetAsync(stage_->loss_accumulator(), 0, 4, comp_), "memset");
+    ck(cudaStreamSynchronize(comp_), "sync");
+    *fwd_ns = static_cast<int64_t>(f / repeats * 1e6 + 0.5);
+    *bwd_ns = static_cast<int64_t>(bw / repeats * 1e6 + 0.5);
+    set_plan(keep_k, keep_b);
+}
+
+}  // namespace ptk

@@ -64,6 +64,7 @@ class Executor {
 
     void set_trace(int link, const EmuTrace& trace);  // outgoing link pacing
     void set_contender(bool on) { contender_on_ = on; }
+    void set_epoch(int64_t epoch_ns);
 
     // Enqueue one training iteration (non-blocking); host_tokens: pinned or
     // pageable int32 [global_batch][seq+1] (NULL -> built-in synthetic data).
@@ -78,12 +79,12 @@ class Executor {
     // Measured compute durations (ns) of F and B at micro-batch size b.
     void profile_compute(int b, int repeats, int64_t* fwd_ns, int64_t* bwd_ns);
 
-    const std::vector<CompRecord>& comp_records() const { return comp_; }
-    const std::vector<XferRecord>& xfer_records() const { return xfer_; }
+    const std::vector<CompRecord>& comp_records() const { return crec_; }
+    const std::vector<XferRecord>& xfer_records() const { return xrec_; }
     cudaEvent_t iteration_start() const { return it_start_; }
     int64_t h2d_bytes() const { return h2d_bytes_; }
     int64_t d2h_bytes() const { return 4; }
-    int64_t kernel_launches() const { return launches_; }
+    long kernel_launches() const { return stage_->launches() + emu_launches_; }
 
   private:
     void alloc_comm();
@@ -113,14 +114,15 @@ class Executor {
     int32_t *tok_dev_ = nullptr, *lab_dev_ = nullptr;
     int32_t* host_stage_ = nullptr;  // pinned [gb][seq+1]
     int64_t h2d_bytes_ = 0;
-    long launches_ = 0;
+    long emu_launches_ = 0;
+    cudaEvent_t h2d_done_ = nullptr;
 
     // event pools and records
     std::vector<cudaEvent_t> pool_;
     size_t pool_used_ = 0;
     cudaEvent_t it_start_ = nullptr, it_end_ = nullptr;
-    std::vector<CompRecord> comp_;
-    std::vector<XferRecord> xfer_;
+    std::vector<CompRecord> crec_;
+    std::vector<XferRecord> xrec_;
 
     // emulator
     Emulator emu_;

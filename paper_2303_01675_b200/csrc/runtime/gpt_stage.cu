@@ -93,6 +93,7 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
         c.micro_batch_size < 1 || c.micro_batches < 1)
         throw std::invalid_argument("GptStage: bad layer range / slots / batch");
     L_ = c.layer_end - c.layer_begin;
+    b_max_ = c.micro_batch_size;
     const float proj_std = 0.02f / std::sqrt(2.f * c.n_layer);
     const uint64_t base = c.seed * 1000003ull;
 
@@ -143,8 +144,6 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
     const int64_t att = static_cast<int64_t>(c.micro_batch_size) * c.heads * c.seq * c.seq;
     stash_.assign(c.slots, std::vector<LayerStash>(L_));
     head_.resize(c.slots);
-    const size_t before = 0;
-    (void)before;
     for (int sl = 0; sl < c.slots; ++sl) {
         size_t bytes = 0;
         for (int i = 0; i < L_; ++i) {
@@ -209,8 +208,20 @@ GptStage::~GptStage() {
     for (void* p : allocs_) cudaFree(p);
 }
 
+void GptStage::kl(int n, cudaError_t e, const char* what) {
+    ck(e, what);
+    launches_ += n;
+}
+
+void GptStage::set_micro_batch(int b, int micro_batches) {
+    if (b < 1 || b > b_max_) throw std::invalid_argument("set_micro_batch: b exceeds the allocated maximum");
+    cfg_.micro_batch_size = b;
+    cfg_.micro_batches = micro_batches;
+}
+
 void GptStage::gemm(ptk_gemm_desc d, cudaStream_t st) {
     const GemmPlan& p = cache_.get(d);
+    ++launches_;
     if (timing_.enabled) {
         if (timing_.used + 2 > timing_.pool.size()) {
             for (int i = 0; i < 256; ++i) {
@@ -238,7 +249,7 @@ void GptStage::layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, _
     const __nv_bfloat16* W = wbf_;
     const int64_t ss = static_cast<int64_t>(n) * n;
 
-    ck(layernorm_fwd(x_in, W + w.ln1_g, W + w.ln1_b, s.ln1, s.mean1, s.rstd1, T, h, 1e-5f, st), "ln1");
+    kl(1, layernorm_fwd(x_in, W + w.ln1_g, W + w.ln1_b, s.ln1, s.mean1, s.rstd1, T, h, 1e-5f, st), "ln1");
     {
         ptk_gemm_desc g = desc(T, 3 * h, h, mat(s.ln1, h), mat(W + w.w_qkv, h), mat(s.qkv, 3 * h), PTK_EPI_BF16);
         g.bias = W + w.b_qkv;
@@ -253,7 +264,7 @@ void GptStage::layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, _
         g.causal = PTK_CAUSAL_TILES;
         gemm(g, st);
     }
-    ck(softmax_causal_fwd(S_, s.P, b * H * n, n, 1.f / std::sqrt(static_cast<float>(d)), st), "softmax");
+    kl(1, softmax_causal_fwd(S_, s.P, b * H * n, n, 1.f / std::sqrt(static_cast<float>(d)), st), "softmax");
     {  // O = P V
         ptk_gemm_desc g = desc(n, d, n, mat(s.P, n, 0, ss, ss * H),
                                mat(s.qkv + 2 * h, 3 * h, 1, d, static_cast<int64_t>(n) * 3 * h),
@@ -269,7 +280,7 @@ void GptStage::layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, _
         g.aux = mat(x_in, h);
         gemm(g, st);
     }
-    ck(layernorm_fwd(s.x_mid, W + w.ln2_g, W + w.ln2_b, s.ln2, s.mean2, s.rstd2, T, h, 1e-5f, st), "ln2");
+    kl(1, layernorm_fwd(s.x_mid, W + w.ln2_g, W + w.ln2_b, s.ln2, s.mean2, s.rstd2, T, h, 1e-5f, st), "ln2");
     {
         ptk_gemm_desc g = desc(T, f, h, mat(s.ln2, h), mat(W + w.w_fc1, h), mat(s.fc1_act, f), PTK_EPI_BIAS_GELU);
         g.bias = W + w.b_fc1;
@@ -301,19 +312,19 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
         gemm(g, st);
     }
     gemm(desc(h, f, T, mat(dy, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
-    ck(colsum_accumulate(dy, G + w.b_fc2, red_, T, h, st), "db2");
+    kl(2, colsum_accumulate(dy, G + w.b_fc2, red_, T, h, st), "db2");
     // FC1: d_ln2 = d_pre W1; dW1 += d_preᵀ ln2; db1 += Σ d_pre
     gemm(desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
     gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.ln2, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
-    ck(colsum_accumulate(d_pre_, G + w.b_fc1, red_, T, f, st), "db1");
+    kl(2, colsum_accumulate(d_pre_, G + w.b_fc1, red_, T, f, st), "db1");
     // LN2 backward + residual: dx_mid = LN2'(d_ln2) + dy
-    ck(layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, G + w.ln2_g, G + w.ln2_b, red_, T, h,
+    kl(4, layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, G + w.ln2_g, G + w.ln2_b, red_, T, h,
                      st),
        "ln2 bwd");
     // out-proj: d_attn = dx_mid Wo; dWo += dx_midᵀ o; dbo += Σ dx_mid
     gemm(desc(T, h, h, mat(dx_mid_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
     gemm(desc(h, h, T, mat(dx_mid_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
-    ck(colsum_accumulate(dx_mid_, G + w.b_o, red_, T, h, st), "dbo");
+    kl(2, colsum_accumulate(dx_mid_, G + w.b_o, red_, T, h, st), "dbo");
     // attention
     {  // dP = dO Vᵀ
         ptk_gemm_desc g = desc(n, n, d, mat(d_attn_, h, 0, d, o_bs), mat(s.qkv + 2 * h, 3 * h, 0, d, qkv_bs),
@@ -323,7 +334,7 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
         g.causal = PTK_CAUSAL_TILES;
         gemm(g, st);
     }
-    ck(softmax_causal_bwd(s.P, S_, dS_, b * H * n, n, 1.f / std::sqrt(static_cast<float>(d)), st), "softmax bwd");
+    kl(1, softmax_causal_bwd(s.P, S_, dS_, b * H * n, n, 1.f / std::sqrt(static_cast<float>(d)), st), "softmax bwd");
     {  // dQ = dS K
         ptk_gemm_desc g = desc(n, d, n, mat(dS_, n, 0, ss, ss * H), mat(s.qkv + h, 3 * h, 1, d, qkv_bs),
                                mat(dqkv_, 3 * h, 0, d, qkv_bs), PTK_EPI_BF16);
@@ -351,9 +362,9 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
     // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv += Σ dqkv
     gemm(desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
     gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
-    ck(colsum_accumulate(dqkv_, G + w.b_qkv, red_, T, 3 * h, st), "dbqkv");
+    kl(2, colsum_accumulate(dqkv_, G + w.b_qkv, red_, T, 3 * h, st), "dbqkv");
     // LN1 backward + residual: dx = LN1'(d_ln1) + dx_mid
-    ck(layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, dx_mid_, dx, G + w.ln1_g, G + w.ln1_b, red_, T, h,
+    kl(4, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, dx_mid_, dx, G + w.ln1_g, G + w.ln1_b, red_, T, h,
                      st),
        "ln1 bwd");
 }
@@ -366,7 +377,7 @@ void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, 
     const __nv_bfloat16* W = wbf_;
     const __nv_bfloat16* cur = x_in;
     if (c.has_embedding) {
-        ck(embedding_fwd(tok, W + wte_, W + wpe_, S[0].x_in, T, c.seq, h, st), "embedding");
+        kl(1, embedding_fwd(tok, W + wte_, W + wpe_, S[0].x_in, T, c.seq, h, st), "embedding");
         cur = S[0].x_in;
     } else if (L_ > 0) {
         S[0].x_in = const_cast<__nv_bfloat16*>(x_in);  // stage input stays live until this slot's backward
@@ -379,10 +390,10 @@ void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, 
     if (c.has_head) {
         HeadStash& hs = head_[slot];
         if (L_ == 0) ck(cudaMemcpyAsync(hs.x_fin, cur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, st), "copy");
-        ck(layernorm_fwd(hs.x_fin, W + lnf_g_, W + lnf_b_, hs.xf, hs.meanf, hs.rstdf, T, h, 1e-5f, st), "lnf");
+        kl(1, layernorm_fwd(hs.x_fin, W + lnf_g_, W + lnf_b_, hs.xf, hs.meanf, hs.rstdf, T, h, 1e-5f, st), "lnf");
         gemm(desc(T, c.vocab, h, mat(hs.xf, h), mat(W + w_head_, h), mat(hs.dlogits, c.vocab), PTK_EPI_BF16), st);
         const float scale = 1.f / (static_cast<float>(T) * c.micro_batches);
-        ck(cross_entropy(hs.dlogits, labels, loss_rows_, loss_acc_, T, c.vocab, scale, scale, st), "xent");
+        kl(2, cross_entropy(hs.dlogits, labels, loss_rows_, loss_acc_, T, c.vocab, scale, scale, st), "xent");
     } else if (L_ == 0) {
         ck(cudaMemcpyAsync(x_out, cur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, st), "copy");
     }
@@ -401,7 +412,7 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
         gemm(desc(T, h, c.vocab, mat(hs.dlogits, c.vocab), mat(W + w_head_, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
         gemm(desc(c.vocab, h, T, mat(hs.dlogits, c.vocab, 1), mat(hs.xf, h, 1), mat(G + w_head_, h), PTK_EPI_ACC_F32),
              st);
-        ck(layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, G + lnf_g_, G + lnf_b_, red_, T,
+        kl(4, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, G + lnf_g_, G + lnf_b_, red_, T,
                          h, st),
            "lnf bwd");
         g = g_a_;
@@ -412,7 +423,7 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
         g = out;
     }
     if (c.has_embedding) {
-        ck(embedding_bwd(tok, g, G + wte_, G + wpe_, T, c.seq, h, c.vocab, st), "embedding bwd");
+        kl(2, embedding_bwd(tok, g, G + wte_, G + wpe_, T, c.seq, h, c.vocab, st), "embedding bwd");
     } else if (L_ == 0) {
         ck(cudaMemcpyAsync(dx, g, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, st), "copy");
     }
@@ -420,7 +431,7 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
 
 void GptStage::optimizer_step(float lr, float wd, cudaStream_t st) {
     ++step_;
-    ck(adamw_step(master_, grad_, adam_m_, adam_v_, wbf_, total_, lr, 0.9f, 0.95f, 1e-8f, wd, step_, st), "adamw");
+    kl(1, adamw_step(master_, grad_, adam_m_, adam_v_, wbf_, total_, lr, 0.9f, 0.95f, 1e-8f, wd, step_, st), "adamw");
 }
 
 void GptStage::collect_timing() {

@@ -72,6 +72,11 @@ class GptStage {
     int64_t param_count() const { return total_; }
     size_t stash_bytes_per_slot() const { return stash_per_slot_; }
 
+    // Run subsequent micro-batches with b <= the allocated maximum (plan switch).
+    void set_micro_batch(int b, int micro_batches);
+    long launches() const { return launches_; }
+    void reset_launches() { launches_ = 0; }
+
     GemmTiming& gemm_timing() { return timing_; }
     // Synchronises the recorded GEMM event pairs into totals and recycles them.
     void collect_timing();
@@ -101,9 +106,12 @@ class GptStage {
     void layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, __nv_bfloat16* x_out, cudaStream_t st);
     void layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st);
     void* alloc(size_t bytes);
+    void kl(int n, cudaError_t e, const char* what);
 
     ptk_gpt_config cfg_;
     int L_ = 0;  // layers on this stage
+    int b_max_ = 1;
+    long launches_ = 0;
     std::vector<ParamInfo> params_;
     std::vector<LayerW> lw_;
     int64_t wte_ = -1, wpe_ = -1, lnf_g_ = -1, lnf_b_ = -1, w_head_ = -1;

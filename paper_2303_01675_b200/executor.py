@@ -1,0 +1,177 @@
+"""Python handle over the kFkB stage executor (ptk_exec_* in include/ptk.h).
+
+The host loop lives in C++ (executor.cu); this module only wires processes
+together: one process per GPU/stage, IPC handles exchanged over a gloo group
+(torch.distributed is plumbing), and the tuner's measurements gathered so
+every rank feeds the same samples to the C++ decision function.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+
+from . import _lib as L
+from .stage import GptConfig, ModelShape, _declare as _declare_stage
+
+
+class ExecConfig(C.Structure):
+    _fields_ = [("gpt", GptConfig), ("stage", C.c_int), ("stages", C.c_int), ("global_batch", C.c_int),
+                ("lr", C.c_float), ("weight_decay", C.c_float), ("data_seed", C.c_uint64)]
+
+
+def _declare(lib):
+    if getattr(lib, "_exec_declared", False):
+        return
+    _declare_stage(lib)
+    V, I, P = C.c_void_p, C.c_int, C.POINTER
+    lib.ptk_exec_create.argtypes = [P(ExecConfig), P(V)]
+    lib.ptk_exec_destroy.argtypes = [V]
+    lib.ptk_exec_export.argtypes = [V, V, C.c_size_t, P(C.c_size_t)]
+    lib.ptk_exec_import.argtypes = [V, I, V, C.c_size_t]
+    lib.ptk_exec_connect_local.argtypes = [V, I, V]
+    lib.ptk_exec_set_plan.argtypes = [V, I, I]
+    lib.ptk_exec_set_trace.argtypes = [V, I, C.c_double, C.c_int64, I, P(C.c_int64), P(C.c_int64), P(C.c_double)]
+    lib.ptk_exec_set_epoch.argtypes = [V, C.c_int64]
+    lib.ptk_globaltimer.restype = C.c_int64
+    lib.ptk_exec_run_iteration.argtypes = [V, I, V]
+    lib.ptk_exec_finish_iteration.argtypes = [V, P(C.c_double)]
+    lib.ptk_exec_read_loss.argtypes = [V, P(C.c_float)]
+    lib.ptk_exec_timeline_json.argtypes = [V, C.c_char_p, C.c_size_t, P(C.c_size_t)]
+    lib.ptk_exec_probe_link.argtypes = [V, I, C.c_int64, I, P(C.c_int64)]
+    lib.ptk_exec_profile_compute.argtypes = [V, I, I, P(C.c_int64), P(C.c_int64)]
+    lib.ptk_exec_gemm_timing.argtypes = [V, I, P(C.c_double), P(C.c_double), P(C.c_long)]
+    lib._exec_declared = True
+
+
+def partition_layers(n_layer: int, stages: int, head_weight: float = 2.0) -> list[tuple[int, int]]:
+    """Contiguous layer ranges minimising the bottleneck stage, counting the LM
+    head (on the last stage) as `head_weight` layer-equivalents."""
+    if stages == 1:
+        return [(0, n_layer)]
+    best = None
+    # binary-search-free exhaustive DP over cut points (n_layer <= 64)
+    from functools import lru_cache
+
+    @lru_cache(None)
+    def solve(start: int, k: int):
+        if k == 1:
+            cost = (n_layer - start) + head_weight
+            return (cost, ((start, n_layer),))
+        out = None
+        for end in range(start + 1, n_layer - k + 2):
+            rest = solve(end, k - 1)
+            cost = max(end - start, rest[0])
+            if out is None or cost < out[0] or (cost == out[0] and end - start > out[1][0][1] - out[1][0][0]):
+                out = (cost, ((start, end),) + rest[1])
+        return out
+
+    best = solve(0, stages)
+    return list(best[1])
+
+
+def max_inflight(stage: int, stages: int, micro_batches: int, k: int) -> int:
+    """Peak in-flight forwards of kFkB at a stage: min(M, min(S-s, ceil(M/k))*k)."""
+    return min(micro_batches, min(stages - stage, math.ceil(micro_batches / k)) * k)
+
+
+class StageExecutor:
+    def __init__(self, shape: ModelShape, stage: int, stages: int, global_batch: int, b_max: int, slots: int,
+                 layers: tuple[int, int] | None = None, seed: int = 42, data_seed: int = 1234, lr: float = 1e-4,
+                 weight_decay: float = 0.0):
+        self.lib = L.lib()
+        _declare(self.lib)
+        lb, le = layers if layers is not None else partition_layers(shape.n_layer, stages)[stage]
+        gpt = GptConfig(shape.n_layer, shape.hidden, shape.heads, shape.ffn, shape.seq, shape.vocab, lb, le,
+                        int(stage == 0), int(stage == stages - 1), b_max, slots, global_batch // b_max, seed)
+        self.cfg = ExecConfig(gpt, stage, stages, global_batch, lr, weight_decay, data_seed)
+        self.shape, self.stage, self.stages, self.global_batch = shape, stage, stages, global_batch
+        h = C.c_void_p()
+        L.check(self.lib.ptk_exec_create(C.byref(self.cfg), C.byref(h)))
+        self.h = h
+
+    # ---- wiring
+    def export_handles(self) -> bytes:
+        buf = C.create_string_buffer(4096)
+        n = C.c_size_t()
+        L.check(self.lib.ptk_exec_export(self.h, buf, len(buf), C.byref(n)))
+        return buf.raw[:n.value]
+
+    def import_peer(self, peer_stage: int, blob: bytes):
+        L.check(self.lib.ptk_exec_import(self.h, peer_stage, blob, len(blob)))
+
+    def connect_local(self, peer_stage: int, peer: "StageExecutor"):
+        L.check(self.lib.ptk_exec_connect_local(self.h, peer_stage, peer.h))
+
+    def connect_dist(self, group=None):
+        """Exchange IPC handles with the neighbouring ranks (rank == stage)."""
+        import torch.distributed as dist
+        blobs = [None] * dist.get_world_size()
+        dist.all_gather_object(blobs, self.export_handles(), group=group)
+        if self.stage + 1 < self.stages:
+            self.import_peer(self.stage + 1, blobs[self.stage + 1])
+        if self.stage > 0:
+            self.import_peer(self.stage - 1, blobs[self.stage - 1])
+
+    # ---- schedule / emulator
+    def set_plan(self, k: int, b: int):
+        L.check(self.lib.ptk_exec_set_plan(self.h, k, b))
+
+    def set_trace(self, link: int, base_bytes_per_ns: float, latency_ns: int, segments):
+        n = len(segments)
+        s = (C.c_int64 * max(n, 1))(*[int(x[0]) for x in segments])
+        e = (C.c_int64 * max(n, 1))(*[int(x[1]) for x in segments])
+        a = (C.c_double * max(n, 1))(*[float(x[2]) for x in segments])
+        L.check(self.lib.ptk_exec_set_trace(self.h, link, base_bytes_per_ns, latency_ns, n, s, e, a))
+
+    def set_epoch(self, epoch_ns: int):
+        L.check(self.lib.ptk_exec_set_epoch(self.h, epoch_ns))
+
+    def globaltimer(self) -> int:
+        return self.lib.ptk_globaltimer()
+
+    # ---- iterations
+    def run_iteration(self, it: int, host_tokens=None):
+        L.check(self.lib.ptk_exec_run_iteration(self.h, it, host_tokens if host_tokens is not None else None))
+
+    def finish_iteration(self) -> float:
+        ms = C.c_double()
+        L.check(self.lib.ptk_exec_finish_iteration(self.h, C.byref(ms)))
+        return ms.value
+
+    def read_loss(self) -> float:
+        v = C.c_float()
+        L.check(self.lib.ptk_exec_read_loss(self.h, C.byref(v)))
+        return v.value
+
+    def timeline(self) -> dict:
+        n = C.c_size_t()
+        buf = C.create_string_buffer(1 << 22)
+        L.check(self.lib.ptk_exec_timeline_json(self.h, buf, len(buf), C.byref(n)))
+        return json.loads(buf.value.decode())
+
+    def probe_link(self, link: int, nbytes: int, repeats: int) -> list[int]:
+        out = (C.c_int64 * repeats)()
+        L.check(self.lib.ptk_exec_probe_link(self.h, link, nbytes, repeats, out))
+        return list(out)
+
+    def profile_compute(self, b: int, repeats: int = 3) -> tuple[int, int]:
+        f, bw = C.c_int64(), C.c_int64()
+        L.check(self.lib.ptk_exec_profile_compute(self.h, b, repeats, C.byref(f), C.byref(bw)))
+        return f.value, bw.value
+
+    def gemm_timing(self, enable: int = -1):
+        fl, ms, n = C.c_double(), C.c_double(), C.c_long()
+        L.check(self.lib.ptk_exec_gemm_timing(self.h, enable, C.byref(fl), C.byref(ms), C.byref(n)))
+        return fl.value, ms.value, n.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ptk_exec_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

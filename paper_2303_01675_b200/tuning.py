@@ -1,0 +1,91 @@
+"""Ada-Grouper online tuning across pipeline ranks (SPEC.md:453-467 on hardware).
+
+A tuning round runs with the pipeline suspended at an iteration boundary:
+  1. compute profiles — measured once per candidate micro-batch size at
+     startup with CUDA events on each rank's own stage;
+  2. link profiles — every rank probes its outgoing links `repeats` times per
+     candidate payload through the (emulated) link, int64 ns samples;
+  3. everything is all-gathered, so every rank holds the same inputs, and each
+     rank calls the C++ decision function (pipetune::tuning_round via
+     ptk_scenario_json op "decide"); the decision is deterministic, so all
+     ranks switch to the same plan at the same boundary.
+The recorded inputs form a replay log: the CPU oracle fed the same samples
+must reproduce the decision bit for bit (tests/test_tuning_replay.py).
+"""
+from __future__ import annotations
+
+from . import pipetune as pt
+
+
+def outgoing_links(stage: int, stages: int) -> list[int]:
+    """2s carries activations s -> s+1, 2s-1 carries grads s -> s-1 (model.hpp:15-24)."""
+    out = []
+    if stage + 1 < stages:
+        out.append(2 * stage)
+    if stage > 0:
+        out.append(2 * stage - 1)
+    return out
+
+
+def pipeline_model(stages: int, global_batch: int, act_bytes_per_sample: int) -> dict:
+    """The pipetune ModelSpec the decision runs on: real per-sample transfer bytes."""
+    return pt.model_dict(pt.ModelSpec([pt.StageProfile(stage_id=s, output_bytes_per_sample_fwd=act_bytes_per_sample,
+                                                       output_bytes_per_sample_bwd=act_bytes_per_sample)
+                                       for s in range(stages)], global_batch))
+
+
+def all_gather(obj, group=None, world: int = 1):
+    if world == 1:
+        return [obj]
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+class OnlineTuner:
+    def __init__(self, ex, rank: int, stages: int, global_batch: int, candidates: list[tuple[int, int]],
+                 act_bytes_per_sample: int, hysteresis: float = 0.02, repeats: int = 3, window: int = 8,
+                 group=None):
+        self.ex, self.rank, self.S = ex, rank, stages
+        self.gb = global_batch
+        self.cands = [[k, b, global_batch // b] for k, b in candidates]
+        self.act = act_bytes_per_sample
+        self.h, self.repeats, self.window, self.group = hysteresis, repeats, window, group
+        self.compute = None
+        self.samples: list[list[int]] = []
+        self.log: list[dict] = []
+        self.model = pipeline_model(stages, global_batch, act_bytes_per_sample)
+
+    def profile_compute(self):
+        """Once, at startup: F/B durations per candidate b on this rank, gathered."""
+        mine = []
+        for b in sorted({c[1] for c in self.cands}):
+            f, bw = self.ex.profile_compute(b, 3)
+            mine += [[self.rank, b, 0, f], [self.rank, b, 1, bw]]
+        self.compute = sorted(x for r in all_gather(mine, self.group, self.S) for x in r)
+
+    def profile_links(self, clock: int = 0):
+        mine = []
+        for b in sorted({c[1] for c in self.cands}):
+            nbytes = b * self.act
+            for link in outgoing_links(self.rank, self.S):
+                for d in self.ex.probe_link(link, nbytes, self.repeats):
+                    mine.append([link, nbytes, clock, d])
+        gathered = sorted(x for r in all_gather(mine, self.group, self.S) for x in r)
+        self.samples += gathered  # ProfileStore keeps the last `window` per bucket
+
+    def decide(self, current, clock: int = 0) -> dict:
+        req = {"op": "decide", "model": self.model, "candidates": self.cands, "compute_profile": self.compute,
+               "samples": self.samples, "hysteresis": self.h, "window": self.window, "clock": clock}
+        if current is not None:
+            req["current"] = list(current)
+        d = pt.scenario(req)["decision"]
+        self.log.append({"request": req, "decision": d})
+        return d
+
+    def round(self, current, clock: int = 0) -> dict:
+        if self.compute is None:
+            self.profile_compute()
+        self.profile_links(clock)
+        return self.decide(current, clock)
