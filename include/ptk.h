@@ -196,6 +196,8 @@ int ptk_exec_timeline_json(ptk_exec* ex, char* buf, size_t cap, size_t* written)
 int ptk_exec_probe_link(ptk_exec* ex, int link, int64_t bytes, int repeats, int64_t* out_ns);
 int ptk_exec_profile_compute(ptk_exec* ex, int micro_batch_size, int repeats, int64_t* fwd_ns, int64_t* bwd_ns);
 int ptk_exec_gemm_timing(ptk_exec* ex, int enable, double* total_flops, double* total_ms, long* launches);
+/* Non-owning view of the executor's stage (weights, grads, parameter table). */
+ptk_stage* ptk_exec_stage(ptk_exec* ex);
 
 #ifdef __cplusplus
 }

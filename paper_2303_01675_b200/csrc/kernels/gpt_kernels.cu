@@ -138,54 +138,69 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(const __nv_bfloat16* __rest
     }
 }
 
-// Per-chunk column partials of dgamma = sum dy*xhat and dbeta = sum dy.
-constexpr int kColRows = 64;
-__global__ void ln_affine_partial_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-                                         const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
-                                         float* __restrict__ part_g, float* __restrict__ part_b, int rows, int cols) {
-    const int c2 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
-    if (c2 >= cols) return;
-    const int r0 = blockIdx.y * kColRows;
-    float g0 = 0.f, g1 = 0.f, b0 = 0.f, b1 = 0.f;
-    for (int r = r0; r < min(rows, r0 + kColRows); ++r) {
-        const int64_t o = static_cast<int64_t>(r) * cols + c2;
-        const float2 d = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy + o));
-        const float2 xv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + o));
-        const float mean = mean_in[r], rstd = rstd_in[r];
-        g0 += d.x * ((xv.x - mean) * rstd);
-        g1 += d.y * ((xv.y - mean) * rstd);
-        b0 += d.x;
-        b1 += d.y;
+// Column partial sums over 32-row chunks, 256 columns per block: thread
+// (rg, cg) accumulates 4 rows x 8 columns with 16-byte loads, then the 8 row
+// groups are combined in smem in a fixed order -> part[chunk][col].
+// AFFINE: part_g += dy * (x - mean) * rstd and part_b += dy (LayerNorm affine
+// grads); otherwise part_b += m (bias grads).
+constexpr int kColRows = 32;
+template <bool AFFINE>
+__global__ void __launch_bounds__(256) colpart_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                      const __nv_bfloat16* __restrict__ x,
+                                                      const float* __restrict__ mean_in,
+                                                      const float* __restrict__ rstd_in, float* __restrict__ part_g,
+                                                      float* __restrict__ part_b, int rows, int cols) {
+    __shared__ float sg[8][257];
+    __shared__ float sb[8][257];
+    const int cg = threadIdx.x & 31, rg = threadIdx.x >> 5;
+    const int c0 = blockIdx.x * 256 + cg * 8;
+    const int r0 = blockIdx.y * kColRows + rg * 4;
+    float ag[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, ab[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int row = r0 + r;
+        if (row >= rows) break;
+        float d[8];
+        load8(dy + static_cast<int64_t>(row) * cols + c0, d);
+        if (AFFINE) {
+            float xv[8];
+            load8(x + static_cast<int64_t>(row) * cols + c0, xv);
+            const float mean = mean_in[row], rstd = rstd_in[row];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) ag[i] += d[i] * ((xv[i] - mean) * rstd);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ab[i] += d[i];
     }
-    part_g[static_cast<int64_t>(blockIdx.y) * cols + c2] = g0;
-    part_g[static_cast<int64_t>(blockIdx.y) * cols + c2 + 1] = g1;
-    part_b[static_cast<int64_t>(blockIdx.y) * cols + c2] = b0;
-    part_b[static_cast<int64_t>(blockIdx.y) * cols + c2 + 1] = b1;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        sb[rg][cg * 8 + i] = ab[i];
+        if (AFFINE) sg[rg][cg * 8 + i] = ag[i];
+    }
+    __syncthreads();
+    const int c = threadIdx.x;
+    float tb = 0.f, tg = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        tb += sb[k][c];
+        if (AFFINE) tg += sg[k][c];
+    }
+    const int64_t o = static_cast<int64_t>(blockIdx.y) * cols + blockIdx.x * 256 + c;
+    part_b[o] = tb;
+    if (AFFINE) part_g[o] = tg;
 }
 
-// out[c] += sum_{p < nparts} part[p][c]   (ascending p)
-__global__ void reduce_partials_kernel(const float* __restrict__ part, float* __restrict__ out, int nparts, int cols) {
+// out[y][c] += sum_{p < nparts} part[y][p][c]   (ascending p; y selects one of two vectors)
+__global__ void reduce_partials_kernel(const float* __restrict__ part0, float* __restrict__ out0,
+                                       const float* __restrict__ part1, float* __restrict__ out1, int nparts,
+                                       int cols) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cols) return;
+    const float* part = blockIdx.y == 0 ? part0 : part1;
+    float* out = blockIdx.y == 0 ? out0 : out1;
     float s = 0.f;
     for (int p = 0; p < nparts; ++p) s += part[static_cast<int64_t>(p) * cols + c];
     out[c] += s;
-}
-
-// Column sums of a bf16 [rows][cols] matrix into per-chunk partials.
-__global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ m, float* __restrict__ part, int rows,
-                                      int cols) {
-    const int c2 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
-    if (c2 >= cols) return;
-    const int r0 = blockIdx.y * kColRows;
-    float s0 = 0.f, s1 = 0.f;
-    for (int r = r0; r < min(rows, r0 + kColRows); ++r) {
-        const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(m + static_cast<int64_t>(r) * cols + c2));
-        s0 += v.x;
-        s1 += v.y;
-    }
-    part[static_cast<int64_t>(blockIdx.y) * cols + c2] = s0;
-    part[static_cast<int64_t>(blockIdx.y) * cols + c2 + 1] = s1;
 }
 
 // --------------------------------------------------------------- softmax (causal)
@@ -528,21 +543,19 @@ cudaError_t layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const
     const int parts = layernorm_bwd_parts(rows);
     float* pg = scratch;
     float* pb = scratch + static_cast<int64_t>(parts) * h;
-    dim3 grid((h / 2 + 127) / 128, parts);
-    ln_affine_partial_kernel<<<grid, 128, 0, st>>>(dy, x, mean, rstd, pg, pb, rows, h);
-    reduce_partials_kernel<<<(h + 255) / 256, 256, 0, st>>>(pg, dgamma, parts, h);
-    reduce_partials_kernel<<<(h + 255) / 256, 256, 0, st>>>(pb, dbeta, parts, h);
+    colpart_kernel<true><<<dim3(h / 256, parts), 256, 0, st>>>(dy, x, mean, rstd, pg, pb, rows, h);
+    reduce_partials_kernel<<<dim3((h + 255) / 256, 2), 256, 0, st>>>(pg, dgamma, pb, dbeta, parts, h);
     return cudaPeekAtLastError();
 }
 
 int colsum_parts(int rows) { return (rows + kColRows - 1) / kColRows; }
 
 cudaError_t colsum_accumulate(const __nv_bfloat16* m, float* out, float* scratch, int rows, int cols, cudaStream_t st) {
-    if (cols % 2) return cudaErrorInvalidValue;
+    if (cols % 256) return cudaErrorInvalidValue;
     const int parts = colsum_parts(rows);
-    dim3 grid((cols / 2 + 127) / 128, parts);
-    colsum_partial_kernel<<<grid, 128, 0, st>>>(m, scratch, rows, cols);
-    reduce_partials_kernel<<<(cols + 255) / 256, 256, 0, st>>>(scratch, out, parts, cols);
+    colpart_kernel<false><<<dim3(cols / 256, parts), 256, 0, st>>>(m, nullptr, nullptr, nullptr, nullptr, scratch,
+                                                                  rows, cols);
+    reduce_partials_kernel<<<dim3((cols + 255) / 256, 1), 256, 0, st>>>(scratch, out, scratch, out, parts, cols);
     return cudaPeekAtLastError();
 }
 

@@ -9,9 +9,12 @@
 #include "executor.h"
 #include "pipetune/errors.hpp"
 
+#include "capi_handles.h"
+
 struct ptk_exec {
     ptk::Executor impl;
-    explicit ptk_exec(const ptk_exec_config& c) : impl(c) {}
+    ptk_stage stage_view;
+    explicit ptk_exec(const ptk_exec_config& c) : impl(c), stage_view(&impl.stage(), false) {}
 };
 
 namespace {
@@ -173,9 +176,12 @@ extern "C" int ptk_exec_gemm_timing(ptk_exec* ex, int enable, double* total_flop
         if (total_ms) *total_ms = t.total_ms;
         if (launches) *launches = t.launches;
         if (enable >= 0) {
-            t.enabled = enable != 0;
+            t.armed = enable != 0;
+            t.enabled = t.armed;
             t.total_flops = t.total_ms = 0.0;
             t.launches = 0;
         }
     });
 }
+
+extern "C" ptk_stage* ptk_exec_stage(ptk_exec* ex) { return ex ? &ex->stage_view : nullptr; }

@@ -309,6 +309,8 @@ void Executor::run_iteration(int iter, const int32_t* host_tokens) {
         const pipetune::TaskNode& n = graph_->node(id);
         const int m = n.micro_batch;
         const int slot = m >= 0 ? m % g.slots : 0;
+        GemmTiming& tm = stage_->gemm_timing();
+        tm.enabled = tm.armed && m >= 0 && m % tm.stride == 0;
         if (n.kind == pipetune::TaskKind::ForwardCompute) {
             if (!first) wait_flag(comp_, act_flag_ + m, static_cast<uint32_t>(iter + 1));
             __nv_bfloat16* out = last ? nullptr : act_send_[static_cast<size_t>(slot)];

@@ -318,7 +318,7 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
     gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.ln2, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
     kl(2, colsum_accumulate(d_pre_, G + w.b_fc1, red_, T, f, st), "db1");
     // LN2 backward + residual: dx_mid = LN2'(d_ln2) + dy
-    kl(4, layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, G + w.ln2_g, G + w.ln2_b, red_, T, h,
+    kl(3, layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, G + w.ln2_g, G + w.ln2_b, red_, T, h,
                      st),
        "ln2 bwd");
     // out-proj: d_attn = dx_mid Wo; dWo += dx_midᵀ o; dbo += Σ dx_mid
@@ -364,7 +364,7 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
     gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
     kl(2, colsum_accumulate(dqkv_, G + w.b_qkv, red_, T, 3 * h, st), "dbqkv");
     // LN1 backward + residual: dx = LN1'(d_ln1) + dx_mid
-    kl(4, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, dx_mid_, dx, G + w.ln1_g, G + w.ln1_b, red_, T, h,
+    kl(3, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, dx_mid_, dx, G + w.ln1_g, G + w.ln1_b, red_, T, h,
                      st),
        "ln1 bwd");
 }
@@ -412,7 +412,7 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
         gemm(desc(T, h, c.vocab, mat(hs.dlogits, c.vocab), mat(W + w_head_, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
         gemm(desc(c.vocab, h, T, mat(hs.dlogits, c.vocab, 1), mat(hs.xf, h, 1), mat(G + w_head_, h), PTK_EPI_ACC_F32),
              st);
-        kl(4, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, G + lnf_g_, G + lnf_b_, red_, T,
+        kl(3, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, G + lnf_g_, G + lnf_b_, red_, T,
                          h, st),
            "lnf bwd");
         g = g_a_;

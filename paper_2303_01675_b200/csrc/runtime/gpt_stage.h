@@ -36,7 +36,9 @@ class GemmCache {
 };
 
 struct GemmTiming {
-    bool enabled = false;
+    bool armed = false;    // user switch
+    bool enabled = false;  // active for the current micro-batch (sampled)
+    int stride = 8;        // time the GEMMs of one micro-batch in `stride`
     std::vector<cudaEvent_t> pool;
     size_t used = 0;
     std::vector<double> flops;  // per recorded launch pair

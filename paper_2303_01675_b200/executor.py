@@ -41,6 +41,8 @@ def _declare(lib):
     lib.ptk_exec_probe_link.argtypes = [V, I, C.c_int64, I, P(C.c_int64)]
     lib.ptk_exec_profile_compute.argtypes = [V, I, I, P(C.c_int64), P(C.c_int64)]
     lib.ptk_exec_gemm_timing.argtypes = [V, I, P(C.c_double), P(C.c_double), P(C.c_long)]
+    lib.ptk_exec_stage.argtypes = [V]
+    lib.ptk_exec_stage.restype = C.c_void_p
     lib._exec_declared = True
 
 
@@ -164,6 +166,10 @@ class StageExecutor:
         fl, ms, n = C.c_double(), C.c_double(), C.c_long()
         L.check(self.lib.ptk_exec_gemm_timing(self.h, enable, C.byref(fl), C.byref(ms), C.byref(n)))
         return fl.value, ms.value, n.value
+
+    def stage_view(self):
+        from .stage import GptStage
+        return GptStage.view(self.lib, self.lib.ptk_exec_stage(self.h), self.shape, self.cfg.gpt.micro_batch_size)
 
     def close(self):
         if getattr(self, "h", None):

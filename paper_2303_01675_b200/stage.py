@@ -98,6 +98,22 @@ class GptStage:
         h = C.c_void_p()
         L.check(self.lib.ptk_stage_create(C.byref(self.cfg), C.byref(h)))
         self.h = h
+        self.owned = True
+        self._attach()
+
+    @classmethod
+    def view(cls, lib, handle: int, shape: ModelShape, micro_batch_size: int) -> "GptStage":
+        """Non-owning wrapper of a stage that lives inside an executor."""
+        self = cls.__new__(cls)
+        self.lib, self.shape, self.owned = lib, shape, False
+        _declare(lib)
+        self.h = C.c_void_p(handle)
+        self.cfg = GptConfig()
+        self.cfg.micro_batch_size = micro_batch_size
+        self._attach()
+        return self
+
+    def _attach(self):
         m, w, g, loss = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         n = C.c_int64()
         L.check(self.lib.ptk_stage_buffers(self.h, C.byref(m), C.byref(w), C.byref(g), C.byref(loss), C.byref(n)))
@@ -151,9 +167,9 @@ class GptStage:
         return self.lib.ptk_stage_stash_bytes(self.h)
 
     def close(self):
-        if self.h:
+        if self.h and self.owned:
             self.lib.ptk_stage_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:
