@@ -37,7 +37,14 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--link-gbps", type=float, default=100.0, help="emulated link bandwidth (Gb/s)")
-    p.add_argument("--availability", type=float, default=0.5, help="constant preempted availability")
+    p.add_argument("--availability", type=float, default=0.5, help="availability while preempted")
+    p.add_argument("--trace", choices=["constant", "two-regime", "bursty", "none"], default="constant")
+    p.add_argument("--regime-ms", type=float, default=2000.0, help="two-regime: preempted for the first X ms")
+    p.add_argument("--on-ms", type=float, default=200.0, help="bursty: mean preempted (ON) burst")
+    p.add_argument("--off-ms", type=float, default=300.0, help="bursty: mean idle (OFF) gap")
+    p.add_argument("--trace-seed", type=int, default=1)
+    p.add_argument("--retune", type=int, default=0, help="re-tune every N steps (0: once at start)")
+    p.add_argument("--tuner-log", type=str, default="")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--timeline", type=str, default="")
     return p.parse_args()
@@ -89,6 +96,27 @@ class ClockSampler:
         reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.strip().lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+def trace_segments(args, link: int):
+    """LinkTrace availability segments (ns from the arm's epoch)."""
+    H = 10**13
+    a = args.availability
+    if args.trace == "none" or a >= 1.0:
+        return []
+    if args.trace == "constant":
+        return [(0, H, a)]
+    if args.trace == "two-regime":
+        return [(0, int(args.regime_ms * 1e6), a)]
+    import random
+    rng = random.Random(args.trace_seed * 1000 + link)  # seeded two-state Markov ON/OFF
+    segs, t = [], 0.0
+    while t < 120e9:
+        t += rng.expovariate(1.0 / (args.off_ms * 1e6))
+        on = rng.expovariate(1.0 / (args.on_ms * 1e6))
+        segs.append((int(t), int(t + on), a))
+        t += on
+    return segs
 
 
 def reference_arm(args):
@@ -154,14 +182,18 @@ def main():
     if S > 1:
         ex.connect_dist(group)
         base = args.link_gbps * 1e9 / 8 / 1e9  # bytes per ns
-        horizon = 10**15
-        seg = [(0, horizon, args.availability)] if args.availability < 1.0 else []
         for link in outgoing_links(rank, S):
-            ex.set_trace(link, base, 0, seg)
+            ex.set_trace(link, base, 0, trace_segments(args, link))
+        trace_desc = {"emulated_link_gbps": args.link_gbps, "trace": args.trace, "availability": args.availability,
+                      "regime_ms": args.regime_ms if args.trace == "two-regime" else None,
+                      "bursty_mean_on_off_ms": [args.on_ms, args.off_ms] if args.trace == "bursty" else None,
+                      "seed": args.trace_seed, "retune_every": args.retune}
+
+    def arm_reset():
+        """Every arm replays the trace from t=0 (per-rank globaltimer epoch after a barrier)."""
         barrier()
-        ex.set_epoch(ex.globaltimer())
-        trace_desc = {"emulated_link_gbps": args.link_gbps, "availability": args.availability,
-                      "kind": "constant duty cycle" if args.availability < 1 else "no contention"}
+        if S > 1:
+            ex.set_epoch(ex.globaltimer())
 
     it = 0
 
@@ -175,32 +207,48 @@ def main():
             it += 1
         return ms
 
+    arm_reset()
     run(args.warmup, 1)
-
-    # ---- Ada-Grouper tuning round (pipeline suspended): live profiles -> C++ decision
-    chosen_k, decision = 1, None
     if S > 1:
-        tuner = OnlineTuner(ex, rank, S, GLOBAL_BATCH, [(k, b) for k in ks], act_bytes // b, group=group)
-        decision = tuner.round([1, b, M])
-        chosen_k = decision["chosen"][0]
-        barrier()
-        run(1, chosen_k)  # warm the chosen plan
+        for k in ks[1:]:
+            run(1, k)  # every candidate plan warmed (GEMM plans cached)
 
-    # ---- timed region: K steps of the chosen plan
-    barrier()
+    # ---- fixed-plan arms (same kernels, same trace from t=0)
+    fixed = {}
+    if S > 1:
+        for k in (1, 2):
+            arm_reset()
+            fixed[k] = run(args.steps, k)
+
+    # ---- timed region: Ada-Grouper (tuning round at start, re-tune every `retune` steps)
+    tuner = OnlineTuner(ex, rank, S, GLOBAL_BATCH, [(k, b) for k in ks], act_bytes // b, group=group) \
+        if S > 1 else None
+    if tuner is not None:
+        tuner.profile_compute()  # once, before the timed region
+    chosen_k, decisions, tune_s = 1, [], 0.0
+    arm_reset()
     with ClockSampler(local) as clk:
         ex.gemm_timing(1)
         t0 = time.perf_counter()
-        ms = run(args.steps, chosen_k)
+        ms, ks_run = [], []
+        for step in range(args.steps):
+            if tuner is not None and (step == 0 or (args.retune > 0 and step % args.retune == 0)):
+                tr0 = time.perf_counter()
+                d = tuner.round(None if step == 0 else [chosen_k, b, M], clock=step)
+                decisions.append(d)
+                chosen_k = d["chosen"][0]
+                barrier()
+                tune_s += time.perf_counter() - tr0
+            ms += run(1, chosen_k)
+            ks_run.append(chosen_k)
         barrier()
         wall = time.perf_counter() - t0
         gemm_flops, gemm_ms, gemm_n = ex.gemm_timing(0)
     tl = ex.timeline()
     loss = ex.read_loss() if rank == S - 1 else None
-    step_ms = sum(ms) / len(ms)
-
-    # ---- 1F1B on the same kernels (reported beside the adaptive plan)
-    ms_1f1b = run(args.steps, 1) if S > 1 else ms
+    if tuner is not None and rank == 0 and args.tuner_log:
+        Path(args.tuner_log).write_text(json.dumps({"trace": trace_desc, "rounds": tuner.log}))
+    ms_1f1b = fixed.get(1, ms)
 
     # ---- e2e: host token buffers through the C ABI, H2D + loss D2H inside the timed steps
     import numpy as np
@@ -225,8 +273,10 @@ def main():
         dist.all_gather_object(out, x, group=group)
         return out
 
-    all_ms = gather(sum(ms))
+    all_ms = gather(sum(ms) + tune_s * 1e3)
     all_1f1b = gather(sum(ms_1f1b))
+    all_k2 = gather(sum(fixed.get(2, ms)))
+    all_loss = gather(loss)
     all_e2e = gather(e2e_s)
     all_launch = gather(tl["launches"] * args.steps)
     all_h2d = gather(tl["h2d_bytes"])
@@ -240,6 +290,8 @@ def main():
     T = max(all_ms) / 1e3
     value = GLOBAL_BATCH * args.steps / T
     v1f1b = GLOBAL_BATCH * args.steps / (max(all_1f1b) / 1e3)
+    vk2 = GLOBAL_BATCH * args.steps / (max(all_k2) / 1e3)
+    loss = all_loss[-1]
     pk, pk_kind = peaks()
     peak_sus = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     gf = sum(g[0] for g in all_gemm)
@@ -260,12 +312,15 @@ def main():
                    "global_batch": GLOBAL_BATCH, "micro_batch": b, "micro_batches": M, "seq_len": 1024,
                    "stages": S, "layers_per_stage": [e - s_ for s_, e in layers],
                    "parallelism": f"pp{S}" if S > 1 else "single stage (no pipeline)",
-                   "schedule": f"Ada-Grouper kFkB (chosen k={chosen_k})" if S > 1 else "1F1B (S=1)",
+                   "schedule": (f"Ada-Grouper adaptive kFkB (k per step {ks_run})" if S > 1 else "1F1B (S=1)"),
                    "emulated_preemption": trace_desc, "l2": "working set (weights + activations) >> 126 MB L2"},
-        "schedules": {"ada_grouper": {"k": chosen_k, "samples_per_s": round(value, 3)},
+        "schedules": {"ada_grouper": {"k_per_step": ks_run, "samples_per_s": round(value, 3),
+                                      "tuning_overhead_s": round(tune_s, 4)},
                       "1f1b": {"k": 1, "samples_per_s": round(v1f1b, 3)},
+                      "kfkb_k2": {"k": 2, "samples_per_s": round(vk2, 3)},
                       "speedup_vs_1f1b": round(value / v1f1b, 4)},
-        "tuner_decision": decision,
+        "tuner_decisions": [{"chosen": d["chosen"], "switched": d["switched"],
+                             "estimates_ns": [e[3] for e in d["estimates"]]} for d in decisions],
         "pipeline_roofline": {"ideal_samples_per_s": round(ideal, 2), "frac": round(value / ideal, 4),
                               "peak_tflops": peak_sus, "peak_kind": f"sustained bf16, {pk_kind}"},
         "roofline": {"bound": "tensor", "kernel": "gemm_bf16_kernel (tcgen05 + TMA, all stage GEMMs)",

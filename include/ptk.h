@@ -182,6 +182,9 @@ int ptk_exec_set_plan(ptk_exec* ex, int k, int micro_batch_size);
 int ptk_exec_set_trace(ptk_exec* ex, int link, double base_bytes_per_ns, int64_t latency_ns, int nseg,
                        const int64_t* start_ns, const int64_t* end_ns, const double* availability);
 int ptk_exec_set_epoch(ptk_exec* ex, int64_t epoch_ns);
+/* Contender kernels: real competing NVLink stores into the peer's scratch block
+ * with duty cycle (1 - availability) while a link trace is preempted. */
+int ptk_exec_set_contender(ptk_exec* ex, int on);
 int64_t ptk_globaltimer(void);
 /* Enqueue iteration `iter` (host_tokens: int32 [2][global_batch*seq] tokens then
  * labels, or NULL for the built-in synthetic corpus); finish blocks and

@@ -103,6 +103,11 @@ extern "C" int ptk_exec_set_epoch(ptk_exec* ex, int64_t epoch) {
     return guarded("ptk_exec_set_epoch", [&] { ex->impl.set_epoch(epoch); });
 }
 
+extern "C" int ptk_exec_set_contender(ptk_exec* ex, int on) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_set_contender", [&] { ex->impl.set_contender(on != 0); });
+}
+
 extern "C" int64_t ptk_globaltimer(void) {
     try {
         return ptk::device_globaltimer(0);

@@ -2,6 +2,7 @@
 #include "emulator.h"
 
 #include <algorithm>
+#include <atomic>
 #include <stdexcept>
 
 namespace ptk {
@@ -185,6 +186,7 @@ cudaError_t Emulator::start_contender(int slot, void* peer_scratch, size_t bytes
         ck(cudaHostGetDevicePointer(&stop_dev_, p, 0), "mapped");
     }
     *stop_host_ = 0;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
     contender_kernel<<<8, 256, 0, st>>>(dev_[slot], static_cast<uint4*>(peer_scratch), bytes / 16, stop_dev_);
     return cudaPeekAtLastError();
 }

@@ -73,7 +73,8 @@ Executor::Executor(const ptk_exec_config& c) : cfg_(c) {
     ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priorities");
     ck(cudaStreamCreateWithPriority(&comp_, cudaStreamNonBlocking, hi), "stream");
     ck(cudaStreamCreateWithPriority(&sendst_, cudaStreamNonBlocking, lo), "stream");
-    ck(cudaStreamCreateWithPriority(&contend_, cudaStreamNonBlocking, lo), "stream");
+    ck(cudaStreamCreateWithPriority(&contend_[0], cudaStreamNonBlocking, lo), "stream");
+    ck(cudaStreamCreateWithPriority(&contend_[1], cudaStreamNonBlocking, lo), "stream");
     stage_ = std::make_unique<GptStage>(c.gpt);
     ck(cudaEventCreate(&it_start_), "event");
     ck(cudaEventCreate(&it_end_), "event");
@@ -97,7 +98,8 @@ Executor::~Executor() {
     if (host_stage_) cudaFreeHost(host_stage_);
     cudaStreamDestroy(comp_);
     cudaStreamDestroy(sendst_);
-    cudaStreamDestroy(contend_);
+    cudaStreamDestroy(contend_[0]);
+    cudaStreamDestroy(contend_[1]);
 }
 
 void Executor::alloc_comm() {
@@ -133,6 +135,7 @@ void Executor::alloc_comm() {
             act_sent_.push_back(e);
         }
     }
+    if (cfg_.stages > 1) scratch_ = dalloc(kScratch);
     const int64_t toks = static_cast<int64_t>(cfg_.global_batch) * g.seq;
     tok_dev_ = static_cast<int32_t*>(dalloc(toks * 4));
     lab_dev_ = static_cast<int32_t*>(dalloc(toks * 4));
@@ -140,9 +143,9 @@ void Executor::alloc_comm() {
 }
 
 std::vector<uint8_t> Executor::export_handles() const {
-    std::vector<uint8_t> out(4 * (1 + kHandle), 0);
-    const void* ptrs[4] = {act_recv_, act_flag_, grad_recv_, grad_flag_};
-    for (int i = 0; i < 4; ++i) {
+    std::vector<uint8_t> out(5 * (1 + kHandle), 0);
+    const void* ptrs[5] = {act_recv_, act_flag_, grad_recv_, grad_flag_, scratch_};
+    for (int i = 0; i < 5; ++i) {
         if (!ptrs[i]) continue;
         cudaIpcMemHandle_t h;
         ck(cudaIpcGetMemHandle(&h, const_cast<void*>(ptrs[i])), "ipc get");
@@ -153,7 +156,7 @@ std::vector<uint8_t> Executor::export_handles() const {
 }
 
 void Executor::import_peer(int peer, const uint8_t* bytes, size_t n) {
-    if (n < 4 * (1 + kHandle)) throw std::invalid_argument("import_peer: short handle blob");
+    if (n < 5 * (1 + kHandle)) throw std::invalid_argument("import_peer: short handle blob");
     auto open = [&](int i) -> void* {
         if (!bytes[i * (1 + kHandle)]) throw std::invalid_argument("import_peer: peer lacks the needed buffer");
         cudaIpcMemHandle_t h;
@@ -166,9 +169,11 @@ void Executor::import_peer(int peer, const uint8_t* bytes, size_t n) {
     if (peer == cfg_.stage + 1) {
         peer_act_recv_ = static_cast<__nv_bfloat16*>(open(0));
         peer_act_flag_ = static_cast<uint32_t*>(open(1));
+        peer_scratch_fwd_ = open(4);
     } else if (peer == cfg_.stage - 1) {
         peer_grad_recv_ = static_cast<__nv_bfloat16*>(open(2));
         peer_grad_flag_ = static_cast<uint32_t*>(open(3));
+        peer_scratch_bwd_ = open(4);
     } else {
         throw std::invalid_argument("import_peer: not an adjacent stage");
     }
@@ -178,9 +183,11 @@ void Executor::connect_local(int peer, Executor& p) {
     if (peer == cfg_.stage + 1) {
         peer_act_recv_ = p.act_recv_;
         peer_act_flag_ = p.act_flag_;
+        peer_scratch_fwd_ = p.scratch_;
     } else if (peer == cfg_.stage - 1) {
         peer_grad_recv_ = p.grad_recv_;
         peer_grad_flag_ = p.grad_flag_;
+        peer_scratch_bwd_ = p.scratch_;
     } else {
         throw std::invalid_argument("connect_local: not an adjacent stage");
     }
@@ -303,6 +310,10 @@ void Executor::run_iteration(int iter, const int32_t* host_tokens) {
     }
     ck(cudaEventRecord(h2d_done_, comp_), "event");
     if (last) ck(cudaMemsetAsync(stage_->loss_accumulator(), 0, 4, comp_), "memset");
+    if (contender_on_) {  // real competing NVLink stores while a trace is in a preempted segment
+        if (peer_scratch_fwd_) ck(emu_.start_contender(0, peer_scratch_fwd_, kScratch, contend_[0]), "contender");
+        if (peer_scratch_bwd_) ck(emu_.start_contender(1, peer_scratch_bwd_, kScratch, contend_[1]), "contender");
+    }
     emu_launches_ = 0;
 
     for (int id : plan_.per_device[static_cast<size_t>(s)]) {
@@ -352,6 +363,11 @@ void Executor::run_iteration(int iter, const int32_t* host_tokens) {
 double Executor::finish_iteration() {
     ck(cudaStreamSynchronize(comp_), "sync compute");
     ck(cudaStreamSynchronize(sendst_), "sync send");
+    if (contender_on_) {
+        emu_.stop_contender();
+        ck(cudaStreamSynchronize(contend_[0]), "sync contender");
+        ck(cudaStreamSynchronize(contend_[1]), "sync contender");
+    }
     float ms = 0.f;
     ck(cudaEventElapsedTime(&ms, it_start_, it_end_), "elapsed");
     return ms;

@@ -99,12 +99,15 @@ class Executor {
     int k_ = 1, b_ = 1, M_ = 1;
     int iter_ = 0;
 
-    cudaStream_t comp_ = nullptr, sendst_ = nullptr, contend_ = nullptr;
+    cudaStream_t comp_ = nullptr, sendst_ = nullptr, contend_[2] = {nullptr, nullptr};
     // receive blocks (owned; written by peers) and flags
     __nv_bfloat16 *act_recv_ = nullptr, *grad_recv_ = nullptr;
     uint32_t *act_flag_ = nullptr, *grad_flag_ = nullptr;
     // peers' blocks (IPC-mapped or same-process)
     __nv_bfloat16 *peer_act_recv_ = nullptr, *peer_grad_recv_ = nullptr;
+    void* scratch_ = nullptr;                  // target of peers' contender traffic
+    void *peer_scratch_fwd_ = nullptr, *peer_scratch_bwd_ = nullptr;
+    static constexpr size_t kScratch = 64ull << 20;
     uint32_t *peer_act_flag_ = nullptr, *peer_grad_flag_ = nullptr;
     std::vector<void*> ipc_opened_;
     // send staging, one per stash slot, with WAR events

@@ -33,6 +33,7 @@ def _declare(lib):
     lib.ptk_exec_set_plan.argtypes = [V, I, I]
     lib.ptk_exec_set_trace.argtypes = [V, I, C.c_double, C.c_int64, I, P(C.c_int64), P(C.c_int64), P(C.c_double)]
     lib.ptk_exec_set_epoch.argtypes = [V, C.c_int64]
+    lib.ptk_exec_set_contender.argtypes = [V, I]
     lib.ptk_globaltimer.restype = C.c_int64
     lib.ptk_exec_run_iteration.argtypes = [V, I, V]
     lib.ptk_exec_finish_iteration.argtypes = [V, P(C.c_double)]
@@ -125,6 +126,9 @@ class StageExecutor:
         e = (C.c_int64 * max(n, 1))(*[int(x[1]) for x in segments])
         a = (C.c_double * max(n, 1))(*[float(x[2]) for x in segments])
         L.check(self.lib.ptk_exec_set_trace(self.h, link, base_bytes_per_ns, latency_ns, n, s, e, a))
+
+    def set_contender(self, on: bool):
+        L.check(self.lib.ptk_exec_set_contender(self.h, int(on)))
 
     def set_epoch(self, epoch_ns: int):
         L.check(self.lib.ptk_exec_set_epoch(self.h, epoch_ns))

@@ -77,7 +77,8 @@ class OnlineTuner:
 
     def decide(self, current, clock: int = 0) -> dict:
         req = {"op": "decide", "model": self.model, "candidates": self.cands, "compute_profile": self.compute,
-               "samples": self.samples, "hysteresis": self.h, "window": self.window, "clock": clock}
+               "samples": [list(x) for x in self.samples], "hysteresis": self.h, "window": self.window,
+               "clock": clock}
         if current is not None:
             req["current"] = list(current)
         d = pt.scenario(req)["decision"]
