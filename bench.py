@@ -45,6 +45,12 @@ def parse():
     p.add_argument("--trace-seed", type=int, default=1)
     p.add_argument("--retune", type=int, default=0, help="re-tune every N steps (0: once at start)")
     p.add_argument("--tuner-log", type=str, default="")
+    p.add_argument("--contender", action="store_true", help="also launch competing NVLink traffic kernels")
+    p.add_argument("--model", choices=["1.3b", "6.7b"], default="1.3b")
+    p.add_argument("--global-batch", type=int, default=GLOBAL_BATCH)
+    p.add_argument("--micro-batch", type=int, default=MICRO_B)
+    p.add_argument("--mem-cap-gb", type=float, default=0.0,
+                   help="imposed per-GPU memory limit: candidates = the (k, b) frontier under it (config 4)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--timeline", type=str, default="")
     return p.parse_args()
@@ -152,8 +158,8 @@ def main():
     import torch.distributed as dist
 
     from paper_2303_01675_b200.executor import StageExecutor, max_inflight, partition_layers
-    from paper_2303_01675_b200.stage import GPT_1_3B
-    from paper_2303_01675_b200.tuning import OnlineTuner, outgoing_links
+    from paper_2303_01675_b200.stage import GPT_1_3B, GPT_6_7B
+    from paper_2303_01675_b200.tuning import OnlineTuner, candidate_set, outgoing_links
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -171,12 +177,20 @@ def main():
         if world > 1:
             dist.barrier(group=group)
 
-    shape = GPT_1_3B
-    S, M, b = world, GLOBAL_BATCH // MICRO_B, MICRO_B
+    shape = GPT_6_7B if args.model == "6.7b" else GPT_1_3B
+    GB = args.global_batch
+    S = world
     layers = partition_layers(shape.n_layer, S)
-    ks = [1, 2, 4, 8] if S > 1 else [1]
-    slots = max(max_inflight(rank, S, M, k) for k in ks)
-    ex = StageExecutor(shape, rank, S, GLOBAL_BATCH, b_max=b, slots=slots, layers=layers[rank])
+    cap = args.mem_cap_gb * 1e9 if args.mem_cap_gb > 0 else None
+    cands = candidate_set(shape, layers, S, GB, cap, fixed_b=args.micro_batch) if S > 1 else \
+        [[1, args.micro_batch, GB // args.micro_batch]]
+    b_max = max(c[1] for c in cands)
+    slots = max(max_inflight(rank, S, c[2], c[0]) * c[1] for c in cands) // b_max
+    slots = max(slots, max(max_inflight(rank, S, c[2], c[0]) for c in cands if c[1] == b_max))
+    ex = StageExecutor(shape, rank, S, GB, b_max=b_max, slots=slots, layers=layers[rank])
+    ks = [c[0] for c in cands]
+    b = cands[0][1]  # plan micro-batch size before tuning (the k=1 candidate)
+    M = GB // b
     act_bytes = b * shape.seq * shape.hidden * 2
     trace_desc = None
     if S > 1:
@@ -184,10 +198,11 @@ def main():
         base = args.link_gbps * 1e9 / 8 / 1e9  # bytes per ns
         for link in outgoing_links(rank, S):
             ex.set_trace(link, base, 0, trace_segments(args, link))
+        ex.set_contender(args.contender)
         trace_desc = {"emulated_link_gbps": args.link_gbps, "trace": args.trace, "availability": args.availability,
                       "regime_ms": args.regime_ms if args.trace == "two-regime" else None,
                       "bursty_mean_on_off_ms": [args.on_ms, args.off_ms] if args.trace == "bursty" else None,
-                      "seed": args.trace_seed, "retune_every": args.retune}
+                      "seed": args.trace_seed, "retune_every": args.retune, "contender_kernels": args.contender}
 
     def arm_reset():
         """Every arm replays the trace from t=0 (per-rank globaltimer epoch after a barrier)."""
@@ -197,9 +212,9 @@ def main():
 
     it = 0
 
-    def run(n, k):
+    def run(n, cfg):
         nonlocal it
-        ex.set_plan(k, b)
+        ex.set_plan(cfg[0], cfg[1])
         ms = []
         for _ in range(n):
             ex.run_iteration(it)
@@ -207,54 +222,57 @@ def main():
             it += 1
         return ms
 
+    by_k = {c[0]: c for c in cands}
     arm_reset()
-    run(args.warmup, 1)
+    run(args.warmup, cands[0])
     if S > 1:
-        for k in ks[1:]:
-            run(1, k)  # every candidate plan warmed (GEMM plans cached)
+        for c in cands[1:]:
+            run(1, c)  # every candidate plan warmed (GEMM / attention plans cached)
 
     # ---- fixed-plan arms (same kernels, same trace from t=0)
     fixed = {}
     if S > 1:
         for k in (1, 2):
-            arm_reset()
-            fixed[k] = run(args.steps, k)
+            if k in by_k:
+                arm_reset()
+                fixed[k] = run(args.steps, by_k[k])
 
     # ---- timed region: Ada-Grouper (tuning round at start, re-tune every `retune` steps)
-    tuner = OnlineTuner(ex, rank, S, GLOBAL_BATCH, [(k, b) for k in ks], act_bytes // b, group=group) \
-        if S > 1 else None
+    tuner = OnlineTuner(ex, rank, S, GB, [(c[0], c[1]) for c in cands], shape.seq * shape.hidden * 2,
+                        group=group) if S > 1 else None
     if tuner is not None:
         tuner.profile_compute()  # once, before the timed region
-    chosen_k, decisions, tune_s = 1, [], 0.0
+    chosen, decisions, tune_s = cands[0], [], 0.0
     arm_reset()
     with ClockSampler(local) as clk:
         ex.gemm_timing(1)
         t0 = time.perf_counter()
-        ms, ks_run = [], []
+        ms, plans_run = [], []
         for step in range(args.steps):
             if tuner is not None and (step == 0 or (args.retune > 0 and step % args.retune == 0)):
                 tr0 = time.perf_counter()
-                d = tuner.round(None if step == 0 else [chosen_k, b, M], clock=step)
+                d = tuner.round(None if step == 0 else list(chosen), clock=step)
                 decisions.append(d)
-                chosen_k = d["chosen"][0]
+                chosen = d["chosen"]
                 barrier()
                 tune_s += time.perf_counter() - tr0
-            ms += run(1, chosen_k)
-            ks_run.append(chosen_k)
+            ms += run(1, chosen)
+            plans_run.append([chosen[0], chosen[1]])
         barrier()
         wall = time.perf_counter() - t0
         gemm_flops, gemm_ms, gemm_n = ex.gemm_timing(0)
     tl = ex.timeline()
     loss = ex.read_loss() if rank == S - 1 else None
     if tuner is not None and rank == 0 and args.tuner_log:
-        Path(args.tuner_log).write_text(json.dumps({"trace": trace_desc, "rounds": tuner.log}))
+        Path(args.tuner_log).write_text(json.dumps({"trace": trace_desc, "candidates": cands, "rounds": tuner.log}))
     ms_1f1b = fixed.get(1, ms)
+    b, M = chosen[1], chosen[2]
 
     # ---- e2e: host token buffers through the C ABI, H2D + loss D2H inside the timed steps
     import numpy as np
     rng = np.random.default_rng(7)
-    host = rng.integers(0, shape.vocab, size=(2, GLOBAL_BATCH * shape.seq), dtype=np.int32)
-    ex.set_plan(chosen_k, b)
+    host = rng.integers(0, shape.vocab, size=(2, GB * shape.seq), dtype=np.int32)
+    ex.set_plan(chosen[0], chosen[1])
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -288,9 +306,9 @@ def main():
         return
 
     T = max(all_ms) / 1e3
-    value = GLOBAL_BATCH * args.steps / T
-    v1f1b = GLOBAL_BATCH * args.steps / (max(all_1f1b) / 1e3)
-    vk2 = GLOBAL_BATCH * args.steps / (max(all_k2) / 1e3)
+    value = GB * args.steps / T
+    v1f1b = GB * args.steps / (max(all_1f1b) / 1e3)
+    vk2 = GB * args.steps / (max(all_k2) / 1e3)
     loss = all_loss[-1]
     pk, pk_kind = peaks()
     peak_sus = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
@@ -308,16 +326,19 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(T * 1e3 / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "GPT-1.3B training step (configs[1]: 24L h2048 32 heads s1024 V50304)",
-                   "global_batch": GLOBAL_BATCH, "micro_batch": b, "micro_batches": M, "seq_len": 1024,
+        "config": {"workload": (f"GPT-{args.model.upper()} training step" +
+                                (" (configs[1]: 24L h2048 32 heads s1024 V50304)" if args.model == "1.3b"
+                                 else " (configs[3]: 32L h4096 32 heads s1024 V50304)")),
+                   "global_batch": GB, "micro_batch": b, "micro_batches": M, "seq_len": shape.seq,
+                   "candidates_kbM": cands, "memory_cap_gb": args.mem_cap_gb or None,
                    "stages": S, "layers_per_stage": [e - s_ for s_, e in layers],
                    "parallelism": f"pp{S}" if S > 1 else "single stage (no pipeline)",
-                   "schedule": (f"Ada-Grouper adaptive kFkB (k per step {ks_run})" if S > 1 else "1F1B (S=1)"),
+                   "schedule": (f"Ada-Grouper adaptive kFkB ((k, b) per step {plans_run})" if S > 1 else "1F1B (S=1)"),
                    "emulated_preemption": trace_desc, "l2": "working set (weights + activations) >> 126 MB L2"},
-        "schedules": {"ada_grouper": {"k_per_step": ks_run, "samples_per_s": round(value, 3),
+        "schedules": {"ada_grouper": {"kb_per_step": plans_run, "samples_per_s": round(value, 3),
                                       "tuning_overhead_s": round(tune_s, 4)},
-                      "1f1b": {"k": 1, "samples_per_s": round(v1f1b, 3)},
-                      "kfkb_k2": {"k": 2, "samples_per_s": round(vk2, 3)},
+                      "1f1b": {"kbM": by_k.get(1), "samples_per_s": round(v1f1b, 3)},
+                      "kfkb_k2": {"kbM": by_k.get(2), "samples_per_s": round(vk2, 3)},
                       "speedup_vs_1f1b": round(value / v1f1b, 4)},
         "tuner_decisions": [{"chosen": d["chosen"], "switched": d["switched"],
                              "estimates_ns": [e[3] for e in d["estimates"]]} for d in decisions],
@@ -329,7 +350,7 @@ def main():
                      "launches": sum(g[2] for g in all_gemm),
                      "note": f"algorithmic GEMM FLOPs / summed CUDA-event GEMM durations over the timed steps; "
                              f"peak = sustained bf16 of {pk_kind} MEASURED_PEAKS.json"},
-        "e2e": {"value": round(GLOBAL_BATCH * args.steps / max(all_e2e), 3), "unit": "samples/s",
+        "e2e": {"value": round(GB * args.steps / max(all_e2e), 3), "unit": "samples/s",
                 "h2d_bytes_per_step": int(sum(all_h2d)), "d2h_bytes_per_step": 4},
         "gpu_launches": int(sum(all_launch)),
         "loss": loss,

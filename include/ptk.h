@@ -77,6 +77,14 @@ typedef struct ptk_gemm_desc {
 
 int ptk_gemm(const ptk_gemm_desc* desc, void* stream);
 
+/* Fused causal attention forward: qkv bf16 [b][s][3][H][d] -> o bf16 [b*s][H*d],
+ * lse fp32 [b][H][s] = log2(sum_k 2^(S_qk * log2(e)/sqrt(d))) (row max included). */
+int ptk_flash_forward(const void* qkv, void* o, float* lse, int b, int s, int H, int d, void* stream);
+/* Its backward: dqkv bf16 [b*s][3*H*d] (dQ | dK | dV sections) from qkv, o, dO = d(o),
+ * lse; dsum: fp32 scratch [b][H][s].  Deterministic (no atomics). */
+int ptk_flash_backward(const void* qkv, const void* o, const void* dO, const float* lse, float* dsum, void* dqkv,
+                       int b, int s, int H, int d, void* stream);
+
 /* ------------------------------------------------------------ planner
  * Mirrors pipetune::StageProfile / ModelSpec (proj/include/pipetune/model.hpp:30-51). */
 typedef struct ptk_stage_profile {

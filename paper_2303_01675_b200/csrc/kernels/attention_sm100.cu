@@ -1,0 +1,704 @@
+// Fused causal attention forward for sm_100a (tcgen05 + TMEM + TMA).
+//
+// One CTA per (128-query block, head, sample).  For each 128-key block j <= i:
+//   S_j  = Q·K_jᵀ            tcgen05.mma into TMEM (double-buffered: S_{j+1} is
+//                            issued while the softmax warps work on S_j)
+//   P_j  = exp2(S_j·c − m)   4 softmax warps, one query row per thread (the row
+//                            max/sum never leave the thread), P written to smem
+//                            in the UMMA K-major 128B-swizzled layout
+//   O   += P_j·V_j           tcgen05.mma into a TMEM accumulator; when the row
+//                            max moves, the thread rescales its O row in TMEM
+// and finally O/l is written as bf16 [T, h] (the out-projection's input) and
+// lse = m + log2(l) (log2 units of the scaled scores) for the backward.
+// Warps: 0 TMA producer, 1 TMEM alloc + MMA issuer, 4-7 softmax/epilogue.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "attention_sm100.h"
+#include "sm100_ptx.cuh"
+
+namespace ptk {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kBlk = 128;      // query rows and key rows per block
+constexpr int kThreads = 256;  // 8 warps
+
+template <int D>
+struct FaCfg {
+    static constexpr int kQBytes = kBlk * D * 2;     // [D/64][128 rows x 128 B]
+    static constexpr int kKBytes = kBlk * D * 2;
+    static constexpr int kVBytes = kBlk * D * 2;     // [2 kv halves][D/64][64 rows x 128 B]
+    static constexpr int kPBytes = kBlk * kBlk * 2;  // [2][128 rows x 128 B]
+    static constexpr int kStages = 2;
+    static constexpr int kSmem = kQBytes + kStages * (kKBytes + kVBytes) + kPBytes + 1024 + 256;
+    static constexpr uint32_t kTmemS0 = 0, kTmemS1 = 128, kTmemO = 256;
+};
+
+struct FaArgs {
+    __nv_bfloat16* o;  // [b*s][h]
+    float* lse;        // [b][H][s], log2 units of the scaled scores
+    int s, H, h;
+    float scale_log2;  // log2(e) / sqrt(d)
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
+                     const __grid_constant__ FaArgs a) {
+    using C = FaCfg<D>;
+    constexpr uint32_t kIdescS = make_idesc_bf16(kBlk, kBlk, false, false);  // Q (K-major) x K (K-major)
+    constexpr uint32_t kIdescO = make_idesc_bf16(kBlk, D, false, true);      // P (K-major) x V (MN-major)
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sK = sQ + C::kQBytes;
+    uint8_t* sV = sK + C::kStages * C::kKBytes;
+    uint8_t* sP = sV + C::kStages * C::kVBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::kPBytes);
+    uint64_t* q_full = bars + 0;
+    uint64_t* kv_full = bars + 1;   // [2]
+    uint64_t* kv_empty = bars + 3;  // [2]
+    uint64_t* s_full = bars + 5;    // [2]
+    uint64_t* s_empty = bars + 7;   // [2]
+    uint64_t* p_full = bars + 9;
+    uint64_t* pv_done = bars + 10;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+    const int warp = threadIdx.x / 32;
+    const uint32_t lane = lane_id();
+    const int nqb = a.s / kBlk;
+    const int qb = nqb - 1 - static_cast<int>(blockIdx.x);  // heaviest blocks first
+    const int head = blockIdx.y, bi = blockIdx.z;
+    const int nkv = qb + 1;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmQK);
+        tma_prefetch_desc(&tmV);
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], 4);
+        }
+        mbar_init(p_full, 4);
+        mbar_init(pv_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            mbar_arrive_expect_tx(q_full, C::kQBytes);
+#pragma unroll
+            for (int kb = 0; kb < D / 64; ++kb)
+                tma_load_4d(&tmQK, q_full, sQ + kb * kBlk * 128, kb * 64, qb * kBlk, head, bi);
+            for (int j = 0; j < nkv; ++j) {
+                const int st = j & 1;
+                mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&kv_full[st], C::kKBytes + C::kVBytes);
+                uint8_t* k = sK + st * C::kKBytes;
+                uint8_t* v = sV + st * C::kVBytes;
+#pragma unroll
+                for (int kb = 0; kb < D / 64; ++kb)
+                    tma_load_4d(&tmQK, &kv_full[st], k + kb * kBlk * 128, kb * 64, j * kBlk, a.H + head, bi);
+#pragma unroll
+                for (int half = 0; half < 2; ++half)
+#pragma unroll
+                    for (int na = 0; na < D / 64; ++na)
+                        tma_load_4d(&tmV, &kv_full[st], v + (half * (D / 64) + na) * 8192, na * 64,
+                                    j * kBlk + half * 64, 2 * a.H + head, bi);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            mbar_wait(q_full, 0);
+            const uint32_t q_base = smem_u32(sQ);
+            auto issue_s = [&](int j) {
+                const int st = j & 1;
+                mbar_wait(&kv_full[st], (j >> 1) & 1);
+                mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t k_base = smem_u32(sK + st * C::kKBytes);
+                const uint32_t d_tmem = tmem + (st ? C::kTmemS1 : C::kTmemS0);
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {
+                    const uint32_t off = (k / 4) * kBlk * 128 + (k % 4) * 32;
+                    mma_bf16_ss(d_tmem, make_sw128_desc(q_base + off, 16, 1024), make_sw128_desc(k_base + off, 16, 1024),
+                                kIdescS, k > 0 ? 1u : 0u);
+                }
+                mma_commit(&s_full[st]);
+            };
+            issue_s(0);
+            for (int j = 0; j < nkv; ++j) {
+                if (j + 1 < nkv) issue_s(j + 1);
+                mbar_wait(p_full, j & 1);
+                tc_fence_after();
+                const int st = j & 1;
+                const uint32_t p_base = smem_u32(sP);
+                const uint32_t v_base = smem_u32(sV + st * C::kVBytes);
+#pragma unroll
+                for (int k = 0; k < kBlk / 16; ++k) {
+                    const uint32_t pa = p_base + (k / 4) * kBlk * 128 + (k % 4) * 32;
+                    const uint32_t vb = v_base + (k / 4) * (D / 64) * 8192 + (k % 4) * 2048;
+                    mma_bf16_ss(tmem + C::kTmemO, make_sw128_desc(pa, 16, 1024), make_sw128_desc(vb, 8192, 1024),
+                                kIdescO, (j > 0 || k > 0) ? 1u : 0u);
+                }
+                mma_commit(pv_done);
+                mma_commit(&kv_empty[st]);
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- softmax / epilogue: thread = query row
+        const int quad = warp & 3;
+        const int r = quad * 32 + static_cast<int>(lane);
+        const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+        float m = -INFINITY, l = 0.f;
+        for (int j = 0; j < nkv; ++j) {
+            const int st = j & 1;
+            mbar_wait(&s_full[st], (j >> 1) & 1);
+            tc_fence_after();
+            float x[kBlk];
+#pragma unroll
+            for (int c = 0; c < kBlk / 32; ++c) {
+                float v[32];
+                tmem_ld_32x32b_x32(tmem + lane_base + (st ? C::kTmemS1 : C::kTmemS0) + c * 32, v);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) x[c * 32 + e] = v[e];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[st]);
+            float mx = m;
+            const bool diag = j == qb;
+#pragma unroll
+            for (int c = 0; c < kBlk; ++c) {
+                x[c] = (diag && c > r) ? -INFINITY : x[c] * a.scale_log2;
+                mx = fmaxf(mx, x[c]);
+            }
+            const float alpha = ex2(m - mx);  // m = -inf on the first block -> 0
+            float sum = 0.f;
+#pragma unroll
+            for (int c = 0; c < kBlk; ++c) {
+                x[c] = ex2(x[c] - mx);
+                sum += x[c];
+            }
+            l = l * alpha + sum;
+            m = mx;
+            if (j > 0) {
+                mbar_wait(pv_done, (j - 1) & 1);  // P buffer free, O stable
+                tc_fence_after();
+            }
+            // P row -> smem, K-major 128B-swizzled (16-byte chunk index ^= row % 8)
+#pragma unroll
+            for (int q = 0; q < kBlk / 8; ++q) {
+                uint4 u;
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(x[q * 8 + 0], x[q * 8 + 1]);
+                __nv_bfloat162 h1 = __floats2bfloat162_rn(x[q * 8 + 2], x[q * 8 + 3]);
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(x[q * 8 + 4], x[q * 8 + 5]);
+                __nv_bfloat162 h3 = __floats2bfloat162_rn(x[q * 8 + 6], x[q * 8 + 7]);
+                u.x = *reinterpret_cast<uint32_t*>(&h0);
+                u.y = *reinterpret_cast<uint32_t*>(&h1);
+                u.z = *reinterpret_cast<uint32_t*>(&h2);
+                u.w = *reinterpret_cast<uint32_t*>(&h3);
+                const int kb2 = q >> 3, c16 = q & 7;
+                *reinterpret_cast<uint4*>(sP + kb2 * (kBlk * 128) + r * 128 + ((c16 ^ (r & 7)) * 16)) = u;
+            }
+            if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rescale this row of O
+#pragma unroll
+                for (int c = 0; c < D / 32; ++c) {
+                    float v[32];
+                    tmem_ld_32x32b_x32(tmem + lane_base + C::kTmemO + c * 32, v);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] *= alpha;
+                    tmem_st_32x32b_x32(tmem + lane_base + C::kTmemO + c * 32, v);
+                }
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
+        }
+        mbar_wait(pv_done, (nkv - 1) & 1);
+        tc_fence_after();
+        const float inv = 1.f / l;
+        const int q = qb * kBlk + r;
+        __nv_bfloat16* orow = a.o + (static_cast<int64_t>(bi) * a.s + q) * a.h + head * D;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+            float v[32];
+            tmem_ld_32x32b_x32(tmem + lane_base + C::kTmemO + c * 32, v);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                uint4 u;
+                uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    __nv_bfloat162 hh = __floats2bfloat162_rn(v[g * 8 + 2 * e] * inv, v[g * 8 + 2 * e + 1] * inv);
+                    w[e] = *reinterpret_cast<uint32_t*>(&hh);
+                }
+                *reinterpret_cast<uint4*>(orow + c * 32 + g * 8) = u;
+            }
+        }
+        a.lse[(static_cast<int64_t>(bi) * a.H + head) * a.s + q] = m + __log2f(l);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// qkv [b][s][3][H][d] viewed as dims {d, s, 3H, b}.
+cudaError_t qkv_map(CUtensorMap* m, const void* qkv, int b, int s, int H, int d, int box_rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    const int64_t h = static_cast<int64_t>(H) * d;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(s), static_cast<cuuint64_t>(3 * H),
+                          static_cast<cuuint64_t>(b)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(3 * h * 2), static_cast<cuuint64_t>(d * 2),
+                             static_cast<cuuint64_t>(s * 3 * h * 2)};
+    cuuint32_t box[4] = {64, static_cast<cuuint32_t>(box_rows), 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(qkv), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int D>
+cudaError_t launch_fwd(const FlashPlan& p, cudaStream_t st) {
+    using C = FaCfg<D>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(flash_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    FaArgs a{p.o, p.lse, p.s, p.H, p.H * p.d, p.scale_log2};
+    dim3 grid(p.s / kBlk, p.H, p.b);
+    flash_fwd_kernel<D><<<grid, kThreads, C::kSmem, st>>>(p.tmQK, p.tmV, a);
+    return cudaPeekAtLastError();
+}
+
+}  // namespace
+
+cudaError_t flash_prepare(const void* qkv, void* o, float* lse, int b, int s, int H, int d, FlashPlan* p) {
+    if ((d != 64 && d != 128) || s % kBlk) return cudaErrorInvalidValue;
+    cudaError_t e = qkv_map(&p->tmQK, qkv, b, s, H, d, kBlk);
+    if (e != cudaSuccess) return e;
+    e = qkv_map(&p->tmV, qkv, b, s, H, d, 64);
+    if (e != cudaSuccess) return e;
+    p->o = static_cast<__nv_bfloat16*>(o);
+    p->lse = lse;
+    p->b = b;
+    p->s = s;
+    p->H = H;
+    p->d = d;
+    p->scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
+    return cudaSuccess;
+}
+
+cudaError_t flash_forward(const FlashPlan& p, cudaStream_t st) {
+    return p.d == 64 ? launch_fwd<64>(p, st) : launch_fwd<128>(p, st);
+}
+
+// ============================================================================
+// Backward.  Deterministic two-kernel form (no atomics):
+//   mode KV: CTA per (key block j, head, sample), loop query blocks i >= j:
+//     Sᵀ = K_j Q_iᵀ, dPᵀ = V_j dO_iᵀ            (TMEM, thread = key row)
+//     Pᵀ = 2^(Sᵀ c - lse2[q]),  dSᵀ = τ Pᵀ (dPᵀ - D[q])   -> smem (bf16)
+//     dV_j += Pᵀ dO_i,  dK_j += dSᵀ Q_i           (TMEM accumulators)
+//   mode Q:  CTA per (query block i, head, sample), loop key blocks j <= i:
+//     S = Q_i K_jᵀ, dP = dO_i V_jᵀ  (thread = query row)
+//     dS = τ P (dP - D[q])  -> smem;  dQ_i += dS K_j
+// A [rows][64-col] 128B-swizzled tile is simultaneously the K-major operand
+// for the score products and the MN-major operand (LBO = 16 KiB between
+// 64-wide column atoms) for the accumulating products, so every operand is
+// loaded once per step.  D = rowsum(dO ∘ O) comes from attn_bwd_dot_kernel.
+// ============================================================================
+namespace {
+
+template <int D>
+struct BwCfg {
+    static constexpr int kTile = kBlk * D * 2;  // one [128][D] tile
+    static constexpr int kStages = D == 64 ? 2 : 1;
+    static constexpr int kPd = kBlk * kBlk * 2;  // one [128][128] bf16 A-operand buffer
+    static constexpr int kSmem = 2 * kTile + kStages * 2 * kTile + 2 * kPd + 2 * 2 * kBlk * 4 + 1024 + 256;
+    static constexpr uint32_t kX = 0, kY = 128, kAcc1 = 256, kAcc2 = 256 + D;
+};
+
+struct BwArgs {
+    __nv_bfloat16* dqkv;  // [b*s][3h]
+    const float* lse;     // [b][H][s]
+    const float* dsum;    // [b][H][s]
+    int s, H, h;
+    float scale_log2, tau;
+};
+
+__device__ __forceinline__ void st_bf16_swz(uint8_t* buf, int r, int c0, const float* v8) {
+    // 8 consecutive columns c0..c0+7 of row r into a [2][128 rows x 128 B] K-major swizzled buffer
+    uint4 u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 hh = __floats2bfloat162_rn(v8[2 * e], v8[2 * e + 1]);
+        w[e] = *reinterpret_cast<uint32_t*>(&hh);
+    }
+    const int kb = c0 >> 6, c16 = (c0 & 63) >> 3;
+    *reinterpret_cast<uint4*>(buf + kb * (kBlk * 128) + r * 128 + ((c16 ^ (r & 7)) * 16)) = u;
+}
+
+template <int D, bool KV>
+__global__ void __launch_bounds__(kThreads, 1)
+    flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
+                     const __grid_constant__ BwArgs a) {
+    using C = BwCfg<D>;
+    constexpr int S = C::kStages;
+    constexpr uint32_t kIdescXY = make_idesc_bf16(kBlk, kBlk, false, false);
+    constexpr uint32_t kIdescAcc = make_idesc_bf16(kBlk, D, false, true);
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sF0 = smem;               // fixed tile 0: K_j (KV) | Q_i (Q)
+    uint8_t* sF1 = sF0 + C::kTile;     // fixed tile 1: V_j (KV) | dO_i (Q)
+    uint8_t* sStep = sF1 + C::kTile;   // [S][2 tiles]: (Q_i, dO_i) (KV) | (K_j, V_j) (Q)
+    uint8_t* sP = sStep + S * 2 * C::kTile;  // Pᵀ (KV only)
+    uint8_t* sDS = sP + C::kPd;              // dSᵀ (KV) | dS (Q)
+    float* sRow = reinterpret_cast<float*>(sDS + C::kPd);  // [2][lse[128], D[128]] (KV only)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sRow + 2 * 2 * kBlk);
+    uint64_t* fix_full = bars + 0;
+    uint64_t* ld_full = bars + 1;   // [2]
+    uint64_t* ld_empty = bars + 3;  // [2]
+    uint64_t* xy_full = bars + 5;
+    uint64_t* xy_free = bars + 6;
+    uint64_t* pd_full = bars + 7;
+    uint64_t* acc_done = bars + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+    const int warp = threadIdx.x / 32;
+    const uint32_t lane = lane_id();
+    const int nb = a.s / kBlk;
+    const int blk = KV ? static_cast<int>(blockIdx.x) : nb - 1 - static_cast<int>(blockIdx.x);
+    const int head = blockIdx.y, bi = blockIdx.z;
+    const int first = KV ? blk : 0;
+    const int nsteps = KV ? nb - blk : blk + 1;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmQKV);
+        tma_prefetch_desc(&tmDO);
+        mbar_init(fix_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&ld_full[i], 1);
+            mbar_init(&ld_empty[i], 1);
+        }
+        mbar_init(xy_full, 1);
+        mbar_init(xy_free, 4);
+        mbar_init(pd_full, 4);
+        mbar_init(acc_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // tile loader: rows [row0, row0+128) of a {d, s, heads, b} map, head coordinate hc
+    auto load_tile = [&](const CUtensorMap* m, uint64_t* bar, uint8_t* dst, int row0, int hc) {
+#pragma unroll
+        for (int kb = 0; kb < D / 64; ++kb) tma_load_4d(m, bar, dst + kb * kBlk * 128, kb * 64, row0, hc, bi);
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            mbar_arrive_expect_tx(fix_full, 2 * C::kTile);
+            if (KV) {
+                load_tile(&tmQKV, fix_full, sF0, blk * kBlk, a.H + head);      // K_j
+                load_tile(&tmQKV, fix_full, sF1, blk * kBlk, 2 * a.H + head);  // V_j
+            } else {
+                load_tile(&tmQKV, fix_full, sF0, blk * kBlk, head);  // Q_i
+                load_tile(&tmDO, fix_full, sF1, blk * kBlk, head);   // dO_i
+            }
+            for (int t = 0; t < nsteps; ++t) {
+                const int st = S == 1 ? 0 : (t & 1);
+                const uint32_t ph = S == 1 ? (t & 1) : ((t >> 1) & 1);
+                mbar_wait(&ld_empty[st], ph ^ 1);
+                mbar_arrive_expect_tx(&ld_full[st], 2 * C::kTile);
+                uint8_t* t0 = sStep + st * 2 * C::kTile;
+                const int row0 = (first + t) * kBlk;
+                if (KV) {
+                    load_tile(&tmQKV, &ld_full[st], t0, row0, head);             // Q_i
+                    load_tile(&tmDO, &ld_full[st], t0 + C::kTile, row0, head);   // dO_i
+                } else {
+                    load_tile(&tmQKV, &ld_full[st], t0, row0, a.H + head);              // K_j
+                    load_tile(&tmQKV, &ld_full[st], t0 + C::kTile, row0, 2 * a.H + head);  // V_j
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            mbar_wait(fix_full, 0);
+            const uint32_t f0 = smem_u32(sF0), f1 = smem_u32(sF1);
+            auto issue_xy = [&](int t) {
+                const int st = S == 1 ? 0 : (t & 1);
+                const uint32_t ph = S == 1 ? (t & 1) : ((t >> 1) & 1);
+                mbar_wait(&ld_full[st], ph);
+                if (t > 0) mbar_wait(xy_free, (t - 1) & 1);
+                tc_fence_after();
+                const uint32_t s0 = smem_u32(sStep + st * 2 * C::kTile), s1 = s0 + C::kTile;
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {
+                    const uint32_t off = (k / 4) * kBlk * 128 + (k % 4) * 32;
+                    // X = F0 · Step0ᵀ,  Y = F1 · Step1ᵀ   (both operands K-major, K = d)
+                    mma_bf16_ss(tmem + C::kX, make_sw128_desc(f0 + off, 16, 1024), make_sw128_desc(s0 + off, 16, 1024),
+                                kIdescXY, k > 0 ? 1u : 0u);
+                    mma_bf16_ss(tmem + C::kY, make_sw128_desc(f1 + off, 16, 1024), make_sw128_desc(s1 + off, 16, 1024),
+                                kIdescXY, k > 0 ? 1u : 0u);
+                }
+                mma_commit(xy_full);
+            };
+            issue_xy(0);
+            for (int t = 0; t < nsteps; ++t) {
+                if (t + 1 < nsteps) issue_xy(t + 1);
+                mbar_wait(pd_full, t & 1);
+                tc_fence_after();
+                const int st = S == 1 ? 0 : (t & 1);
+                const uint32_t s0 = smem_u32(sStep + st * 2 * C::kTile), s1 = s0 + C::kTile;
+                const uint32_t pb = smem_u32(sP), db = smem_u32(sDS);
+#pragma unroll
+                for (int k = 0; k < kBlk / 16; ++k) {
+                    const uint32_t aoff = (k / 4) * kBlk * 128 + (k % 4) * 32;  // K-major A, k over 128 columns
+                    const uint32_t boff = k * 2048;                            // MN-major B, k over 128 rows
+                    const uint32_t acc = (t > 0 || k > 0) ? 1u : 0u;
+                    if (KV) {
+                        // dV += Pᵀ dO_i ; dK += dSᵀ Q_i
+                        mma_bf16_ss(tmem + C::kAcc1, make_sw128_desc(pb + aoff, 16, 1024),
+                                    make_sw128_desc(s1 + boff, kBlk * 128, 1024), kIdescAcc, acc);
+                        mma_bf16_ss(tmem + C::kAcc2, make_sw128_desc(db + aoff, 16, 1024),
+                                    make_sw128_desc(s0 + boff, kBlk * 128, 1024), kIdescAcc, acc);
+                    } else {
+                        // dQ += dS K_j
+                        mma_bf16_ss(tmem + C::kAcc1, make_sw128_desc(db + aoff, 16, 1024),
+                                    make_sw128_desc(s0 + boff, kBlk * 128, 1024), kIdescAcc, acc);
+                    }
+                }
+                mma_commit(acc_done);
+                mma_commit(&ld_empty[st]);
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- elementwise warps: thread = row of the fixed block
+        const int quad = warp & 3;
+        const int r = quad * 32 + static_cast<int>(lane);
+        const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+        const int64_t rowbase = (static_cast<int64_t>(bi) * a.H + head) * a.s;
+        float my_lse = 0.f, my_d = 0.f;
+        if (!KV) {
+            my_lse = a.lse[rowbase + blk * kBlk + r];
+            my_d = a.dsum[rowbase + blk * kBlk + r];
+        }
+        for (int t = 0; t < nsteps; ++t) {
+            const int other = first + t;  // index of the stepped block
+            float* rowv = sRow + (t & 1) * 2 * kBlk;
+            if (KV) {  // this step's per-query lse / D -> smem (named barrier over the 4 warps)
+                rowv[r] = a.lse[rowbase + other * kBlk + r];
+                rowv[kBlk + r] = a.dsum[rowbase + other * kBlk + r];
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            }
+            mbar_wait(xy_full, t & 1);
+            tc_fence_after();
+            if (t > 0) {
+                mbar_wait(acc_done, (t - 1) & 1);  // previous step's MMAs done reading sP / sDS
+            }
+            const bool diag = other == blk;
+#pragma unroll 1
+            for (int c = 0; c < kBlk / 32; ++c) {
+                float x[32], y[32];
+                tmem_ld_32x32b_x32(tmem + lane_base + C::kX + c * 32, x);
+                tmem_ld_32x32b_x32(tmem + lane_base + C::kY + c * 32, y);
+                if (c == kBlk / 32 - 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(xy_free);
+                }
+                float p[32], ds[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int col = c * 32 + e;
+                    // KV: row = key, col = query -> valid iff query >= key ; Q: row = query, col = key
+                    const bool valid = !diag || (KV ? col >= r : col <= r);
+                    const float l2 = KV ? rowv[col] : my_lse;
+                    const float dd = KV ? rowv[kBlk + col] : my_d;
+                    const float pv = valid ? ex2(x[e] * a.scale_log2 - l2) : 0.f;
+                    p[e] = pv;
+                    ds[e] = a.tau * pv * (y[e] - dd);
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    if (KV) st_bf16_swz(sP, r, c * 32 + g * 8, p + g * 8);
+                    st_bf16_swz(sDS, r, c * 32 + g * 8, ds + g * 8);
+                }
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(pd_full);
+        }
+        mbar_wait(acc_done, (nsteps - 1) & 1);
+        tc_fence_after();
+        // epilogue: accumulators -> dqkv (bf16); KV: acc1 = dV (section 2), acc2 = dK (section 1); Q: acc1 = dQ
+        const int row = blk * kBlk + r;
+        __nv_bfloat16* base = a.dqkv + (static_cast<int64_t>(bi) * a.s + row) * (3 * a.h) + head * D;
+#pragma unroll
+        for (int which = 0; which < (KV ? 2 : 1); ++which) {
+            __nv_bfloat16* dst = base + (KV ? (which == 0 ? 2 * a.h : a.h) : 0);
+            const uint32_t col0 = which == 0 ? C::kAcc1 : C::kAcc2;
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                float v[32];
+                tmem_ld_32x32b_x32(tmem + lane_base + col0 + c * 32, v);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    uint4 u;
+                    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        __nv_bfloat162 hh = __floats2bfloat162_rn(v[g * 8 + 2 * e], v[g * 8 + 2 * e + 1]);
+                        w[e] = *reinterpret_cast<uint32_t*>(&hh);
+                    }
+                    *reinterpret_cast<uint4*>(dst + c * 32 + g * 8) = u;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+// D[b][H][q] = sum_dd dO[q][hh*d+dd] * O[q][hh*d+dd]; one thread per (row, head).
+template <int D>
+__global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
+                                    float* __restrict__ dsum, int rows, int s, int H) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * H) return;
+    const int row = idx / H, head = idx % H;
+    const int64_t off = static_cast<int64_t>(row) * H * D + head * D;
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < D; c += 8) {
+        const uint4 a = *reinterpret_cast<const uint4*>(dO + off + c);
+        const uint4 b = *reinterpret_cast<const uint4*>(O + off + c);
+        const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
+        const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 x = __bfloat1622float2(ha[e]), y = __bfloat1622float2(hb[e]);
+            acc += x.x * y.x + x.y * y.y;
+        }
+    }
+    const int bi = row / s, q = row % s;
+    dsum[(static_cast<int64_t>(bi) * H + head) * s + q] = acc;
+}
+
+// dO [b*s][H*d] viewed as dims {d, s, H, b}, box {64, 128}.
+cudaError_t do_map(CUtensorMap* m, const void* dO, int b, int s, int H, int d) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    const int64_t h = static_cast<int64_t>(H) * d;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(s), static_cast<cuuint64_t>(H),
+                          static_cast<cuuint64_t>(b)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(h * 2), static_cast<cuuint64_t>(d * 2),
+                             static_cast<cuuint64_t>(s * h * 2)};
+    cuuint32_t box[4] = {64, static_cast<cuuint32_t>(kBlk), 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(dO), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int D, bool KV>
+cudaError_t launch_bwd(const FlashBwdPlan& p, cudaStream_t st) {
+    using C = BwCfg<D>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e =
+            cudaFuncSetAttribute(flash_bwd_kernel<D, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    BwArgs a{p.dqkv, p.lse, p.dsum, p.s, p.H, p.H * p.d, p.scale_log2, 1.f / sqrtf(static_cast<float>(p.d))};
+    dim3 grid(p.s / kBlk, p.H, p.b);
+    flash_bwd_kernel<D, KV><<<grid, kThreads, C::kSmem, st>>>(p.tmQKV, p.tmDO, a);
+    return cudaPeekAtLastError();
+}
+
+}  // namespace
+
+cudaError_t flash_bwd_prepare(const void* qkv, const void* o, const void* dO, const float* lse, float* dsum,
+                              void* dqkv, int b, int s, int H, int d, FlashBwdPlan* p) {
+    if ((d != 64 && d != 128) || s % kBlk) return cudaErrorInvalidValue;
+    cudaError_t e = qkv_map(&p->tmQKV, qkv, b, s, H, d, kBlk);
+    if (e != cudaSuccess) return e;
+    e = do_map(&p->tmDO, dO, b, s, H, d);
+    if (e != cudaSuccess) return e;
+    p->o = static_cast<const __nv_bfloat16*>(o);
+    p->dO = static_cast<const __nv_bfloat16*>(dO);
+    p->lse = lse;
+    p->dsum = dsum;
+    p->dqkv = static_cast<__nv_bfloat16*>(dqkv);
+    p->b = b;
+    p->s = s;
+    p->H = H;
+    p->d = d;
+    p->scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
+    return cudaSuccess;
+}
+
+cudaError_t flash_backward(const FlashBwdPlan& p, cudaStream_t st) {
+    const int rows = p.b * p.s;
+    const int n = rows * p.H;
+    if (p.d == 64)
+        attn_bwd_dot_kernel<64><<<(n + 255) / 256, 256, 0, st>>>(p.dO, p.o, p.dsum, rows, p.s, p.H);
+    else
+        attn_bwd_dot_kernel<128><<<(n + 255) / 256, 256, 0, st>>>(p.dO, p.o, p.dsum, rows, p.s, p.H);
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return e;
+    e = p.d == 64 ? launch_bwd<64, true>(p, st) : launch_bwd<128, true>(p, st);
+    if (e != cudaSuccess) return e;
+    return p.d == 64 ? launch_bwd<64, false>(p, st) : launch_bwd<128, false>(p, st);
+}
+
+}  // namespace ptk

@@ -383,58 +383,79 @@ __global__ void __launch_bounds__(128) embed_fwd_kernel(const int32_t* __restric
     }
 }
 
-// Owner-computes token-embedding gradient: each warp owns vocabulary rows,
-// scans the micro-batch's tokens (in smem) in position order and accumulates
-// matching dX rows; dwte[v] += sum.  Deterministic, no atomics.
-template <int V>
-__global__ void __launch_bounds__(256) embed_bwd_wte_kernel(const int32_t* __restrict__ tok,
-                                                            const __nv_bfloat16* __restrict__ dx,
-                                                            float* __restrict__ dwte, int rows, int vocab) {
-    constexpr int H = V * 256;
-    extern __shared__ int32_t stok[];
-    for (int i = threadIdx.x; i < rows; i += blockDim.x) stok[i] = tok[i];
+// Token-embedding gradient, deterministic and atomic-free:
+//  1) one block bitonic-sorts (token, position) keys of the micro-batch in smem
+//     (positions ascending within a token);
+//  2) one warp per sorted slot that starts a run of equal tokens sums the run's
+//     dX rows in that order and adds the sum to dwte[token].
+__global__ void __launch_bounds__(1024) embed_sort_kernel(const int32_t* __restrict__ tok, int32_t* __restrict__ order,
+                                                          int rows) {
+    extern __shared__ uint64_t keys[];  // pow2 >= rows
+    int n = 1;
+    while (n < rows) n <<= 1;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        keys[i] = i < rows ? (static_cast<uint64_t>(static_cast<uint32_t>(tok[i])) << 32) | static_cast<uint32_t>(i)
+                           : ~0ull;
     __syncthreads();
-    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-    const int nwarps = blockDim.x / 32;
-    for (int v = blockIdx.x * nwarps + warp; v < vocab; v += gridDim.x * nwarps) {
-        float acc[V][8];
-        bool any = false;
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
-        for (int base = 0; base < rows; base += 32) {
-            const int idx = base + lane;
-            unsigned mask = __ballot_sync(0xffffffffu, idx < rows && stok[idx] == v);
-            while (mask) {
-                const int r = base + __ffs(mask) - 1;
-                mask &= mask - 1;
-                any = true;
-#pragma unroll
-                for (int j = 0; j < V; ++j) {
-                    float f[8];
-                    load8(dx + static_cast<int64_t>(r) * H + j * 256 + lane * 8, f);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[j][i] += f[i];
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    const uint64_t a = keys[i], b = keys[ixj];
+                    if ((a > b) == up) {
+                        keys[i] = b;
+                        keys[ixj] = a;
+                    }
                 }
             }
+            __syncthreads();
         }
-        if (!any) continue;
+    }
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) order[i] = static_cast<int32_t>(keys[i] & 0xffffffffu);
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) embed_bwd_runs_kernel(const int32_t* __restrict__ tok,
+                                                             const int32_t* __restrict__ order,
+                                                             const __nv_bfloat16* __restrict__ dx,
+                                                             float* __restrict__ dwte, int rows) {
+    constexpr int H = V * 256;
+    const int slot = blockIdx.x * 8 + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (slot >= rows) return;
+    const int t0 = tok[order[slot]];
+    if (slot > 0 && tok[order[slot - 1]] == t0) return;  // not the start of a run
+    float acc[V][8];
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
+    for (int k = slot; k < rows && tok[order[k]] == t0; ++k) {
+        const int r = order[k];
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            float4* d = reinterpret_cast<float4*>(dwte + static_cast<int64_t>(v) * H + j * 256 + lane * 8);
-            float4 a = d[0], b = d[1];
-            a.x += acc[j][0];
-            a.y += acc[j][1];
-            a.z += acc[j][2];
-            a.w += acc[j][3];
-            b.x += acc[j][4];
-            b.y += acc[j][5];
-            b.z += acc[j][6];
-            b.w += acc[j][7];
-            d[0] = a;
-            d[1] = b;
+            float f[8];
+            load8(dx + static_cast<int64_t>(r) * H + j * 256 + lane * 8, f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[j][i] += f[i];
         }
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        float4* d = reinterpret_cast<float4*>(dwte + static_cast<int64_t>(t0) * H + j * 256 + lane * 8);
+        float4 a = d[0], b = d[1];
+        a.x += acc[j][0];
+        a.y += acc[j][1];
+        a.z += acc[j][2];
+        a.w += acc[j][3];
+        b.x += acc[j][4];
+        b.y += acc[j][5];
+        b.z += acc[j][6];
+        b.w += acc[j][7];
+        d[0] = a;
+        d[1] = b;
     }
 }
 
@@ -587,11 +608,14 @@ cudaError_t embedding_fwd(const int32_t* tok, const __nv_bfloat16* wte, const __
     return cudaPeekAtLastError();
 }
 
-cudaError_t embedding_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* dwte, float* dwpe, int rows, int seq,
-                          int h, int vocab, cudaStream_t st) {
-    if (h % 256 || h > 2048) return cudaErrorInvalidValue;
-    const size_t smem = static_cast<size_t>(rows) * sizeof(int32_t);
-    PTK_DISPATCH_V(h, (embed_bwd_wte_kernel<V><<<148 * 4, 256, smem, st>>>(tok, dx, dwte, rows, vocab)));
+cudaError_t embedding_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* dwte, float* dwpe, int32_t* order,
+                          int rows, int seq, int h, int vocab, cudaStream_t st) {
+    (void)vocab;
+    if (h % 256 || h > 4096 || rows > 8192) return cudaErrorInvalidValue;
+    int n = 1;
+    while (n < rows) n <<= 1;
+    embed_sort_kernel<<<1, 1024, static_cast<size_t>(n) * 8, st>>>(tok, order, rows);
+    PTK_DISPATCH_V(h, (embed_bwd_runs_kernel<V><<<(rows + 7) / 8, 256, 0, st>>>(tok, order, dx, dwte, rows)));
     dim3 grid((h + 255) / 256, seq);
     embed_bwd_wpe_kernel<<<grid, 256, 0, st>>>(dx, dwpe, seq, rows / seq, h);
     return cudaPeekAtLastError();

@@ -26,8 +26,9 @@ cudaError_t cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* l
                           int vocab, float grad_scale, float loss_scale, cudaStream_t st);
 cudaError_t embedding_fwd(const int32_t* tok, const __nv_bfloat16* wte, const __nv_bfloat16* wpe, __nv_bfloat16* x,
                           int rows, int seq, int h, cudaStream_t st);
-cudaError_t embedding_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* dwte, float* dwpe, int rows, int seq,
-                          int h, int vocab, cudaStream_t st);
+// order: int32 scratch [rows] (token-sorted positions).
+cudaError_t embedding_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* dwte, float* dwpe, int32_t* order,
+                          int rows, int seq, int h, int vocab, cudaStream_t st);
 cudaError_t adamw_step(float* w, float* g, float* m, float* v, __nv_bfloat16* wb, int64_t n, float lr, float b1,
                        float b2, float eps, float wd, int step, cudaStream_t st);
 cudaError_t init_normal(float* w, int64_t n, uint64_t seed, float std, float mean, cudaStream_t st);

@@ -4,6 +4,7 @@
 #include <string>
 
 #include "../../../include/ptk.h"
+#include "../kernels/attention_sm100.h"
 #include "../kernels/gemm_sm100.h"
 #include "errors.h"
 
@@ -15,5 +16,24 @@ extern "C" int ptk_gemm(const ptk_gemm_desc* desc, void* stream) {
     rc = ptk::gemm_run(plan, static_cast<cudaStream_t>(stream));
     if (rc != PTK_OK) return ptk::set_error(rc, std::string("ptk_gemm: launch failed: ") +
                                                      cudaGetErrorString(cudaGetLastError()));
+    return PTK_OK;
+}
+
+extern "C" int ptk_flash_forward(const void* qkv, void* o, float* lse, int b, int s, int H, int d, void* stream) {
+    ptk::FlashPlan p;
+    cudaError_t e = ptk::flash_prepare(qkv, o, lse, b, s, H, d, &p);
+    if (e != cudaSuccess) return ptk::set_error(PTK_ERR_ARG, "ptk_flash_forward: unsupported shape (d in {64,128}, s%128)");
+    e = ptk::flash_forward(p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return ptk::set_error(PTK_ERR_CUDA, std::string("ptk_flash_forward: ") + cudaGetErrorString(e));
+    return PTK_OK;
+}
+
+extern "C" int ptk_flash_backward(const void* qkv, const void* o, const void* dO, const float* lse, float* dsum,
+                                  void* dqkv, int b, int s, int H, int d, void* stream) {
+    ptk::FlashBwdPlan p;
+    cudaError_t e = ptk::flash_bwd_prepare(qkv, o, dO, lse, dsum, dqkv, b, s, H, d, &p);
+    if (e != cudaSuccess) return ptk::set_error(PTK_ERR_ARG, "ptk_flash_backward: unsupported shape");
+    e = ptk::flash_backward(p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return ptk::set_error(PTK_ERR_CUDA, std::string("ptk_flash_backward: ") + cudaGetErrorString(e));
     return PTK_OK;
 }

@@ -2,8 +2,8 @@
 //
 // Per layer forward (T = b*s tokens, h hidden, H heads, d = h/H):
 //   ln1 = LN(x)                          qkv = ln1·Wqkvᵀ + b           (tcgen05 GEMM)
-//   S = Q·Kᵀ (fp32, causal tiles)        P = softmax(S/√d) (bf16)
-//   o = P·V                              x_mid = o·Woᵀ + b + x        (residual in epilogue)
+//   o, lse = causal flash attention(qkv) (tcgen05, S/P never leave TMEM/smem)
+//   x_mid = o·Woᵀ + b + x                (residual in the GEMM epilogue)
 //   ln2 = LN(x_mid)                      pre = ln2·W1ᵀ + b, a = gelu(pre) (one epilogue)
 //   x_out = a·W2ᵀ + b + x_mid
 // Backward mirrors it; every weight gradient is a K = T GEMM accumulated in
@@ -141,7 +141,6 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
 
     // ---- activation stash
     const int64_t T = tokens();
-    const int64_t att = static_cast<int64_t>(c.micro_batch_size) * c.heads * c.seq * c.seq;
     stash_.assign(c.slots, std::vector<LayerStash>(L_));
     head_.resize(c.slots);
     for (int sl = 0; sl < c.slots; ++sl) {
@@ -159,7 +158,6 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
             s.x_in = (i == 0 && !c.has_embedding) ? nullptr : bf(T * h);  // layer 0 reads the stage input
             s.ln1 = bf(T * h);
             s.qkv = bf(T * 3 * h);
-            s.P = bf(att);
             s.attn_o = bf(T * h);
             s.x_mid = bf(T * h);
             s.ln2 = bf(T * h);
@@ -169,6 +167,7 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
             s.rstd1 = fl(T);
             s.mean2 = fl(T);
             s.rstd2 = fl(T);
+            s.lse = fl(static_cast<int64_t>(c.micro_batch_size) * c.heads * c.seq);
         }
         if (c.has_head) {
             HeadStash& hs = head_[sl];
@@ -185,8 +184,7 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
     // (layer_forward writes x_out of layer i into stash[i+1].x_in)
 
     // ---- scratch
-    S_ = static_cast<float*>(alloc(att * 4));
-    dS_ = static_cast<__nv_bfloat16*>(alloc(att * 2));
+    dsum_ = static_cast<float*>(alloc(static_cast<int64_t>(c.micro_batch_size) * c.heads * c.seq * 4));
     const int64_t wide = std::max<int64_t>(std::max<int64_t>(3 * h, f), h);
     g_a_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
     g_b_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
@@ -198,6 +196,7 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
     const int64_t parts = std::max(colsum_parts(static_cast<int>(T)), layernorm_bwd_parts(static_cast<int>(T)));
     red_ = static_cast<float*>(alloc(2 * parts * std::max<int64_t>(wide, V) * 4));
     loss_rows_ = static_cast<float*>(alloc(T * 4));
+    order_ = static_cast<int32_t*>(alloc(T * 4));
     loss_acc_ = static_cast<float*>(alloc(64));
     ck(cudaMemset(loss_acc_, 0, 64), "memset");
     ck(cudaDeviceSynchronize(), "stage init");
@@ -247,7 +246,6 @@ void GptStage::layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, _
     const LayerW& w = lw_[li];
     const int T = tokens(), h = c.hidden, f = c.ffn, H = c.heads, d = h / H, n = c.seq, b = c.micro_batch_size;
     const __nv_bfloat16* W = wbf_;
-    const int64_t ss = static_cast<int64_t>(n) * n;
 
     kl(1, layernorm_fwd(x_in, W + w.ln1_g, W + w.ln1_b, s.ln1, s.mean1, s.rstd1, T, h, 1e-5f, st), "ln1");
     {
@@ -255,24 +253,15 @@ void GptStage::layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, _
         g.bias = W + w.b_qkv;
         gemm(g, st);
     }
-    {  // S = Q Kᵀ per (head, sample), lower-triangular tiles only
-        ptk_gemm_desc g = desc(n, n, d, mat(s.qkv, 3 * h, 0, d, static_cast<int64_t>(n) * 3 * h),
-                               mat(s.qkv + h, 3 * h, 0, d, static_cast<int64_t>(n) * 3 * h),
-                               mat(S_, n, 0, ss, ss * H), PTK_EPI_F32);
-        g.batch[0] = H;
-        g.batch[1] = b;
-        g.causal = PTK_CAUSAL_TILES;
-        gemm(g, st);
-    }
-    kl(1, softmax_causal_fwd(S_, s.P, b * H * n, n, 1.f / std::sqrt(static_cast<float>(d)), st), "softmax");
-    {  // O = P V
-        ptk_gemm_desc g = desc(n, d, n, mat(s.P, n, 0, ss, ss * H),
-                               mat(s.qkv + 2 * h, 3 * h, 1, d, static_cast<int64_t>(n) * 3 * h),
-                               mat(s.attn_o, h, 0, d, static_cast<int64_t>(n) * h), PTK_EPI_BF16);
-        g.batch[0] = H;
-        g.batch[1] = b;
-        g.causal = PTK_CAUSAL_KHEAD;
-        gemm(g, st);
+    {  // fused causal attention (tcgen05): o = softmax(QKᵀ/√d) V, lse for the backward
+        const std::string key = std::to_string(reinterpret_cast<uintptr_t>(s.qkv)) + "." + std::to_string(b);
+        auto it = flash_fwd_.find(key);
+        if (it == flash_fwd_.end()) {
+            auto p = std::make_unique<FlashPlan>();
+            ck(flash_prepare(s.qkv, s.attn_o, s.lse, b, n, H, d, p.get()), "flash prepare");
+            it = flash_fwd_.emplace(key, std::move(p)).first;
+        }
+        kl(1, flash_forward(*it->second, st), "flash fwd");
     }
     {  // x_mid = o Woᵀ + b + x
         ptk_gemm_desc g = desc(T, h, h, mat(s.attn_o, h), mat(W + w.w_o, h), mat(s.x_mid, h), PTK_EPI_BF16);
@@ -301,9 +290,6 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
     const int T = tokens(), h = c.hidden, f = c.ffn, H = c.heads, d = h / H, n = c.seq, b = c.micro_batch_size;
     const __nv_bfloat16* W = wbf_;
     float* G = grad_;
-    const int64_t ss = static_cast<int64_t>(n) * n;
-    const int64_t qkv_bs = static_cast<int64_t>(n) * 3 * h;
-    const int64_t o_bs = static_cast<int64_t>(n) * h;
 
     // FC2: d_pre = (dy W2) * gelu'(pre); dW2 += dyᵀ a; db2 += Σ dy
     {
@@ -325,39 +311,16 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
     gemm(desc(T, h, h, mat(dx_mid_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
     gemm(desc(h, h, T, mat(dx_mid_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
     kl(2, colsum_accumulate(dx_mid_, G + w.b_o, red_, T, h, st), "dbo");
-    // attention
-    {  // dP = dO Vᵀ
-        ptk_gemm_desc g = desc(n, n, d, mat(d_attn_, h, 0, d, o_bs), mat(s.qkv + 2 * h, 3 * h, 0, d, qkv_bs),
-                               mat(S_, n, 0, ss, ss * H), PTK_EPI_F32);
-        g.batch[0] = H;
-        g.batch[1] = b;
-        g.causal = PTK_CAUSAL_TILES;
-        gemm(g, st);
-    }
-    kl(1, softmax_causal_bwd(s.P, S_, dS_, b * H * n, n, 1.f / std::sqrt(static_cast<float>(d)), st), "softmax bwd");
-    {  // dQ = dS K
-        ptk_gemm_desc g = desc(n, d, n, mat(dS_, n, 0, ss, ss * H), mat(s.qkv + h, 3 * h, 1, d, qkv_bs),
-                               mat(dqkv_, 3 * h, 0, d, qkv_bs), PTK_EPI_BF16);
-        g.batch[0] = H;
-        g.batch[1] = b;
-        g.causal = PTK_CAUSAL_KHEAD;
-        gemm(g, st);
-    }
-    {  // dK = dSᵀ Q
-        ptk_gemm_desc g = desc(n, d, n, mat(dS_, n, 1, ss, ss * H), mat(s.qkv, 3 * h, 1, d, qkv_bs),
-                               mat(dqkv_ + h, 3 * h, 0, d, qkv_bs), PTK_EPI_BF16);
-        g.batch[0] = H;
-        g.batch[1] = b;
-        g.causal = PTK_CAUSAL_KTAIL;
-        gemm(g, st);
-    }
-    {  // dV = Pᵀ dO
-        ptk_gemm_desc g = desc(n, d, n, mat(s.P, n, 1, ss, ss * H), mat(d_attn_, h, 1, d, o_bs),
-                               mat(dqkv_ + 2 * h, 3 * h, 0, d, qkv_bs), PTK_EPI_BF16);
-        g.batch[0] = H;
-        g.batch[1] = b;
-        g.causal = PTK_CAUSAL_KTAIL;
-        gemm(g, st);
+    // attention: dqkv = flash backward (dK/dV per key block, dQ per query block; deterministic)
+    {
+        const std::string key = std::to_string(reinterpret_cast<uintptr_t>(s.qkv)) + "." + std::to_string(b);
+        auto it = flash_bwd_.find(key);
+        if (it == flash_bwd_.end()) {
+            auto p = std::make_unique<FlashBwdPlan>();
+            ck(flash_bwd_prepare(s.qkv, s.attn_o, d_attn_, s.lse, dsum_, dqkv_, b, n, H, d, p.get()), "flash bwd prep");
+            it = flash_bwd_.emplace(key, std::move(p)).first;
+        }
+        kl(3, flash_backward(*it->second, st), "flash bwd");
     }
     // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv += Σ dqkv
     gemm(desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
@@ -423,7 +386,7 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
         g = out;
     }
     if (c.has_embedding) {
-        kl(2, embedding_bwd(tok, g, G + wte_, G + wpe_, T, c.seq, h, c.vocab, st), "embedding bwd");
+        kl(3, embedding_bwd(tok, g, G + wte_, G + wpe_, order_, T, c.seq, h, c.vocab, st), "embedding bwd");
     } else if (L_ == 0) {
         ck(cudaMemcpyAsync(dx, g, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, st), "copy");
     }

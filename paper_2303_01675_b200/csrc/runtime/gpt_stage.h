@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../../include/ptk.h"
+#include "../kernels/attention_sm100.h"
 #include "../kernels/gemm_sm100.h"
 
 namespace ptk {
@@ -88,8 +89,8 @@ class GptStage {
         int64_t ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_fc1, b_fc1, w_fc2, b_fc2;
     };
     struct LayerStash {
-        __nv_bfloat16 *x_in, *ln1, *qkv, *P, *attn_o, *x_mid, *ln2, *fc1_pre, *fc1_act;
-        float *mean1, *rstd1, *mean2, *rstd2;
+        __nv_bfloat16 *x_in, *ln1, *qkv, *attn_o, *x_mid, *ln2, *fc1_pre, *fc1_act;
+        float *mean1, *rstd1, *mean2, *rstd2, *lse;
     };
     struct HeadStash {
         __nv_bfloat16 *x_fin, *xf, *dlogits;
@@ -127,12 +128,15 @@ class GptStage {
     size_t stash_per_slot_ = 0;
 
     // scratch (one micro-batch in flight on the compute stream at a time)
-    float *S_ = nullptr, *red_ = nullptr, *loss_rows_ = nullptr, *loss_acc_ = nullptr;
-    __nv_bfloat16 *dS_ = nullptr, *g_a_ = nullptr, *g_b_ = nullptr, *d_pre_ = nullptr, *d_ln_ = nullptr,
+    int32_t* order_ = nullptr;
+    float *dsum_ = nullptr, *red_ = nullptr, *loss_rows_ = nullptr, *loss_acc_ = nullptr;
+    __nv_bfloat16 *g_a_ = nullptr, *g_b_ = nullptr, *d_pre_ = nullptr, *d_ln_ = nullptr,
                   *d_attn_ = nullptr, *dqkv_ = nullptr, *dx_mid_ = nullptr;
 
     std::vector<void*> allocs_;
     GemmCache cache_;
+    std::unordered_map<std::string, std::unique_ptr<FlashPlan>> flash_fwd_;
+    std::unordered_map<std::string, std::unique_ptr<FlashBwdPlan>> flash_bwd_;
     GemmTiming timing_;
 };
 

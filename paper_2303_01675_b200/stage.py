@@ -43,6 +43,26 @@ class ModelShape:
         return 3.0 * s * (l * per_tok_layer + 2 * h * V)
 
 
+    def param_count(self, n_layers: int, has_embedding: bool, has_head: bool) -> int:
+        h, V = self.hidden, self.vocab
+        n = n_layers * self.params_per_layer()
+        if has_embedding:
+            n += V * h + self.seq * h
+        if has_head:
+            n += V * h + 2 * h
+        return n
+
+    def stash_bytes_per_sample(self, n_layers: int, has_head: bool) -> int:
+        """Activation bytes one in-flight sample keeps on a stage until its backward
+        (mirrors GptStage's stash: bf16 activations, fp32 LN stats and attention lse)."""
+        s, h, f, H = self.seq, self.hidden, self.ffn, self.heads
+        per_layer = (5 * s * h + 3 * s * h + 2 * s * f) * 2 + 4 * s * 4 + H * s * 4
+        out = n_layers * per_layer
+        if has_head:
+            out += 2 * s * h * 2 + s * self.vocab * 2 + 2 * s * 4
+        return out
+
+
 GPT_1_3B = ModelShape(24, 2048, 32, 8192, 1024, 50304)
 GPT_6_7B = ModelShape(32, 4096, 32, 16384, 1024, 50304)
 TOY = ModelShape(4, 256, 4, 1024, 128, 512)
