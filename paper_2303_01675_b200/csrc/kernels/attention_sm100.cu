@@ -488,7 +488,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             issue_xy(0);
             for (int t = 0; t < nsteps; ++t) {
-                if (t + 1 < nsteps) issue_xy(t + 1);
+                // with two operand stages, score products of step t+1 overlap the
+                // elementwise work of step t; with one stage they must wait for
+                // step t's accumulating products to release the operands
+                if (S > 1 && t + 1 < nsteps) issue_xy(t + 1);
                 mbar_wait(pd_full, t & 1);
                 tc_fence_after();
                 const int st = S == 1 ? 0 : (t & 1);
@@ -513,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 mma_commit(acc_done);
                 mma_commit(&ld_empty[st]);
+                if (S == 1 && t + 1 < nsteps) issue_xy(t + 1);
             }
         }
     } else if (warp >= 4) {  // ---------------- elementwise warps: thread = row of the fixed block
