@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--retune", type=int, default=0, help="re-tune every N steps (0: once at start)")
     p.add_argument("--tuner-log", type=str, default="")
     p.add_argument("--contender", action="store_true", help="also launch competing NVLink traffic kernels")
-    p.add_argument("--model", choices=["1.3b", "6.7b"], default="1.3b")
+    p.add_argument("--model", choices=["1.3b", "6.7b", "bert-large"], default="1.3b")
     p.add_argument("--global-batch", type=int, default=GLOBAL_BATCH)
     p.add_argument("--micro-batch", type=int, default=MICRO_B)
     p.add_argument("--mem-cap-gb", type=float, default=0.0,
@@ -158,7 +158,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2303_01675_b200.executor import StageExecutor, max_inflight, partition_layers
-    from paper_2303_01675_b200.stage import GPT_1_3B, GPT_6_7B
+    from paper_2303_01675_b200.stage import BERT_LARGE, GPT_1_3B, GPT_6_7B
     from paper_2303_01675_b200.tuning import OnlineTuner, candidate_set, outgoing_links
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -177,10 +177,10 @@ def main():
         if world > 1:
             dist.barrier(group=group)
 
-    shape = GPT_6_7B if args.model == "6.7b" else GPT_1_3B
+    shape = {"6.7b": GPT_6_7B, "bert-large": BERT_LARGE}.get(args.model, GPT_1_3B)
     GB = args.global_batch
     S = world
-    layers = partition_layers(shape.n_layer, S)
+    layers = partition_layers(shape.n_layer, S, head_weight=2.3 if shape.arch == "bert" else 2.0)
     cap = args.mem_cap_gb * 1e9 if args.mem_cap_gb > 0 else None
     cands = candidate_set(shape, layers, S, GB, cap, fixed_b=args.micro_batch) if S > 1 else \
         [[1, args.micro_batch, GB // args.micro_batch]]
@@ -326,9 +326,10 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(T * 1e3 / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": (f"GPT-{args.model.upper()} training step" +
-                                (" (configs[1]: 24L h2048 32 heads s1024 V50304)" if args.model == "1.3b"
-                                 else " (configs[3]: 32L h4096 32 heads s1024 V50304)")),
+        "config": {"workload": {"1.3b": "GPT-1.3B training step (configs[1]: 24L h2048 32 heads s1024 V50304)",
+                                "6.7b": "GPT-6.7B training step (configs[3]: 32L h4096 32 heads s1024 V50304)",
+                                "bert-large": "BERT-large MLM training step (configs[4]: 24L h1024 16 heads s512 "
+                                              "V30528, post-LN, bidirectional)"}[args.model],
                    "global_batch": GB, "micro_batch": b, "micro_batches": M, "seq_len": shape.seq,
                    "candidates_kbM": cands, "memory_cap_gb": args.mem_cap_gb or None,
                    "stages": S, "layers_per_stage": [e - s_ for s_, e in layers],

@@ -77,13 +77,13 @@ typedef struct ptk_gemm_desc {
 
 int ptk_gemm(const ptk_gemm_desc* desc, void* stream);
 
-/* Fused causal attention forward: qkv bf16 [b][s][3][H][d] -> o bf16 [b*s][H*d],
+/* Fused attention forward (causal = 1: key <= query; 0: bidirectional): qkv bf16 [b][s][3][H][d] -> o bf16 [b*s][H*d],
  * lse fp32 [b][H][s] = log2(sum_k 2^(S_qk * log2(e)/sqrt(d))) (row max included). */
-int ptk_flash_forward(const void* qkv, void* o, float* lse, int b, int s, int H, int d, void* stream);
+int ptk_flash_forward(const void* qkv, void* o, float* lse, int b, int s, int H, int d, int causal, void* stream);
 /* Its backward: dqkv bf16 [b*s][3*H*d] (dQ | dK | dV sections) from qkv, o, dO = d(o),
  * lse; dsum: fp32 scratch [b][H][s].  Deterministic (no atomics). */
 int ptk_flash_backward(const void* qkv, const void* o, const void* dO, const float* lse, float* dsum, void* dqkv,
-                       int b, int s, int H, int d, void* stream);
+                       int b, int s, int H, int d, int causal, void* stream);
 
 /* ------------------------------------------------------------ planner
  * Mirrors pipetune::StageProfile / ModelSpec (proj/include/pipetune/model.hpp:30-51). */
@@ -137,6 +137,8 @@ typedef struct ptk_gpt_config {
     int micro_batch_size;  /* b */
     int slots;             /* activation-stash slots = max in-flight micro-batches */
     int micro_batches;     /* M: loss and gradients are the mean over M*b*seq tokens */
+    int arch;              /* 0: GPT (pre-LN, causal, LM head); 1: BERT (post-LN, bidirectional,
+                              embedding LayerNorm, MLM head = dense+GELU+LN+decoder over all positions) */
     uint64_t seed;
 } ptk_gpt_config;
 

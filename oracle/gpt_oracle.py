@@ -39,19 +39,39 @@ def layer_forward(x, w, p, heads):
     return x + u @ w[p + "w_fc2"].T + w[p + "b_fc2"]
 
 
+def bert_layer_forward(x, w, p, heads):
+    """One post-LN BERT block (bidirectional attention, tanh-GELU as in the GPU epilogue)."""
+    B, S, h = x.shape
+    d = h // heads
+    qkv = x @ w[p + "w_qkv"].T + w[p + "b_qkv"]
+    q, k, v = qkv.view(B, S, 3, heads, d).permute(2, 0, 3, 1, 4)
+    att = ((q @ k.transpose(-1, -2)) / math.sqrt(d)).softmax(-1)
+    o = (att @ v).transpose(1, 2).reshape(B, S, h)
+    x = F.layer_norm(x + o @ w[p + "w_o"].T + w[p + "b_o"], (h,), w[p + "ln1_g"], w[p + "ln1_b"], 1e-12)
+    u = F.gelu(x @ w[p + "w_fc1"].T + w[p + "b_fc1"], approximate="tanh")
+    return F.layer_norm(x + u @ w[p + "w_fc2"].T + w[p + "b_fc2"], (h,), w[p + "ln2_g"], w[p + "ln2_b"], 1e-12)
+
+
 def stage_forward(w, shape, layer_begin, layer_end, has_embedding, has_head, tok=None, x_in=None, labels=None,
                   micro_batches=1):
     """Returns (x_out or None, loss contribution or None)."""
+    bert = getattr(shape, "arch", "gpt") == "bert"
     if has_embedding:
         B, S = tok.shape
         x = w["wte"][tok] + w["wpe"][:S].unsqueeze(0)
+        if bert:
+            x = F.layer_norm(x, (shape.hidden,), w["lne_g"], w["lne_b"], 1e-12)
     else:
         x = x_in
     for l in range(layer_begin, layer_end):
-        x = layer_forward(x, w, f"h{l}.", shape.heads)
+        x = (bert_layer_forward if bert else layer_forward)(x, w, f"h{l}.", shape.heads)
     if not has_head:
         return x, None
-    xf = F.layer_norm(x, (shape.hidden,), w["lnf_g"], w["lnf_b"], 1e-5)
+    if bert:  # MLM head over all positions: dense + GELU + LN, then the decoder
+        t = F.gelu(x @ w["w_t"].T + w["b_t"], approximate="tanh")
+        xf = F.layer_norm(t, (shape.hidden,), w["lnf_g"], w["lnf_b"], 1e-12)
+    else:
+        xf = F.layer_norm(x, (shape.hidden,), w["lnf_g"], w["lnf_b"], 1e-5)
     logits = xf @ w["w_head"].T
     loss = F.cross_entropy(logits.reshape(-1, shape.vocab), labels.reshape(-1), reduction="sum")
     return None, loss / (labels.numel() * micro_batches)

@@ -45,6 +45,7 @@ struct FaArgs {
     float* lse;        // [b][H][s], log2 units of the scaled scores
     int s, H, h;
     float scale_log2;  // log2(e) / sqrt(d)
+    int causal;        // 1: GPT (key <= query), 0: bidirectional (BERT)
 };
 
 template <int D>
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nqb = a.s / kBlk;
     const int qb = nqb - 1 - static_cast<int>(blockIdx.x);  // heaviest blocks first
     const int head = blockIdx.y, bi = blockIdx.z;
-    const int nkv = qb + 1;
+    const int nkv = a.causal ? qb + 1 : nqb;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmQK);
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[st]);
             float mx = m;
-            const bool diag = j == qb;
+            const bool diag = a.causal && j == qb;
 #pragma unroll
             for (int c = 0; c < kBlk; ++c) {
                 x[c] = (diag && c > r) ? -INFINITY : x[c] * a.scale_log2;
@@ -303,7 +304,7 @@ cudaError_t launch_fwd(const FlashPlan& p, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    FaArgs a{p.o, p.lse, p.s, p.H, p.H * p.d, p.scale_log2};
+    FaArgs a{p.o, p.lse, p.s, p.H, p.H * p.d, p.scale_log2, p.causal};
     dim3 grid(p.s / kBlk, p.H, p.b);
     flash_fwd_kernel<D><<<grid, kThreads, C::kSmem, st>>>(p.tmQK, p.tmV, a);
     return cudaPeekAtLastError();
@@ -311,7 +312,8 @@ cudaError_t launch_fwd(const FlashPlan& p, cudaStream_t st) {
 
 }  // namespace
 
-cudaError_t flash_prepare(const void* qkv, void* o, float* lse, int b, int s, int H, int d, FlashPlan* p) {
+cudaError_t flash_prepare(const void* qkv, void* o, float* lse, int b, int s, int H, int d, FlashPlan* p,
+                          int causal) {
     if ((d != 64 && d != 128) || s % kBlk) return cudaErrorInvalidValue;
     cudaError_t e = qkv_map(&p->tmQK, qkv, b, s, H, d, kBlk);
     if (e != cudaSuccess) return e;
@@ -324,6 +326,7 @@ cudaError_t flash_prepare(const void* qkv, void* o, float* lse, int b, int s, in
     p->H = H;
     p->d = d;
     p->scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
+    p->causal = causal;
     return cudaSuccess;
 }
 
@@ -362,6 +365,7 @@ struct BwArgs {
     const float* dsum;    // [b][H][s]
     int s, H, h;
     float scale_log2, tau;
+    int causal;
 };
 
 __device__ __forceinline__ void st_bf16_swz(uint8_t* buf, int r, int c0, const float* v8) {
@@ -409,8 +413,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nb = a.s / kBlk;
     const int blk = KV ? static_cast<int>(blockIdx.x) : nb - 1 - static_cast<int>(blockIdx.x);
     const int head = blockIdx.y, bi = blockIdx.z;
-    const int first = KV ? blk : 0;
-    const int nsteps = KV ? nb - blk : blk + 1;
+    const int first = (KV && a.causal) ? blk : 0;
+    const int nsteps = !a.causal ? nb : (KV ? nb - blk : blk + 1);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmQKV);
@@ -542,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (t > 0) {
                 mbar_wait(acc_done, (t - 1) & 1);  // previous step's MMAs done reading sP / sDS
             }
-            const bool diag = other == blk;
+            const bool diag = a.causal && other == blk;
 #pragma unroll 1
             for (int c = 0; c < kBlk / 32; ++c) {
                 float x[32], y[32];
@@ -663,7 +667,8 @@ cudaError_t launch_bwd(const FlashBwdPlan& p, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    BwArgs a{p.dqkv, p.lse, p.dsum, p.s, p.H, p.H * p.d, p.scale_log2, 1.f / sqrtf(static_cast<float>(p.d))};
+    BwArgs a{p.dqkv, p.lse, p.dsum, p.s, p.H, p.H * p.d, p.scale_log2, 1.f / sqrtf(static_cast<float>(p.d)),
+             p.causal};
     dim3 grid(p.s / kBlk, p.H, p.b);
     flash_bwd_kernel<D, KV><<<grid, kThreads, C::kSmem, st>>>(p.tmQKV, p.tmDO, a);
     return cudaPeekAtLastError();
@@ -672,7 +677,7 @@ cudaError_t launch_bwd(const FlashBwdPlan& p, cudaStream_t st) {
 }  // namespace
 
 cudaError_t flash_bwd_prepare(const void* qkv, const void* o, const void* dO, const float* lse, float* dsum,
-                              void* dqkv, int b, int s, int H, int d, FlashBwdPlan* p) {
+                              void* dqkv, int b, int s, int H, int d, FlashBwdPlan* p, int causal) {
     if ((d != 64 && d != 128) || s % kBlk) return cudaErrorInvalidValue;
     cudaError_t e = qkv_map(&p->tmQKV, qkv, b, s, H, d, kBlk);
     if (e != cudaSuccess) return e;
@@ -688,6 +693,7 @@ cudaError_t flash_bwd_prepare(const void* qkv, const void* o, const void* dO, co
     p->H = H;
     p->d = d;
     p->scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
+    p->causal = causal;
     return cudaSuccess;
 }
 

@@ -14,10 +14,12 @@ struct FlashPlan {
     float* lse = nullptr;          // [b][H][s] (log2 units of scaled scores)
     int b = 0, s = 0, H = 0, d = 0;
     float scale_log2 = 0.f;
+    int causal = 1;
 };
 
 // qkv: bf16 [b][s][3][H][d] (the QKV projection output, row stride 3*H*d).
-cudaError_t flash_prepare(const void* qkv, void* o, float* lse, int b, int s, int H, int d, FlashPlan* p);
+cudaError_t flash_prepare(const void* qkv, void* o, float* lse, int b, int s, int H, int d, FlashPlan* p,
+                          int causal = 1);
 cudaError_t flash_forward(const FlashPlan& p, cudaStream_t st);
 
 struct FlashBwdPlan {
@@ -30,11 +32,12 @@ struct FlashBwdPlan {
     __nv_bfloat16* dqkv = nullptr;  // [b*s][3*H*d]
     int b = 0, s = 0, H = 0, d = 0;
     float scale_log2 = 0.f;
+    int causal = 1;
 };
 
 // dqkv (all three sections) from qkv, the forward output o, its gradient dO and lse.
 cudaError_t flash_bwd_prepare(const void* qkv, const void* o, const void* dO, const float* lse, float* dsum,
-                              void* dqkv, int b, int s, int H, int d, FlashBwdPlan* p);
+                              void* dqkv, int b, int s, int H, int d, FlashBwdPlan* p, int causal = 1);
 cudaError_t flash_backward(const FlashBwdPlan& p, cudaStream_t st);
 
 }  // namespace ptk

@@ -470,6 +470,29 @@ __global__ void embed_bwd_wpe_kernel(const __nv_bfloat16* __restrict__ dx, float
     dwpe[static_cast<int64_t>(p) * h + c] += s;
 }
 
+// --------------------------------------------------------------- GELU backward (elementwise)
+__device__ __forceinline__ float gelu_grad_tanh(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const float x2 = x * x;
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(k0 * (x + k1 * x * x2)));
+    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x2);
+}
+
+// out = dy * gelu'(pre)   (8 elements per thread)
+__global__ void dgelu_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ pre,
+                             __nv_bfloat16* __restrict__ out, int64_t n8) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float d[8], p[8];
+        load8(dy + i * 8, d);
+        load8(pre + i * 8, p);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) d[e] *= gelu_grad_tanh(p[e]);
+        store8(out + i * 8, d);
+    }
+}
+
 // --------------------------------------------------------------- optimizer / init
 __global__ void adamw_kernel(float* __restrict__ w, float* __restrict__ g, float* __restrict__ m,
                              float* __restrict__ v, __nv_bfloat16* __restrict__ wb, int64_t n, float lr, float b1,
@@ -618,6 +641,13 @@ cudaError_t embedding_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* dw
     PTK_DISPATCH_V(h, (embed_bwd_runs_kernel<V><<<(rows + 7) / 8, 256, 0, st>>>(tok, order, dx, dwte, rows)));
     dim3 grid((h + 255) / 256, seq);
     embed_bwd_wpe_kernel<<<grid, 256, 0, st>>>(dx, dwpe, seq, rows / seq, h);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t dgelu_mul(const __nv_bfloat16* dy, const __nv_bfloat16* pre, __nv_bfloat16* out, int64_t n,
+                      cudaStream_t st) {
+    if (n % 8) return cudaErrorInvalidValue;
+    dgelu_kernel<<<grid_for(n / 8, 256), 256, 0, st>>>(dy, pre, out, n / 8);
     return cudaPeekAtLastError();
 }
 

@@ -29,6 +29,9 @@ cudaError_t embedding_fwd(const int32_t* tok, const __nv_bfloat16* wte, const __
 // order: int32 scratch [rows] (token-sorted positions).
 cudaError_t embedding_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* dwte, float* dwpe, int32_t* order,
                           int rows, int seq, int h, int vocab, cudaStream_t st);
+// out = dy * gelu'(pre) (tanh form), n % 8 == 0
+cudaError_t dgelu_mul(const __nv_bfloat16* dy, const __nv_bfloat16* pre, __nv_bfloat16* out, int64_t n,
+                      cudaStream_t st);
 cudaError_t adamw_step(float* w, float* g, float* m, float* v, __nv_bfloat16* wb, int64_t n, float lr, float b1,
                        float b2, float eps, float wd, int step, cudaStream_t st);
 cudaError_t init_normal(float* w, int64_t n, uint64_t seed, float std, float mean, cudaStream_t st);

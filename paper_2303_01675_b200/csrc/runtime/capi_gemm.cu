@@ -19,9 +19,10 @@ extern "C" int ptk_gemm(const ptk_gemm_desc* desc, void* stream) {
     return PTK_OK;
 }
 
-extern "C" int ptk_flash_forward(const void* qkv, void* o, float* lse, int b, int s, int H, int d, void* stream) {
+extern "C" int ptk_flash_forward(const void* qkv, void* o, float* lse, int b, int s, int H, int d, int causal,
+                                 void* stream) {
     ptk::FlashPlan p;
-    cudaError_t e = ptk::flash_prepare(qkv, o, lse, b, s, H, d, &p);
+    cudaError_t e = ptk::flash_prepare(qkv, o, lse, b, s, H, d, &p, causal);
     if (e != cudaSuccess) return ptk::set_error(PTK_ERR_ARG, "ptk_flash_forward: unsupported shape (d in {64,128}, s%128)");
     e = ptk::flash_forward(p, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return ptk::set_error(PTK_ERR_CUDA, std::string("ptk_flash_forward: ") + cudaGetErrorString(e));
@@ -29,9 +30,9 @@ extern "C" int ptk_flash_forward(const void* qkv, void* o, float* lse, int b, in
 }
 
 extern "C" int ptk_flash_backward(const void* qkv, const void* o, const void* dO, const float* lse, float* dsum,
-                                  void* dqkv, int b, int s, int H, int d, void* stream) {
+                                  void* dqkv, int b, int s, int H, int d, int causal, void* stream) {
     ptk::FlashBwdPlan p;
-    cudaError_t e = ptk::flash_bwd_prepare(qkv, o, dO, lse, dsum, dqkv, b, s, H, d, &p);
+    cudaError_t e = ptk::flash_bwd_prepare(qkv, o, dO, lse, dsum, dqkv, b, s, H, d, &p, causal);
     if (e != cudaSuccess) return ptk::set_error(PTK_ERR_ARG, "ptk_flash_backward: unsupported shape");
     e = ptk::flash_backward(p, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return ptk::set_error(PTK_ERR_CUDA, std::string("ptk_flash_backward: ") + cudaGetErrorString(e));

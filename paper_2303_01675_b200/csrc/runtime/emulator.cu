@@ -77,18 +77,33 @@ __global__ void timer_kernel(int64_t* out) { *out = gtimer(); }
 
 // Contender: while the link is in a preempted segment (availability a < 1),
 // stream 16-byte stores to the peer for a (1-a) fraction of every 50 us.
+// Only thread 0 of each CTA polls the host-mapped stop flag and the trace
+// (once per burst) and broadcasts through shared memory, so the contender does
+// not flood PCIe with uncached reads.
 __global__ void contender_kernel(const DevTrace* tr, uint4* peer, size_t n16, const volatile int* stop) {
+    __shared__ int s_state;  // 0 off, 1 on, 2 stop
     const int64_t period = 50000;
     size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
     const uint4 v = make_uint4(0xdeadbeef, threadIdx.x, blockIdx.x, 0);
     for (;;) {
-        if (*stop) break;
-        const int64_t now = gtimer();
-        const double a = avail_at(tr, now);
-        const bool on = a < 1.0 && static_cast<double>(now % period) < (1.0 - a) * period;
-        if (!on) {
-            __nanosleep(5000);
+        if (threadIdx.x == 0) {
+            int st = 0;
+            if (*stop) {
+                st = 2;
+            } else {
+                const int64_t now = gtimer();
+                const double a = avail_at(tr, now);
+                st = (a < 1.0 && static_cast<double>(now % period) < (1.0 - a) * period) ? 1 : 0;
+            }
+            s_state = st;
+        }
+        __syncthreads();
+        const int st = s_state;
+        __syncthreads();
+        if (st == 2) break;
+        if (st == 0) {
+            __nanosleep(10000);
             continue;
         }
         for (int r = 0; r < 64; ++r) {
@@ -187,7 +202,7 @@ cudaError_t Emulator::start_contender(int slot, void* peer_scratch, size_t bytes
     }
     *stop_host_ = 0;
     std::atomic_thread_fence(std::memory_order_seq_cst);
-    contender_kernel<<<8, 256, 0, st>>>(dev_[slot], static_cast<uint4*>(peer_scratch), bytes / 16, stop_dev_);
+    contender_kernel<<<4, 128, 0, st>>>(dev_[slot], static_cast<uint4*>(peer_scratch), bytes / 16, stop_dev_);
     return cudaPeekAtLastError();
 }
 

@@ -89,6 +89,7 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
     const int h = c.hidden, f = c.ffn, V = c.vocab;
     if (h % 256 || c.heads <= 0 || h % c.heads || (h / c.heads) % 64 || c.seq % 128 || f % 64 || V % 64)
         throw std::invalid_argument("GptStage: unsupported shape (h%256, d%64, seq%128, ffn%64, vocab%64)");
+    if (c.arch != 0 && c.arch != 1) throw std::invalid_argument("GptStage: arch must be 0 (GPT) or 1 (BERT)");
     if (c.layer_begin < 0 || c.layer_end < c.layer_begin || c.layer_end > c.n_layer || c.slots < 1 ||
         c.micro_batch_size < 1 || c.micro_batches < 1)
         throw std::invalid_argument("GptStage: bad layer range / slots / batch");
@@ -102,6 +103,10 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
     if (c.has_embedding) {
         wte_ = add_param("wte", V, h, 0.02f, 0.f, base + 1);
         wpe_ = add_param("wpe", c.seq, h, 0.02f, 0.f, base + 2);
+        if (c.arch == 1) {
+            lne_g_ = add_param("lne_g", 1, h, 0.f, 1.f, base + 6);
+            lne_b_ = add_param("lne_b", 1, h, 0.f, 0.f, base + 7);
+        }
     }
     for (int i = 0; i < L_; ++i) {
         const int l = c.layer_begin + i;
@@ -123,6 +128,10 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
         lw_.push_back(w);
     }
     if (c.has_head) {
+        if (c.arch == 1) {
+            w_t_ = add_param("w_t", h, h, 0.02f, 0.f, base + 8);
+            b_t_ = add_param("b_t", 1, h, 0.f, 0.f, base + 9);
+        }
         lnf_g_ = add_param("lnf_g", 1, h, 0.f, 1.f, base + 3);
         lnf_b_ = add_param("lnf_b", 1, h, 0.f, 0.f, base + 4);
         w_head_ = add_param("w_head", V, h, 0.02f, 0.f, base + 5);
@@ -177,6 +186,20 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
             hs.meanf = static_cast<float*>(alloc(T * 4));
             hs.rstdf = static_cast<float*>(alloc(T * 4));
             bytes += T * h * 4 + T * V * 2 + T * 8;
+            hs.t_pre = hs.t_act = nullptr;
+            if (c.arch == 1) {
+                hs.t_pre = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+                hs.t_act = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+                bytes += T * h * 4;
+            }
+        }
+        if (c.has_embedding && c.arch == 1) {
+            EmbStash e;
+            e.sum = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+            e.mean = static_cast<float*>(alloc(T * 4));
+            e.rstd = static_cast<float*>(alloc(T * 4));
+            bytes += T * h * 2 + T * 8;
+            emb_.push_back(e);
         }
         stash_per_slot_ = bytes;
     }
@@ -193,6 +216,7 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
     d_attn_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
     dqkv_ = static_cast<__nv_bfloat16*>(alloc(T * 3 * h * 2));
     dx_mid_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+    dy_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
     const int64_t parts = std::max(colsum_parts(static_cast<int>(T)), layernorm_bwd_parts(static_cast<int>(T)));
     red_ = static_cast<float*>(alloc(2 * parts * std::max<int64_t>(wide, V) * 4));
     loss_rows_ = static_cast<float*>(alloc(T * 4));
@@ -240,6 +264,113 @@ void GptStage::gemm(ptk_gemm_desc d, cudaStream_t st) {
     if (gemm_run(p, st) != PTK_OK) throw std::runtime_error("gemm launch failed");
 }
 
+void GptStage::attention_forward(LayerStash& s, cudaStream_t st) {
+    // fused attention (tcgen05): o = softmax(QKᵀ/√d [causal for GPT]) V, lse for the backward
+    const ptk_gpt_config& c = cfg_;
+    const int b = c.micro_batch_size, d = c.hidden / c.heads;
+    const std::string key = std::to_string(reinterpret_cast<uintptr_t>(s.qkv)) + "." + std::to_string(b);
+    auto it = flash_fwd_.find(key);
+    if (it == flash_fwd_.end()) {
+        auto p = std::make_unique<FlashPlan>();
+        ck(flash_prepare(s.qkv, s.attn_o, s.lse, b, c.seq, c.heads, d, p.get(), bert() ? 0 : 1), "flash prepare");
+        it = flash_fwd_.emplace(key, std::move(p)).first;
+    }
+    kl(1, flash_forward(*it->second, st), "flash fwd");
+}
+
+void GptStage::attention_backward(LayerStash& s, cudaStream_t st) {
+    // dqkv = flash backward (dK/dV per key block, dQ per query block; deterministic)
+    const ptk_gpt_config& c = cfg_;
+    const int b = c.micro_batch_size, d = c.hidden / c.heads;
+    const std::string key = std::to_string(reinterpret_cast<uintptr_t>(s.qkv)) + "." + std::to_string(b);
+    auto it = flash_bwd_.find(key);
+    if (it == flash_bwd_.end()) {
+        auto p = std::make_unique<FlashBwdPlan>();
+        ck(flash_bwd_prepare(s.qkv, s.attn_o, d_attn_, s.lse, dsum_, dqkv_, b, c.seq, c.heads, d, p.get(),
+                             bert() ? 0 : 1),
+           "flash bwd prep");
+        it = flash_bwd_.emplace(key, std::move(p)).first;
+    }
+    kl(3, flash_backward(*it->second, st), "flash bwd");
+}
+
+void GptStage::bert_layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, __nv_bfloat16* x_out,
+                                  cudaStream_t st) {
+    // post-LN: y = x + attn(x); x_mid = LN1(y); z = x_mid + ffn(x_mid); x_out = LN2(z)
+    const ptk_gpt_config& c = cfg_;
+    const LayerW& w = lw_[li];
+    const int T = tokens(), h = c.hidden, f = c.ffn;
+    const __nv_bfloat16* W = wbf_;
+    {
+        ptk_gemm_desc g = desc(T, 3 * h, h, mat(x_in, h), mat(W + w.w_qkv, h), mat(s.qkv, 3 * h), PTK_EPI_BF16);
+        g.bias = W + w.b_qkv;
+        gemm(g, st);
+    }
+    attention_forward(s, st);
+    {
+        ptk_gemm_desc g = desc(T, h, h, mat(s.attn_o, h), mat(W + w.w_o, h), mat(s.ln1, h), PTK_EPI_BF16);
+        g.bias = W + w.b_o;
+        g.aux = mat(x_in, h);
+        gemm(g, st);
+    }
+    kl(1, layernorm_fwd(s.ln1, W + w.ln1_g, W + w.ln1_b, s.x_mid, s.mean1, s.rstd1, T, h, 1e-12f, st), "ln1");
+    {
+        ptk_gemm_desc g = desc(T, f, h, mat(s.x_mid, h), mat(W + w.w_fc1, h), mat(s.fc1_act, f), PTK_EPI_BIAS_GELU);
+        g.bias = W + w.b_fc1;
+        g.c2 = s.fc1_pre;
+        gemm(g, st);
+    }
+    {
+        ptk_gemm_desc g = desc(T, h, f, mat(s.fc1_act, f), mat(W + w.w_fc2, f), mat(s.ln2, h), PTK_EPI_BF16);
+        g.bias = W + w.b_fc2;
+        g.aux = mat(s.x_mid, h);
+        gemm(g, st);
+    }
+    kl(1, layernorm_fwd(s.ln2, W + w.ln2_g, W + w.ln2_b, x_out, s.mean2, s.rstd2, T, h, 1e-12f, st), "ln2");
+}
+
+void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __nv_bfloat16* dx,
+                                   cudaStream_t st) {
+    const ptk_gpt_config& c = cfg_;
+    const LayerW& w = lw_[li];
+    const int T = tokens(), h = c.hidden, f = c.ffn;
+    const __nv_bfloat16* W = wbf_;
+    float* G = grad_;
+    // dz = LN2'(dy)
+    kl(3, layernorm_bwd(dy, s.ln2, s.mean2, s.rstd2, W + w.ln2_g, nullptr, d_ln_, G + w.ln2_g, G + w.ln2_b, red_, T,
+                        h, st),
+       "ln2 bwd");
+    {  // d_pre = dz W2 * gelu'(pre)
+        ptk_gemm_desc g = desc(T, f, h, mat(d_ln_, h), mat(W + w.w_fc2, f, 1), mat(d_pre_, f), PTK_EPI_DGELU);
+        g.aux = mat(s.fc1_pre, f);
+        gemm(g, st);
+    }
+    gemm(desc(h, f, T, mat(d_ln_, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
+    kl(2, colsum_accumulate(d_ln_, G + w.b_fc2, red_, T, h, st), "db2");
+    {  // d_xmid = d_pre W1 + dz   (residual around the FFN)
+        ptk_gemm_desc g = desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(dx_mid_, h), PTK_EPI_BF16);
+        g.aux = mat(d_ln_, h);
+        gemm(g, st);
+    }
+    gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.x_mid, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
+    kl(2, colsum_accumulate(d_pre_, G + w.b_fc1, red_, T, f, st), "db1");
+    // dy_ = LN1'(d_xmid)
+    kl(3, layernorm_bwd(dx_mid_, s.ln1, s.mean1, s.rstd1, W + w.ln1_g, nullptr, dy_, G + w.ln1_g, G + w.ln1_b, red_,
+                        T, h, st),
+       "ln1 bwd");
+    gemm(desc(T, h, h, mat(dy_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
+    gemm(desc(h, h, T, mat(dy_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
+    kl(2, colsum_accumulate(dy_, G + w.b_o, red_, T, h, st), "dbo");
+    attention_backward(s, st);
+    gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.x_in, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
+    kl(2, colsum_accumulate(dqkv_, G + w.b_qkv, red_, T, 3 * h, st), "dbqkv");
+    {  // dx = dqkv Wqkv + dy_   (residual around attention)
+        ptk_gemm_desc g = desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(dx, h), PTK_EPI_BF16);
+        g.aux = mat(dy_, h);
+        gemm(g, st);
+    }
+}
+
 void GptStage::layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, __nv_bfloat16* x_out,
                              cudaStream_t st) {
     const ptk_gpt_config& c = cfg_;
@@ -253,16 +384,7 @@ void GptStage::layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, _
         g.bias = W + w.b_qkv;
         gemm(g, st);
     }
-    {  // fused causal attention (tcgen05): o = softmax(QKᵀ/√d) V, lse for the backward
-        const std::string key = std::to_string(reinterpret_cast<uintptr_t>(s.qkv)) + "." + std::to_string(b);
-        auto it = flash_fwd_.find(key);
-        if (it == flash_fwd_.end()) {
-            auto p = std::make_unique<FlashPlan>();
-            ck(flash_prepare(s.qkv, s.attn_o, s.lse, b, n, H, d, p.get()), "flash prepare");
-            it = flash_fwd_.emplace(key, std::move(p)).first;
-        }
-        kl(1, flash_forward(*it->second, st), "flash fwd");
-    }
+    attention_forward(s, st);
     {  // x_mid = o Woᵀ + b + x
         ptk_gemm_desc g = desc(T, h, h, mat(s.attn_o, h), mat(W + w.w_o, h), mat(s.x_mid, h), PTK_EPI_BF16);
         g.bias = W + w.b_o;
@@ -311,17 +433,7 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
     gemm(desc(T, h, h, mat(dx_mid_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
     gemm(desc(h, h, T, mat(dx_mid_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
     kl(2, colsum_accumulate(dx_mid_, G + w.b_o, red_, T, h, st), "dbo");
-    // attention: dqkv = flash backward (dK/dV per key block, dQ per query block; deterministic)
-    {
-        const std::string key = std::to_string(reinterpret_cast<uintptr_t>(s.qkv)) + "." + std::to_string(b);
-        auto it = flash_bwd_.find(key);
-        if (it == flash_bwd_.end()) {
-            auto p = std::make_unique<FlashBwdPlan>();
-            ck(flash_bwd_prepare(s.qkv, s.attn_o, d_attn_, s.lse, dsum_, dqkv_, b, n, H, d, p.get()), "flash bwd prep");
-            it = flash_bwd_.emplace(key, std::move(p)).first;
-        }
-        kl(3, flash_backward(*it->second, st), "flash bwd");
-    }
+    attention_backward(s, st);
     // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv += Σ dqkv
     gemm(desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
     gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
@@ -339,7 +451,13 @@ void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, 
     auto& S = stash_.at(static_cast<size_t>(slot));
     const __nv_bfloat16* W = wbf_;
     const __nv_bfloat16* cur = x_in;
-    if (c.has_embedding) {
+    if (c.has_embedding && bert()) {  // BERT: LN(wte[tok] + wpe[pos])
+        EmbStash& e = emb_[static_cast<size_t>(slot)];
+        kl(1, embedding_fwd(tok, W + wte_, W + wpe_, e.sum, T, c.seq, h, st), "embedding");
+        __nv_bfloat16* dst = L_ > 0 ? S[0].x_in : head_[slot].x_fin;
+        kl(1, layernorm_fwd(e.sum, W + lne_g_, W + lne_b_, dst, e.mean, e.rstd, T, h, 1e-12f, st), "emb ln");
+        cur = dst;
+    } else if (c.has_embedding) {
         kl(1, embedding_fwd(tok, W + wte_, W + wpe_, S[0].x_in, T, c.seq, h, st), "embedding");
         cur = S[0].x_in;
     } else if (L_ > 0) {
@@ -347,13 +465,25 @@ void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, 
     }
     for (int i = 0; i < L_; ++i) {
         __nv_bfloat16* out = (i + 1 < L_) ? S[i + 1].x_in : (c.has_head ? head_[slot].x_fin : x_out);
-        layer_forward(i, S[i], cur, out, st);
+        if (bert())
+            bert_layer_forward(i, S[i], cur, out, st);
+        else
+            layer_forward(i, S[i], cur, out, st);
         cur = out;
     }
     if (c.has_head) {
         HeadStash& hs = head_[slot];
-        if (L_ == 0) ck(cudaMemcpyAsync(hs.x_fin, cur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, st), "copy");
-        kl(1, layernorm_fwd(hs.x_fin, W + lnf_g_, W + lnf_b_, hs.xf, hs.meanf, hs.rstdf, T, h, 1e-5f, st), "lnf");
+        if (L_ == 0 && cur != hs.x_fin)
+            ck(cudaMemcpyAsync(hs.x_fin, cur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, st), "copy");
+        if (bert()) {  // MLM transform: t = gelu(x Wtᵀ + b), xf = LN(t)
+            ptk_gemm_desc g = desc(T, h, h, mat(hs.x_fin, h), mat(W + w_t_, h), mat(hs.t_act, h), PTK_EPI_BIAS_GELU);
+            g.bias = W + b_t_;
+            g.c2 = hs.t_pre;
+            gemm(g, st);
+            kl(1, layernorm_fwd(hs.t_act, W + lnf_g_, W + lnf_b_, hs.xf, hs.meanf, hs.rstdf, T, h, 1e-12f, st), "lnh");
+        } else {
+            kl(1, layernorm_fwd(hs.x_fin, W + lnf_g_, W + lnf_b_, hs.xf, hs.meanf, hs.rstdf, T, h, 1e-5f, st), "lnf");
+        }
         gemm(desc(T, c.vocab, h, mat(hs.xf, h), mat(W + w_head_, h), mat(hs.dlogits, c.vocab), PTK_EPI_BF16), st);
         const float scale = 1.f / (static_cast<float>(T) * c.micro_batches);
         kl(2, cross_entropy(hs.dlogits, labels, loss_rows_, loss_acc_, T, c.vocab, scale, scale, st), "xent");
@@ -375,15 +505,37 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
         gemm(desc(T, h, c.vocab, mat(hs.dlogits, c.vocab), mat(W + w_head_, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
         gemm(desc(c.vocab, h, T, mat(hs.dlogits, c.vocab, 1), mat(hs.xf, h, 1), mat(G + w_head_, h), PTK_EPI_ACC_F32),
              st);
-        kl(3, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, G + lnf_g_, G + lnf_b_, red_, T,
-                         h, st),
-           "lnf bwd");
+        if (bert()) {
+            // dt = LN_h'(dxf); d_tpre = dt * gelu'(t_pre); dx_fin = d_tpre Wt; dWt += d_tpreᵀ x_fin
+            kl(3, layernorm_bwd(d_ln_, hs.t_act, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, dx_mid_, G + lnf_g_,
+                                G + lnf_b_, red_, T, h, st),
+               "lnh bwd");
+            kl(1, dgelu_mul(dx_mid_, hs.t_pre, dy_, static_cast<int64_t>(T) * h, st), "dgelu");
+            gemm(desc(T, h, h, mat(dy_, h), mat(W + w_t_, h, 1), mat(g_a_, h), PTK_EPI_BF16), st);
+            gemm(desc(h, h, T, mat(dy_, h, 1), mat(hs.x_fin, h, 1), mat(G + w_t_, h), PTK_EPI_ACC_F32), st);
+            kl(2, colsum_accumulate(dy_, G + b_t_, red_, T, h, st), "dbt");
+        } else {
+            kl(3, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, G + lnf_g_, G + lnf_b_,
+                                red_, T, h, st),
+               "lnf bwd");
+        }
         g = g_a_;
     }
     for (int i = L_ - 1; i >= 0; --i) {
         __nv_bfloat16* out = (i == 0 && !c.has_embedding) ? dx : (g == g_a_ ? g_b_ : g_a_);
-        layer_backward(i, S[i], g, out, st);
+        if (bert())
+            bert_layer_backward(i, S[i], g, out, st);
+        else
+            layer_backward(i, S[i], g, out, st);
         g = out;
+    }
+    if (c.has_embedding && bert()) {  // through the embedding LayerNorm
+        EmbStash& e = emb_[static_cast<size_t>(slot)];
+        __nv_bfloat16* dsum_bf = (g == g_a_) ? g_b_ : g_a_;
+        kl(3, layernorm_bwd(g, e.sum, e.mean, e.rstd, W + lne_g_, nullptr, dsum_bf, G + lne_g_, G + lne_b_, red_, T, h,
+                            st),
+           "emb ln bwd");
+        g = dsum_bf;
     }
     if (c.has_embedding) {
         kl(3, embedding_bwd(tok, g, G + wte_, G + wpe_, order_, T, c.seq, h, c.vocab, st), "embedding bwd");

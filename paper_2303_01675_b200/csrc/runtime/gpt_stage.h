@@ -92,10 +92,23 @@ class GptStage {
         __nv_bfloat16 *x_in, *ln1, *qkv, *attn_o, *x_mid, *ln2, *fc1_pre, *fc1_act;
         float *mean1, *rstd1, *mean2, *rstd2, *lse;
     };
+    // GPT: ln1/ln2 hold the pre-LN outputs, x_mid the post-attention residual.
+    // BERT (post-LN): ln1 holds y = attn + x (pre-LN1), x_mid = LN1(y),
+    //                 ln2 holds z = ffn + x_mid (pre-LN2); the layer output is LN2(z).
     struct HeadStash {
         __nv_bfloat16 *x_fin, *xf, *dlogits;
         float *meanf, *rstdf;
+        __nv_bfloat16 *t_pre, *t_act;  // BERT MLM transform
     };
+    struct EmbStash {  // BERT: embedding sum before its LayerNorm
+        __nv_bfloat16* sum;
+        float *mean, *rstd;
+    };
+    bool bert() const { return cfg_.arch == 1; }
+    void bert_layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, __nv_bfloat16* x_out, cudaStream_t st);
+    void bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st);
+    void attention_forward(LayerStash& s, cudaStream_t st);
+    void attention_backward(LayerStash& s, cudaStream_t st);
 
     struct InitSpec {
         int64_t offset, numel;
@@ -118,6 +131,8 @@ class GptStage {
     std::vector<ParamInfo> params_;
     std::vector<LayerW> lw_;
     int64_t wte_ = -1, wpe_ = -1, lnf_g_ = -1, lnf_b_ = -1, w_head_ = -1;
+    int64_t lne_g_ = -1, lne_b_ = -1, w_t_ = -1, b_t_ = -1;  // BERT embedding LN, MLM transform
+    std::vector<EmbStash> emb_;
     int64_t total_ = 0;
     float *master_ = nullptr, *grad_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
     __nv_bfloat16* wbf_ = nullptr;
@@ -131,7 +146,7 @@ class GptStage {
     int32_t* order_ = nullptr;
     float *dsum_ = nullptr, *red_ = nullptr, *loss_rows_ = nullptr, *loss_acc_ = nullptr;
     __nv_bfloat16 *g_a_ = nullptr, *g_b_ = nullptr, *d_pre_ = nullptr, *d_ln_ = nullptr,
-                  *d_attn_ = nullptr, *dqkv_ = nullptr, *dx_mid_ = nullptr;
+                  *d_attn_ = nullptr, *dqkv_ = nullptr, *dx_mid_ = nullptr, *dy_ = nullptr;
 
     std::vector<void*> allocs_;
     GemmCache cache_;

@@ -86,7 +86,8 @@ class StageExecutor:
         _declare(self.lib)
         lb, le = layers if layers is not None else partition_layers(shape.n_layer, stages)[stage]
         gpt = GptConfig(shape.n_layer, shape.hidden, shape.heads, shape.ffn, shape.seq, shape.vocab, lb, le,
-                        int(stage == 0), int(stage == stages - 1), b_max, slots, global_batch // b_max, seed)
+                        int(stage == 0), int(stage == stages - 1), b_max, slots, global_batch // b_max,
+                        shape.arch_id, seed)
         self.cfg = ExecConfig(gpt, stage, stages, global_batch, lr, weight_decay, data_seed)
         self.shape, self.stage, self.stages, self.global_batch = shape, stage, stages, global_batch
         h = C.c_void_p()

@@ -19,7 +19,7 @@ class GptConfig(C.Structure):
         ("n_layer", C.c_int), ("hidden", C.c_int), ("heads", C.c_int), ("ffn", C.c_int), ("seq", C.c_int),
         ("vocab", C.c_int), ("layer_begin", C.c_int), ("layer_end", C.c_int), ("has_embedding", C.c_int),
         ("has_head", C.c_int), ("micro_batch_size", C.c_int), ("slots", C.c_int), ("micro_batches", C.c_int),
-        ("seed", C.c_uint64),
+        ("arch", C.c_int), ("seed", C.c_uint64),
     ]
 
 
@@ -31,6 +31,11 @@ class ModelShape:
     ffn: int
     seq: int
     vocab: int
+    arch: str = "gpt"  # "gpt": pre-LN causal + LM head; "bert": post-LN bidirectional + MLM head
+
+    @property
+    def arch_id(self) -> int:
+        return 1 if self.arch == "bert" else 0
 
     def params_per_layer(self) -> int:
         h, f = self.hidden, self.ffn
@@ -39,17 +44,19 @@ class ModelShape:
     def flops_per_sample(self) -> float:
         """Training FLOPs per sample (fwd + bwd = 3x fwd), causal attention at half."""
         h, f, s, l, V = self.hidden, self.ffn, self.seq, self.n_layer, self.vocab
-        per_tok_layer = 2 * (3 * h * h + h * h + 2 * h * f) + 2 * s * h  # GEMMs + QKᵀ/PV at causal half
-        return 3.0 * s * (l * per_tok_layer + 2 * h * V)
+        att = 2 * s * h if self.arch == "gpt" else 4 * s * h  # QKᵀ + PV, causal counted at half
+        per_tok_layer = 2 * (3 * h * h + h * h + 2 * h * f) + att
+        head = 2 * h * V + (2 * h * h if self.arch == "bert" else 0)  # BERT MLM transform
+        return 3.0 * s * (l * per_tok_layer + head)
 
 
     def param_count(self, n_layers: int, has_embedding: bool, has_head: bool) -> int:
         h, V = self.hidden, self.vocab
         n = n_layers * self.params_per_layer()
         if has_embedding:
-            n += V * h + self.seq * h
+            n += V * h + self.seq * h + (2 * h if self.arch == "bert" else 0)
         if has_head:
-            n += V * h + 2 * h
+            n += V * h + 2 * h + (h * h + h if self.arch == "bert" else 0)
         return n
 
     def stash_bytes_per_sample(self, n_layers: int, has_head: bool) -> int:
@@ -66,6 +73,8 @@ class ModelShape:
 GPT_1_3B = ModelShape(24, 2048, 32, 8192, 1024, 50304)
 GPT_6_7B = ModelShape(32, 4096, 32, 16384, 1024, 50304)
 TOY = ModelShape(4, 256, 4, 1024, 128, 512)
+BERT_LARGE = ModelShape(24, 1024, 16, 4096, 512, 30528, "bert")
+TOY_BERT = ModelShape(4, 256, 4, 1024, 128, 512, "bert")
 
 
 class _CAI:
@@ -114,7 +123,7 @@ class GptStage:
         self.shape = shape
         self.cfg = GptConfig(shape.n_layer, shape.hidden, shape.heads, shape.ffn, shape.seq, shape.vocab,
                              layer_begin, layer_end, int(has_embedding), int(has_head), micro_batch_size, slots,
-                             micro_batches, seed)
+                             micro_batches, shape.arch_id, seed)
         h = C.c_void_p()
         L.check(self.lib.ptk_stage_create(C.byref(self.cfg), C.byref(h)))
         self.h = h

@@ -11,49 +11,52 @@ from paper_2303_01675_b200 import _lib as L
 pytestmark = pytest.mark.gpu
 
 
-def _ref(qkv, b, s, H, d):
+def _ref(qkv, b, s, H, d, causal=1):
     q, k, v = qkv.float().view(b, s, 3, H, d).permute(2, 0, 3, 1, 4)
     att = (q @ k.transpose(-1, -2)) / math.sqrt(d)
-    mask = torch.ones(s, s, dtype=torch.bool, device=qkv.device).tril()
-    att = att.masked_fill(~mask, float("-inf"))
+    if causal:
+        mask = torch.ones(s, s, dtype=torch.bool, device=qkv.device).tril()
+        att = att.masked_fill(~mask, float("-inf"))
     lse2 = torch.logsumexp(att, -1) / math.log(2.0)
     o = att.softmax(-1) @ v
     return o.transpose(1, 2).reshape(b * s, H * d), lse2
 
 
+@pytest.mark.parametrize("causal", [1, 0])
 @pytest.mark.parametrize("b,s,H,d", [(1, 128, 1, 64), (2, 256, 2, 64), (2, 1024, 4, 64), (1, 512, 2, 128),
                                      (2, 1024, 32, 64)])
-def test_flash_forward(cuda, b, s, H, d):
+def test_flash_forward(cuda, b, s, H, d, causal):
     torch.manual_seed(b * 1000 + s + H + d)
     qkv = (torch.randn(b * s, 3 * H * d, device=cuda) * 1.5).bfloat16()
     o = torch.full((b * s, H * d), float("nan"), device=cuda, dtype=torch.bfloat16)
     lse = torch.full((b, H, s), float("nan"), device=cuda)
-    L.check(L.lib().ptk_flash_forward(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), b, s, H, d,
+    L.check(L.lib().ptk_flash_forward(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), b, s, H, d, causal,
                                       torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
-    ro, rl = _ref(qkv, b, s, H, d)
+    ro, rl = _ref(qkv, b, s, H, d, causal)
     err = (o.float() - ro).abs().max().item()
     assert err <= 2e-2 * ro.abs().max().item(), err
     assert (lse - rl).abs().max().item() <= 1e-2
 
 
+@pytest.mark.parametrize("causal", [1, 0])
 @pytest.mark.parametrize("b,s,H,d", [(1, 128, 1, 64), (2, 256, 2, 64), (2, 1024, 4, 64), (1, 512, 2, 128),
                                      (2, 1024, 32, 64)])
-def test_flash_backward(cuda, b, s, H, d):
+def test_flash_backward(cuda, b, s, H, d, causal):
     torch.manual_seed(7 + b + s + H + d)
     qkv = (torch.randn(b * s, 3 * H * d, device=cuda) * 1.5).bfloat16()
     o = torch.empty((b * s, H * d), device=cuda, dtype=torch.bfloat16)
     lse = torch.empty((b, H, s), device=cuda)
     st = torch.cuda.current_stream().cuda_stream
-    L.check(L.lib().ptk_flash_forward(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), b, s, H, d, st))
+    L.check(L.lib().ptk_flash_forward(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), b, s, H, d, causal, st))
     dO = torch.randn(b * s, H * d, device=cuda).bfloat16()
     dsum = torch.empty((b, H, s), device=cuda)
     dqkv = torch.full_like(qkv, float("nan"))
     L.check(L.lib().ptk_flash_backward(qkv.data_ptr(), o.data_ptr(), dO.data_ptr(), lse.data_ptr(), dsum.data_ptr(),
-                                       dqkv.data_ptr(), b, s, H, d, st))
+                                       dqkv.data_ptr(), b, s, H, d, causal, st))
     torch.cuda.synchronize()
     x = qkv.float().requires_grad_(True)
-    ro, _ = _ref(x, b, s, H, d)
+    ro, _ = _ref(x, b, s, H, d, causal)
     ro.backward(dO.float())
     ref = x.grad
     for sec in range(3):  # dQ, dK, dV sections
@@ -72,12 +75,12 @@ def test_flash_backward_deterministic(cuda):
     dO = torch.randn(b * s, H * d, device=cuda).bfloat16()
     dsum = torch.empty((b, H, s), device=cuda)
     st = torch.cuda.current_stream().cuda_stream
-    L.check(L.lib().ptk_flash_forward(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), b, s, H, d, st))
+    L.check(L.lib().ptk_flash_forward(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), b, s, H, d, 1, st))
     outs = []
     for _ in range(2):
         g = torch.empty_like(qkv)
         L.check(L.lib().ptk_flash_backward(qkv.data_ptr(), o.data_ptr(), dO.data_ptr(), lse.data_ptr(),
-                                           dsum.data_ptr(), g.data_ptr(), b, s, H, d, st))
+                                           dsum.data_ptr(), g.data_ptr(), b, s, H, d, 1, st))
         outs.append(g)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])

@@ -16,7 +16,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from oracle import gpt_oracle as G  # noqa: E402
-from paper_2303_01675_b200.stage import TOY, GptStage, ModelShape  # noqa: E402
+from paper_2303_01675_b200.stage import TOY, TOY_BERT, GptStage, ModelShape  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -47,28 +47,30 @@ def _oracle_grads(stage: GptStage, shape, batches, micro_batches, device="cpu"):
     return total, {n: t.grad.detach().cpu() for n, t in w.items()}
 
 
-def test_toy_single_stage_matches_oracle(cuda):
+@pytest.mark.parametrize("shape", [TOY, TOY_BERT], ids=["gpt", "bert"])
+def test_toy_single_stage_matches_oracle(cuda, shape):
     b, M = 2, 2
-    st = GptStage(TOY, 0, TOY.n_layer, True, True, b, slots=1, micro_batches=M)
-    batches = _batches(TOY, b, M)
+    st = GptStage(shape, 0, shape.n_layer, True, True, b, slots=1, micro_batches=M)
+    batches = _batches(shape, b, M)
     st.loss.zero_()
     for tok, lab, _, _ in batches:
         st.forward(0, tok=tok, labels=lab)
         st.backward(0, tok=tok)
     torch.cuda.synchronize()
-    loss_ref, grads_ref = _oracle_grads(st, TOY, batches, M)
+    loss_ref, grads_ref = _oracle_grads(st, shape, batches, M)
     loss = st.loss.item()
     assert abs(loss - loss_ref) <= LOSS_TOL * abs(loss_ref), (loss, loss_ref)
     worst = max((_rel(st.param(n, "grads").cpu(), grads_ref[n]), n) for n in st.params)
     assert worst[0] <= GRAD_TOL, worst
 
 
-def test_two_stage_split_bit_identical(cuda):
+@pytest.mark.parametrize("shape", [TOY, TOY_BERT], ids=["gpt", "bert"])
+def test_two_stage_split_bit_identical(cuda, shape):
     b, M = 2, 2
-    full = GptStage(TOY, 0, 4, True, True, b, slots=1, micro_batches=M)
-    s0 = GptStage(TOY, 0, 2, True, False, b, slots=1, micro_batches=M)
-    s1 = GptStage(TOY, 2, 4, False, True, b, slots=1, micro_batches=M)
-    batches = _batches(TOY, b, M, seed=7)
+    full = GptStage(shape, 0, 4, True, True, b, slots=1, micro_batches=M)
+    s0 = GptStage(shape, 0, 2, True, False, b, slots=1, micro_batches=M)
+    s1 = GptStage(shape, 2, 4, False, True, b, slots=1, micro_batches=M)
+    batches = _batches(shape, b, M, seed=7)
     T, h = b * TOY.seq, TOY.hidden
     act = torch.empty(T, h, dtype=torch.bfloat16, device="cuda")
     grad = torch.empty(T, h, dtype=torch.bfloat16, device="cuda")
