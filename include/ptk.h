@@ -73,6 +73,7 @@ typedef struct ptk_gemm_desc {
     int epilogue;
     int causal;
     int bn_hint;       /* 0 = auto, else 64 / 128 / 256 */
+    int multicast;     /* 1: allow the 2-CTA cluster B-multicast variant (dense, BN=256) */
 } ptk_gemm_desc;
 
 int ptk_gemm(const ptk_gemm_desc* desc, void* stream);

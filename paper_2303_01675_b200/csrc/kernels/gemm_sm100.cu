@@ -106,12 +106,19 @@ struct TileCoord {
     int z1, z2, m0, n0, kb0, kb1;
 };
 
-__device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t) {
+// MC: a 2-CTA cluster owns a pair of m-tiles sharing one n-tile; t indexes
+// pairs and `rank` picks the CTA's half of the pair.
+template <bool MC>
+__device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t, int rank) {
     TileCoord c;
     const int z = t / a.tiles_per_batch;
     int r = t - z * a.tiles_per_batch;
     int mb, nb;
-    if (a.causal == PTK_CAUSAL_TILES) {
+    if (MC) {
+        const int mpairs = (a.tiles_m + 1) / 2;
+        nb = r / mpairs;
+        mb = 2 * (r - nb * mpairs) + rank;
+    } else if (a.causal == PTK_CAUSAL_TILES) {
         // r enumerates the lower triangle row by row: row i holds i+1 tiles.
         mb = static_cast<int>((sqrtf(8.f * r + 1.f) - 1.f) * 0.5f);
         while ((mb + 1) * (mb + 2) / 2 <= r) ++mb;
@@ -137,7 +144,7 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t) {
     return c;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmArgs args) {
@@ -156,13 +163,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
+    const int rank = MC ? static_cast<int>(cluster_ctarank()) : 0;
+    const int t_begin = MC ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+    const int t_step = MC ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            mbar_init(&empty[i], MC ? 2 : 1);  // MC: both CTAs must release a stage (B is shared)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
@@ -173,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
     tc_fence_before();
     __syncthreads();
+    if (MC) cluster_sync();  // peer barriers initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -181,8 +192,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ---------------- TMA producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
-                const TileCoord tc = decode_tile(args, t);
+            for (int t = t_begin; t < args.num_tiles; t += t_step) {
+                const TileCoord tc = decode_tile<MC>(args, t, rank);
                 for (int kb = tc.kb0; kb < tc.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
@@ -196,7 +207,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < kBM / 64; ++j)
                             tma_load_4d(&tmA, &full[stage], sa + j * 64 * kBK * 2, tc.m0 + 64 * j, k0, tc.z1, tc.z2);
                     }
-                    if (!B_MN) {
+                    if (MC) {
+                        // this CTA fetches its half of the shared B tile into both CTAs
+                        if (!B_MN) {
+                            tma_load_4d_mc(&tmB, &full[stage], sb + rank * (BN / 2) * 128, k0, tc.n0 + rank * (BN / 2),
+                                           tc.z1, tc.z2, 0x3);
+                        } else {
+#pragma unroll
+                            for (int j = rank * (BN / 128); j < (rank + 1) * (BN / 128); ++j)
+                                tma_load_4d_mc(&tmB, &full[stage], sb + j * 64 * kBK * 2, tc.n0 + 64 * j, k0, tc.z1,
+                                               tc.z2, 0x3);
+                        }
+                    } else if (!B_MN) {
                         tma_load_4d(&tmB, &full[stage], sb, k0, tc.n0, tc.z1, tc.z2);
                     } else {
 #pragma unroll
@@ -217,8 +239,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
-                const TileCoord tc = decode_tile(args, t);
+            for (int t = t_begin; t < args.num_tiles; t += t_step) {
+                const TileCoord tc = decode_tile<MC>(args, t, rank);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -237,7 +259,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  : make_sw128_desc(b_base + k * 32, 16, 1024);
                         mma_bf16_ss(d_tmem, da, db, kIdesc, (kb > tc.kb0 || k > 0) ? 1u : 0u);
                     }
-                    mma_commit(&empty[stage]);
+                    if (MC)
+                        mma_commit_mc(&empty[stage], 0x3);  // release the stage in both CTAs
+                    else
+                        mma_commit(&empty[stage]);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -261,8 +286,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool f32_out = args.epi == PTK_EPI_F32 || args.epi == PTK_EPI_ACC_F32;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
-            const TileCoord tc = decode_tile(args, t);
+        for (int t = t_begin; t < args.num_tiles; t += t_step) {
+            const TileCoord tc = decode_tile<MC>(args, t, rank);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int64_t zoff_c = tc.z1 * args.c_bs1 + tc.z2 * args.c_bs2;
@@ -360,6 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (MC) cluster_sync();  // no CTA leaves while its peer may still signal it
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<C::kTmemCols>(tmem_base);
@@ -408,26 +434,42 @@ int encode_operand(CUtensorMap* map, const ptk_matrix& m, int contig_extent, int
     return r == CUDA_SUCCESS ? PTK_OK : PTK_ERR_CUDA;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool MC>
 int launch_impl(const GemmPlan& p, cudaStream_t stream) {
     using C = Cfg<BN>;
     static bool attr_set = false;
+    auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, MC>;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(gemm_bf16_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 C::kSmemBytes) != cudaSuccess)
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
             return PTK_ERR_CUDA;
         attr_set = true;
     }
-    gemm_bf16_kernel<BN, A_MN, B_MN><<<p.grid, kThreads, C::kSmemBytes, stream>>>(p.tmA, p.tmB, p.args);
+    if (!MC) {
+        kern<<<p.grid, kThreads, C::kSmemBytes, stream>>>(p.tmA, p.tmB, p.args);
+    } else {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(p.grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = C::kSmemBytes;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.args) != cudaSuccess) return PTK_ERR_CUDA;
+    }
     return cudaPeekAtLastError() == cudaSuccess ? PTK_OK : PTK_ERR_CUDA;
 }
 
-template <int BN>
+template <int BN, bool MC>
 GemmPlan::Launcher pick(bool a_mn, bool b_mn) {
-    if (!a_mn && !b_mn) return &launch_impl<BN, false, false>;
-    if (!a_mn && b_mn) return &launch_impl<BN, false, true>;
-    if (a_mn && !b_mn) return &launch_impl<BN, true, false>;
-    return &launch_impl<BN, true, true>;
+    if (!a_mn && !b_mn) return &launch_impl<BN, false, false, MC>;
+    if (!a_mn && b_mn) return &launch_impl<BN, false, true, MC>;
+    if (a_mn && !b_mn) return &launch_impl<BN, true, false, MC>;
+    return &launch_impl<BN, true, true, MC>;
 }
 
 int num_sms() {
@@ -478,9 +520,10 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     else
         rc = encode_operand(&p.tmA, d.a, d.m, d.k, kBK, b1, b2);
     if (rc != PTK_OK) return rc;
-    // B: logical [N][K]
+    // B: logical [N][K]; with multicast each CTA of the pair fetches half the K-major rows
+    const bool mc_pre = d.causal == PTK_CAUSAL_NONE && bn == 256 && tiles_m >= 2 && d.multicast != 0 && !d.b.mn_major;
     if (!d.b.mn_major)
-        rc = encode_operand(&p.tmB, d.b, d.k, d.n, bn, b1, b2);
+        rc = encode_operand(&p.tmB, d.b, d.k, d.n, mc_pre ? bn / 2 : bn, b1, b2);
     else
         rc = encode_operand(&p.tmB, d.b, d.n, d.k, kBK, b1, b2);
     if (rc != PTK_OK) return rc;
@@ -511,14 +554,26 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
         return PTK_ERR_ARG;
 
     const int sms = num_sms();
-    p.grid = a.num_tiles < sms ? a.num_tiles : sms;
+    // B-tile multicast across a 2-CTA cluster halves the L2 -> SM operand
+    // traffic per FLOP (dense, non-causal GEMMs with at least two m-tiles).
+    const bool mc = mc_pre;
     p.flops = 2.0 * d.m * static_cast<double>(d.n) * d.k * b1 * b2;
     if (d.causal != PTK_CAUSAL_NONE) p.flops *= 0.5;
-    switch (bn) {
-        case 64: p.launch = pick<64>(d.a.mn_major, d.b.mn_major); break;
-        case 128: p.launch = pick<128>(d.a.mn_major, d.b.mn_major); break;
-        default: p.launch = pick<256>(d.a.mn_major, d.b.mn_major); break;
+    if (mc) {
+        a.tiles_per_batch = ((tiles_m + 1) / 2) * a.tiles_n;
+        a.num_tiles = a.tiles_per_batch * b1 * b2;
+        const int clusters = a.num_tiles < sms / 2 ? a.num_tiles : sms / 2;
+        p.grid = 2 * clusters;
+        p.launch = pick<256, true>(d.a.mn_major, d.b.mn_major);
+    } else {
+        p.grid = a.num_tiles < sms ? a.num_tiles : sms;
+        switch (bn) {
+            case 64: p.launch = pick<64, false>(d.a.mn_major, d.b.mn_major); break;
+            case 128: p.launch = pick<128, false>(d.a.mn_major, d.b.mn_major); break;
+            default: p.launch = pick<256, false>(d.a.mn_major, d.b.mn_major); break;
+        }
     }
+    p.multicast = mc;
     *out = p;
     return PTK_OK;
 }

@@ -29,6 +29,7 @@ struct GemmPlan {
     GemmArgs args;
     int grid = 0;
     double flops = 0.0;  // algorithmic FLOPs of one launch
+    bool multicast = false;
     Launcher launch = nullptr;
 };
 

@@ -9,6 +9,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2303_01675_b200 import _lib as L  # noqa: E402
 
 
+MC = int(__import__("os").environ.get("PTK_MC", "1"))
+
+
 def gemm_desc(m, n, k, A, a_mn, B, b_mn, Cm, epi):
     d = L.GemmDesc()
     d.m, d.n, d.k = m, n, k
@@ -18,6 +21,7 @@ def gemm_desc(m, n, k, A, a_mn, B, b_mn, Cm, epi):
     d.c = L.matrix(Cm.data_ptr(), n)
     d.aux = L.matrix(0, 0)
     d.epilogue = epi
+    d.multicast = MC
     return d
 
 

@@ -23,7 +23,7 @@ def _run(desc):
     L.check(L.lib().ptk_gemm(desc, torch.cuda.current_stream().cuda_stream))
 
 
-def _desc(m, n, k, a, b, c, epi=L.EPI_BF16, bias=None, aux=None, c2=None, causal=0, batch=(1, 1), bn=0):
+def _desc(m, n, k, a, b, c, epi=L.EPI_BF16, bias=None, aux=None, c2=None, causal=0, batch=(1, 1), bn=0, mc=0):
     d = L.GemmDesc()
     d.m, d.n, d.k = m, n, k
     d.batch[0], d.batch[1] = batch
@@ -31,7 +31,7 @@ def _desc(m, n, k, a, b, c, epi=L.EPI_BF16, bias=None, aux=None, c2=None, causal
     d.aux = aux if aux is not None else L.matrix(0, 0)
     d.c2 = c2 or 0
     d.bias = bias or 0
-    d.epilogue, d.causal, d.bn_hint = epi, causal, bn
+    d.epilogue, d.causal, d.bn_hint, d.multicast = epi, causal, bn, mc
     return d
 
 
@@ -42,9 +42,9 @@ def _close(out, ref, tol=1.5e-2):
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("shape", [(128, 64, 64), (300, 520, 200), (256, 384, 1024)])
-@pytest.mark.parametrize("bn", [0, 64, 128, 256])
-def test_gemm_majors(cuda, a_mn, b_mn, shape, bn):
+@pytest.mark.parametrize("shape", [(128, 64, 64), (300, 520, 200), (256, 384, 1024), (640, 768, 320)])
+@pytest.mark.parametrize("bn,mc", [(0, 0), (64, 0), (128, 0), (256, 0), (256, 1)])
+def test_gemm_majors(cuda, a_mn, b_mn, shape, bn, mc):
     m, n, k = shape
     if a_mn and m % 8:
         m += 8 - m % 8
@@ -56,7 +56,7 @@ def test_gemm_majors(cuda, a_mn, b_mn, shape, bn):
     Bs = (B.T.contiguous() if b_mn else B).to(cuda)
     Cd = torch.zeros(m, n, dtype=torch.bfloat16, device=cuda)
     d = _desc(m, n, k, L.matrix(As.data_ptr(), m if a_mn else k, a_mn),
-              L.matrix(Bs.data_ptr(), n if b_mn else k, b_mn), L.matrix(Cd.data_ptr(), n), bn=bn)
+              L.matrix(Bs.data_ptr(), n if b_mn else k, b_mn), L.matrix(Cd.data_ptr(), n), bn=bn, mc=mc)
     _run(d)
     torch.cuda.synchronize()
     _close(Cd, ref)
@@ -166,7 +166,7 @@ def test_gemm_large_dense(cuda):
     A = (torch.randn(m, k) * 0.5).bfloat16().to(cuda)
     B = (torch.randn(n, k) * 0.02).bfloat16().to(cuda)
     C = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
-    _run(_desc(m, n, k, L.matrix(A.data_ptr(), k), L.matrix(B.data_ptr(), k), L.matrix(C.data_ptr(), n)))
+    _run(_desc(m, n, k, L.matrix(A.data_ptr(), k), L.matrix(B.data_ptr(), k), L.matrix(C.data_ptr(), n), mc=1))
     ref = (A.float() @ B.float().T)  # fp32 on the GPU (TF32 disabled by default for matmul)
     torch.cuda.synchronize()
     err = (C.float() - ref).abs().max().item()
