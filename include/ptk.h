@@ -73,7 +73,8 @@ typedef struct ptk_gemm_desc {
     int epilogue;
     int causal;
     int bn_hint;       /* 0 = auto, else 64 / 128 / 256 */
-    int multicast;     /* 1: allow the 2-CTA cluster B-multicast variant (dense, BN=256) */
+    int multicast;     /* dense BN=256 only: 1 = 2-CTA cluster with B-tile multicast (K-major B);
+                          2 = CTA-pair tcgen05.mma.cta_group::2 (256x256 pair tile) */
 } ptk_gemm_desc;
 
 int ptk_gemm(const ptk_gemm_desc* desc, void* stream);

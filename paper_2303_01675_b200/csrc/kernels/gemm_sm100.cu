@@ -144,6 +144,98 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t, int r
     return c;
 }
 
+// Epilogue of one accumulator tile held in TMEM columns [tmem_col, tmem_col + BN)
+// of lane quadrant `quad`; this warp handles the 32-column chunks c = half, half+2, ...
+template <int BN>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& args, const TileCoord& tc, uint32_t tmem_col, int quad,
+                                              int half, uint32_t lane, float4* stage_buf) {
+    const int q = static_cast<int>(lane & 7);
+    const int r0 = static_cast<int>(lane >> 3);
+    const bool f32_out = args.epi == PTK_EPI_F32 || args.epi == PTK_EPI_ACC_F32;
+    const int64_t zoff_c = tc.z1 * args.c_bs1 + tc.z2 * args.c_bs2;
+    const int64_t zoff_x = tc.z1 * args.aux_bs1 + tc.z2 * args.aux_bs2;
+    const int row_base = tc.m0 + quad * 32;
+#pragma unroll 1
+    for (int c = half; c < BN / 32; c += 2) {
+        float v[32];
+        __syncwarp();
+        tmem_ld_32x32b_x32(tmem_col + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(c * 32),
+                           v);
+        if (f32_out) {
+            // fp32 output: transpose through smem so each warp store covers
+            // 4 rows x 128 contiguous bytes; all loads issued before stores.
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                stage_buf[lane * 8 + (j ^ (lane & 7))] =
+                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            __syncwarp();
+            const int gn = tc.n0 + c * 32 + q * 4;
+            if (gn < args.N) {
+                float* cbase = static_cast<float*>(args.C) + zoff_c + gn;
+                float4 prev[8];
+                if (args.epi == PTK_EPI_ACC_F32) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int gm = row_base + r0 + 4 * i;
+                        prev[i] = gm < args.M ? *reinterpret_cast<const float4*>(cbase + static_cast<int64_t>(gm) * args.ldc)
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) prev[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int r = r0 + 4 * i;
+                    const int gm = row_base + r;
+                    const float4 a4 = stage_buf[r * 8 + (q ^ (r & 7))];
+                    if (gm < args.M)
+                        *reinterpret_cast<float4*>(cbase + static_cast<int64_t>(gm) * args.ldc) =
+                            make_float4(prev[i].x + a4.x, prev[i].y + a4.y, prev[i].z + a4.z, prev[i].w + a4.w);
+                }
+            }
+            continue;
+        }
+        // bf16 output: thread = row, 16-byte stores of 8 columns
+        const int gm = row_base + static_cast<int>(lane);
+        const int gn0 = tc.n0 + c * 32;
+        if (gm >= args.M) continue;
+        const int64_t rowoff = zoff_c + static_cast<int64_t>(gm) * args.ldc;
+        const int64_t xrowoff = zoff_x + static_cast<int64_t>(gm) * args.ld_aux;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gn = gn0 + 8 * j;
+            if (gn >= args.N) continue;
+            float* f = v + 8 * j;
+            if (args.bias != nullptr) {
+                float b[8];
+                unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.bias) + gn), b);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] += b[i];
+            }
+            if (args.epi == PTK_EPI_BF16 && args.aux != nullptr) {
+                float r[8];
+                unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.aux) + xrowoff + gn), r);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] += r[i];
+            } else if (args.epi == PTK_EPI_BIAS_GELU) {
+                const uint4 pre = pack_bf16x8(f);
+                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C2) + rowoff + gn) = pre;
+                float p[8];
+                unpack_bf16x8(pre, p);  // gelu of the rounded pre-activation, as stored
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] = gelu_tanh(p[i]);
+            } else if (args.epi == PTK_EPI_DGELU) {
+                float p[8];
+                unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.aux) + xrowoff + gn), p);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] *= gelu_tanh_grad(p[i]);
+            }
+            *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + rowoff + gn) = pack_bf16x8(f);
+        }
+    }
+}
+
 template <int BN, bool A_MN, bool B_MN, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -281,98 +373,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quad = warp & 3;
         const int half = (warp - 2) >> 2;  // 0 or 1
         float4* stage_buf = reinterpret_cast<float4*>(epi_smem) + (warp - 2) * 256;  // 32 rows x 8 float4
-        const int q = static_cast<int>(lane & 7);
-        const int r0 = static_cast<int>(lane >> 3);
-        const bool f32_out = args.epi == PTK_EPI_F32 || args.epi == PTK_EPI_ACC_F32;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = t_begin; t < args.num_tiles; t += t_step) {
             const TileCoord tc = decode_tile<MC>(args, t, rank);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int64_t zoff_c = tc.z1 * args.c_bs1 + tc.z2 * args.c_bs2;
-            const int64_t zoff_x = tc.z1 * args.aux_bs1 + tc.z2 * args.aux_bs2;
-            const int row_base = tc.m0 + quad * 32;
-#pragma unroll 1
-            for (int c = half; c < BN / 32; c += 2) {
-                float v[32];
-                __syncwarp();
-                tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                                       static_cast<uint32_t>(acc * BN + c * 32),
-                                   v);
-                if (f32_out) {
-                    // fp32 output: transpose through smem so each warp store covers
-                    // 4 rows x 128 contiguous bytes; all loads issued before stores.
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        stage_buf[lane * 8 + (j ^ (lane & 7))] =
-                            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                    __syncwarp();
-                    const int gn = tc.n0 + c * 32 + q * 4;
-                    if (gn < args.N) {
-                        float* cbase = static_cast<float*>(args.C) + zoff_c + gn;
-                        float4 prev[8];
-                        if (args.epi == PTK_EPI_ACC_F32) {
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                const int gm = row_base + r0 + 4 * i;
-                                prev[i] = gm < args.M ? *reinterpret_cast<const float4*>(cbase + static_cast<int64_t>(gm) * args.ldc)
-                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-                            }
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) prev[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                        }
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int r = r0 + 4 * i;
-                            const int gm = row_base + r;
-                            const float4 a4 = stage_buf[r * 8 + (q ^ (r & 7))];
-                            if (gm < args.M)
-                                *reinterpret_cast<float4*>(cbase + static_cast<int64_t>(gm) * args.ldc) =
-                                    make_float4(prev[i].x + a4.x, prev[i].y + a4.y, prev[i].z + a4.z, prev[i].w + a4.w);
-                        }
-                    }
-                    continue;
-                }
-                // bf16 output: thread = row, 16-byte stores of 8 columns
-                const int gm = row_base + static_cast<int>(lane);
-                const int gn0 = tc.n0 + c * 32;
-                if (gm >= args.M) continue;
-                const int64_t rowoff = zoff_c + static_cast<int64_t>(gm) * args.ldc;
-                const int64_t xrowoff = zoff_x + static_cast<int64_t>(gm) * args.ld_aux;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int gn = gn0 + 8 * j;
-                    if (gn >= args.N) continue;
-                    float* f = v + 8 * j;
-                    if (args.bias != nullptr) {
-                        float b[8];
-                        unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.bias) + gn), b);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) f[i] += b[i];
-                    }
-                    if (args.epi == PTK_EPI_BF16 && args.aux != nullptr) {
-                        float r[8];
-                        unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.aux) + xrowoff + gn), r);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) f[i] += r[i];
-                    } else if (args.epi == PTK_EPI_BIAS_GELU) {
-                        const uint4 pre = pack_bf16x8(f);
-                        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C2) + rowoff + gn) = pre;
-                        float p[8];
-                        unpack_bf16x8(pre, p);  // gelu of the rounded pre-activation, as stored
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) f[i] = gelu_tanh(p[i]);
-                    } else if (args.epi == PTK_EPI_DGELU) {
-                        float p[8];
-                        unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.aux) + xrowoff + gn), p);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) f[i] *= gelu_tanh_grad(p[i]);
-                    }
-                    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + rowoff + gn) = pack_bf16x8(f);
-                }
-            }
+            epilogue_tile<BN>(args, tc, tmem_base + static_cast<uint32_t>(acc * BN), quad, half, lane, stage_buf);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -389,6 +396,186 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<C::kTmemCols>(tmem_base);
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// CTA-pair GEMM: tcgen05.mma.cta_group::2 with a 256 x 256 pair tile.  Each
+// CTA stages only its own 128 rows of A and 128 rows (N) of B per k-step
+// (32 KiB, 6 stages), the leader issues M=256 MMAs that read both CTAs' smem,
+// and each CTA's TMEM receives its own 128 output rows.  TMA completion bytes
+// of both CTAs land on the leader's full barrier; the leader's commits are
+// multicast to both CTAs' empty / tmem-full barriers; both CTAs' epilogue
+// warps release the accumulator on the leader's tmem-empty barrier.
+constexpr int k2smStages = 6;
+constexpr int k2smStageBytes = 2 * 128 * kBK * 2;  // A half + B half
+constexpr int k2smSmem = k2smStages * k2smStageBytes + 1024 + 512 + 8 * 32 * 32 * 4;
+
+__device__ __forceinline__ TileCoord decode_pair_tile(const GemmArgs& a, int t, int rank) {
+    // t indexes 256 x 256 pair tiles; this CTA's rows are m0 + rank*128
+    TileCoord c;
+    const int z = t / a.tiles_per_batch;
+    const int r = t - z * a.tiles_per_batch;
+    const int mpairs = (a.tiles_m + 1) / 2;
+    const int nb = r / mpairs;
+    const int mp = r - nb * mpairs;
+    c.z1 = z % a.batch1;
+    c.z2 = z / a.batch1;
+    c.m0 = mp * 256 + rank * 128;
+    c.n0 = nb * 256;
+    c.kb0 = 0;
+    c.kb1 = (a.K + kBK - 1) / kBK;
+    return c;
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ GemmArgs args) {
+    constexpr int S = k2smStages;
+    constexpr int kHalf = 128 * kBK * 2;  // 16 KiB
+    constexpr uint32_t kIdesc = make_idesc_bf16(256, 256, A_MN, B_MN);
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * k2smStageBytes);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint8_t* epi_smem = smem + S * k2smStageBytes + 512;
+
+    const int warp = threadIdx.x / 32;
+    const uint32_t lane = lane_id();
+    const int rank = static_cast<int>(cluster_ctarank());
+    const bool leader = rank == 0;
+    const int t_begin = static_cast<int>(blockIdx.x) / 2;
+    const int t_step = static_cast<int>(gridDim.x) / 2;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 16);  // 8 epilogue warps x 2 CTAs (leader's copy is the one used)
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_2sm<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = t_begin; t < args.num_tiles; t += t_step) {
+                const TileCoord tc = decode_pair_tile(args, t, rank);
+                const int nrow = tc.n0 + rank * 128;  // this CTA's half of the B rows
+                for (int kb = tc.kb0; kb < tc.kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2smStageBytes);
+                    uint8_t* sa = smem + stage * k2smStageBytes;
+                    uint8_t* sb = sa + kHalf;
+                    const int k0 = kb * kBK;
+                    if (!A_MN) {
+                        tma_load_4d_2sm(&tmA, &full[stage], sa, k0, tc.m0, tc.z1, tc.z2);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            tma_load_4d_2sm(&tmA, &full[stage], sa + j * 64 * kBK * 2, tc.m0 + 64 * j, k0, tc.z1, tc.z2);
+                    }
+                    if (!B_MN) {
+                        tma_load_4d_2sm(&tmB, &full[stage], sb, k0, nrow, tc.z1, tc.z2);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            tma_load_4d_2sm(&tmB, &full[stage], sb + j * 64 * kBK * 2, nrow + 64 * j, k0, tc.z1, tc.z2);
+                    }
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {  // ---------------- MMA issuer (leader CTA only)
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = t_begin; t < args.num_tiles; t += t_step) {
+                const TileCoord tc = decode_pair_tile(args, t, rank);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
+                for (int kb = tc.kb0; kb < tc.kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(smem + stage * k2smStageBytes);
+                    const uint32_t b_base = a_base + kHalf;
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        const uint64_t da = A_MN ? make_sw128_desc(a_base + k * 2048, 64 * kBK * 2, 1024)
+                                                 : make_sw128_desc(a_base + k * 32, 16, 1024);
+                        const uint64_t db = B_MN ? make_sw128_desc(b_base + k * 2048, 64 * kBK * 2, 1024)
+                                                 : make_sw128_desc(b_base + k * 32, 16, 1024);
+                        mma_bf16_ss_2sm(d_tmem, da, db, kIdesc, (kb > tc.kb0 || k > 0) ? 1u : 0u);
+                    }
+                    mma_commit_2sm_mc(&empty[stage], 0x3);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit_2sm_mc(&tfull[acc], 0x3);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {  // ---------------- epilogue warps (both CTAs): this CTA's 128 rows
+        const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;
+        float4* stage_buf = reinterpret_cast<float4*>(epi_smem) + (warp - 2) * 256;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = t_begin; t < args.num_tiles; t += t_step) {
+            const TileCoord tc = decode_pair_tile(args, t, rank);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            epilogue_tile<256>(args, tc, tmem_base + static_cast<uint32_t>(acc * 256), quad, half, lane, stage_buf);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (leader)
+                    mbar_arrive(&tempty[acc]);
+                else
+                    mbar_arrive_remote(&tempty[acc], 0);
+            }
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_2sm<512>(tmem_base);
     }
 }
 
@@ -464,6 +651,38 @@ int launch_impl(const GemmPlan& p, cudaStream_t stream) {
     return cudaPeekAtLastError() == cudaSuccess ? PTK_OK : PTK_ERR_CUDA;
 }
 
+template <bool A_MN, bool B_MN>
+int launch_2sm(const GemmPlan& p, cudaStream_t stream) {
+    static bool attr_set = false;
+    auto kern = gemm_bf16_2sm_kernel<A_MN, B_MN>;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k2smSmem) != cudaSuccess)
+            return PTK_ERR_CUDA;
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = k2smSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.args) != cudaSuccess) return PTK_ERR_CUDA;
+    return cudaPeekAtLastError() == cudaSuccess ? PTK_OK : PTK_ERR_CUDA;
+}
+
+GemmPlan::Launcher pick_2sm(bool a_mn, bool b_mn) {
+    if (!a_mn && !b_mn) return &launch_2sm<false, false>;
+    if (!a_mn && b_mn) return &launch_2sm<false, true>;
+    if (a_mn && !b_mn) return &launch_2sm<true, false>;
+    return &launch_2sm<true, true>;
+}
+
 template <int BN, bool MC>
 GemmPlan::Launcher pick(bool a_mn, bool b_mn) {
     if (!a_mn && !b_mn) return &launch_impl<BN, false, false, MC>;
@@ -520,10 +739,12 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     else
         rc = encode_operand(&p.tmA, d.a, d.m, d.k, kBK, b1, b2);
     if (rc != PTK_OK) return rc;
-    // B: logical [N][K]; with multicast each CTA of the pair fetches half the K-major rows
-    const bool mc_pre = d.causal == PTK_CAUSAL_NONE && bn == 256 && tiles_m >= 2 && d.multicast != 0 && !d.b.mn_major;
+    // B: logical [N][K]; with multicast / CTA pairs each CTA fetches half the K-major rows
+    const bool pair = d.causal == PTK_CAUSAL_NONE && bn == 256 && tiles_m >= 2 && d.multicast == 2;
+    const bool mc_pre = !pair && d.causal == PTK_CAUSAL_NONE && bn == 256 && tiles_m >= 2 && d.multicast == 1 &&
+                        !d.b.mn_major;
     if (!d.b.mn_major)
-        rc = encode_operand(&p.tmB, d.b, d.k, d.n, mc_pre ? bn / 2 : bn, b1, b2);
+        rc = encode_operand(&p.tmB, d.b, d.k, d.n, (mc_pre || pair) ? bn / 2 : bn, b1, b2);
     else
         rc = encode_operand(&p.tmB, d.b, d.n, d.k, kBK, b1, b2);
     if (rc != PTK_OK) return rc;
@@ -559,7 +780,13 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     const bool mc = mc_pre;
     p.flops = 2.0 * d.m * static_cast<double>(d.n) * d.k * b1 * b2;
     if (d.causal != PTK_CAUSAL_NONE) p.flops *= 0.5;
-    if (mc) {
+    if (pair) {
+        a.tiles_per_batch = ((tiles_m + 1) / 2) * a.tiles_n;
+        a.num_tiles = a.tiles_per_batch * b1 * b2;
+        const int clusters = a.num_tiles < sms / 2 ? a.num_tiles : sms / 2;
+        p.grid = 2 * clusters;
+        p.launch = pick_2sm(d.a.mn_major, d.b.mn_major);
+    } else if (mc) {
         a.tiles_per_batch = ((tiles_m + 1) / 2) * a.tiles_n;
         a.num_tiles = a.tiles_per_batch * b1 * b2;
         const int clusters = a.num_tiles < sms / 2 ? a.num_tiles : sms / 2;
@@ -573,7 +800,7 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
             default: p.launch = pick<256, false>(d.a.mn_major, d.b.mn_major); break;
         }
     }
-    p.multicast = mc;
+    p.multicast = mc || pair;
     *out = p;
     return PTK_OK;
 }

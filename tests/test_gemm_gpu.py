@@ -43,7 +43,7 @@ def _close(out, ref, tol=1.5e-2):
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("shape", [(128, 64, 64), (300, 520, 200), (256, 384, 1024), (640, 768, 320)])
-@pytest.mark.parametrize("bn,mc", [(0, 0), (64, 0), (128, 0), (256, 0), (256, 1)])
+@pytest.mark.parametrize("bn,mc", [(0, 0), (64, 0), (128, 0), (256, 0), (256, 1), (256, 2)])
 def test_gemm_majors(cuda, a_mn, b_mn, shape, bn, mc):
     m, n, k = shape
     if a_mn and m % 8:
@@ -160,14 +160,36 @@ def test_gemm_batched_pv_and_grads(cuda):
     _close(dV, ref)
 
 
-def test_gemm_large_dense(cuda):
+@pytest.mark.parametrize("mc", [1, 2])
+def test_gemm_large_dense(cuda, mc):
     m, n, k = 2048, 6144, 2048
     torch.manual_seed(5)
     A = (torch.randn(m, k) * 0.5).bfloat16().to(cuda)
     B = (torch.randn(n, k) * 0.02).bfloat16().to(cuda)
     C = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
-    _run(_desc(m, n, k, L.matrix(A.data_ptr(), k), L.matrix(B.data_ptr(), k), L.matrix(C.data_ptr(), n), mc=1))
+    _run(_desc(m, n, k, L.matrix(A.data_ptr(), k), L.matrix(B.data_ptr(), k), L.matrix(C.data_ptr(), n), mc=mc))
     ref = (A.float() @ B.float().T)  # fp32 on the GPU (TF32 disabled by default for matmul)
     torch.cuda.synchronize()
     err = (C.float() - ref).abs().max().item()
     assert err <= 1e-2 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("mc", [0, 2])
+def test_gemm_pair_epilogues_and_wgrad(cuda, mc):
+    """The CTA-pair kernel with the fused epilogues and MN-major (wgrad) operands."""
+    m, n, k = 768, 1280, 512
+    torch.manual_seed(11)
+    A = torch.randn(k, m).bfloat16()  # MN-major A (stored [k][m])
+    B = torch.randn(k, n).bfloat16()  # MN-major B (stored [k][n])
+    acc = A.double().T @ B.double()
+    Ad, Bd = A.to(cuda), B.to(cuda)
+    F = torch.ones(m, n, dtype=torch.float32, device=cuda)
+    _run(_desc(m, n, k, L.matrix(Ad.data_ptr(), m, 1), L.matrix(Bd.data_ptr(), n, 1), L.matrix(F.data_ptr(), n),
+               epi=L.EPI_ACC_F32, mc=mc))
+    _close(F, (acc + 1.0).float(), tol=1e-4)
+    bias = torch.randn(n).bfloat16().to(cuda)
+    G = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    P = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    _run(_desc(m, n, k, L.matrix(Ad.data_ptr(), m, 1), L.matrix(Bd.data_ptr(), n, 1), L.matrix(G.data_ptr(), n),
+               epi=L.EPI_BIAS_GELU, bias=bias.data_ptr(), c2=P.data_ptr(), mc=mc))
+    _close(P, (acc + bias.double().cpu()).float())
