@@ -48,7 +48,7 @@ ptk_gemm_desc desc(int m, int n, int k, ptk_matrix a, ptk_matrix b, ptk_matrix c
     d.b = b;
     d.c = c;
     d.epilogue = epi;
-    d.multicast = 1;
+    d.multicast = 2;  // CTA-pair tcgen05 kernel for every dense BN=256 GEMM
     return d;
 }
 
