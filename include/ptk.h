@@ -152,7 +152,8 @@ int ptk_stage_destroy(ptk_stage* st);
  * [b*seq, hidden], other stages), labels (int32, head stage), x_out (bf16, non-head). */
 int ptk_stage_forward(ptk_stage* st, int slot, const int32_t* tok, const void* x_in, const int32_t* labels,
                       void* x_out, void* stream);
-/* B(m) of stash slot `slot`: dy (bf16, non-head stages), dx (bf16, non-embedding). */
+/* B(m) of stash slot `slot`: dy (bf16, non-head stages), dx (bf16, non-embedding).
+ * Parameter gradients are accumulated (+=) and complete in stream order on return. */
 int ptk_stage_backward(ptk_stage* st, int slot, const int32_t* tok, const void* dy, void* dx, void* stream);
 /* GradAccum finalisation: AdamW on the accumulated gradients, then zero them. */
 int ptk_stage_optimizer_step(ptk_stage* st, float lr, float weight_decay, void* stream);

@@ -40,13 +40,43 @@ def reference_order(stages: int, micro_batches: int, b: int, k: int) -> tuple[li
     return seq, "port"
 
 
-def time_cpu_training(shape, b: int, micro_batches_to_run: int, k: int = 1, threads: int | None = None,
-                      seed: int = 1234) -> dict:
-    """fwd+bwd of `micro_batches_to_run` micro-batches of size b of the full model
-    (single stage, S=1) on the host cores, in the reference planner's order."""
-    threads = threads or os.cpu_count() or 1
-    torch.set_num_threads(threads)
-    seq, kind = reference_order(1, micro_batches_to_run, b, k)
+class CpuTrainer:
+    """The CPU path, weights initialised once; step() times one bounded sample."""
+
+    def __init__(self, shape, b: int, micro_batches_to_run: int, k: int = 1, threads: int | None = None,
+                 seed: int = 1234):
+        self.shape, self.b, self.M, self.k, self.seed = shape, b, micro_batches_to_run, k, seed
+        self.threads = threads or os.cpu_count() or 1
+        torch.set_num_threads(self.threads)
+        self.seq, self.kind = reference_order(1, micro_batches_to_run, b, k)
+        self.w = init_weights(shape)
+
+    def step(self) -> dict:
+        shape, b = self.shape, self.b
+        for t in self.w.values():
+            t.grad = None
+        stash = {}
+        t0 = time.perf_counter()
+        for tok_name in self.seq:
+            if tok_name == "GA":
+                continue
+            m = int(tok_name[1:])
+            if tok_name[0] == "F":
+                tok, lab = G.synthetic_batch(self.seed, m, b, shape.seq, shape.vocab)
+                _, loss = G.stage_forward(self.w, shape, 0, shape.n_layer, True, True, tok=tok, labels=lab,
+                                          micro_batches=self.M)
+                stash[m] = loss
+            else:
+                stash.pop(m).backward()
+        dt = time.perf_counter() - t0
+        samples = b * self.M
+        return {"value": samples / dt, "unit": "samples/s", "cores": self.threads, "kind": self.kind,
+                "sample": f"{shape.n_layer}-layer h={shape.hidden} s={shape.seq} {shape.arch.upper()} fp32 fwd+bwd "
+                          f"of {samples} sample(s) (b={b}) on the host cores in the reference planner's order; "
+                          f"{dt:.1f} s"}
+
+
+def init_weights(shape):
     g = torch.Generator().manual_seed(42)
     h, f, V, s = shape.hidden, shape.ffn, shape.vocab, shape.seq
     w = {"wte": torch.randn(V, h, generator=g) * 0.02, "wpe": torch.randn(s, h, generator=g) * 0.02,
@@ -59,23 +89,15 @@ def time_cpu_training(shape, b: int, micro_batches_to_run: int, k: int = 1, thre
                   p + "ln2_g": torch.ones(h), p + "ln2_b": torch.zeros(h),
                   p + "w_fc1": torch.randn(f, h, generator=g) * 0.02, p + "b_fc1": torch.zeros(f),
                   p + "w_fc2": torch.randn(h, f, generator=g) * 0.02, p + "b_fc2": torch.zeros(h)})
+    if shape.arch == "bert":
+        w.update({"lne_g": torch.ones(h), "lne_b": torch.zeros(h), "w_t": torch.randn(h, h, generator=g) * 0.02,
+                  "b_t": torch.zeros(h)})
     for t in w.values():
         t.requires_grad_(True)
-    stash = {}
-    t0 = time.perf_counter()
-    for tok_name in seq:
-        if tok_name == "GA":
-            continue
-        m = int(tok_name[1:])
-        if tok_name[0] == "F":
-            tok, lab = G.synthetic_batch(seed, m, b, s, V)
-            _, loss = G.stage_forward(w, shape, 0, shape.n_layer, True, True, tok=tok, labels=lab,
-                                      micro_batches=micro_batches_to_run)
-            stash[m] = loss
-        else:
-            stash.pop(m).backward()
-    dt = time.perf_counter() - t0
-    samples = b * micro_batches_to_run
-    return {"value": samples / dt, "unit": "samples/s", "cores": threads, "kind": kind,
-            "sample": f"{shape.n_layer}-layer h={h} s={s} GPT fp32 fwd+bwd of {samples} sample(s) "
-                      f"(b={b}) on the host cores in the reference planner's order; {dt:.1f} s"}
+    return w
+
+
+def time_cpu_training(shape, b: int, micro_batches_to_run: int, k: int = 1, threads: int | None = None,
+                      seed: int = 1234) -> dict:
+    """One bounded sample: fwd+bwd of `micro_batches_to_run` micro-batches of size b."""
+    return CpuTrainer(shape, b, micro_batches_to_run, k, threads, seed).step()

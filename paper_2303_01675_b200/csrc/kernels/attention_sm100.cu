@@ -1,16 +1,26 @@
-// Fused causal attention forward for sm_100a (tcgen05 + TMEM + TMA).
+// Fused attention forward for sm_100a (tcgen05 + TMEM + TMA), persistent.
 //
-// One CTA per (128-query block, head, sample).  For each 128-key block j <= i:
-//   S_j  = Q·K_jᵀ            tcgen05.mma into TMEM (double-buffered: S_{j+1} is
-//                            issued while the softmax warps work on S_j)
-//   P_j  = exp2(S_j·c − m)   4 softmax warps, one query row per thread (the row
-//                            max/sum never leave the thread), P written to smem
-//                            in the UMMA K-major 128B-swizzled layout
-//   O   += P_j·V_j           tcgen05.mma into a TMEM accumulator; when the row
-//                            max moves, the thread rescales its O row in TMEM
+// One CTA per SM walks a static list of (128-query block, head, sample)
+// tiles, heaviest causal blocks first, assigned boustrophedon (CTA i takes
+// tiles i, 2G-1-i, 2G+i, ...) so heavy and light blocks pair up.  The TMA,
+// MMA and softmax roles each walk the same list, so loads and score
+// products for the next tile run under the current tile's softmax/epilogue.
+// For each 128-key block j of a tile:
+//   S_j  = Q·K_jᵀ            tcgen05.mma into TMEM (double-buffered: S_{j+1} —
+//                            possibly of the next tile — is issued while the
+//                            softmax warps work on S_j)
+//   P_j  = exp2(S_j·c − m)   8 softmax warps in two column halves: a thread owns
+//                            64 columns of one query row; the two halves of a
+//                            row swap their maxima through smem (one 64-thread
+//                            named barrier per block), P is written to smem in
+//                            the UMMA K-major 128B-swizzled layout
+//   O   += P_j·V_j           tcgen05.mma into a TMEM accumulator (double-buffered
+//                            across tiles); when the row max moves, the thread
+//                            rescales its half of the O row in TMEM
 // and finally O/l is written as bf16 [T, h] (the out-projection's input) and
 // lse = m + log2(l) (log2 units of the scaled scores) for the backward.
-// Warps: 0 TMA producer, 1 TMEM alloc + MMA issuer, 4-7 softmax/epilogue.
+// Warps: 0 TMA producer, 1 TMEM alloc + MMA issuer, 4-11 softmax/epilogue
+// (warp 4+q and 8+q share TMEM lane quarter q: columns 0-63 and 64-127).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -27,7 +37,18 @@ using namespace sm100;
 namespace {
 
 constexpr int kBlk = 128;      // query rows and key rows per block
-constexpr int kThreads = 256;  // 8 warps
+constexpr int kThreads = 384;  // 12 warps: TMA, MMA, 2 idle, 8 row-parallel elementwise warps
+
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
 
 template <int D>
 struct FaCfg {
@@ -35,61 +56,95 @@ struct FaCfg {
     static constexpr int kKBytes = kBlk * D * 2;
     static constexpr int kVBytes = kBlk * D * 2;     // [2 kv halves][D/64][64 rows x 128 B]
     static constexpr int kPBytes = kBlk * kBlk * 2;  // [2][128 rows x 128 B]
-    static constexpr int kStages = 2;
-    static constexpr int kSmem = kQBytes + kStages * (kKBytes + kVBytes) + kPBytes + 1024 + 256;
-    static constexpr uint32_t kTmemS0 = 0, kTmemS1 = 128, kTmemO = 256;
+    static constexpr int kQBuf = D == 64 ? 2 : 1;
+    static constexpr int kStages = D == 64 ? 3 : 2;
+    static constexpr int kXchg = (2 * 2 + 2 * 2) * kBlk * 4;  // row maxima [2][2][128], row sums [2][2][128]
+    static constexpr int kSmem =
+        kQBuf * kQBytes + kStages * (kKBytes + kVBytes) + kPBytes + kXchg + 1024 + 256;
+    static constexpr uint32_t kTmemS0 = 0, kTmemS1 = 128, kTmemO = 256;  // O buffers at 256, 256 + D
 };
 
 struct FaArgs {
     __nv_bfloat16* o;  // [b*s][h]
     float* lse;        // [b][H][s], log2 units of the scaled scores
-    int s, H, h;
+    int s, H, h, b;
     float scale_log2;  // log2(e) / sqrt(d)
     int causal;        // 1: GPT (key <= query), 0: bidirectional (BERT)
 };
+
+// Position in a CTA's tile list: tile k of this CTA, key block j of that tile.
+struct FaCursor {
+    int k, qb, head, bi, nkv, j;
+    bool valid;
+};
+
+__device__ __forceinline__ void fa_tile(const FaArgs& a, int k, FaCursor& c) {
+    const int G = gridDim.x, i = blockIdx.x;
+    const int nqb = a.s / kBlk;
+    const int per = a.H * a.b;
+    const int t = (k & 1) ? (k + 1) * G - 1 - i : k * G + i;
+    c.k = k;
+    c.j = 0;
+    c.valid = t < nqb * per;
+    const int rank = t / per, rem = t % per;
+    c.qb = nqb - 1 - rank;  // heaviest first
+    c.head = rem % a.H;
+    c.bi = rem / a.H;
+    c.nkv = a.causal ? c.qb + 1 : nqb;
+}
+
+__device__ __forceinline__ void fa_next(const FaArgs& a, FaCursor& c) {
+    if (++c.j == c.nkv) fa_tile(a, c.k + 1, c);
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
                      const __grid_constant__ FaArgs a) {
     using C = FaCfg<D>;
+    constexpr int S = C::kStages, QB = C::kQBuf;
     constexpr uint32_t kIdescS = make_idesc_bf16(kBlk, kBlk, false, false);  // Q (K-major) x K (K-major)
     constexpr uint32_t kIdescO = make_idesc_bf16(kBlk, D, false, true);      // P (K-major) x V (MN-major)
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;
-    uint8_t* sK = sQ + C::kQBytes;
-    uint8_t* sV = sK + C::kStages * C::kKBytes;
-    uint8_t* sP = sV + C::kStages * C::kVBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::kPBytes);
-    uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;   // [2]
-    uint64_t* kv_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;    // [2]
-    uint64_t* s_empty = bars + 7;   // [2]
-    uint64_t* p_full = bars + 9;
-    uint64_t* pv_done = bars + 10;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint8_t* sQ = smem;                         // [QB]
+    uint8_t* sK = sQ + QB * C::kQBytes;         // [S]
+    uint8_t* sV = sK + S * C::kKBytes;          // [S]
+    uint8_t* sP = sV + S * C::kVBytes;
+    float* sX = reinterpret_cast<float*>(sP + C::kPBytes);  // row-max [2][2][128], row-sum [2][2][128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::kPBytes + C::kXchg);
+    uint64_t* q_full = bars + 0;         // [2]
+    uint64_t* q_empty = bars + 2;        // [2]
+    uint64_t* kv_full = bars + 4;        // [S <= 3]
+    uint64_t* kv_empty = bars + 7;       // [S]
+    uint64_t* s_full = bars + 10;        // [2]
+    uint64_t* s_empty = bars + 12;       // [2]
+    uint64_t* p_full = bars + 14;
+    uint64_t* pv_done = bars + 15;
+    uint64_t* o_full = bars + 16;        // [2]
+    uint64_t* o_empty = bars + 18;       // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
-    const int nqb = a.s / kBlk;
-    const int qb = nqb - 1 - static_cast<int>(blockIdx.x);  // heaviest blocks first
-    const int head = blockIdx.y, bi = blockIdx.z;
-    const int nkv = a.causal ? qb + 1 : nqb;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmQK);
         tma_prefetch_desc(&tmV);
-        mbar_init(q_full, 1);
         for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], 8);
+            mbar_init(&o_full[i], 1);
+            mbar_init(&o_empty[i], 8);
+        }
+        for (int i = 0; i < S; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
-            mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], 4);
         }
-        mbar_init(p_full, 4);
+        mbar_init(p_full, 8);
         mbar_init(pv_done, 1);
         fence_barrier_init();
     }
@@ -101,157 +156,201 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
-            mbar_arrive_expect_tx(q_full, C::kQBytes);
-#pragma unroll
-            for (int kb = 0; kb < D / 64; ++kb)
-                tma_load_4d(&tmQK, q_full, sQ + kb * kBlk * 128, kb * 64, qb * kBlk, head, bi);
-            for (int j = 0; j < nkv; ++j) {
-                const int st = j & 1;
-                mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&kv_full[st], C::kKBytes + C::kVBytes);
-                uint8_t* k = sK + st * C::kKBytes;
-                uint8_t* v = sV + st * C::kVBytes;
+            int n = 0;  // key blocks loaded so far (all tiles)
+            FaCursor c;
+            for (fa_tile(a, 0, c); c.valid; fa_tile(a, c.k + 1, c)) {
+                const int qbuf = c.k % QB;
+                mbar_wait(&q_empty[qbuf], ((c.k / QB) & 1) ^ 1);
+                mbar_arrive_expect_tx(&q_full[qbuf], C::kQBytes);
 #pragma unroll
                 for (int kb = 0; kb < D / 64; ++kb)
-                    tma_load_4d(&tmQK, &kv_full[st], k + kb * kBlk * 128, kb * 64, j * kBlk, a.H + head, bi);
+                    tma_load_4d(&tmQK, &q_full[qbuf], sQ + qbuf * C::kQBytes + kb * kBlk * 128, kb * 64, c.qb * kBlk,
+                                c.head, c.bi);
+                for (int j = 0; j < c.nkv; ++j, ++n) {
+                    const int st = n % S;
+                    mbar_wait(&kv_empty[st], ((n / S) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&kv_full[st], C::kKBytes + C::kVBytes);
+                    uint8_t* k = sK + st * C::kKBytes;
+                    uint8_t* v = sV + st * C::kVBytes;
 #pragma unroll
-                for (int half = 0; half < 2; ++half)
+                    for (int kb = 0; kb < D / 64; ++kb)
+                        tma_load_4d(&tmQK, &kv_full[st], k + kb * kBlk * 128, kb * 64, j * kBlk, a.H + c.head, c.bi);
 #pragma unroll
-                    for (int na = 0; na < D / 64; ++na)
-                        tma_load_4d(&tmV, &kv_full[st], v + (half * (D / 64) + na) * 8192, na * 64,
-                                    j * kBlk + half * 64, 2 * a.H + head, bi);
+                    for (int half = 0; half < 2; ++half)
+#pragma unroll
+                        for (int na = 0; na < D / 64; ++na)
+                            tma_load_4d(&tmV, &kv_full[st], v + (half * (D / 64) + na) * 8192, na * 64,
+                                        j * kBlk + half * 64, 2 * a.H + c.head, c.bi);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
-            mbar_wait(q_full, 0);
-            const uint32_t q_base = smem_u32(sQ);
-            auto issue_s = [&](int j) {
-                const int st = j & 1;
-                mbar_wait(&kv_full[st], (j >> 1) & 1);
-                mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+            auto issue_s = [&](const FaCursor& c, int n) {
+                const int st = n % S, sb = n & 1, qbuf = c.k % QB;
+                if (c.j == 0) mbar_wait(&q_full[qbuf], (c.k / QB) & 1);
+                mbar_wait(&kv_full[st], (n / S) & 1);
+                mbar_wait(&s_empty[sb], ((n >> 1) & 1) ^ 1);
                 tc_fence_after();
+                const uint32_t q_base = smem_u32(sQ + qbuf * C::kQBytes);
                 const uint32_t k_base = smem_u32(sK + st * C::kKBytes);
-                const uint32_t d_tmem = tmem + (st ? C::kTmemS1 : C::kTmemS0);
+                const uint32_t d_tmem = tmem + (sb ? C::kTmemS1 : C::kTmemS0);
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {
                     const uint32_t off = (k / 4) * kBlk * 128 + (k % 4) * 32;
                     mma_bf16_ss(d_tmem, make_sw128_desc(q_base + off, 16, 1024), make_sw128_desc(k_base + off, 16, 1024),
                                 kIdescS, k > 0 ? 1u : 0u);
                 }
-                mma_commit(&s_full[st]);
+                mma_commit(&s_full[sb]);
+                if (c.j == c.nkv - 1) mma_commit(&q_empty[qbuf]);
             };
-            issue_s(0);
-            for (int j = 0; j < nkv; ++j) {
-                if (j + 1 < nkv) issue_s(j + 1);
-                mbar_wait(p_full, j & 1);
+            FaCursor cs, cp;
+            fa_tile(a, 0, cs);
+            fa_tile(a, 0, cp);
+            int ns = 0, np = 0;
+            if (cs.valid) {
+                issue_s(cs, ns++);
+                fa_next(a, cs);
+            }
+            while (cp.valid) {
+                if (cs.valid) {  // one score product ahead, across tile boundaries
+                    issue_s(cs, ns++);
+                    fa_next(a, cs);
+                }
+                const int st = np % S, ob = cp.k & 1;
+                mbar_wait(p_full, np & 1);
+                if (cp.j == 0) mbar_wait(&o_empty[ob], ((cp.k >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const int st = j & 1;
                 const uint32_t p_base = smem_u32(sP);
                 const uint32_t v_base = smem_u32(sV + st * C::kVBytes);
+                const uint32_t o_tmem = tmem + C::kTmemO + ob * D;
 #pragma unroll
                 for (int k = 0; k < kBlk / 16; ++k) {
                     const uint32_t pa = p_base + (k / 4) * kBlk * 128 + (k % 4) * 32;
                     const uint32_t vb = v_base + (k / 4) * (D / 64) * 8192 + (k % 4) * 2048;
-                    mma_bf16_ss(tmem + C::kTmemO, make_sw128_desc(pa, 16, 1024), make_sw128_desc(vb, 8192, 1024),
-                                kIdescO, (j > 0 || k > 0) ? 1u : 0u);
+                    mma_bf16_ss(o_tmem, make_sw128_desc(pa, 16, 1024), make_sw128_desc(vb, 8192, 1024), kIdescO,
+                                (cp.j > 0 || k > 0) ? 1u : 0u);
                 }
                 mma_commit(pv_done);
                 mma_commit(&kv_empty[st]);
+                if (cp.j == cp.nkv - 1) mma_commit(&o_full[ob]);
+                fa_next(a, cp);
+                ++np;
             }
         }
-    } else if (warp >= 4) {  // ---------------- softmax / epilogue: thread = query row
+    } else if (warp >= 4) {  // ---------------- softmax / epilogue: thread = (query row, column half)
         const int quad = warp & 3;
+        const int half = (warp - 4) >> 2;  // columns [64*half, 64*half + 64) of S, [D/2*half, ..) of O
         const int r = quad * 32 + static_cast<int>(lane);
         const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
-        float m = -INFINITY, l = 0.f;
-        for (int j = 0; j < nkv; ++j) {
-            const int st = j & 1;
-            mbar_wait(&s_full[st], (j >> 1) & 1);
-            tc_fence_after();
-            float x[kBlk];
-#pragma unroll
-            for (int c = 0; c < kBlk / 32; ++c) {
-                float v[32];
-                tmem_ld_32x32b_x32(tmem + lane_base + (st ? C::kTmemS1 : C::kTmemS0) + c * 32, v);
-#pragma unroll
-                for (int e = 0; e < 32; ++e) x[c * 32 + e] = v[e];
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[st]);
-            float mx = m;
-            const bool diag = a.causal && j == qb;
-#pragma unroll
-            for (int c = 0; c < kBlk; ++c) {
-                x[c] = (diag && c > r) ? -INFINITY : x[c] * a.scale_log2;
-                mx = fmaxf(mx, x[c]);
-            }
-            const float alpha = ex2(m - mx);  // m = -inf on the first block -> 0
-            float sum = 0.f;
-#pragma unroll
-            for (int c = 0; c < kBlk; ++c) {
-                x[c] = ex2(x[c] - mx);
-                sum += x[c];
-            }
-            l = l * alpha + sum;
-            m = mx;
-            if (j > 0) {
-                mbar_wait(pv_done, (j - 1) & 1);  // P buffer free, O stable
+        constexpr int kHc = kBlk / 2;  // S columns per thread
+        constexpr int kOc = D / 2;     // O columns per thread
+        int n = 0;                     // key blocks processed so far (all tiles)
+        FaCursor c;
+        for (fa_tile(a, 0, c); c.valid; fa_tile(a, c.k + 1, c)) {
+            const int ob = c.k & 1;
+            const uint32_t o_cols = tmem + lane_base + C::kTmemO + ob * D + half * kOc;
+            float m = -INFINITY, l = 0.f;  // m in log2 units of the scaled scores; l = this half's row sum
+            for (int j = 0; j < c.nkv; ++j, ++n) {
+                const int sb = n & 1;
+                mbar_wait(&s_full[sb], (n >> 1) & 1);
                 tc_fence_after();
+                float x[kHc];
+#pragma unroll
+                for (int cc = 0; cc < kHc / 32; ++cc)
+                    tmem_ld_32x32b_x32_nw(tmem + lane_base + (sb ? C::kTmemS1 : C::kTmemS0) + half * kHc + cc * 32,
+                                          x + cc * 32);
+                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_empty[sb]);
+                float mraw = -INFINITY;
+                if (a.causal && j == c.qb) {  // diagonal block: key > query masked
+#pragma unroll
+                    for (int e = 0; e < kHc; ++e) {
+                        if (half * kHc + e > r) x[e] = -INFINITY;
+                        mraw = fmaxf(mraw, x[e]);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < kHc; ++e) mraw = fmaxf(mraw, x[e]);
+                }
+                // swap the half-row maxima with the partner warp (same rows, other half)
+                const uint32_t xb = smem_u32(sX) + (n & 1) * 2 * kBlk * 4;
+                sts32f(xb + (half * kBlk + r) * 4, mraw);
+                asm volatile("bar.sync %0, 64;" ::"r"(2 + quad) : "memory");
+                const float mx = fmaxf(m, fmaxf(lds32f(xb + r * 4), lds32f(xb + (kBlk + r) * 4)) * a.scale_log2);
+                const float alpha = ex2(m - mx);  // m = -inf on the first block -> 0
+                float sum = 0.f;
+#pragma unroll
+                for (int e = 0; e < kHc; ++e) {
+                    x[e] = ex2(fmaf(x[e], a.scale_log2, -mx));
+                    sum += x[e];
+                }
+                l = l * alpha + sum;
+                m = mx;
+                if (n > 0) {
+                    mbar_wait(pv_done, (n - 1) & 1);  // P buffer free (and O of this tile stable)
+                    tc_fence_after();
+                }
+                // P half-row -> smem, K-major 128B-swizzled (16-byte chunk index ^= row % 8);
+                // columns [64*half, +64) are exactly swizzle atom `half`
+                const uint32_t prow = smem_u32(sP) + half * (kBlk * 128) + r * 128;
+#pragma unroll
+                for (int q = 0; q < kHc / 8; ++q) {
+                    uint4 u;
+                    u.x = pack_bf16(x[q * 8 + 0], x[q * 8 + 1]);
+                    u.y = pack_bf16(x[q * 8 + 2], x[q * 8 + 3]);
+                    u.z = pack_bf16(x[q * 8 + 4], x[q * 8 + 5]);
+                    u.w = pack_bf16(x[q * 8 + 6], x[q * 8 + 7]);
+                    sts128(prow + ((q ^ (r & 7)) * 16), u);
+                }
+                if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rescale this thread's half of the O row
+#pragma unroll
+                    for (int cc = 0; cc < kOc / 32; ++cc) {
+                        float v[32];
+                        tmem_ld_32x32b_x32(o_cols + cc * 32, v);
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) v[e] *= alpha;
+                        tmem_st_32x32b_x32(o_cols + cc * 32, v);
+                    }
+                }
+                fence_proxy_async_smem();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full);
             }
-            // P row -> smem, K-major 128B-swizzled (16-byte chunk index ^= row % 8)
+            // total row sum = both halves (same m sequence, so the partial sums add)
+            const uint32_t lb = smem_u32(sX) + (4 * kBlk + (c.k & 1) * 2 * kBlk) * 4;
+            sts32f(lb + (half * kBlk + r) * 4, l);
+            asm volatile("bar.sync %0, 64;" ::"r"(2 + quad) : "memory");
+            const float lt = lds32f(lb + r * 4) + lds32f(lb + (kBlk + r) * 4);
+            mbar_wait(&o_full[ob], (c.k >> 1) & 1);
+            tc_fence_after();
+            const float inv = 1.f / lt;
+            const int q = c.qb * kBlk + r;
+            __nv_bfloat16* orow = a.o + (static_cast<int64_t>(c.bi) * a.s + q) * a.h + c.head * D + half * kOc;
 #pragma unroll
-            for (int q = 0; q < kBlk / 8; ++q) {
-                uint4 u;
-                __nv_bfloat162 h0 = __floats2bfloat162_rn(x[q * 8 + 0], x[q * 8 + 1]);
-                __nv_bfloat162 h1 = __floats2bfloat162_rn(x[q * 8 + 2], x[q * 8 + 3]);
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(x[q * 8 + 4], x[q * 8 + 5]);
-                __nv_bfloat162 h3 = __floats2bfloat162_rn(x[q * 8 + 6], x[q * 8 + 7]);
-                u.x = *reinterpret_cast<uint32_t*>(&h0);
-                u.y = *reinterpret_cast<uint32_t*>(&h1);
-                u.z = *reinterpret_cast<uint32_t*>(&h2);
-                u.w = *reinterpret_cast<uint32_t*>(&h3);
-                const int kb2 = q >> 3, c16 = q & 7;
-                *reinterpret_cast<uint4*>(sP + kb2 * (kBlk * 128) + r * 128 + ((c16 ^ (r & 7)) * 16)) = u;
-            }
-            if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rescale this row of O
+            for (int cc = 0; cc < kOc / 32; ++cc) {
+                float v[32];
+                tmem_ld_32x32b_x32(o_cols + cc * 32, v);
 #pragma unroll
-                for (int c = 0; c < D / 32; ++c) {
-                    float v[32];
-                    tmem_ld_32x32b_x32(tmem + lane_base + C::kTmemO + c * 32, v);
+                for (int g = 0; g < 4; ++g) {
+                    uint4 u;
+                    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] *= alpha;
-                    tmem_st_32x32b_x32(tmem + lane_base + C::kTmemO + c * 32, v);
+                    for (int e = 0; e < 4; ++e) {
+                        __nv_bfloat162 hh = __floats2bfloat162_rn(v[g * 8 + 2 * e] * inv, v[g * 8 + 2 * e + 1] * inv);
+                        w[e] = *reinterpret_cast<uint32_t*>(&hh);
+                    }
+                    *reinterpret_cast<uint4*>(orow + cc * 32 + g * 8) = u;
                 }
             }
-            fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(p_full);
+            if (lane == 0) mbar_arrive(&o_empty[ob]);
+            if (half == 0) a.lse[(static_cast<int64_t>(c.bi) * a.H + c.head) * a.s + q] = m + __log2f(lt);
         }
-        mbar_wait(pv_done, (nkv - 1) & 1);
-        tc_fence_after();
-        const float inv = 1.f / l;
-        const int q = qb * kBlk + r;
-        __nv_bfloat16* orow = a.o + (static_cast<int64_t>(bi) * a.s + q) * a.h + head * D;
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-            float v[32];
-            tmem_ld_32x32b_x32(tmem + lane_base + C::kTmemO + c * 32, v);
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                uint4 u;
-                uint32_t* w = reinterpret_cast<uint32_t*>(&u);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    __nv_bfloat162 hh = __floats2bfloat162_rn(v[g * 8 + 2 * e] * inv, v[g * 8 + 2 * e + 1] * inv);
-                    w[e] = *reinterpret_cast<uint32_t*>(&hh);
-                }
-                *reinterpret_cast<uint4*>(orow + c * 32 + g * 8) = u;
-            }
-        }
-        a.lse[(static_cast<int64_t>(bi) * a.H + head) * a.s + q] = m + __log2f(l);
     }
     tc_fence_before();
     __syncthreads();
@@ -304,8 +403,9 @@ cudaError_t launch_fwd(const FlashPlan& p, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    FaArgs a{p.o, p.lse, p.s, p.H, p.H * p.d, p.scale_log2, p.causal};
-    dim3 grid(p.s / kBlk, p.H, p.b);
+    FaArgs a{p.o, p.lse, p.s, p.H, p.H * p.d, p.b, p.scale_log2, p.causal};
+    const int tiles = p.s / kBlk * p.H * p.b;
+    const int grid = tiles < sm_count() ? tiles : sm_count();
     flash_fwd_kernel<D><<<grid, kThreads, C::kSmem, st>>>(p.tmQK, p.tmV, a);
     return cudaPeekAtLastError();
 }
@@ -368,17 +468,15 @@ struct BwArgs {
     int causal;
 };
 
-__device__ __forceinline__ void st_bf16_swz(uint8_t* buf, int r, int c0, const float* v8) {
+__device__ __forceinline__ void st_bf16_swz(uint32_t buf, int r, int c0, const float* v8) {
     // 8 consecutive columns c0..c0+7 of row r into a [2][128 rows x 128 B] K-major swizzled buffer
     uint4 u;
-    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        __nv_bfloat162 hh = __floats2bfloat162_rn(v8[2 * e], v8[2 * e + 1]);
-        w[e] = *reinterpret_cast<uint32_t*>(&hh);
-    }
+    u.x = pack_bf16(v8[0], v8[1]);
+    u.y = pack_bf16(v8[2], v8[3]);
+    u.z = pack_bf16(v8[4], v8[5]);
+    u.w = pack_bf16(v8[6], v8[7]);
     const int kb = c0 >> 6, c16 = (c0 & 63) >> 3;
-    *reinterpret_cast<uint4*>(buf + kb * (kBlk * 128) + r * 128 + ((c16 ^ (r & 7)) * 16)) = u;
+    sts128(buf + kb * (kBlk * 128) + r * 128 + ((c16 ^ (r & 7)) * 16), u);
 }
 
 template <int D, bool KV>
@@ -425,8 +523,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&ld_empty[i], 1);
         }
         mbar_init(xy_full, 1);
-        mbar_init(xy_free, 4);
-        mbar_init(pd_full, 4);
+        mbar_init(xy_free, 8);
+        mbar_init(pd_full, 8);
         mbar_init(acc_done, 1);
         fence_barrier_init();
     }
@@ -523,8 +621,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (S == 1 && t + 1 < nsteps) issue_xy(t + 1);
             }
         }
-    } else if (warp >= 4) {  // ---------------- elementwise warps: thread = row of the fixed block
+    } else if (warp >= 4) {  // ---------------- elementwise warps: thread = (row of the fixed block, column half)
         const int quad = warp & 3;
+        const int half = (warp - 4) >> 2;  // columns [64*half, 64*half + 64) of X/Y
         const int r = quad * 32 + static_cast<int>(lane);
         const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
         const int64_t rowbase = (static_cast<int64_t>(bi) * a.H + head) * a.s;
@@ -533,47 +632,48 @@ __global__ void __launch_bounds__(kThreads, 1)
             my_lse = a.lse[rowbase + blk * kBlk + r];
             my_d = a.dsum[rowbase + blk * kBlk + r];
         }
+        const uint32_t rowv0 = smem_u32(sRow);
         for (int t = 0; t < nsteps; ++t) {
             const int other = first + t;  // index of the stepped block
-            float* rowv = sRow + (t & 1) * 2 * kBlk;
-            if (KV) {  // this step's per-query lse / D -> smem (named barrier over the 4 warps)
-                rowv[r] = a.lse[rowbase + other * kBlk + r];
-                rowv[kBlk + r] = a.dsum[rowbase + other * kBlk + r];
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+            const uint32_t rowv = rowv0 + (t & 1) * 2 * kBlk * 4;
+            if (KV) {  // this step's per-query lse (half 0) / D (half 1) -> smem, named barrier over the 8 warps
+                sts32f(rowv + (half * kBlk + r) * 4, (half == 0 ? a.lse : a.dsum)[rowbase + other * kBlk + r]);
+                asm volatile("bar.sync 1, 256;" ::: "memory");
             }
             mbar_wait(xy_full, t & 1);
             tc_fence_after();
+            // this thread's 64 columns of X and Y, then release the score accumulators
+            float x[64], y[64];
+            tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kX + half * 64, x);
+            tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kX + half * 64 + 32, x + 32);
+            tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kY + half * 64, y);
+            tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kY + half * 64 + 32, y + 32);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(xy_free);
+            const bool diag = a.causal && other == blk;
+            // P (into x) and dS (into y) in registers, before waiting for the previous
+            // step's accumulating products to release the smem operands
+#pragma unroll
+            for (int e = 0; e < 64; ++e) {
+                const int col = half * 64 + e;
+                // KV: row = key, col = query -> valid iff query >= key ; Q: row = query, col = key
+                const bool valid = !diag || (KV ? col >= r : col <= r);
+                const float l2 = KV ? lds32f(rowv + col * 4) : my_lse;
+                const float dd = KV ? lds32f(rowv + (kBlk + col) * 4) : my_d;
+                const float pv = valid ? ex2(fmaf(x[e], a.scale_log2, -l2)) : 0.f;
+                x[e] = pv;
+                y[e] = a.tau * pv * (y[e] - dd);
+            }
             if (t > 0) {
                 mbar_wait(acc_done, (t - 1) & 1);  // previous step's MMAs done reading sP / sDS
             }
-            const bool diag = a.causal && other == blk;
-#pragma unroll 1
-            for (int c = 0; c < kBlk / 32; ++c) {
-                float x[32], y[32];
-                tmem_ld_32x32b_x32(tmem + lane_base + C::kX + c * 32, x);
-                tmem_ld_32x32b_x32(tmem + lane_base + C::kY + c * 32, y);
-                if (c == kBlk / 32 - 1) {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(xy_free);
-                }
-                float p[32], ds[32];
+            const uint32_t pbuf = smem_u32(sP), dbuf = smem_u32(sDS);
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int col = c * 32 + e;
-                    // KV: row = key, col = query -> valid iff query >= key ; Q: row = query, col = key
-                    const bool valid = !diag || (KV ? col >= r : col <= r);
-                    const float l2 = KV ? rowv[col] : my_lse;
-                    const float dd = KV ? rowv[kBlk + col] : my_d;
-                    const float pv = valid ? ex2(x[e] * a.scale_log2 - l2) : 0.f;
-                    p[e] = pv;
-                    ds[e] = a.tau * pv * (y[e] - dd);
-                }
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    if (KV) st_bf16_swz(sP, r, c * 32 + g * 8, p + g * 8);
-                    st_bf16_swz(sDS, r, c * 32 + g * 8, ds + g * 8);
-                }
+            for (int g = 0; g < 8; ++g) {
+                if (KV) st_bf16_swz(pbuf, r, half * 64 + g * 8, x + g * 8);
+                st_bf16_swz(dbuf, r, half * 64 + g * 8, y + g * 8);
             }
             fence_proxy_async_smem();
             tc_fence_before();
@@ -582,28 +682,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(acc_done, (nsteps - 1) & 1);
         tc_fence_after();
-        // epilogue: accumulators -> dqkv (bf16); KV: acc1 = dV (section 2), acc2 = dK (section 1); Q: acc1 = dQ
+        // epilogue: accumulators -> dqkv (bf16).  KV: half 0 writes dV (acc1, section 2),
+        // half 1 writes dK (acc2, section 1).  Q: acc1 = dQ, half h writes columns [h*D/2, +D/2).
         const int row = blk * kBlk + r;
         __nv_bfloat16* base = a.dqkv + (static_cast<int64_t>(bi) * a.s + row) * (3 * a.h) + head * D;
+        __nv_bfloat16* dst = KV ? base + (half == 0 ? 2 * a.h : a.h) : base + half * (D / 2);
+        const uint32_t col0 = KV ? (half == 0 ? C::kAcc1 : C::kAcc2) : C::kAcc1 + half * (D / 2);
+        constexpr int kCols = KV ? D : D / 2;
 #pragma unroll
-        for (int which = 0; which < (KV ? 2 : 1); ++which) {
-            __nv_bfloat16* dst = base + (KV ? (which == 0 ? 2 * a.h : a.h) : 0);
-            const uint32_t col0 = which == 0 ? C::kAcc1 : C::kAcc2;
+        for (int c = 0; c < kCols / 32; ++c) {
+            float v[32];
+            tmem_ld_32x32b_x32(tmem + lane_base + col0 + c * 32, v);
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                float v[32];
-                tmem_ld_32x32b_x32(tmem + lane_base + col0 + c * 32, v);
+            for (int g = 0; g < 4; ++g) {
+                uint4 u;
+                uint32_t* w = reinterpret_cast<uint32_t*>(&u);
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    uint4 u;
-                    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        __nv_bfloat162 hh = __floats2bfloat162_rn(v[g * 8 + 2 * e], v[g * 8 + 2 * e + 1]);
-                        w[e] = *reinterpret_cast<uint32_t*>(&hh);
-                    }
-                    *reinterpret_cast<uint4*>(dst + c * 32 + g * 8) = u;
+                for (int e = 0; e < 4; ++e) {
+                    __nv_bfloat162 hh = __floats2bfloat162_rn(v[g * 8 + 2 * e], v[g * 8 + 2 * e + 1]);
+                    w[e] = *reinterpret_cast<uint32_t*>(&hh);
                 }
+                *reinterpret_cast<uint4*>(dst + c * 32 + g * 8) = u;
             }
         }
     }

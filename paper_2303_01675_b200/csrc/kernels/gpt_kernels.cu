@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "gpt_kernels.h"
@@ -138,28 +139,30 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(const __nv_bfloat16* __rest
     }
 }
 
-// Column partial sums over 32-row chunks, 256 columns per block: thread
-// (rg, cg) accumulates 4 rows x 8 columns with 16-byte loads, then the 8 row
-// groups are combined in smem in a fixed order -> part[chunk][col].
+// Column sums into persistent per-parameter partials part[kVecParts][cols]
+// (+=).  Block (cx, p) owns rows [p*rows/P, (p+1)*rows/P) x 256 columns:
+// thread (rg, cg) accumulates every 8th row of the range over 8 columns with
+// 16-byte loads, the 8 row groups are combined in smem in a fixed order and
+// added to its own partial row.  Every (p, c) has one owner and micro-batches
+// run in stream order, so the sums are deterministic; vec_grad_finalize folds
+// the P partials into the gradient once per iteration (not per micro-batch).
 // AFFINE: part_g += dy * (x - mean) * rstd and part_b += dy (LayerNorm affine
 // grads); otherwise part_b += m (bias grads).
-constexpr int kColRows = 32;
 template <bool AFFINE>
 __global__ void __launch_bounds__(256) colpart_kernel(const __nv_bfloat16* __restrict__ dy,
                                                       const __nv_bfloat16* __restrict__ x,
                                                       const float* __restrict__ mean_in,
                                                       const float* __restrict__ rstd_in, float* __restrict__ part_g,
                                                       float* __restrict__ part_b, int rows, int cols) {
-    __shared__ float sg[8][257];
+    __shared__ float sg[AFFINE ? 8 : 1][257];
     __shared__ float sb[8][257];
     const int cg = threadIdx.x & 31, rg = threadIdx.x >> 5;
     const int c0 = blockIdx.x * 256 + cg * 8;
-    const int r0 = blockIdx.y * kColRows + rg * 4;
+    const int per = rows / kVecParts;
+    const int r_end = (blockIdx.y + 1) * per;
     float ag[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, ab[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int row = r0 + r;
-        if (row >= rows) break;
+#pragma unroll 4
+    for (int row = blockIdx.y * per + rg; row < r_end; row += 8) {
         float d[8];
         load8(dy + static_cast<int64_t>(row) * cols + c0, d);
         if (AFFINE) {
@@ -186,21 +189,26 @@ __global__ void __launch_bounds__(256) colpart_kernel(const __nv_bfloat16* __res
         if (AFFINE) tg += sg[k][c];
     }
     const int64_t o = static_cast<int64_t>(blockIdx.y) * cols + blockIdx.x * 256 + c;
-    part_b[o] = tb;
-    if (AFFINE) part_g[o] = tg;
+    part_b[o] += tb;
+    if (AFFINE) part_g[o] += tg;
 }
 
-// out[y][c] += sum_{p < nparts} part[y][p][c]   (ascending p; y selects one of two vectors)
-__global__ void reduce_partials_kernel(const float* __restrict__ part0, float* __restrict__ out0,
-                                       const float* __restrict__ part1, float* __restrict__ out1, int nparts,
-                                       int cols) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= cols) return;
-    const float* part = blockIdx.y == 0 ? part0 : part1;
-    float* out = blockIdx.y == 0 ? out0 : out1;
-    float s = 0.f;
-    for (int p = 0; p < nparts; ++p) s += part[static_cast<int64_t>(p) * cols + c];
-    out[c] += s;
+// grad[c] += sum_{p < P} part[p][c] (ascending p), part zeroed: one block row
+// per 1-D parameter of the stage, one launch per iteration.
+__global__ void __launch_bounds__(256) vec_finalize_kernel(const VecGradSeg* __restrict__ segs) {
+    const VecGradSeg sg = segs[blockIdx.y];
+    for (int c = blockIdx.x * 256 + threadIdx.x; c < sg.cols; c += gridDim.x * 256) {
+        float v[kVecParts];
+#pragma unroll
+        for (int p = 0; p < kVecParts; ++p) v[p] = sg.part[static_cast<int64_t>(p) * sg.cols + c];
+        float acc = 0.f;
+#pragma unroll
+        for (int p = 0; p < kVecParts; ++p) {
+            acc += v[p];
+            sg.part[static_cast<int64_t>(p) * sg.cols + c] = 0.f;
+        }
+        sg.grad[c] += acc;
+    }
 }
 
 // --------------------------------------------------------------- softmax (causal)
@@ -577,29 +585,27 @@ cudaError_t layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const 
     return cudaPeekAtLastError();
 }
 
-int layernorm_bwd_parts(int rows) { return (rows + kColRows - 1) / kColRows; }
-
 cudaError_t layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* mean, const float* rstd,
-                          const __nv_bfloat16* g, const __nv_bfloat16* resid, __nv_bfloat16* dx, float* dgamma,
-                          float* dbeta, float* scratch, int rows, int h, cudaStream_t st) {
-    if (h % 256) return cudaErrorInvalidValue;
+                          const __nv_bfloat16* g, const __nv_bfloat16* resid, __nv_bfloat16* dx, float* part_g,
+                          float* part_b, int rows, int h, cudaStream_t st) {
+    if (h % 256 || rows % kVecParts) return cudaErrorInvalidValue;
     PTK_DISPATCH_V(h, (ln_bwd_kernel<V><<<(rows + 3) / 4, 128, 0, st>>>(dy, x, mean, rstd, g, resid, dx, rows)));
-    const int parts = layernorm_bwd_parts(rows);
-    float* pg = scratch;
-    float* pb = scratch + static_cast<int64_t>(parts) * h;
-    colpart_kernel<true><<<dim3(h / 256, parts), 256, 0, st>>>(dy, x, mean, rstd, pg, pb, rows, h);
-    reduce_partials_kernel<<<dim3((h + 255) / 256, 2), 256, 0, st>>>(pg, dgamma, pb, dbeta, parts, h);
+    colpart_kernel<true><<<dim3(h / 256, kVecParts), 256, 0, st>>>(dy, x, mean, rstd, part_g, part_b, rows, h);
     return cudaPeekAtLastError();
 }
 
-int colsum_parts(int rows) { return (rows + kColRows - 1) / kColRows; }
+cudaError_t colsum_partial(const __nv_bfloat16* m, float* part, int rows, int cols, cudaStream_t st) {
+    if (cols % 256 || rows % kVecParts) return cudaErrorInvalidValue;
+    colpart_kernel<false><<<dim3(cols / 256, kVecParts), 256, 0, st>>>(m, nullptr, nullptr, nullptr, nullptr, part,
+                                                                      rows, cols);
+    return cudaPeekAtLastError();
+}
 
-cudaError_t colsum_accumulate(const __nv_bfloat16* m, float* out, float* scratch, int rows, int cols, cudaStream_t st) {
-    if (cols % 256) return cudaErrorInvalidValue;
-    const int parts = colsum_parts(rows);
-    colpart_kernel<false><<<dim3(cols / 256, parts), 256, 0, st>>>(m, nullptr, nullptr, nullptr, nullptr, scratch,
-                                                                  rows, cols);
-    reduce_partials_kernel<<<dim3((cols + 255) / 256, 1), 256, 0, st>>>(scratch, out, scratch, out, parts, cols);
+cudaError_t vec_grad_finalize(const VecGradSeg* segs_dev, int nseg, int max_cols, cudaStream_t st) {
+    if (nseg <= 0) return cudaSuccess;
+    if (nseg > 65535) return cudaErrorInvalidValue;
+    const int gx = std::min(16, (max_cols + 255) / 256);
+    vec_finalize_kernel<<<dim3(gx, nseg), 256, 0, st>>>(segs_dev);
     return cudaPeekAtLastError();
 }
 
@@ -634,10 +640,16 @@ cudaError_t embedding_fwd(const int32_t* tok, const __nv_bfloat16* wte, const __
 cudaError_t embedding_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* dwte, float* dwpe, int32_t* order,
                           int rows, int seq, int h, int vocab, cudaStream_t st) {
     (void)vocab;
-    if (h % 256 || h > 4096 || rows > 8192) return cudaErrorInvalidValue;
+    if (h % 256 || h > 4096 || rows > 16384) return cudaErrorInvalidValue;
     int n = 1;
     while (n < rows) n <<= 1;
-    embed_sort_kernel<<<1, 1024, static_cast<size_t>(n) * 8, st>>>(tok, order, rows);
+    const size_t smem = static_cast<size_t>(n) * 8;
+    if (smem > 48 * 1024) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(embed_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    embed_sort_kernel<<<1, 1024, smem, st>>>(tok, order, rows);
     PTK_DISPATCH_V(h, (embed_bwd_runs_kernel<V><<<(rows + 7) / 8, 256, 0, st>>>(tok, order, dx, dwte, rows)));
     dim3 grid((h + 255) / 256, seq);
     embed_bwd_wpe_kernel<<<grid, 256, 0, st>>>(dx, dwpe, seq, rows / seq, h);

@@ -10,14 +10,24 @@ namespace ptk {
 
 cudaError_t layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const __nv_bfloat16* b, __nv_bfloat16* y,
                           float* mean, float* rstd, int rows, int h, float eps, cudaStream_t st);
-// scratch: 2 * layernorm_bwd_parts(rows) * h floats.  dgamma/dbeta accumulate (+=).
-int layernorm_bwd_parts(int rows);
+// 1-D parameter gradients (LayerNorm affine, biases) accumulate into
+// per-parameter partials float[kVecParts][cols] over the micro-batches of an
+// iteration; vec_grad_finalize adds them into the gradient (fixed order) and
+// clears them.  rows % kVecParts == 0.
+constexpr int kVecParts = 64;
+struct VecGradSeg {
+    float* grad;
+    float* part;
+    int cols;
+};
+// dx = LN'(dy) (+ resid); part_g/part_b += the gamma/beta column partials.
 cudaError_t layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* mean, const float* rstd,
-                          const __nv_bfloat16* g, const __nv_bfloat16* resid, __nv_bfloat16* dx, float* dgamma,
-                          float* dbeta, float* scratch, int rows, int h, cudaStream_t st);
-// out[c] += sum_r m[r][c]; scratch: colsum_parts(rows) * cols floats.
-int colsum_parts(int rows);
-cudaError_t colsum_accumulate(const __nv_bfloat16* m, float* out, float* scratch, int rows, int cols, cudaStream_t st);
+                          const __nv_bfloat16* g, const __nv_bfloat16* resid, __nv_bfloat16* dx, float* part_g,
+                          float* part_b, int rows, int h, cudaStream_t st);
+// part[p][c] += sum over row block p of m[r][c].
+cudaError_t colsum_partial(const __nv_bfloat16* m, float* part, int rows, int cols, cudaStream_t st);
+// segs_dev: device array of nseg segments; max_cols: the widest segment.
+cudaError_t vec_grad_finalize(const VecGradSeg* segs_dev, int nseg, int max_cols, cudaStream_t st);
 cudaError_t softmax_causal_fwd(const float* S, __nv_bfloat16* P, int rows, int n, float scale, cudaStream_t st);
 cudaError_t softmax_causal_bwd(const __nv_bfloat16* P, const float* dP, __nv_bfloat16* dS, int rows, int n,
                                float scale, cudaStream_t st);

@@ -55,6 +55,7 @@ extern "C" int ptk_stage_backward(ptk_stage* st, int slot, const int32_t* tok, c
     return guarded("ptk_stage_backward", [&] {
         st->impl->backward(slot, tok, static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx),
                           static_cast<cudaStream_t>(stream));
+        st->impl->finalize_grads(static_cast<cudaStream_t>(stream));  // grads complete in stream order
     });
 }
 

@@ -209,7 +209,6 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
 
     // ---- scratch
     dsum_ = static_cast<float*>(alloc(static_cast<int64_t>(c.micro_batch_size) * c.heads * c.seq * 4));
-    const int64_t wide = std::max<int64_t>(std::max<int64_t>(3 * h, f), h);
     g_a_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
     g_b_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
     d_pre_ = static_cast<__nv_bfloat16*>(alloc(T * f * 2));
@@ -218,8 +217,24 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
     dqkv_ = static_cast<__nv_bfloat16*>(alloc(T * 3 * h * 2));
     dx_mid_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
     dy_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
-    const int64_t parts = std::max(colsum_parts(static_cast<int>(T)), layernorm_bwd_parts(static_cast<int>(T)));
-    red_ = static_cast<float*>(alloc(2 * parts * std::max<int64_t>(wide, V) * 4));
+    // 1-D parameter gradient partials (see vec_grad_finalize)
+    {
+        std::vector<VecGradSeg> segs;
+        for (const ParamInfo& p : params_) {
+            if (p.rows != 1) continue;
+            float* part = static_cast<float*>(alloc(static_cast<size_t>(kVecParts) * p.cols * 4));
+            ck(cudaMemset(part, 0, static_cast<size_t>(kVecParts) * p.cols * 4), "memset");
+            vparts_[p.offset] = part;
+            segs.push_back({grad_ + p.offset, part, static_cast<int>(p.cols)});
+            vparts_bytes_ += static_cast<size_t>(kVecParts) * p.cols * 4;
+            vseg_max_cols_ = std::max<int>(vseg_max_cols_, static_cast<int>(p.cols));
+        }
+        nvseg_ = static_cast<int>(segs.size());
+        if (nvseg_ > 0) {
+            vsegs_ = static_cast<VecGradSeg*>(alloc(segs.size() * sizeof(VecGradSeg)));
+            ck(cudaMemcpy(vsegs_, segs.data(), segs.size() * sizeof(VecGradSeg), cudaMemcpyHostToDevice), "copy");
+        }
+    }
     loss_rows_ = static_cast<float*>(alloc(T * 4));
     order_ = static_cast<int32_t*>(alloc(T * 4));
     loss_acc_ = static_cast<float*>(alloc(64));
@@ -338,7 +353,7 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
     const __nv_bfloat16* W = wbf_;
     float* G = grad_;
     // dz = LN2'(dy)
-    kl(3, layernorm_bwd(dy, s.ln2, s.mean2, s.rstd2, W + w.ln2_g, nullptr, d_ln_, G + w.ln2_g, G + w.ln2_b, red_, T,
+    kl(2, layernorm_bwd(dy, s.ln2, s.mean2, s.rstd2, W + w.ln2_g, nullptr, d_ln_, vp(w.ln2_g), vp(w.ln2_b), T,
                         h, st),
        "ln2 bwd");
     {  // d_pre = dz W2 * gelu'(pre)
@@ -347,24 +362,24 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
         gemm(g, st);
     }
     gemm(desc(h, f, T, mat(d_ln_, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
-    kl(2, colsum_accumulate(d_ln_, G + w.b_fc2, red_, T, h, st), "db2");
+    kl(1, colsum_partial(d_ln_, vp(w.b_fc2), T, h, st), "db2");
     {  // d_xmid = d_pre W1 + dz   (residual around the FFN)
         ptk_gemm_desc g = desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(dx_mid_, h), PTK_EPI_BF16);
         g.aux = mat(d_ln_, h);
         gemm(g, st);
     }
     gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.x_mid, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
-    kl(2, colsum_accumulate(d_pre_, G + w.b_fc1, red_, T, f, st), "db1");
+    kl(1, colsum_partial(d_pre_, vp(w.b_fc1), T, f, st), "db1");
     // dy_ = LN1'(d_xmid)
-    kl(3, layernorm_bwd(dx_mid_, s.ln1, s.mean1, s.rstd1, W + w.ln1_g, nullptr, dy_, G + w.ln1_g, G + w.ln1_b, red_,
+    kl(2, layernorm_bwd(dx_mid_, s.ln1, s.mean1, s.rstd1, W + w.ln1_g, nullptr, dy_, vp(w.ln1_g), vp(w.ln1_b),
                         T, h, st),
        "ln1 bwd");
     gemm(desc(T, h, h, mat(dy_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
     gemm(desc(h, h, T, mat(dy_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
-    kl(2, colsum_accumulate(dy_, G + w.b_o, red_, T, h, st), "dbo");
+    kl(1, colsum_partial(dy_, vp(w.b_o), T, h, st), "dbo");
     attention_backward(s, st);
     gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.x_in, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
-    kl(2, colsum_accumulate(dqkv_, G + w.b_qkv, red_, T, 3 * h, st), "dbqkv");
+    kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
     {  // dx = dqkv Wqkv + dy_   (residual around attention)
         ptk_gemm_desc g = desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(dx, h), PTK_EPI_BF16);
         g.aux = mat(dy_, h);
@@ -421,26 +436,26 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
         gemm(g, st);
     }
     gemm(desc(h, f, T, mat(dy, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
-    kl(2, colsum_accumulate(dy, G + w.b_fc2, red_, T, h, st), "db2");
+    kl(1, colsum_partial(dy, vp(w.b_fc2), T, h, st), "db2");
     // FC1: d_ln2 = d_pre W1; dW1 += d_preᵀ ln2; db1 += Σ d_pre
     gemm(desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
     gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.ln2, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
-    kl(2, colsum_accumulate(d_pre_, G + w.b_fc1, red_, T, f, st), "db1");
+    kl(1, colsum_partial(d_pre_, vp(w.b_fc1), T, f, st), "db1");
     // LN2 backward + residual: dx_mid = LN2'(d_ln2) + dy
-    kl(3, layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, G + w.ln2_g, G + w.ln2_b, red_, T, h,
+    kl(2, layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, vp(w.ln2_g), vp(w.ln2_b), T, h,
                      st),
        "ln2 bwd");
     // out-proj: d_attn = dx_mid Wo; dWo += dx_midᵀ o; dbo += Σ dx_mid
     gemm(desc(T, h, h, mat(dx_mid_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
     gemm(desc(h, h, T, mat(dx_mid_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
-    kl(2, colsum_accumulate(dx_mid_, G + w.b_o, red_, T, h, st), "dbo");
+    kl(1, colsum_partial(dx_mid_, vp(w.b_o), T, h, st), "dbo");
     attention_backward(s, st);
     // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv += Σ dqkv
     gemm(desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
     gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
-    kl(2, colsum_accumulate(dqkv_, G + w.b_qkv, red_, T, 3 * h, st), "dbqkv");
+    kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
     // LN1 backward + residual: dx = LN1'(d_ln1) + dx_mid
-    kl(3, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, dx_mid_, dx, G + w.ln1_g, G + w.ln1_b, red_, T, h,
+    kl(2, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, dx_mid_, dx, vp(w.ln1_g), vp(w.ln1_b), T, h,
                      st),
        "ln1 bwd");
 }
@@ -508,16 +523,16 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
              st);
         if (bert()) {
             // dt = LN_h'(dxf); d_tpre = dt * gelu'(t_pre); dx_fin = d_tpre Wt; dWt += d_tpreᵀ x_fin
-            kl(3, layernorm_bwd(d_ln_, hs.t_act, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, dx_mid_, G + lnf_g_,
-                                G + lnf_b_, red_, T, h, st),
+            kl(2, layernorm_bwd(d_ln_, hs.t_act, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, dx_mid_, vp(lnf_g_),
+                                vp(lnf_b_), T, h, st),
                "lnh bwd");
             kl(1, dgelu_mul(dx_mid_, hs.t_pre, dy_, static_cast<int64_t>(T) * h, st), "dgelu");
             gemm(desc(T, h, h, mat(dy_, h), mat(W + w_t_, h, 1), mat(g_a_, h), PTK_EPI_BF16), st);
             gemm(desc(h, h, T, mat(dy_, h, 1), mat(hs.x_fin, h, 1), mat(G + w_t_, h), PTK_EPI_ACC_F32), st);
-            kl(2, colsum_accumulate(dy_, G + b_t_, red_, T, h, st), "dbt");
+            kl(1, colsum_partial(dy_, vp(b_t_), T, h, st), "dbt");
         } else {
-            kl(3, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, G + lnf_g_, G + lnf_b_,
-                                red_, T, h, st),
+            kl(2, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, vp(lnf_g_),
+                                vp(lnf_b_), T, h, st),
                "lnf bwd");
         }
         g = g_a_;
@@ -533,7 +548,7 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
     if (c.has_embedding && bert()) {  // through the embedding LayerNorm
         EmbStash& e = emb_[static_cast<size_t>(slot)];
         __nv_bfloat16* dsum_bf = (g == g_a_) ? g_b_ : g_a_;
-        kl(3, layernorm_bwd(g, e.sum, e.mean, e.rstd, W + lne_g_, nullptr, dsum_bf, G + lne_g_, G + lne_b_, red_, T, h,
+        kl(2, layernorm_bwd(g, e.sum, e.mean, e.rstd, W + lne_g_, nullptr, dsum_bf, vp(lne_g_), vp(lne_b_), T, h,
                             st),
            "emb ln bwd");
         g = dsum_bf;
@@ -545,7 +560,18 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
     }
 }
 
+float* GptStage::vp(int64_t offset) {
+    auto it = vparts_.find(offset);
+    if (it == vparts_.end()) throw std::logic_error("no gradient partials for a 1-D parameter");
+    return it->second;
+}
+
+void GptStage::finalize_grads(cudaStream_t st) {
+    kl(1, vec_grad_finalize(vsegs_, nvseg_, vseg_max_cols_, st), "finalize grads");
+}
+
 void GptStage::optimizer_step(float lr, float wd, cudaStream_t st) {
+    finalize_grads(st);
     ++step_;
     kl(1, adamw_step(master_, grad_, adam_m_, adam_v_, wbf_, total_, lr, 0.9f, 0.95f, 1e-8f, wd, step_, st), "adamw");
 }
@@ -563,6 +589,14 @@ void GptStage::collect_timing() {
     timing_.flops.clear();
 }
 
-void GptStage::zero_grads(cudaStream_t st) { ck(cudaMemsetAsync(grad_, 0, total_ * 4, st), "zero grads"); }
+void GptStage::zero_grads(cudaStream_t st) {
+    ck(cudaMemsetAsync(grad_, 0, total_ * 4, st), "zero grads");
+    for (const auto& kv : vparts_) {
+        const ParamInfo* p = nullptr;
+        for (const ParamInfo& q : params_)
+            if (q.offset == kv.first) p = &q;
+        ck(cudaMemsetAsync(kv.second, 0, static_cast<size_t>(kVecParts) * p->cols * 4, st), "zero partials");
+    }
+}
 
 }  // namespace ptk

@@ -16,6 +16,7 @@
 #include "../../../include/ptk.h"
 #include "../kernels/attention_sm100.h"
 #include "../kernels/gemm_sm100.h"
+#include "../kernels/gpt_kernels.h"
 
 namespace ptk {
 
@@ -64,6 +65,9 @@ class GptStage {
     // dy: device bf16 [T, h] gradient of this stage's output (ignored on the
     // head stage); dx: gradient of the input (ignored on the embedding stage).
     void backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st);
+    // Folds the 1-D parameter partials of the micro-batches run so far into
+    // grads() (one launch; idempotent).  optimizer_step() calls it first.
+    void finalize_grads(cudaStream_t st);
     void optimizer_step(float lr, float wd, cudaStream_t st);
     void zero_grads(cudaStream_t st);
 
@@ -144,9 +148,16 @@ class GptStage {
 
     // scratch (one micro-batch in flight on the compute stream at a time)
     int32_t* order_ = nullptr;
-    float *dsum_ = nullptr, *red_ = nullptr, *loss_rows_ = nullptr, *loss_acc_ = nullptr;
+    float *dsum_ = nullptr, *loss_rows_ = nullptr, *loss_acc_ = nullptr;
     __nv_bfloat16 *g_a_ = nullptr, *g_b_ = nullptr, *d_pre_ = nullptr, *d_ln_ = nullptr,
                   *d_attn_ = nullptr, *dqkv_ = nullptr, *dx_mid_ = nullptr, *dy_ = nullptr;
+
+    // 1-D parameter gradient partials: grad offset -> float[kVecParts][cols]
+    std::unordered_map<int64_t, float*> vparts_;
+    VecGradSeg* vsegs_ = nullptr;  // device table for vec_grad_finalize
+    int nvseg_ = 0, vseg_max_cols_ = 0;
+    size_t vparts_bytes_ = 0;
+    float* vp(int64_t offset);
 
     std::vector<void*> allocs_;
     GemmCache cache_;

@@ -5,6 +5,7 @@ Same layer shapes as the bench (h2048, 32 heads, s1024, V50304, b=2) but
 """
 import argparse
 import sys
+import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -16,9 +17,16 @@ p = argparse.ArgumentParser()
 p.add_argument("--layers", type=int, default=2)
 p.add_argument("--mb", type=int, default=2)
 p.add_argument("--iters", type=int, default=2)
+p.add_argument("--model", choices=["gpt", "bert"], default="gpt")
+p.add_argument("--b", type=int, default=0, help="micro-batch size (default 2 GPT / 4 BERT)")
 a = p.parse_args()
-shape = ModelShape(a.layers, 2048, 32, 8192, 1024, 50304)
-ex = StageExecutor(shape, 0, 1, 2 * a.mb, b_max=2, slots=1, layers=(0, a.layers))
+if a.model == "bert":
+    shape, b = ModelShape(a.layers, 1024, 16, 4096, 512, 30528, "bert"), a.b or 4
+else:
+    shape, b = ModelShape(a.layers, 2048, 32, 8192, 1024, 50304), a.b or 2
+ex = StageExecutor(shape, 0, 1, b * a.mb, b_max=b, slots=1, layers=(0, a.layers))
 for i in range(a.iters):
+    t0 = time.perf_counter()
     ex.run_iteration(i)
-    print(f"iter {i}: {ex.finish_iteration():.2f} ms", flush=True)
+    host = (time.perf_counter() - t0) * 1e3
+    print(f"iter {i}: {ex.finish_iteration():.2f} ms (host enqueue {host:.2f} ms)", flush=True)
