@@ -435,38 +435,90 @@ cudaError_t flash_forward(const FlashPlan& p, cudaStream_t st) {
 }
 
 // ============================================================================
-// Backward.  Deterministic two-kernel form (no atomics):
-//   mode KV: CTA per (key block j, head, sample), loop query blocks i >= j:
+// Backward.  Deterministic two-kernel form (no atomics), both persistent:
+//   mode KV: tile = (key block j, head, sample), steps over query blocks i >= j:
 //     Sᵀ = K_j Q_iᵀ, dPᵀ = V_j dO_iᵀ            (TMEM, thread = key row)
 //     Pᵀ = 2^(Sᵀ c - lse2[q]),  dSᵀ = τ Pᵀ (dPᵀ - D[q])   -> smem (bf16)
 //     dV_j += Pᵀ dO_i,  dK_j += dSᵀ Q_i           (TMEM accumulators)
-//   mode Q:  CTA per (query block i, head, sample), loop key blocks j <= i:
+//   mode Q:  tile = (query block i, head, sample), steps over key blocks j <= i:
 //     S = Q_i K_jᵀ, dP = dO_i V_jᵀ  (thread = query row)
 //     dS = τ P (dP - D[q])  -> smem;  dQ_i += dS K_j
 // A [rows][64-col] 128B-swizzled tile is simultaneously the K-major operand
 // for the score products and the MN-major operand (LBO = 16 KiB between
 // 64-wide column atoms) for the accumulating products, so every operand is
 // loaded once per step.  D = rowsum(dO ∘ O) comes from attn_bwd_dot_kernel.
+// One CTA per SM walks its tiles (heaviest first, boustrophedon); the fixed
+// tiles and the accumulators are double-buffered across tiles (d = 64) so a
+// tile's epilogue and the next tile's loads/score products overlap.  The
+// elementwise warps compute P/dS of step t in registers while the
+// accumulating products of step t-1 still read the smem operands.
 // ============================================================================
 namespace {
 
-template <int D>
+template <int D, bool KV>
 struct BwCfg {
     static constexpr int kTile = kBlk * D * 2;  // one [128][D] tile
     static constexpr int kStages = D == 64 ? 2 : 1;
-    static constexpr int kPd = kBlk * kBlk * 2;  // one [128][128] bf16 A-operand buffer
-    static constexpr int kSmem = 2 * kTile + kStages * 2 * kTile + 2 * kPd + 2 * 2 * kBlk * 4 + 1024 + 256;
-    static constexpr uint32_t kX = 0, kY = 128, kAcc1 = 256, kAcc2 = 256 + D;
+    static constexpr int kFixBuf = D == 64 ? 2 : 1;
+    static constexpr int kAccBuf = (KV && D == 128) ? 1 : 2;
+    static constexpr int kAccCols = KV ? 2 * D : D;  // per accumulator buffer
+    static constexpr int kPd = kBlk * kBlk * 2;      // one [128][128] bf16 A-operand buffer
+    static constexpr int kSmem =
+        kFixBuf * 2 * kTile + kStages * 2 * kTile + 2 * kPd + 2 * 2 * kBlk * 4 + 1024 + 256;
+    static constexpr uint32_t kX = 0, kY = 128, kAcc = 256;
 };
 
 struct BwArgs {
     __nv_bfloat16* dqkv;  // [b*s][3h]
     const float* lse;     // [b][H][s]
     const float* dsum;    // [b][H][s]
-    int s, H, h;
+    int s, H, h, b;
     float scale_log2, tau;
     int causal;
 };
+
+#ifdef PTK_ATTN_TRACE
+// Debug timeline of CTA 0 (clock64): [role][step][event], see scripts/attn_trace.cu.
+__device__ unsigned long long g_attn_trace[2][64][8];
+__device__ int g_attn_trace_kv = 1;  // which backward kernel records (1: KV, 0: Q)
+#define ATRACE(role, step, ev)                                                                        \
+    do {                                                                                              \
+        if (blockIdx.x == 0 && (step) < 64 && g_attn_trace_kv == (KV ? 1 : 0))                       \
+            g_attn_trace[role][step][ev] = clock64();                                                 \
+    } while (0)
+#else
+#define ATRACE(role, step, ev) \
+    do {                       \
+    } while (0)
+#endif
+
+// Position in a CTA's tile list (see fa_tile): tile k, step j of that tile.
+struct BwCursor {
+    int k, blk, head, bi, first, nsteps, j;
+    bool valid;
+};
+
+template <bool KV>
+__device__ __forceinline__ void bw_tile(const BwArgs& a, int k, BwCursor& c) {
+    const int G = gridDim.x, i = blockIdx.x;
+    const int nb = a.s / kBlk;
+    const int per = a.H * a.b;
+    const int t = (k & 1) ? (k + 1) * G - 1 - i : k * G + i;
+    c.k = k;
+    c.j = 0;
+    c.valid = t < nb * per;
+    const int rank = t / per, rem = t % per;
+    c.blk = KV ? rank : nb - 1 - rank;  // heaviest first under the causal mask
+    c.head = rem % a.H;
+    c.bi = rem / a.H;
+    c.first = (KV && a.causal) ? c.blk : 0;
+    c.nsteps = !a.causal ? nb : (KV ? nb - c.blk : c.blk + 1);
+}
+
+template <bool KV>
+__device__ __forceinline__ void bw_next(const BwArgs& a, BwCursor& c) {
+    if (++c.j == c.nsteps) bw_tile<KV>(a, c.k + 1, c);
+}
 
 __device__ __forceinline__ void st_bf16_swz(uint32_t buf, int r, int c0, const float* v8) {
     // 8 consecutive columns c0..c0+7 of row r into a [2][128 rows x 128 B] K-major swizzled buffer
@@ -479,53 +531,99 @@ __device__ __forceinline__ void st_bf16_swz(uint32_t buf, int r, int c0, const f
     sts128(buf + kb * (kBlk * 128) + r * 128 + ((c16 ^ (r & 7)) * 16), u);
 }
 
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+// 32 columns [cb0, cb0+32) of one row: P = 2^(X c - lse) and dS = P (τ Y - τ D),
+// packed to bf16 pairs.  KV: the per-column (query) lse / τD come from smem
+// (rowv); Q: the row's own my_lse / my_d.  MASK only on diagonal blocks.
+template <bool KV, bool MASK>
+__device__ __forceinline__ void bw_pass(const float (&x)[32], const float (&y)[32], uint32_t rowv, int cb0, int r,
+                                        float sc, float tau, float my_lse, float my_d, uint32_t* pk_p,
+                                        uint32_t* pk_d) {
+#pragma unroll
+    for (int e4 = 0; e4 < 8; ++e4) {
+        const int cb = cb0 + e4 * 4;
+        float l2[4], dd[4];
+        if (KV) {
+            const float4 lv = lds128f(rowv + cb * 4);
+            const float4 dv = lds128f(rowv + (kBlk + cb) * 4);
+            l2[0] = lv.x, l2[1] = lv.y, l2[2] = lv.z, l2[3] = lv.w;
+            dd[0] = dv.x, dd[1] = dv.y, dd[2] = dv.z, dd[3] = dv.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) l2[u] = my_lse, dd[u] = my_d;
+        }
+        float pv[4], dv4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float xs = x[e4 * 4 + u];
+            if (MASK) {
+                // KV: row = key, col = query -> valid iff query >= key ; Q: row = query, col = key
+                const int col = cb + u;
+                if (KV ? col < r : col > r) xs = -INFINITY;  // exp2(-inf) = 0
+            }
+            pv[u] = ex2(fmaf(xs, sc, -l2[u]));
+            dv4[u] = pv[u] * fmaf(tau, y[e4 * 4 + u], -dd[u]);
+        }
+        pk_p[e4 * 2] = pack_bf16(pv[0], pv[1]);
+        pk_p[e4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
+        pk_d[e4 * 2] = pack_bf16(dv4[0], dv4[1]);
+        pk_d[e4 * 2 + 1] = pack_bf16(dv4[2], dv4[3]);
+    }
+}
+
 template <int D, bool KV>
 __global__ void __launch_bounds__(kThreads, 1)
     flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                      const __grid_constant__ BwArgs a) {
-    using C = BwCfg<D>;
-    constexpr int S = C::kStages;
+    using C = BwCfg<D, KV>;
+    constexpr int S = C::kStages, FB = C::kFixBuf, AB = C::kAccBuf;
     constexpr uint32_t kIdescXY = make_idesc_bf16(kBlk, kBlk, false, false);
     constexpr uint32_t kIdescAcc = make_idesc_bf16(kBlk, D, false, true);
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sF0 = smem;               // fixed tile 0: K_j (KV) | Q_i (Q)
-    uint8_t* sF1 = sF0 + C::kTile;     // fixed tile 1: V_j (KV) | dO_i (Q)
-    uint8_t* sStep = sF1 + C::kTile;   // [S][2 tiles]: (Q_i, dO_i) (KV) | (K_j, V_j) (Q)
-    uint8_t* sP = sStep + S * 2 * C::kTile;  // Pᵀ (KV only)
-    uint8_t* sDS = sP + C::kPd;              // dSᵀ (KV) | dS (Q)
+    uint8_t* sFix = smem;                           // [FB][2 tiles]: (K_j, V_j) (KV) | (Q_i, dO_i) (Q)
+    uint8_t* sStep = sFix + FB * 2 * C::kTile;      // [S][2 tiles]: (Q_i, dO_i) (KV) | (K_j, V_j) (Q)
+    uint8_t* sP = sStep + S * 2 * C::kTile;         // Pᵀ (KV only)
+    uint8_t* sDS = sP + C::kPd;                     // dSᵀ (KV) | dS (Q)
     float* sRow = reinterpret_cast<float*>(sDS + C::kPd);  // [2][lse[128], D[128]] (KV only)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sRow + 2 * 2 * kBlk);
-    uint64_t* fix_full = bars + 0;
-    uint64_t* ld_full = bars + 1;   // [2]
-    uint64_t* ld_empty = bars + 3;  // [2]
-    uint64_t* xy_full = bars + 5;
-    uint64_t* xy_free = bars + 6;
-    uint64_t* pd_full = bars + 7;
-    uint64_t* acc_done = bars + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    uint64_t* fix_full = bars + 0;   // [2]
+    uint64_t* fix_empty = bars + 2;  // [2]
+    uint64_t* ld_full = bars + 4;    // [2]
+    uint64_t* ld_empty = bars + 6;   // [2]
+    uint64_t* xy_full = bars + 8;
+    uint64_t* xy_free = bars + 9;
+    uint64_t* pd_full = bars + 10;
+    uint64_t* pd_free = bars + 11;
+    uint64_t* acc_full = bars + 12;   // [2]
+    uint64_t* acc_empty = bars + 14;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
-    const int nb = a.s / kBlk;
-    const int blk = KV ? static_cast<int>(blockIdx.x) : nb - 1 - static_cast<int>(blockIdx.x);
-    const int head = blockIdx.y, bi = blockIdx.z;
-    const int first = (KV && a.causal) ? blk : 0;
-    const int nsteps = !a.causal ? nb : (KV ? nb - blk : blk + 1);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmQKV);
         tma_prefetch_desc(&tmDO);
-        mbar_init(fix_full, 1);
         for (int i = 0; i < 2; ++i) {
+            mbar_init(&fix_full[i], 1);
+            mbar_init(&fix_empty[i], 1);
             mbar_init(&ld_full[i], 1);
             mbar_init(&ld_empty[i], 1);
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 8);
         }
         mbar_init(xy_full, 1);
         mbar_init(xy_free, 8);
         mbar_init(pd_full, 8);
-        mbar_init(acc_done, 1);
+        mbar_init(pd_free, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -534,48 +632,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    // tile loader: rows [row0, row0+128) of a {d, s, heads, b} map, head coordinate hc
-    auto load_tile = [&](const CUtensorMap* m, uint64_t* bar, uint8_t* dst, int row0, int hc) {
-#pragma unroll
-        for (int kb = 0; kb < D / 64; ++kb) tma_load_4d(m, bar, dst + kb * kBlk * 128, kb * 64, row0, hc, bi);
-    };
-
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
-            mbar_arrive_expect_tx(fix_full, 2 * C::kTile);
-            if (KV) {
-                load_tile(&tmQKV, fix_full, sF0, blk * kBlk, a.H + head);      // K_j
-                load_tile(&tmQKV, fix_full, sF1, blk * kBlk, 2 * a.H + head);  // V_j
-            } else {
-                load_tile(&tmQKV, fix_full, sF0, blk * kBlk, head);  // Q_i
-                load_tile(&tmDO, fix_full, sF1, blk * kBlk, head);   // dO_i
-            }
-            for (int t = 0; t < nsteps; ++t) {
-                const int st = S == 1 ? 0 : (t & 1);
-                const uint32_t ph = S == 1 ? (t & 1) : ((t >> 1) & 1);
-                mbar_wait(&ld_empty[st], ph ^ 1);
-                mbar_arrive_expect_tx(&ld_full[st], 2 * C::kTile);
-                uint8_t* t0 = sStep + st * 2 * C::kTile;
-                const int row0 = (first + t) * kBlk;
+            // tile loader: rows [row0, row0+128) of a {d, s, heads, b} map, head coordinate hc
+            auto load_tile = [&](const CUtensorMap* m, uint64_t* bar, uint8_t* dst, int row0, int hc, int bi) {
+#pragma unroll
+                for (int kb = 0; kb < D / 64; ++kb) tma_load_4d(m, bar, dst + kb * kBlk * 128, kb * 64, row0, hc, bi);
+            };
+            int n = 0;  // steps loaded so far (all tiles)
+            BwCursor c;
+            for (bw_tile<KV>(a, 0, c); c.valid; bw_tile<KV>(a, c.k + 1, c)) {
+                const int fb = c.k % FB;
+                uint8_t* f = sFix + fb * 2 * C::kTile;
+                mbar_wait(&fix_empty[fb], ((c.k / FB) & 1) ^ 1);
+                mbar_arrive_expect_tx(&fix_full[fb], 2 * C::kTile);
                 if (KV) {
-                    load_tile(&tmQKV, &ld_full[st], t0, row0, head);             // Q_i
-                    load_tile(&tmDO, &ld_full[st], t0 + C::kTile, row0, head);   // dO_i
+                    load_tile(&tmQKV, &fix_full[fb], f, c.blk * kBlk, a.H + c.head, c.bi);                // K_j
+                    load_tile(&tmQKV, &fix_full[fb], f + C::kTile, c.blk * kBlk, 2 * a.H + c.head, c.bi);  // V_j
                 } else {
-                    load_tile(&tmQKV, &ld_full[st], t0, row0, a.H + head);              // K_j
-                    load_tile(&tmQKV, &ld_full[st], t0 + C::kTile, row0, 2 * a.H + head);  // V_j
+                    load_tile(&tmQKV, &fix_full[fb], f, c.blk * kBlk, c.head, c.bi);           // Q_i
+                    load_tile(&tmDO, &fix_full[fb], f + C::kTile, c.blk * kBlk, c.head, c.bi);  // dO_i
+                }
+                for (int t = 0; t < c.nsteps; ++t, ++n) {
+                    const int st = n % S;
+                    mbar_wait(&ld_empty[st], ((n / S) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&ld_full[st], 2 * C::kTile);
+                    uint8_t* t0 = sStep + st * 2 * C::kTile;
+                    const int row0 = (c.first + t) * kBlk;
+                    if (KV) {
+                        load_tile(&tmQKV, &ld_full[st], t0, row0, c.head, c.bi);            // Q_i
+                        load_tile(&tmDO, &ld_full[st], t0 + C::kTile, row0, c.head, c.bi);  // dO_i
+                    } else {
+                        load_tile(&tmQKV, &ld_full[st], t0, row0, a.H + c.head, c.bi);                  // K_j
+                        load_tile(&tmQKV, &ld_full[st], t0 + C::kTile, row0, 2 * a.H + c.head, c.bi);  // V_j
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
-            mbar_wait(fix_full, 0);
-            const uint32_t f0 = smem_u32(sF0), f1 = smem_u32(sF1);
-            auto issue_xy = [&](int t) {
-                const int st = S == 1 ? 0 : (t & 1);
-                const uint32_t ph = S == 1 ? (t & 1) : ((t >> 1) & 1);
-                mbar_wait(&ld_full[st], ph);
-                if (t > 0) mbar_wait(xy_free, (t - 1) & 1);
+            auto issue_xy = [&](const BwCursor& c, int n) {
+                ATRACE(1, n, 0);
+                const int st = n % S, fb = c.k % FB;
+                if (c.j == 0) mbar_wait(&fix_full[fb], (c.k / FB) & 1);
+                mbar_wait(&ld_full[st], (n / S) & 1);
+                mbar_wait(xy_free, (n & 1) ^ 1);  // elementwise warps have read the previous X/Y
                 tc_fence_after();
+                const uint32_t f0 = smem_u32(sFix + fb * 2 * C::kTile), f1 = f0 + C::kTile;
                 const uint32_t s0 = smem_u32(sStep + st * 2 * C::kTile), s1 = s0 + C::kTile;
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {
@@ -587,38 +690,60 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 kIdescXY, k > 0 ? 1u : 0u);
                 }
                 mma_commit(xy_full);
+                ATRACE(1, n, 1);
+                if (c.j == c.nsteps - 1) mma_commit(&fix_empty[fb]);
             };
-            issue_xy(0);
-            for (int t = 0; t < nsteps; ++t) {
-                // with two operand stages, score products of step t+1 overlap the
-                // elementwise work of step t; with one stage they must wait for
-                // step t's accumulating products to release the operands
-                if (S > 1 && t + 1 < nsteps) issue_xy(t + 1);
-                mbar_wait(pd_full, t & 1);
+            BwCursor cx, ca;
+            bw_tile<KV>(a, 0, cx);
+            bw_tile<KV>(a, 0, ca);
+            int nx = 0, na = 0;
+            if (cx.valid) {
+                issue_xy(cx, nx++);
+                bw_next<KV>(a, cx);
+            }
+            while (ca.valid) {
+                // with two operand stages, score products of the next step (possibly of
+                // the next tile) overlap the elementwise work of this one; with one stage
+                // they must wait for this step's accumulating products to release it
+                if (S > 1 && cx.valid) {
+                    issue_xy(cx, nx++);
+                    bw_next<KV>(a, cx);
+                }
+                const int st = na % S, ab = AB == 1 ? 0 : (ca.k & 1);
+                mbar_wait(pd_full, na & 1);
+                ATRACE(1, na, 2);
+                if (ca.j == 0) mbar_wait(&acc_empty[ab], ((ca.k / AB) & 1) ^ 1);
                 tc_fence_after();
-                const int st = S == 1 ? 0 : (t & 1);
                 const uint32_t s0 = smem_u32(sStep + st * 2 * C::kTile), s1 = s0 + C::kTile;
                 const uint32_t pb = smem_u32(sP), db = smem_u32(sDS);
+                const uint32_t acc0 = tmem + C::kAcc + ab * C::kAccCols;
 #pragma unroll
                 for (int k = 0; k < kBlk / 16; ++k) {
                     const uint32_t aoff = (k / 4) * kBlk * 128 + (k % 4) * 32;  // K-major A, k over 128 columns
                     const uint32_t boff = k * 2048;                            // MN-major B, k over 128 rows
-                    const uint32_t acc = (t > 0 || k > 0) ? 1u : 0u;
+                    const uint32_t acc = (ca.j > 0 || k > 0) ? 1u : 0u;
                     if (KV) {
                         // dV += Pᵀ dO_i ; dK += dSᵀ Q_i
-                        mma_bf16_ss(tmem + C::kAcc1, make_sw128_desc(pb + aoff, 16, 1024),
+                        mma_bf16_ss(acc0, make_sw128_desc(pb + aoff, 16, 1024),
                                     make_sw128_desc(s1 + boff, kBlk * 128, 1024), kIdescAcc, acc);
-                        mma_bf16_ss(tmem + C::kAcc2, make_sw128_desc(db + aoff, 16, 1024),
+                        mma_bf16_ss(acc0 + D, make_sw128_desc(db + aoff, 16, 1024),
                                     make_sw128_desc(s0 + boff, kBlk * 128, 1024), kIdescAcc, acc);
                     } else {
                         // dQ += dS K_j
-                        mma_bf16_ss(tmem + C::kAcc1, make_sw128_desc(db + aoff, 16, 1024),
+                        mma_bf16_ss(acc0, make_sw128_desc(db + aoff, 16, 1024),
                                     make_sw128_desc(s0 + boff, kBlk * 128, 1024), kIdescAcc, acc);
                     }
                 }
-                mma_commit(acc_done);
+                mma_commit(pd_free);
+                ATRACE(1, na, 3);
                 mma_commit(&ld_empty[st]);
-                if (S == 1 && t + 1 < nsteps) issue_xy(t + 1);
+                if (ca.j == ca.nsteps - 1) mma_commit(&acc_full[ab]);
+                if (S == 1 && cx.valid) {
+                    issue_xy(cx, nx++);
+                    bw_next<KV>(a, cx);
+                }
+                bw_next<KV>(a, ca);
+                ++na;
             }
         }
     } else if (warp >= 4) {  // ---------------- elementwise warps: thread = (row of the fixed block, column half)
@@ -626,84 +751,120 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int half = (warp - 4) >> 2;  // columns [64*half, 64*half + 64) of X/Y
         const int r = quad * 32 + static_cast<int>(lane);
         const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
-        const int64_t rowbase = (static_cast<int64_t>(bi) * a.H + head) * a.s;
-        float my_lse = 0.f, my_d = 0.f;
-        if (!KV) {
-            my_lse = a.lse[rowbase + blk * kBlk + r];
-            my_d = a.dsum[rowbase + blk * kBlk + r];
-        }
         const uint32_t rowv0 = smem_u32(sRow);
-        for (int t = 0; t < nsteps; ++t) {
-            const int other = first + t;  // index of the stepped block
-            const uint32_t rowv = rowv0 + (t & 1) * 2 * kBlk * 4;
-            if (KV) {  // this step's per-query lse (half 0) / D (half 1) -> smem, named barrier over the 8 warps
-                sts32f(rowv + (half * kBlk + r) * 4, (half == 0 ? a.lse : a.dsum)[rowbase + other * kBlk + r]);
-                asm volatile("bar.sync 1, 256;" ::: "memory");
+        const uint32_t pbuf = smem_u32(sP), dbuf = smem_u32(sDS);
+        const float sc = a.scale_log2, tau = a.tau;
+        // per-row softmax statistics, prefetched one step ahead (global loads off the critical path)
+        //   KV: the stepped query block's lse (half 0) / D (half 1) at row r of that block
+        //   Q:  this tile's own lse and D at row r
+        auto stats = [&](const BwCursor& q, float& s0, float& s1) {
+            const int64_t rb = (static_cast<int64_t>(q.bi) * a.H + q.head) * a.s;
+            if (KV) {
+                s0 = (half == 0 ? a.lse : a.dsum)[rb + (q.first + q.j) * kBlk + r];
+                s1 = 0.f;
+            } else {
+                s0 = a.lse[rb + q.blk * kBlk + r];
+                s1 = a.dsum[rb + q.blk * kBlk + r];
             }
-            mbar_wait(xy_full, t & 1);
-            tc_fence_after();
-            // this thread's 64 columns of X and Y, then release the score accumulators
-            float x[64], y[64];
-            tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kX + half * 64, x);
-            tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kX + half * 64 + 32, x + 32);
-            tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kY + half * 64, y);
-            tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kY + half * 64 + 32, y + 32);
-            tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(xy_free);
-            const bool diag = a.causal && other == blk;
-            // P (into x) and dS (into y) in registers, before waiting for the previous
-            // step's accumulating products to release the smem operands
-#pragma unroll
-            for (int e = 0; e < 64; ++e) {
-                const int col = half * 64 + e;
-                // KV: row = key, col = query -> valid iff query >= key ; Q: row = query, col = key
-                const bool valid = !diag || (KV ? col >= r : col <= r);
-                const float l2 = KV ? lds32f(rowv + col * 4) : my_lse;
-                const float dd = KV ? lds32f(rowv + (kBlk + col) * 4) : my_d;
-                const float pv = valid ? ex2(fmaf(x[e], a.scale_log2, -l2)) : 0.f;
-                x[e] = pv;
-                y[e] = a.tau * pv * (y[e] - dd);
-            }
-            if (t > 0) {
-                mbar_wait(acc_done, (t - 1) & 1);  // previous step's MMAs done reading sP / sDS
-            }
-            const uint32_t pbuf = smem_u32(sP), dbuf = smem_u32(sDS);
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                if (KV) st_bf16_swz(pbuf, r, half * 64 + g * 8, x + g * 8);
-                st_bf16_swz(dbuf, r, half * 64 + g * 8, y + g * 8);
-            }
-            fence_proxy_async_smem();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(pd_full);
-        }
-        mbar_wait(acc_done, (nsteps - 1) & 1);
-        tc_fence_after();
-        // epilogue: accumulators -> dqkv (bf16).  KV: half 0 writes dV (acc1, section 2),
-        // half 1 writes dK (acc2, section 1).  Q: acc1 = dQ, half h writes columns [h*D/2, +D/2).
-        const int row = blk * kBlk + r;
-        __nv_bfloat16* base = a.dqkv + (static_cast<int64_t>(bi) * a.s + row) * (3 * a.h) + head * D;
-        __nv_bfloat16* dst = KV ? base + (half == 0 ? 2 * a.h : a.h) : base + half * (D / 2);
-        const uint32_t col0 = KV ? (half == 0 ? C::kAcc1 : C::kAcc2) : C::kAcc1 + half * (D / 2);
-        constexpr int kCols = KV ? D : D / 2;
-#pragma unroll
-        for (int c = 0; c < kCols / 32; ++c) {
-            float v[32];
-            tmem_ld_32x32b_x32(tmem + lane_base + col0 + c * 32, v);
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                uint4 u;
-                uint32_t* w = reinterpret_cast<uint32_t*>(&u);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    __nv_bfloat162 hh = __floats2bfloat162_rn(v[g * 8 + 2 * e], v[g * 8 + 2 * e + 1]);
-                    w[e] = *reinterpret_cast<uint32_t*>(&hh);
+        };
+        int n = 0;  // steps processed so far (all tiles)
+        BwCursor c, cn;
+        bw_tile<KV>(a, 0, c);
+        cn = c;
+        float pre0 = 0.f, pre1 = 0.f;
+        if (c.valid) stats(c, pre0, pre1);
+        for (; c.valid; ++n) {
+            const float cur0 = pre0, cur1 = pre1;
+            bw_next<KV>(a, cn);
+            if (cn.valid) stats(cn, pre0, pre1);
+            {
+                const int t = c.j;
+                const int other = c.first + t;  // index of the stepped block
+                const float my_lse = cur0, my_d = cur1 * a.tau;
+                const uint32_t rowv = rowv0 + (n & 1) * 2 * kBlk * 4;
+                if (KV) {  // this step's per-query lse (half 0) / τ·D (half 1) -> smem, barrier over the 8 warps
+                    sts32f(rowv + (half * kBlk + r) * 4, half == 0 ? cur0 : cur0 * a.tau);
+                    asm volatile("bar.sync 1, 256;" ::: "memory");
                 }
-                *reinterpret_cast<uint4*>(dst + c * 32 + g * 8) = u;
+                mbar_wait(xy_full, n & 1);
+                if (warp == 4 && lane == 0) ATRACE(0, n, 0);
+                tc_fence_after();
+                const bool diag = a.causal && other == c.blk;
+                // this thread's 64 columns of X and Y in two 32-column passes (the score
+                // accumulators are released after the second pass's loads); P and
+                // dS = P (τ dP - τ D) are packed to bf16 pairs in registers, before waiting
+                // for the previous step's accumulating products to release the smem operands
+                uint32_t pk_p[32], pk_d[32];
+#pragma unroll
+                for (int pass = 0; pass < 2; ++pass) {
+                    float x[32], y[32];
+                    tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kX + half * 64 + pass * 32, x);
+                    tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kY + half * 64 + pass * 32, y);
+                    tmem_ld_wait();
+                    if (pass == 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(xy_free);
+                        if (warp == 4 && lane == 0) ATRACE(0, n, 1);
+                    }
+                    const int cb0 = half * 64 + pass * 32;
+                    if (diag)
+                        bw_pass<KV, true>(x, y, rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16, pk_d + pass * 16);
+                    else
+                        bw_pass<KV, false>(x, y, rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16, pk_d + pass * 16);
+                }
+                if (warp == 4 && lane == 0) ATRACE(0, n, 2);
+                if (n > 0) {
+                    mbar_wait(pd_free, (n - 1) & 1);  // previous step's MMAs done reading sP / sDS
+                }
+                if (warp == 4 && lane == 0) ATRACE(0, n, 3);
+                // columns [64*half, +64) are swizzle atom `half` of each [128][128] operand
+                const uint32_t prow = pbuf + half * (kBlk * 128) + r * 128;
+                const uint32_t drow = dbuf + half * (kBlk * 128) + r * 128;
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const uint32_t sw = (g ^ (r & 7)) * 16;
+                    if (KV) sts128(prow + sw, make_uint4(pk_p[g * 4], pk_p[g * 4 + 1], pk_p[g * 4 + 2], pk_p[g * 4 + 3]));
+                    sts128(drow + sw, make_uint4(pk_d[g * 4], pk_d[g * 4 + 1], pk_d[g * 4 + 2], pk_d[g * 4 + 3]));
+                }
+                fence_proxy_async_smem();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(pd_full);
+                if (warp == 4 && lane == 0) ATRACE(0, n, 4);
             }
+            if (c.j < c.nsteps - 1) {
+                bw_next<KV>(a, c);
+                continue;
+            }
+            const int ab = AB == 1 ? 0 : (c.k & 1);
+            mbar_wait(&acc_full[ab], (c.k / AB) & 1);
+            tc_fence_after();
+            // epilogue: accumulators -> dqkv (bf16).  KV: half 0 writes dV (section 2),
+            // half 1 writes dK (section 1).  Q: dQ, half h writes columns [h*D/2, +D/2).
+            const int row = c.blk * kBlk + r;
+            __nv_bfloat16* base = a.dqkv + (static_cast<int64_t>(c.bi) * a.s + row) * (3 * a.h) + c.head * D;
+            __nv_bfloat16* dst = KV ? base + (half == 0 ? 2 * a.h : a.h) : base + half * (D / 2);
+            const uint32_t col0 = C::kAcc + ab * C::kAccCols + (KV ? half * D : half * (D / 2));
+            constexpr int kCols = KV ? D : D / 2;
+#pragma unroll
+            for (int cc = 0; cc < kCols / 32; ++cc) {
+                float v[32];
+                tmem_ld_32x32b_x32(tmem + lane_base + col0 + cc * 32, v);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    uint4 u;
+                    u.x = pack_bf16(v[g * 8 + 0], v[g * 8 + 1]);
+                    u.y = pack_bf16(v[g * 8 + 2], v[g * 8 + 3]);
+                    u.z = pack_bf16(v[g * 8 + 4], v[g * 8 + 5]);
+                    u.w = pack_bf16(v[g * 8 + 6], v[g * 8 + 7]);
+                    *reinterpret_cast<uint4*>(dst + cc * 32 + g * 8) = u;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            bw_next<KV>(a, c);
         }
     }
     tc_fence_before();
@@ -714,29 +875,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// D[b][H][q] = sum_dd dO[q][hh*d+dd] * O[q][hh*d+dd]; one thread per (row, head).
+// D[b][H][q] = sum_dd dO[q][hh*d+dd] * O[q][hh*d+dd]: one warp per token row,
+// coalesced 16-byte loads over the whole row, per-head sums reduced across the
+// d/8 lanes that hold a head (fixed shuffle order: deterministic).
 template <int D>
-__global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
-                                    float* __restrict__ dsum, int rows, int s, int H) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= rows * H) return;
-    const int row = idx / H, head = idx % H;
-    const int64_t off = static_cast<int64_t>(row) * H * D + head * D;
-    float acc = 0.f;
+__global__ void __launch_bounds__(256) attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ dO,
+                                                           const __nv_bfloat16* __restrict__ O,
+                                                           float* __restrict__ dsum, int rows, int s, int H) {
+    constexpr int kLanesPerHead = D / 8;
+    const int row = blockIdx.x * 8 + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int chunks = H * kLanesPerHead;  // 16-byte chunks per row
+    const int64_t off = static_cast<int64_t>(row) * H * D;
+    const int bi = row / s, q = row % s;
+    for (int c0 = 0; c0 < chunks; c0 += 32) {
+        const int ci = c0 + lane;
+        float acc = 0.f;
+        if (ci < chunks) {
+            const uint4 ua = *reinterpret_cast<const uint4*>(dO + off + ci * 8);
+            const uint4 ub = *reinterpret_cast<const uint4*>(O + off + ci * 8);
+            const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&ua);
+            const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&ub);
 #pragma unroll
-    for (int c = 0; c < D; c += 8) {
-        const uint4 a = *reinterpret_cast<const uint4*>(dO + off + c);
-        const uint4 b = *reinterpret_cast<const uint4*>(O + off + c);
-        const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
-        const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
+            for (int e = 0; e < 4; ++e) {
+                const float2 x = __bfloat1622float2(ha[e]), y = __bfloat1622float2(hb[e]);
+                acc += x.x * y.x + x.y * y.y;
+            }
+        }
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 x = __bfloat1622float2(ha[e]), y = __bfloat1622float2(hb[e]);
-            acc += x.x * y.x + x.y * y.y;
+        for (int o = 1; o < kLanesPerHead; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (ci < chunks && (lane % kLanesPerHead) == 0) {
+            const int head = ci / kLanesPerHead;
+            dsum[(static_cast<int64_t>(bi) * H + head) * s + q] = acc;
         }
     }
-    const int bi = row / s, q = row % s;
-    dsum[(static_cast<int64_t>(bi) * H + head) * s + q] = acc;
 }
 
 // dO [b*s][H*d] viewed as dims {d, s, H, b}, box {64, 128}.
@@ -758,7 +931,7 @@ cudaError_t do_map(CUtensorMap* m, const void* dO, int b, int s, int H, int d) {
 
 template <int D, bool KV>
 cudaError_t launch_bwd(const FlashBwdPlan& p, cudaStream_t st) {
-    using C = BwCfg<D>;
+    using C = BwCfg<D, KV>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e =
@@ -766,9 +939,10 @@ cudaError_t launch_bwd(const FlashBwdPlan& p, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    BwArgs a{p.dqkv, p.lse, p.dsum, p.s, p.H, p.H * p.d, p.scale_log2, 1.f / sqrtf(static_cast<float>(p.d)),
+    BwArgs a{p.dqkv, p.lse, p.dsum, p.s, p.H, p.H * p.d, p.b, p.scale_log2, 1.f / sqrtf(static_cast<float>(p.d)),
              p.causal};
-    dim3 grid(p.s / kBlk, p.H, p.b);
+    const int tiles = p.s / kBlk * p.H * p.b;
+    const int grid = tiles < sm_count() ? tiles : sm_count();
     flash_bwd_kernel<D, KV><<<grid, kThreads, C::kSmem, st>>>(p.tmQKV, p.tmDO, a);
     return cudaPeekAtLastError();
 }
@@ -798,11 +972,10 @@ cudaError_t flash_bwd_prepare(const void* qkv, const void* o, const void* dO, co
 
 cudaError_t flash_backward(const FlashBwdPlan& p, cudaStream_t st) {
     const int rows = p.b * p.s;
-    const int n = rows * p.H;
     if (p.d == 64)
-        attn_bwd_dot_kernel<64><<<(n + 255) / 256, 256, 0, st>>>(p.dO, p.o, p.dsum, rows, p.s, p.H);
+        attn_bwd_dot_kernel<64><<<(rows + 7) / 8, 256, 0, st>>>(p.dO, p.o, p.dsum, rows, p.s, p.H);
     else
-        attn_bwd_dot_kernel<128><<<(n + 255) / 256, 256, 0, st>>>(p.dO, p.o, p.dsum, rows, p.s, p.H);
+        attn_bwd_dot_kernel<128><<<(rows + 7) / 8, 256, 0, st>>>(p.dO, p.o, p.dsum, rows, p.s, p.H);
     cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) return e;
     e = p.d == 64 ? launch_bwd<64, true>(p, st) : launch_bwd<128, true>(p, st);

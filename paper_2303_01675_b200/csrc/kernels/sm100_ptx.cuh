@@ -128,6 +128,16 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32_nw(uint32_t taddr, float* v) 
           "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 }
+// Per-warpgroup register budget (all 4 warps of the warpgroup execute it).
+template <uint32_t kRegs>
+__device__ __forceinline__ void reg_dealloc() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void reg_alloc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+
 // Shared-state-space accesses by 32-bit shared address (no generic-address path).
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)

@@ -1,0 +1,57 @@
+// Debug tool: per-step timeline (SM clock cycles) of CTA 0 of the flash
+// attention backward kernels at the GPT-1.3B shape.  Not part of the library.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DPTK_ATTN_TRACE \
+//        -o scripts/attn_trace scripts/attn_trace.cu
+#include <cstdio>
+#include <vector>
+
+#include "../paper_2303_01675_b200/csrc/kernels/attention_sm100.cu"
+
+__global__ void fill(__nv_bfloat16* p, size_t n, unsigned seed) {
+    for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        unsigned x = static_cast<unsigned>(i) * 2654435761u ^ seed;
+        x ^= x >> 13;
+        x *= 0x5bd1e995u;
+        x ^= x >> 15;
+        p[i] = __float2bfloat16((static_cast<float>(x & 0xffff) / 65536.f - 0.5f));
+    }
+}
+
+int main(int argc, char** argv) {
+    const int kv = argc > 1 ? atoi(argv[1]) : 1;
+    const int b = 2, s = 1024, H = 32, d = 64, h = H * d;
+    const size_t T = static_cast<size_t>(b) * s;
+    __nv_bfloat16 *qkv, *o, *dO, *dqkv;
+    float *lse, *dsum;
+    cudaMalloc(&qkv, T * 3 * h * 2);
+    cudaMalloc(&o, T * h * 2);
+    cudaMalloc(&dO, T * h * 2);
+    cudaMalloc(&dqkv, T * 3 * h * 2);
+    cudaMalloc(&lse, T * H * 4);
+    cudaMalloc(&dsum, T * H * 4);
+    fill<<<512, 256>>>(qkv, T * 3 * h, 1);
+    fill<<<512, 256>>>(dO, T * h, 2);
+    cudaMemcpyToSymbol(ptk::g_attn_trace_kv, &kv, sizeof kv);
+    ptk::FlashPlan fp;
+    ptk::FlashBwdPlan bp;
+    if (ptk::flash_prepare(qkv, o, lse, b, s, H, d, &fp, 1) != cudaSuccess) return 1;
+    if (ptk::flash_bwd_prepare(qkv, o, dO, lse, dsum, dqkv, b, s, H, d, &bp, 1) != cudaSuccess) return 1;
+    ptk::flash_forward(fp, 0);
+    for (int i = 0; i < 3; ++i) ptk::flash_backward(bp, 0);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        printf("error %s\n", cudaGetErrorString(e));
+        return 1;
+    }
+    unsigned long long tr[2][64][8];
+    cudaMemcpyFromSymbol(tr, ptk::g_attn_trace, sizeof tr);
+    const unsigned long long t0 = tr[1][0][0];
+    printf("%s kernel, CTA 0, cycles since the first XY issue\n", kv ? "KV" : "Q");
+    printf("step | mma: xy_issue_begin xy_issued pd_full_seen acc_issued | ew: xy_full xy_free computed pd_free stored\n");
+    for (int n = 0; n < 20; ++n) {
+        auto f = [&](int r, int ev) { return static_cast<long long>(tr[r][n][ev] - t0); };
+        printf("%3d | %8lld %8lld %8lld %8lld | %8lld %8lld %8lld %8lld %8lld\n", n, f(1, 0), f(1, 1), f(1, 2), f(1, 3),
+               f(0, 0), f(0, 1), f(0, 2), f(0, 3), f(0, 4));
+    }
+    return 0;
+}
