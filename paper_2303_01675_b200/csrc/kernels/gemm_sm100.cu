@@ -51,7 +51,7 @@ struct Cfg {
     static constexpr int kABytes = kBM * kBK * 2;
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kEpiBytes = 8 * 32 * 32 * 4;
+    static constexpr int kEpiBytes = 8 * 32 * 32 * 4 + 2 * BN * 2;  // transpose buffers + 2 bias slices
     static constexpr int kStagesRaw = (kSmemBudget - 2048 - kEpiBytes) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
     static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
@@ -144,46 +144,108 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t, int r
     return c;
 }
 
-// Epilogue of one accumulator tile held in TMEM columns [tmem_col, tmem_col + BN)
-// of lane quadrant `quad`; this warp handles the 32-column chunks c = half, half+2, ...
+// ---------------------------------------------------------------- epilogue
+// Every global input of a tile's epilogue that does not depend on the
+// accumulator (bias slice, residual / pre-activation aux rows, the previous
+// fp32 C of a wgrad accumulation) is fetched BEFORE the epilogue waits for the
+// accumulator, so its latency hides under the main loop; later chunks are
+// fetched one or two chunks ahead.  Warp (quad, half) owns TMEM lanes
+// [32 quad, +32) and the 32-column chunks c = half, half+2, ... of the tile.
+template <int BN>
+struct EpiIn {
+    static constexpr int kChunks = (BN / 32 + 1) / 2;  // chunks per warp
+    // one register buffer, by epilogue kind:
+    //   aux (BF16 residual / DGELU): words [4 (i & 1), +4) hold chunk i's 4 x 8 bf16 of this row
+    //   ACC_F32: 8 float4 of the next chunk's previous C (transposed mapping)
+    uint4 buf[8];
+    __device__ __forceinline__ uint4 (&aux(int slot))[4] { return *reinterpret_cast<uint4(*)[4]>(buf + 4 * slot); }
+    __device__ __forceinline__ float4 (&prev())[8] { return *reinterpret_cast<float4(*)[8]>(buf); }
+};
+
+__device__ __forceinline__ bool epi_has_aux(const GemmArgs& a) {
+    return (a.epi == PTK_EPI_BF16 && a.aux != nullptr) || a.epi == PTK_EPI_DGELU;
+}
+
+__device__ __forceinline__ void epi_fetch_aux(const GemmArgs& args, const TileCoord& tc, int c, int quad,
+                                              uint32_t lane, uint4 (&aux)[4]) {
+    const int gm = tc.m0 + quad * 32 + static_cast<int>(lane);
+    const int64_t xrow = tc.z1 * args.aux_bs1 + tc.z2 * args.aux_bs2 + static_cast<int64_t>(gm) * args.ld_aux;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int gn = tc.n0 + c * 32 + 8 * j;
+        aux[j] = (gm < args.M && gn < args.N)
+                     ? *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.aux) + xrow + gn)
+                     : make_uint4(0u, 0u, 0u, 0u);
+    }
+}
+
+__device__ __forceinline__ void epi_fetch_prev(const GemmArgs& args, const TileCoord& tc, int c, int quad,
+                                               uint32_t lane, float4 (&prev)[8]) {
+    const int q = static_cast<int>(lane & 7), r0 = static_cast<int>(lane >> 3);
+    const int gn = tc.n0 + c * 32 + q * 4;
+    const float* cbase = static_cast<const float*>(args.C) + tc.z1 * args.c_bs1 + tc.z2 * args.c_bs2 + gn;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int gm = tc.m0 + quad * 32 + r0 + 4 * i;
+        prev[i] = (gn < args.N && gm < args.M) ? *reinterpret_cast<const float4*>(cbase + static_cast<int64_t>(gm) * args.ldc)
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// Before the accumulator wait: this warp's first chunks' inputs, and the tile's
+// bias slice into smem (bias_s: BN bf16; the 8 epilogue warps sync on named
+// barrier 1 — the buffer is double-buffered by the caller per accumulator).
+template <int BN>
+__device__ __forceinline__ void epi_prefetch(const GemmArgs& args, const TileCoord& tc, int quad, int half,
+                                             uint32_t lane, int et, __nv_bfloat16* bias_s, EpiIn<BN>& in) {
+    if (args.epi == PTK_EPI_ACC_F32) {
+        epi_fetch_prev(args, tc, half, quad, lane, in.prev());
+    } else if (epi_has_aux(args)) {
+        epi_fetch_aux(args, tc, half, quad, lane, in.aux(0));
+        if (EpiIn<BN>::kChunks > 1) epi_fetch_aux(args, tc, half + 2, quad, lane, in.aux(1));
+    }
+    if (args.bias != nullptr) {
+        if (et < BN / 8) {
+            const int gn = tc.n0 + et * 8;
+            const uint4 v = gn < args.N ? *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.bias) + gn)
+                                        : make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(bias_s + et * 8) = v;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
+}
+
+// Epilogue of one accumulator tile held in TMEM columns [tmem_col, tmem_col + BN).
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, const TileCoord& tc, uint32_t tmem_col, int quad,
-                                              int half, uint32_t lane, float4* stage_buf) {
+                                              int half, uint32_t lane, float4* stage_buf,
+                                              const __nv_bfloat16* bias_s, EpiIn<BN>& in) {
     const int q = static_cast<int>(lane & 7);
     const int r0 = static_cast<int>(lane >> 3);
     const bool f32_out = args.epi == PTK_EPI_F32 || args.epi == PTK_EPI_ACC_F32;
     const int64_t zoff_c = tc.z1 * args.c_bs1 + tc.z2 * args.c_bs2;
-    const int64_t zoff_x = tc.z1 * args.aux_bs1 + tc.z2 * args.aux_bs2;
     const int row_base = tc.m0 + quad * 32;
-#pragma unroll 1
-    for (int c = half; c < BN / 32; c += 2) {
+#pragma unroll
+    for (int ci = 0; ci < EpiIn<BN>::kChunks; ++ci) {
+        const int c = half + 2 * ci;
+        if (c >= BN / 32) break;
         float v[32];
         __syncwarp();
         tmem_ld_32x32b_x32(tmem_col + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(c * 32),
                            v);
         if (f32_out) {
             // fp32 output: transpose through smem so each warp store covers
-            // 4 rows x 128 contiguous bytes; all loads issued before stores.
+            // 4 rows x 128 contiguous bytes
 #pragma unroll
             for (int j = 0; j < 8; ++j)
                 stage_buf[lane * 8 + (j ^ (lane & 7))] =
                     make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             __syncwarp();
+            float4(&prev)[8] = in.prev();
             const int gn = tc.n0 + c * 32 + q * 4;
             if (gn < args.N) {
                 float* cbase = static_cast<float*>(args.C) + zoff_c + gn;
-                float4 prev[8];
-                if (args.epi == PTK_EPI_ACC_F32) {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int gm = row_base + r0 + 4 * i;
-                        prev[i] = gm < args.M ? *reinterpret_cast<const float4*>(cbase + static_cast<int64_t>(gm) * args.ldc)
-                                              : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) prev[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
+                const bool acc = args.epi == PTK_EPI_ACC_F32;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const int r = r0 + 4 * i;
@@ -191,31 +253,34 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, const TileCo
                     const float4 a4 = stage_buf[r * 8 + (q ^ (r & 7))];
                     if (gm < args.M)
                         *reinterpret_cast<float4*>(cbase + static_cast<int64_t>(gm) * args.ldc) =
-                            make_float4(prev[i].x + a4.x, prev[i].y + a4.y, prev[i].z + a4.z, prev[i].w + a4.w);
+                            acc ? make_float4(prev[i].x + a4.x, prev[i].y + a4.y, prev[i].z + a4.z, prev[i].w + a4.w)
+                                : a4;
                 }
             }
+            if (args.epi == PTK_EPI_ACC_F32 && ci + 1 < EpiIn<BN>::kChunks && c + 2 < BN / 32)
+                epi_fetch_prev(args, tc, c + 2, quad, lane, in.prev());  // next chunk, in flight during its tmem load
             continue;
         }
         // bf16 output: thread = row, 16-byte stores of 8 columns
         const int gm = row_base + static_cast<int>(lane);
         const int gn0 = tc.n0 + c * 32;
-        if (gm >= args.M) continue;
+        uint4(&xa)[4] = in.aux(ci & 1);
+        if (gm < args.M) {
         const int64_t rowoff = zoff_c + static_cast<int64_t>(gm) * args.ldc;
-        const int64_t xrowoff = zoff_x + static_cast<int64_t>(gm) * args.ld_aux;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int gn = gn0 + 8 * j;
             if (gn >= args.N) continue;
             float* f = v + 8 * j;
             if (args.bias != nullptr) {
-                float b[8];
-                unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.bias) + gn), b);
+                float bb[8];
+                unpack_bf16x8(*reinterpret_cast<const uint4*>(bias_s + c * 32 + 8 * j), bb);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) f[i] += b[i];
+                for (int i = 0; i < 8; ++i) f[i] += bb[i];
             }
             if (args.epi == PTK_EPI_BF16 && args.aux != nullptr) {
                 float r[8];
-                unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.aux) + xrowoff + gn), r);
+                unpack_bf16x8(xa[j], r);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) f[i] += r[i];
             } else if (args.epi == PTK_EPI_BIAS_GELU) {
@@ -227,12 +292,15 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, const TileCo
                 for (int i = 0; i < 8; ++i) f[i] = gelu_tanh(p[i]);
             } else if (args.epi == PTK_EPI_DGELU) {
                 float p[8];
-                unpack_bf16x8(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.aux) + xrowoff + gn), p);
+                unpack_bf16x8(xa[j], p);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) f[i] *= gelu_tanh_grad(p[i]);
             }
             *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + rowoff + gn) = pack_bf16x8(f);
         }
+        }
+        if (epi_has_aux(args) && ci + 2 < EpiIn<BN>::kChunks && c + 4 < BN / 32)
+            epi_fetch_aux(args, tc, c + 4, quad, lane, in.aux(ci & 1));  // two chunks ahead
     }
 }
 
@@ -373,13 +441,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quad = warp & 3;
         const int half = (warp - 2) >> 2;  // 0 or 1
         float4* stage_buf = reinterpret_cast<float4*>(epi_smem) + (warp - 2) * 256;  // 32 rows x 8 float4
+        __nv_bfloat16* bias_s = reinterpret_cast<__nv_bfloat16*>(epi_smem + 8 * 32 * 32 * 4);  // [2][BN]
+        const int et = (warp - 2) * 32 + static_cast<int>(lane);
         int acc = 0;
         uint32_t acc_phase = 0;
+        EpiIn<BN> in;
         for (int t = t_begin; t < args.num_tiles; t += t_step) {
             const TileCoord tc = decode_tile<MC>(args, t, rank);
+            epi_prefetch<BN>(args, tc, quad, half, lane, et, bias_s + acc * BN, in);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            epilogue_tile<BN>(args, tc, tmem_base + static_cast<uint32_t>(acc * BN), quad, half, lane, stage_buf);
+            epilogue_tile<BN>(args, tc, tmem_base + static_cast<uint32_t>(acc * BN), quad, half, lane, stage_buf,
+                              bias_s + acc * BN, in);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -410,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // warps release the accumulator on the leader's tmem-empty barrier.
 constexpr int k2smStages = 6;
 constexpr int k2smStageBytes = 2 * 128 * kBK * 2;  // A half + B half
-constexpr int k2smSmem = k2smStages * k2smStageBytes + 1024 + 512 + 8 * 32 * 32 * 4;
+constexpr int k2smSmem = k2smStages * k2smStageBytes + 1024 + 512 + 8 * 32 * 32 * 4 + 2 * 256 * 2;
 
 __device__ __forceinline__ TileCoord decode_pair_tile(const GemmArgs& a, int t, int rank) {
     // t indexes 256 x 256 pair tiles; this CTA's rows are m0 + rank*128
@@ -548,13 +621,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quad = warp & 3;
         const int half = (warp - 2) >> 2;
         float4* stage_buf = reinterpret_cast<float4*>(epi_smem) + (warp - 2) * 256;
+        __nv_bfloat16* bias_s = reinterpret_cast<__nv_bfloat16*>(epi_smem + 8 * 32 * 32 * 4);  // [2][256]
+        const int et = (warp - 2) * 32 + static_cast<int>(lane);
         int acc = 0;
         uint32_t acc_phase = 0;
+        EpiIn<256> in;
         for (int t = t_begin; t < args.num_tiles; t += t_step) {
             const TileCoord tc = decode_pair_tile(args, t, rank);
+            epi_prefetch<256>(args, tc, quad, half, lane, et, bias_s + acc * 256, in);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            epilogue_tile<256>(args, tc, tmem_base + static_cast<uint32_t>(acc * 256), quad, half, lane, stage_buf);
+            epilogue_tile<256>(args, tc, tmem_base + static_cast<uint32_t>(acc * 256), quad, half, lane, stage_buf,
+                               bias_s + acc * 256, in);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {

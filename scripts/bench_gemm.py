@@ -9,7 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2303_01675_b200 import _lib as L  # noqa: E402
 
 
-MC = int(__import__("os").environ.get("PTK_MC", "1"))
+MC = int(__import__("os").environ.get("PTK_MC", "2"))
 
 
 def gemm_desc(m, n, k, A, a_mn, B, b_mn, Cm, epi):
@@ -40,32 +40,69 @@ def timeit(fn, iters=20):
 
 def main():
     dev = torch.device("cuda:0")
-    T = 2048
-    shapes = [  # (name, m, n, k, a_mn, b_mn, epi)
-        ("qkv_fwd", T, 6144, 2048, 0, 0, L.EPI_BF16),
-        ("fc1_fwd", T, 8192, 2048, 0, 0, L.EPI_BF16),
-        ("fc2_fwd", T, 2048, 8192, 0, 0, L.EPI_BF16),
-        ("out_fwd", T, 2048, 2048, 0, 0, L.EPI_BF16),
-        ("fc1_dgrad", T, 2048, 8192, 0, 1, L.EPI_BF16),
-        ("fc1_wgrad", 8192, 2048, T, 1, 1, L.EPI_ACC_F32),
-        ("qkv_wgrad", 6144, 2048, T, 1, 1, L.EPI_ACC_F32),
-        ("head_fwd", T, 50304, 2048, 0, 0, L.EPI_BF16),
+    T, h, f, V = 2048, 2048, 8192, 50304
+    B_ = L.EPI_BF16
+    shapes = [  # (name, m, n, k, a_mn, b_mn, epi, bias, aux, c2)
+        ("qkv_fwd", T, 3 * h, h, 0, 0, B_, 1, 0, 0),
+        ("out_fwd", T, h, h, 0, 0, B_, 1, 1, 0),
+        ("fc1_fwd", T, f, h, 0, 0, L.EPI_BIAS_GELU, 1, 0, 1),
+        ("fc2_fwd", T, h, f, 0, 0, B_, 1, 1, 0),
+        ("fc2_dgrad", T, f, h, 0, 1, L.EPI_DGELU, 0, 1, 0),
+        ("fc2_wgrad", h, f, T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
+        ("fc1_dgrad", T, h, f, 0, 1, B_, 0, 0, 0),
+        ("fc1_wgrad", f, h, T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
+        ("out_dgrad", T, h, h, 0, 1, B_, 0, 0, 0),
+        ("out_wgrad", h, h, T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
+        ("qkv_dgrad", T, h, 3 * h, 0, 1, B_, 0, 0, 0),
+        ("qkv_wgrad", 3 * h, h, T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
+        ("head_fwd", T, V, h, 0, 0, B_, 0, 0, 0),
+        ("head_dgrad", T, h, V, 0, 1, B_, 0, 0, 0),
+        ("head_wgrad", V, h, T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
+        # epilogue isolation (same shapes, plain bf16 store)
+        ("x_fc1_plain", T, f, h, 0, 0, B_, 0, 0, 0),
+        ("x_fc1_bias", T, f, h, 0, 0, B_, 1, 0, 0),
+        ("x_fc2dgrad_plain", T, f, h, 0, 1, B_, 0, 0, 0),
+        ("x_out_plain", T, h, h, 0, 0, B_, 0, 0, 0),
+        ("x_out_aux", T, h, h, 0, 0, B_, 0, 1, 0),
+        ("x_fc2wgrad_f32", h, f, T, 1, 1, L.EPI_F32, 0, 0, 0),
+        ("x_fc2wgrad_bf16", h, f, T, 1, 1, B_, 0, 0, 0),
     ]
     stream = torch.cuda.current_stream().cuda_stream
     out = []
-    for name, m, n, k, a_mn, b_mn, epi in shapes:
+    tot_ptk = tot_cub = tot_fl = 0.0
+    for name, m, n, k, a_mn, b_mn, epi, bias, aux, c2 in shapes:
         A = torch.randn((k, m) if a_mn else (m, k), device=dev).bfloat16()
         B = torch.randn((k, n) if b_mn else (n, k), device=dev).bfloat16()
         Cm = torch.zeros(m, n, device=dev, dtype=torch.float32 if epi == L.EPI_ACC_F32 else torch.bfloat16)
         d = gemm_desc(m, n, k, A, a_mn, B, b_mn, Cm, epi)
+        keep = []
+        if bias:
+            bv = torch.randn(n, device=dev).bfloat16()
+            keep.append(bv)
+            d.bias = bv.data_ptr()
+        if aux:
+            av = torch.randn(m, n, device=dev).bfloat16()
+            keep.append(av)
+            d.aux = L.matrix(av.data_ptr(), n)
+        if c2:
+            cv = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+            keep.append(cv)
+            d.c2 = cv.data_ptr()
         t = timeit(lambda: L.check(L.lib().ptk_gemm(d, stream)))
         Ab = A.T if a_mn else A
         Bb = B if b_mn else B.T
         tc = timeit(lambda: torch.matmul(Ab, Bb))
         fl = 2.0 * m * n * k
+        if not name.startswith("head") and not name.startswith("x_"):
+            tot_ptk += t
+            tot_cub += tc
+            tot_fl += fl
         out.append({"gemm": name, "ptk_us": round(t * 1e6, 1), "ptk_tflops": round(fl / t / 1e12, 1),
                     "cublas_us": round(tc * 1e6, 1), "cublas_tflops": round(fl / tc / 1e12, 1)})
         print(json.dumps(out[-1]), flush=True)
+    print(json.dumps({"layer_total_us": round(tot_ptk * 1e6, 1), "layer_tflops": round(tot_fl / tot_ptk / 1e12, 1),
+                      "cublas_layer_us": round(tot_cub * 1e6, 1),
+                      "cublas_layer_tflops": round(tot_fl / tot_cub / 1e12, 1)}), flush=True)
 
 
 if __name__ == "__main__":
