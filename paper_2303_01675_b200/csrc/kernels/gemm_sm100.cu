@@ -145,65 +145,43 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t, int r
 }
 
 // ---------------------------------------------------------------- epilogue
-// Every global input of a tile's epilogue that does not depend on the
-// accumulator (bias slice, residual / pre-activation aux rows, the previous
-// fp32 C of a wgrad accumulation) is fetched BEFORE the epilogue waits for the
-// accumulator, so its latency hides under the main loop; later chunks are
-// fetched one or two chunks ahead.  Warp (quad, half) owns TMEM lanes
-// [32 quad, +32) and the 32-column chunks c = half, half+2, ... of the tile.
-template <int BN>
-struct EpiIn {
-    static constexpr int kChunks = (BN / 32 + 1) / 2;  // chunks per warp
-    // one register buffer, by epilogue kind:
-    //   aux (BF16 residual / DGELU): words [4 (i & 1), +4) hold chunk i's 4 x 8 bf16 of this row
-    //   ACC_F32: 8 float4 of the next chunk's previous C (transposed mapping)
-    uint4 buf[8];
-    __device__ __forceinline__ uint4 (&aux(int slot))[4] { return *reinterpret_cast<uint4(*)[4]>(buf + 4 * slot); }
-    __device__ __forceinline__ float4 (&prev())[8] { return *reinterpret_cast<float4(*)[8]>(buf); }
-};
-
 __device__ __forceinline__ bool epi_has_aux(const GemmArgs& a) {
     return (a.epi == PTK_EPI_BF16 && a.aux != nullptr) || a.epi == PTK_EPI_DGELU;
 }
 
-__device__ __forceinline__ void epi_fetch_aux(const GemmArgs& args, const TileCoord& tc, int c, int quad,
-                                              uint32_t lane, uint4 (&aux)[4]) {
+// Every global input of a tile's epilogue that does not depend on the
+// accumulator (bias slice -> smem, residual / pre-activation aux rows) is
+// fetched BEFORE the epilogue waits for the accumulator, so its latency hides
+// under the main loop; the next step's aux is fetched during this step.
+// Warp (quad, half) owns TMEM lanes [32 quad, +32).
+// bf16 outputs leave in 64-column steps (s = half, half+2, ... of BN/64),
+// fp32 outputs in 32-column chunks (c = half, half+2, ...): the warp writes
+// its 32 rows of the step into its own 4 KB staging buffer in the 128B-swizzled
+// layout (16-byte chunk j of row r at (j ^ r%8)), and one lane issues a TMA
+// store of the [32 x 128 B] box — full-line writes that bypass the LSU, so the
+// epilogue does not compete with the tensor core for L1/smem wavefronts.
+// EPI_ACC_F32 uses the TMA reduce-add (C += tile, one fp32 add per element).
+struct EpiTmaIn {
+    uint4 aux[8];  // next step's aux: 8 x (8 bf16) of this thread's row
+};
+
+__device__ __forceinline__ void epi_fetch_aux64(const GemmArgs& args, const TileCoord& tc, int step, int quad,
+                                                uint32_t lane, uint4 (&aux)[8]) {
     const int gm = tc.m0 + quad * 32 + static_cast<int>(lane);
     const int64_t xrow = tc.z1 * args.aux_bs1 + tc.z2 * args.aux_bs2 + static_cast<int64_t>(gm) * args.ld_aux;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int gn = tc.n0 + c * 32 + 8 * j;
+    for (int j = 0; j < 8; ++j) {
+        const int gn = tc.n0 + step * 64 + 8 * j;
         aux[j] = (gm < args.M && gn < args.N)
                      ? *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(args.aux) + xrow + gn)
                      : make_uint4(0u, 0u, 0u, 0u);
     }
 }
 
-__device__ __forceinline__ void epi_fetch_prev(const GemmArgs& args, const TileCoord& tc, int c, int quad,
-                                               uint32_t lane, float4 (&prev)[8]) {
-    const int q = static_cast<int>(lane & 7), r0 = static_cast<int>(lane >> 3);
-    const int gn = tc.n0 + c * 32 + q * 4;
-    const float* cbase = static_cast<const float*>(args.C) + tc.z1 * args.c_bs1 + tc.z2 * args.c_bs2 + gn;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int gm = tc.m0 + quad * 32 + r0 + 4 * i;
-        prev[i] = (gn < args.N && gm < args.M) ? *reinterpret_cast<const float4*>(cbase + static_cast<int64_t>(gm) * args.ldc)
-                                               : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-}
-
-// Before the accumulator wait: this warp's first chunks' inputs, and the tile's
-// bias slice into smem (bias_s: BN bf16; the 8 epilogue warps sync on named
-// barrier 1 — the buffer is double-buffered by the caller per accumulator).
 template <int BN>
-__device__ __forceinline__ void epi_prefetch(const GemmArgs& args, const TileCoord& tc, int quad, int half,
-                                             uint32_t lane, int et, __nv_bfloat16* bias_s, EpiIn<BN>& in) {
-    if (args.epi == PTK_EPI_ACC_F32) {
-        epi_fetch_prev(args, tc, half, quad, lane, in.prev());
-    } else if (epi_has_aux(args)) {
-        epi_fetch_aux(args, tc, half, quad, lane, in.aux(0));
-        if (EpiIn<BN>::kChunks > 1) epi_fetch_aux(args, tc, half + 2, quad, lane, in.aux(1));
-    }
+__device__ __forceinline__ void epi_prefetch_tma(const GemmArgs& args, const TileCoord& tc, int quad, int half,
+                                                 uint32_t lane, int et, __nv_bfloat16* bias_s, EpiTmaIn& in) {
+    if (epi_has_aux(args) && half < BN / 64) epi_fetch_aux64(args, tc, half, quad, lane, in.aux);
     if (args.bias != nullptr) {
         if (et < BN / 8) {
             const int gn = tc.n0 + et * 8;
@@ -215,98 +193,102 @@ __device__ __forceinline__ void epi_prefetch(const GemmArgs& args, const TileCoo
     }
 }
 
-// Epilogue of one accumulator tile held in TMEM columns [tmem_col, tmem_col + BN).
-template <int BN>
-__device__ __forceinline__ void epilogue_tile(const GemmArgs& args, const TileCoord& tc, uint32_t tmem_col, int quad,
-                                              int half, uint32_t lane, float4* stage_buf,
-                                              const __nv_bfloat16* bias_s, EpiIn<BN>& in) {
-    const int q = static_cast<int>(lane & 7);
-    const int r0 = static_cast<int>(lane >> 3);
-    const bool f32_out = args.epi == PTK_EPI_F32 || args.epi == PTK_EPI_ACC_F32;
-    const int64_t zoff_c = tc.z1 * args.c_bs1 + tc.z2 * args.c_bs2;
-    const int row_base = tc.m0 + quad * 32;
+// 8 x 16 bytes of this lane's row into the swizzled staging buffer, then one TMA store.
+__device__ __forceinline__ void epi_stage_store(const CUtensorMap* map, uint8_t* stage, uint32_t lane,
+                                                const uint4 (&row)[8], int c0, int c1, int c2, int c3, bool reduce) {
+    if (lane == 0) tma_store_wait_read();  // the previous store from this buffer has read it
+    __syncwarp();
+    const uint32_t base = smem_u32(stage) + lane * 128;
 #pragma unroll
-    for (int ci = 0; ci < EpiIn<BN>::kChunks; ++ci) {
-        const int c = half + 2 * ci;
-        if (c >= BN / 32) break;
-        float v[32];
-        __syncwarp();
-        tmem_ld_32x32b_x32(tmem_col + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(c * 32),
-                           v);
-        if (f32_out) {
-            // fp32 output: transpose through smem so each warp store covers
-            // 4 rows x 128 contiguous bytes
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t a = base + ((j ^ (lane & 7)) * 16);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(row[j].x), "r"(row[j].y),
+                     "r"(row[j].z), "r"(row[j].w)
+                     : "memory");
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        if (reduce)
+            tma_reduce_add_4d(map, stage, c0, c1, c2, c3);
+        else
+            tma_store_4d(map, stage, c0, c1, c2, c3);
+        tma_store_commit();
+    }
+}
+
+template <int BN>
+__device__ __forceinline__ void epilogue_tile_tma(const CUtensorMap* tmC, const CUtensorMap* tmC2,
+                                                  const GemmArgs& args, const TileCoord& tc, uint32_t tmem_col,
+                                                  int quad, int half, uint32_t lane, uint8_t* stage,
+                                                  const __nv_bfloat16* bias_s, EpiTmaIn& in) {
+    const uint32_t lane_addr = static_cast<uint32_t>(quad * 32) << 16;
+    const int row0 = tc.m0 + quad * 32;
+    if (args.epi == PTK_EPI_F32 || args.epi == PTK_EPI_ACC_F32) {
+        const bool reduce = args.epi == PTK_EPI_ACC_F32;
+#pragma unroll 1
+        for (int c = half; c < BN / 32; c += 2) {
+            float v[32];
+            tmem_ld_32x32b_x32(tmem_col + lane_addr + static_cast<uint32_t>(c * 32), v);
+            uint4 row[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-                stage_buf[lane * 8 + (j ^ (lane & 7))] =
-                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            __syncwarp();
-            float4(&prev)[8] = in.prev();
-            const int gn = tc.n0 + c * 32 + q * 4;
-            if (gn < args.N) {
-                float* cbase = static_cast<float*>(args.C) + zoff_c + gn;
-                const bool acc = args.epi == PTK_EPI_ACC_F32;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int r = r0 + 4 * i;
-                    const int gm = row_base + r;
-                    const float4 a4 = stage_buf[r * 8 + (q ^ (r & 7))];
-                    if (gm < args.M)
-                        *reinterpret_cast<float4*>(cbase + static_cast<int64_t>(gm) * args.ldc) =
-                            acc ? make_float4(prev[i].x + a4.x, prev[i].y + a4.y, prev[i].z + a4.z, prev[i].w + a4.w)
-                                : a4;
-                }
-            }
-            if (args.epi == PTK_EPI_ACC_F32 && ci + 1 < EpiIn<BN>::kChunks && c + 2 < BN / 32)
-                epi_fetch_prev(args, tc, c + 2, quad, lane, in.prev());  // next chunk, in flight during its tmem load
-            continue;
+                row[j] = make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                                    __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+            epi_stage_store(tmC, stage, lane, row, tc.n0 + c * 32, row0, tc.z1, tc.z2, reduce);
         }
-        // bf16 output: thread = row, 16-byte stores of 8 columns
-        const int gm = row_base + static_cast<int>(lane);
-        const int gn0 = tc.n0 + c * 32;
-        uint4(&xa)[4] = in.aux(ci & 1);
-        if (gm < args.M) {
-        const int64_t rowoff = zoff_c + static_cast<int64_t>(gm) * args.ldc;
+        return;
+    }
+#pragma unroll 1
+    for (int st = half; st < BN / 64; st += 2) {
+        float v[64];
+        tmem_ld_32x32b_x32_nw(tmem_col + lane_addr + static_cast<uint32_t>(st * 64), v);
+        tmem_ld_32x32b_x32_nw(tmem_col + lane_addr + static_cast<uint32_t>(st * 64 + 32), v + 32);
+        tmem_ld_wait();
+        uint4 out[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int gn = gn0 + 8 * j;
-            if (gn >= args.N) continue;
+        for (int j = 0; j < 8; ++j) {
             float* f = v + 8 * j;
             if (args.bias != nullptr) {
                 float bb[8];
-                unpack_bf16x8(*reinterpret_cast<const uint4*>(bias_s + c * 32 + 8 * j), bb);
+                unpack_bf16x8(*reinterpret_cast<const uint4*>(bias_s + st * 64 + 8 * j), bb);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) f[i] += bb[i];
             }
             if (args.epi == PTK_EPI_BF16 && args.aux != nullptr) {
                 float r[8];
-                unpack_bf16x8(xa[j], r);
+                unpack_bf16x8(in.aux[j], r);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) f[i] += r[i];
-            } else if (args.epi == PTK_EPI_BIAS_GELU) {
-                const uint4 pre = pack_bf16x8(f);
-                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C2) + rowoff + gn) = pre;
-                float p[8];
-                unpack_bf16x8(pre, p);  // gelu of the rounded pre-activation, as stored
-#pragma unroll
-                for (int i = 0; i < 8; ++i) f[i] = gelu_tanh(p[i]);
             } else if (args.epi == PTK_EPI_DGELU) {
                 float p[8];
-                unpack_bf16x8(xa[j], p);
+                unpack_bf16x8(in.aux[j], p);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) f[i] *= gelu_tanh_grad(p[i]);
             }
-            *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + rowoff + gn) = pack_bf16x8(f);
+            out[j] = pack_bf16x8(f);
         }
+        if (epi_has_aux(args) && st + 2 < BN / 64) epi_fetch_aux64(args, tc, st + 2, quad, lane, in.aux);
+        if (args.epi == PTK_EPI_BIAS_GELU) {
+            // out holds the rounded pre-activation: store it (C2), then C = gelu(pre as stored)
+            epi_stage_store(tmC2, stage, lane, out, tc.n0 + st * 64, row0, tc.z1, tc.z2, false);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float p[8];
+                unpack_bf16x8(out[j], p);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) p[i] = gelu_tanh(p[i]);
+                out[j] = pack_bf16x8(p);
+            }
         }
-        if (epi_has_aux(args) && ci + 2 < EpiIn<BN>::kChunks && c + 4 < BN / 32)
-            epi_fetch_aux(args, tc, c + 4, quad, lane, in.aux(ci & 1));  // two chunks ahead
+        epi_stage_store(tmC, stage, lane, out, tc.n0 + st * 64, row0, tc.z1, tc.z2, false);
     }
 }
 
 template <int BN, bool A_MN, bool B_MN, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                      const __grid_constant__ GemmArgs args) {
     using C = Cfg<BN>;
     constexpr int S = C::kStages;
@@ -314,12 +296,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    uint8_t* epi_smem = smem + S * C::kStageBytes;  // 8 warps x 4 KB staging (1024-aligned), then 2 bias slices
+    uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + C::kEpiBytes);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    uint8_t* epi_smem = smem + S * C::kStageBytes + 512;  // 8 warps x 4 KB transpose buffers
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
@@ -440,19 +422,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (warp % 4); the pair splits the 32-column chunks of a tile.
         const int quad = warp & 3;
         const int half = (warp - 2) >> 2;  // 0 or 1
-        float4* stage_buf = reinterpret_cast<float4*>(epi_smem) + (warp - 2) * 256;  // 32 rows x 8 float4
+        uint8_t* stage = epi_smem + (warp - 2) * 4096;  // 32 rows x 128 B, 128B-swizzled
         __nv_bfloat16* bias_s = reinterpret_cast<__nv_bfloat16*>(epi_smem + 8 * 32 * 32 * 4);  // [2][BN]
         const int et = (warp - 2) * 32 + static_cast<int>(lane);
         int acc = 0;
         uint32_t acc_phase = 0;
-        EpiIn<BN> in;
+        EpiTmaIn tin;
         for (int t = t_begin; t < args.num_tiles; t += t_step) {
             const TileCoord tc = decode_tile<MC>(args, t, rank);
-            epi_prefetch<BN>(args, tc, quad, half, lane, et, bias_s + acc * BN, in);
+            epi_prefetch_tma<BN>(args, tc, quad, half, lane, et, bias_s + acc * BN, tin);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            epilogue_tile<BN>(args, tc, tmem_base + static_cast<uint32_t>(acc * BN), quad, half, lane, stage_buf,
-                              bias_s + acc * BN, in);
+            epilogue_tile_tma<BN>(&tmC, &tmC2, args, tc, tmem_base + static_cast<uint32_t>(acc * BN), quad, half, lane,
+                                  stage, bias_s + acc * BN, tin);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -461,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_phase ^= 1;
             }
         }
+        if (lane == 0) tma_store_wait_all();  // staging must outlive the stores
     }
 
     tc_fence_before();
@@ -505,6 +488,7 @@ __device__ __forceinline__ TileCoord decode_pair_tile(const GemmArgs& a, int t, 
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                          const __grid_constant__ GemmArgs args) {
     constexpr int S = k2smStages;
     constexpr int kHalf = 128 * kBK * 2;  // 16 KiB
@@ -512,12 +496,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * k2smStageBytes);
+    uint8_t* epi_smem = smem + S * k2smStageBytes;  // 8 warps x 4 KB staging (1024-aligned), then 2 bias slices
+    uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + 8 * 32 * 32 * 4 + 2 * 256 * 2);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    uint8_t* epi_smem = smem + S * k2smStageBytes + 512;
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
@@ -620,19 +604,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {  // ---------------- epilogue warps (both CTAs): this CTA's 128 rows
         const int quad = warp & 3;
         const int half = (warp - 2) >> 2;
-        float4* stage_buf = reinterpret_cast<float4*>(epi_smem) + (warp - 2) * 256;
+        uint8_t* stage = epi_smem + (warp - 2) * 4096;  // 32 rows x 128 B, 128B-swizzled
         __nv_bfloat16* bias_s = reinterpret_cast<__nv_bfloat16*>(epi_smem + 8 * 32 * 32 * 4);  // [2][256]
         const int et = (warp - 2) * 32 + static_cast<int>(lane);
         int acc = 0;
         uint32_t acc_phase = 0;
-        EpiIn<256> in;
+        EpiTmaIn tin;
         for (int t = t_begin; t < args.num_tiles; t += t_step) {
             const TileCoord tc = decode_pair_tile(args, t, rank);
-            epi_prefetch<256>(args, tc, quad, half, lane, et, bias_s + acc * 256, in);
+            epi_prefetch_tma<256>(args, tc, quad, half, lane, et, bias_s + acc * 256, tin);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            epilogue_tile<256>(args, tc, tmem_base + static_cast<uint32_t>(acc * 256), quad, half, lane, stage_buf,
-                               bias_s + acc * 256, in);
+            epilogue_tile_tma<256>(&tmC, &tmC2, args, tc, tmem_base + static_cast<uint32_t>(acc * 256), quad, half,
+                                   lane, stage, bias_s + acc * 256, tin);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -646,6 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_phase ^= 1;
             }
         }
+        if (lane == 0) tma_store_wait_all();  // staging must outlive the stores
     }
 
     tc_fence_before();
@@ -699,6 +684,30 @@ int encode_operand(CUtensorMap* map, const ptk_matrix& m, int contig_extent, int
     return r == CUDA_SUCCESS ? PTK_OK : PTK_ERR_CUDA;
 }
 
+// Output map: dims = {N, M, batch1, batch2}; box = {128 B of columns, 32 rows}, 128B swizzle.
+int encode_output(CUtensorMap* map, void* ptr, int64_t ld, int64_t bs1, int64_t bs2, int M, int N, int batch1,
+                  int batch2, bool f32) {
+    EncodeTiledFn enc = encode_fn();
+    if (enc == nullptr || ptr == nullptr) return PTK_ERR_CUDA;
+    const int64_t es = f32 ? 4 : 2;
+    if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || (ld * es) % 16 != 0) return PTK_ERR_ALIGN;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(batch1),
+                          static_cast<cuuint64_t>(batch2)};
+    const int64_t row_bytes = ld * es;
+    int64_t s1 = bs1 * es, s2 = bs2 * es;
+    if (batch1 <= 1) s1 = row_bytes * M;
+    if (batch2 <= 1) s2 = s1 * (batch1 > 0 ? batch1 : 1);
+    if (s1 % 16 != 0 || s2 % 16 != 0 || s1 <= 0 || s2 <= 0) return PTK_ERR_ALIGN;
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(row_bytes), static_cast<cuuint64_t>(s1),
+                             static_cast<cuuint64_t>(s2)};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(128 / es), 32, 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, ptr, dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? PTK_OK : PTK_ERR_CUDA;
+}
+
 template <int BN, bool A_MN, bool B_MN, bool MC>
 int launch_impl(const GemmPlan& p, cudaStream_t stream) {
     using C = Cfg<BN>;
@@ -710,7 +719,7 @@ int launch_impl(const GemmPlan& p, cudaStream_t stream) {
         attr_set = true;
     }
     if (!MC) {
-        kern<<<p.grid, kThreads, C::kSmemBytes, stream>>>(p.tmA, p.tmB, p.args);
+        kern<<<p.grid, kThreads, C::kSmemBytes, stream>>>(p.tmA, p.tmB, p.tmC, p.tmC2, p.args);
     } else {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(p.grid);
@@ -724,7 +733,7 @@ int launch_impl(const GemmPlan& p, cudaStream_t stream) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.args) != cudaSuccess) return PTK_ERR_CUDA;
+        if (cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.tmC, p.tmC2, p.args) != cudaSuccess) return PTK_ERR_CUDA;
     }
     return cudaPeekAtLastError() == cudaSuccess ? PTK_OK : PTK_ERR_CUDA;
 }
@@ -750,7 +759,7 @@ int launch_2sm(const GemmPlan& p, cudaStream_t stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.args) != cudaSuccess) return PTK_ERR_CUDA;
+    if (cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.tmC, p.tmC2, p.args) != cudaSuccess) return PTK_ERR_CUDA;
     return cudaPeekAtLastError() == cudaSuccess ? PTK_OK : PTK_ERR_CUDA;
 }
 
@@ -851,6 +860,14 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     a.bias = d.bias;
     if ((a.epi == PTK_EPI_DGELU && a.aux == nullptr) || (a.epi == PTK_EPI_BIAS_GELU && (a.C2 == nullptr)))
         return PTK_ERR_ARG;
+    {  // TMA-store epilogue when the output layout allows it (16-byte aligned rows and batches)
+        const bool f32 = a.epi == PTK_EPI_F32 || a.epi == PTK_EPI_ACC_F32;
+        bool ok = encode_output(&p.tmC, a.C, a.ldc, a.c_bs1, a.c_bs2, d.m, d.n, b1, b2, f32) == PTK_OK;
+        if (ok && a.epi == PTK_EPI_BIAS_GELU)
+            ok = encode_output(&p.tmC2, a.C2, a.ldc, a.c_bs1, a.c_bs2, d.m, d.n, b1, b2, false) == PTK_OK;
+        if (!ok) return PTK_ERR_ALIGN;  // outputs leave through TMA: 16-byte aligned rows and batches
+        a.tma_store = 1;
+    }
 
     const int sms = num_sms();
     // B-tile multicast across a 2-CTA cluster halves the L2 -> SM operand

@@ -70,7 +70,10 @@ def main():
     stream = torch.cuda.current_stream().cuda_stream
     out = []
     tot_ptk = tot_cub = tot_fl = 0.0
+    only = __import__("os").environ.get("PTK_ONLY", "")
     for name, m, n, k, a_mn, b_mn, epi, bias, aux, c2 in shapes:
+        if only and name not in only.split(","):
+            continue
         A = torch.randn((k, m) if a_mn else (m, k), device=dev).bfloat16()
         B = torch.randn((k, n) if b_mn else (n, k), device=dev).bfloat16()
         Cm = torch.zeros(m, n, device=dev, dtype=torch.float32 if epi == L.EPI_ACC_F32 else torch.bfloat16)
@@ -100,6 +103,8 @@ def main():
         out.append({"gemm": name, "ptk_us": round(t * 1e6, 1), "ptk_tflops": round(fl / t / 1e12, 1),
                     "cublas_us": round(tc * 1e6, 1), "cublas_tflops": round(fl / tc / 1e12, 1)})
         print(json.dumps(out[-1]), flush=True)
+    if only:
+        return
     print(json.dumps({"layer_total_us": round(tot_ptk * 1e6, 1), "layer_tflops": round(tot_fl / tot_ptk / 1e12, 1),
                       "cublas_layer_us": round(tot_cub * 1e6, 1),
                       "cublas_layer_tflops": round(tot_fl / tot_cub / 1e12, 1)}), flush=True)
