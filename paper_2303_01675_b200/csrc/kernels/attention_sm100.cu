@@ -28,6 +28,7 @@
 #include <mutex>
 
 #include "attention_sm100.h"
+#include "launch.cuh"
 #include "sm100_ptx.cuh"
 
 namespace ptk {
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_begin();  // previous kernel complete: its outputs (qkv, lse, dO, ...) are visible
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -406,8 +408,7 @@ cudaError_t launch_fwd(const FlashPlan& p, cudaStream_t st) {
     FaArgs a{p.o, p.lse, p.s, p.H, p.H * p.d, p.b, p.scale_log2, p.causal};
     const int tiles = p.s / kBlk * p.H * p.b;
     const int grid = tiles < sm_count() ? tiles : sm_count();
-    flash_fwd_kernel<D><<<grid, kThreads, C::kSmem, st>>>(p.tmQK, p.tmV, a);
-    return cudaPeekAtLastError();
+    return launch_kernel(flash_fwd_kernel<D>, grid, kThreads, C::kSmem, st, 1, p.tmQK, p.tmV, a);
 }
 
 }  // namespace
@@ -631,6 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_begin();  // previous kernel complete: its outputs (qkv, lse, dO, ...) are visible
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -882,6 +884,7 @@ template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ dO,
                                                            const __nv_bfloat16* __restrict__ O,
                                                            float* __restrict__ dsum, int rows, int s, int H) {
+    pdl_begin();
     constexpr int kLanesPerHead = D / 8;
     const int row = blockIdx.x * 8 + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -943,8 +946,7 @@ cudaError_t launch_bwd(const FlashBwdPlan& p, cudaStream_t st) {
              p.causal};
     const int tiles = p.s / kBlk * p.H * p.b;
     const int grid = tiles < sm_count() ? tiles : sm_count();
-    flash_bwd_kernel<D, KV><<<grid, kThreads, C::kSmem, st>>>(p.tmQKV, p.tmDO, a);
-    return cudaPeekAtLastError();
+    return launch_kernel(flash_bwd_kernel<D, KV>, grid, kThreads, C::kSmem, st, 1, p.tmQKV, p.tmDO, a);
 }
 
 }  // namespace
@@ -972,11 +974,11 @@ cudaError_t flash_bwd_prepare(const void* qkv, const void* o, const void* dO, co
 
 cudaError_t flash_backward(const FlashBwdPlan& p, cudaStream_t st) {
     const int rows = p.b * p.s;
+    cudaError_t e;
     if (p.d == 64)
-        attn_bwd_dot_kernel<64><<<(rows + 7) / 8, 256, 0, st>>>(p.dO, p.o, p.dsum, rows, p.s, p.H);
+        e = launch_kernel(attn_bwd_dot_kernel<64>, (rows + 7) / 8, 256, 0, st, 1, p.dO, p.o, p.dsum, rows, p.s, p.H);
     else
-        attn_bwd_dot_kernel<128><<<(rows + 7) / 8, 256, 0, st>>>(p.dO, p.o, p.dsum, rows, p.s, p.H);
-    cudaError_t e = cudaPeekAtLastError();
+        e = launch_kernel(attn_bwd_dot_kernel<128>, (rows + 7) / 8, 256, 0, st, 1, p.dO, p.o, p.dsum, rows, p.s, p.H);
     if (e != cudaSuccess) return e;
     e = p.d == 64 ? launch_bwd<64, true>(p, st) : launch_bwd<128, true>(p, st);
     if (e != cudaSuccess) return e;

@@ -33,6 +33,7 @@
 
 #include "../../../include/ptk.h"
 #include "gemm_sm100.h"
+#include "launch.cuh"
 #include "sm100_ptx.cuh"
 
 namespace ptk {
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (MC) cluster_sync();  // peer barriers initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_begin();  // previous kernel complete: operands / aux / C visible
 
     if (warp == 0) {
         if (lane == 0) {
@@ -529,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_begin();  // previous kernel complete: operands / aux / C visible
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
@@ -718,23 +721,9 @@ int launch_impl(const GemmPlan& p, cudaStream_t stream) {
             return PTK_ERR_CUDA;
         attr_set = true;
     }
-    if (!MC) {
-        kern<<<p.grid, kThreads, C::kSmemBytes, stream>>>(p.tmA, p.tmB, p.tmC, p.tmC2, p.args);
-    } else {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(p.grid);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = C::kSmemBytes;
-        cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.tmC, p.tmC2, p.args) != cudaSuccess) return PTK_ERR_CUDA;
-    }
+    if (launch_kernel(kern, p.grid, kThreads, C::kSmemBytes, stream, MC ? 2 : 1, p.tmA, p.tmB, p.tmC, p.tmC2,
+                      p.args) != cudaSuccess)
+        return PTK_ERR_CUDA;
     return cudaPeekAtLastError() == cudaSuccess ? PTK_OK : PTK_ERR_CUDA;
 }
 
@@ -747,19 +736,8 @@ int launch_2sm(const GemmPlan& p, cudaStream_t stream) {
             return PTK_ERR_CUDA;
         attr_set = true;
     }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(p.grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = k2smSmem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.tmC, p.tmC2, p.args) != cudaSuccess) return PTK_ERR_CUDA;
+    if (launch_kernel(kern, p.grid, kThreads, k2smSmem, stream, 2, p.tmA, p.tmB, p.tmC, p.tmC2, p.args) != cudaSuccess)
+        return PTK_ERR_CUDA;
     return cudaPeekAtLastError() == cudaSuccess ? PTK_OK : PTK_ERR_CUDA;
 }
 

@@ -10,6 +10,7 @@
 #include <cstdint>
 
 #include "gpt_kernels.h"
+#include "launch.cuh"
 
 namespace ptk {
 namespace {
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(128) ln_fwd_kernel(const __nv_bfloat16* __rest
                                                      const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y,
                                                      float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                      int rows, float eps) {
+    pdl_begin();
     constexpr int H = V * 256;
     const int row = blockIdx.x * 4 + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -102,6 +104,7 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(const __nv_bfloat16* __rest
                                                      const __nv_bfloat16* __restrict__ g,
                                                      const __nv_bfloat16* __restrict__ resid,
                                                      __nv_bfloat16* __restrict__ dx, int rows) {
+    pdl_begin();
     constexpr int H = V * 256;
     const int row = blockIdx.x * 4 + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -154,6 +157,7 @@ __global__ void __launch_bounds__(256) colpart_kernel(const __nv_bfloat16* __res
                                                       const float* __restrict__ mean_in,
                                                       const float* __restrict__ rstd_in, float* __restrict__ part_g,
                                                       float* __restrict__ part_b, int rows, int cols) {
+    pdl_begin();
     __shared__ float sg[AFFINE ? 8 : 1][257];
     __shared__ float sb[8][257];
     const int cg = threadIdx.x & 31, rg = threadIdx.x >> 5;
@@ -196,6 +200,7 @@ __global__ void __launch_bounds__(256) colpart_kernel(const __nv_bfloat16* __res
 // grad[c] += sum_{p < P} part[p][c] (ascending p), part zeroed: one block row
 // per 1-D parameter of the stage, one launch per iteration.
 __global__ void __launch_bounds__(256) vec_finalize_kernel(const VecGradSeg* __restrict__ segs) {
+    pdl_begin();
     const VecGradSeg sg = segs[blockIdx.y];
     for (int c = blockIdx.x * 256 + threadIdx.x; c < sg.cols; c += gridDim.x * 256) {
         float v[kVecParts];
@@ -217,6 +222,7 @@ __global__ void __launch_bounds__(256) vec_finalize_kernel(const VecGradSeg* __r
 __global__ void __launch_bounds__(128) softmax_causal_fwd_kernel(const float* __restrict__ S,
                                                                  __nv_bfloat16* __restrict__ P, int rows, int n,
                                                                  float scale_log2) {
+    pdl_begin();
     const int row = blockIdx.x * 4 + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
@@ -261,6 +267,7 @@ __global__ void __launch_bounds__(128) softmax_causal_bwd_kernel(const __nv_bflo
                                                                  const float* __restrict__ dP,
                                                                  __nv_bfloat16* __restrict__ dS, int rows, int n,
                                                                  float scale) {
+    pdl_begin();
     const int row = blockIdx.x * 4 + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
@@ -302,6 +309,7 @@ __global__ void __launch_bounds__(128) softmax_causal_bwd_kernel(const __nv_bflo
 __global__ void __launch_bounds__(512) xent_kernel(__nv_bfloat16* __restrict__ logits,
                                                    const int32_t* __restrict__ labels, float* __restrict__ loss_rows,
                                                    int V, float grad_scale) {
+    pdl_begin();
     __shared__ float red[32];
     const int row = blockIdx.x;
     __nv_bfloat16* z = logits + static_cast<int64_t>(row) * V;
@@ -355,6 +363,7 @@ __global__ void __launch_bounds__(512) xent_kernel(__nv_bfloat16* __restrict__ l
 // loss_out[0] += sum(loss_rows) * scale  (single block, fixed order)
 __global__ void loss_sum_kernel(const float* __restrict__ loss_rows, float* __restrict__ loss_out, int rows,
                                 float scale) {
+    pdl_begin();
     __shared__ float red[32];
     float s = 0.f;
     for (int i = threadIdx.x; i < rows; i += blockDim.x) s += loss_rows[i];
@@ -374,6 +383,7 @@ __global__ void __launch_bounds__(128) embed_fwd_kernel(const int32_t* __restric
                                                         const __nv_bfloat16* __restrict__ wte,
                                                         const __nv_bfloat16* __restrict__ wpe,
                                                         __nv_bfloat16* __restrict__ x, int rows, int seq) {
+    pdl_begin();
     constexpr int H = V * 256;
     const int row = blockIdx.x * 4 + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -398,6 +408,7 @@ __global__ void __launch_bounds__(128) embed_fwd_kernel(const int32_t* __restric
 //     dX rows in that order and adds the sum to dwte[token].
 __global__ void __launch_bounds__(1024) embed_sort_kernel(const int32_t* __restrict__ tok, int32_t* __restrict__ order,
                                                           int rows) {
+    pdl_begin();
     extern __shared__ uint64_t keys[];  // pow2 >= rows
     int n = 1;
     while (n < rows) n <<= 1;
@@ -429,6 +440,7 @@ __global__ void __launch_bounds__(256) embed_bwd_runs_kernel(const int32_t* __re
                                                              const int32_t* __restrict__ order,
                                                              const __nv_bfloat16* __restrict__ dx,
                                                              float* __restrict__ dwte, int rows) {
+    pdl_begin();
     constexpr int H = V * 256;
     const int slot = blockIdx.x * 8 + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -470,6 +482,7 @@ __global__ void __launch_bounds__(256) embed_bwd_runs_kernel(const int32_t* __re
 // dwpe[p] += sum over samples (ascending) of dx[sample*seq + p]
 __global__ void embed_bwd_wpe_kernel(const __nv_bfloat16* __restrict__ dx, float* __restrict__ dwpe, int seq,
                                      int samples, int h) {
+    pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int p = blockIdx.y;
     if (c >= h) return;
@@ -490,6 +503,7 @@ __device__ __forceinline__ float gelu_grad_tanh(float x) {
 // out = dy * gelu'(pre)   (8 elements per thread)
 __global__ void dgelu_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ pre,
                              __nv_bfloat16* __restrict__ out, int64_t n8) {
+    pdl_begin();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         float d[8], p[8];
@@ -505,6 +519,7 @@ __global__ void dgelu_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bf
 __global__ void adamw_kernel(float* __restrict__ w, float* __restrict__ g, float* __restrict__ m,
                              float* __restrict__ v, __nv_bfloat16* __restrict__ wb, int64_t n, float lr, float b1,
                              float b2, float eps, float wd, float bc1, float bc2) {
+    pdl_begin();
     for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 4; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x * 4) {
         float4 ww = *reinterpret_cast<float4*>(w + i), gg = *reinterpret_cast<float4*>(g + i);
@@ -541,6 +556,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 
 // Counter-based normal init: element i of stream `seed` -> N(0, std) (+ mean for LN gamma).
 __global__ void init_normal_kernel(float* __restrict__ w, int64_t n, uint64_t seed, float std, float mean) {
+    pdl_begin();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         if (std == 0.f) {
@@ -555,6 +571,7 @@ __global__ void init_normal_kernel(float* __restrict__ w, int64_t n, uint64_t se
 }
 
 __global__ void cast_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int64_t n) {
+    pdl_begin();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         dst[i] = __float2bfloat16_rn(src[i]);
@@ -581,7 +598,7 @@ cudaError_t layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const 
                           float* mean, float* rstd, int rows, int h, float eps, cudaStream_t st) {
     if (h % 256) return cudaErrorInvalidValue;
     const int grid = (rows + 3) / 4;
-    PTK_DISPATCH_V(h, (ln_fwd_kernel<V><<<grid, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps)));
+    PTK_DISPATCH_V(h, (launch_kernel(ln_fwd_kernel<V>, grid, 128, 0, st, 1, x, g, b, y, mean, rstd, rows, eps)));
     return cudaPeekAtLastError();
 }
 
@@ -589,14 +606,14 @@ cudaError_t layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const
                           const __nv_bfloat16* g, const __nv_bfloat16* resid, __nv_bfloat16* dx, float* part_g,
                           float* part_b, int rows, int h, cudaStream_t st) {
     if (h % 256 || rows % kVecParts) return cudaErrorInvalidValue;
-    PTK_DISPATCH_V(h, (ln_bwd_kernel<V><<<(rows + 3) / 4, 128, 0, st>>>(dy, x, mean, rstd, g, resid, dx, rows)));
-    colpart_kernel<true><<<dim3(h / 256, kVecParts), 256, 0, st>>>(dy, x, mean, rstd, part_g, part_b, rows, h);
+    PTK_DISPATCH_V(h, (launch_kernel(ln_bwd_kernel<V>, (rows + 3) / 4, 128, 0, st, 1, dy, x, mean, rstd, g, resid, dx, rows)));
+    launch_kernel(colpart_kernel<true>, dim3(h / 256, kVecParts), 256, 0, st, 1, dy, x, mean, rstd, part_g, part_b, rows, h);
     return cudaPeekAtLastError();
 }
 
 cudaError_t colsum_partial(const __nv_bfloat16* m, float* part, int rows, int cols, cudaStream_t st) {
     if (cols % 256 || rows % kVecParts) return cudaErrorInvalidValue;
-    colpart_kernel<false><<<dim3(cols / 256, kVecParts), 256, 0, st>>>(m, nullptr, nullptr, nullptr, nullptr, part,
+    launch_kernel(colpart_kernel<false>, dim3(cols / 256, kVecParts), 256, 0, st, 1, m, nullptr, nullptr, nullptr, nullptr, part,
                                                                       rows, cols);
     return cudaPeekAtLastError();
 }
@@ -605,35 +622,35 @@ cudaError_t vec_grad_finalize(const VecGradSeg* segs_dev, int nseg, int max_cols
     if (nseg <= 0) return cudaSuccess;
     if (nseg > 65535) return cudaErrorInvalidValue;
     const int gx = std::min(16, (max_cols + 255) / 256);
-    vec_finalize_kernel<<<dim3(gx, nseg), 256, 0, st>>>(segs_dev);
+    launch_kernel(vec_finalize_kernel, dim3(gx, nseg), 256, 0, st, 1, segs_dev);
     return cudaPeekAtLastError();
 }
 
 cudaError_t softmax_causal_fwd(const float* S, __nv_bfloat16* P, int rows, int n, float scale, cudaStream_t st) {
     if (n % 128) return cudaErrorInvalidValue;
-    softmax_causal_fwd_kernel<<<(rows + 3) / 4, 128, 0, st>>>(S, P, rows, n, scale * 1.4426950408889634f);
+    launch_kernel(softmax_causal_fwd_kernel, (rows + 3) / 4, 128, 0, st, 1, S, P, rows, n, scale * 1.4426950408889634f);
     return cudaPeekAtLastError();
 }
 
 cudaError_t softmax_causal_bwd(const __nv_bfloat16* P, const float* dP, __nv_bfloat16* dS, int rows, int n,
                                float scale, cudaStream_t st) {
     if (n % 128) return cudaErrorInvalidValue;
-    softmax_causal_bwd_kernel<<<(rows + 3) / 4, 128, 0, st>>>(P, dP, dS, rows, n, scale);
+    launch_kernel(softmax_causal_bwd_kernel, (rows + 3) / 4, 128, 0, st, 1, P, dP, dS, rows, n, scale);
     return cudaPeekAtLastError();
 }
 
 cudaError_t cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss_rows, float* loss_out, int rows,
                           int vocab, float grad_scale, float loss_scale, cudaStream_t st) {
     if (vocab % 8) return cudaErrorInvalidValue;
-    xent_kernel<<<rows, 512, 0, st>>>(logits, labels, loss_rows, vocab, grad_scale);
-    loss_sum_kernel<<<1, 1024, 0, st>>>(loss_rows, loss_out, rows, loss_scale);
+    launch_kernel(xent_kernel, rows, 512, 0, st, 1, logits, labels, loss_rows, vocab, grad_scale);
+    launch_kernel(loss_sum_kernel, 1, 1024, 0, st, 1, loss_rows, loss_out, rows, loss_scale);
     return cudaPeekAtLastError();
 }
 
 cudaError_t embedding_fwd(const int32_t* tok, const __nv_bfloat16* wte, const __nv_bfloat16* wpe, __nv_bfloat16* x,
                           int rows, int seq, int h, cudaStream_t st) {
     if (h % 256) return cudaErrorInvalidValue;
-    PTK_DISPATCH_V(h, (embed_fwd_kernel<V><<<(rows + 3) / 4, 128, 0, st>>>(tok, wte, wpe, x, rows, seq)));
+    PTK_DISPATCH_V(h, (launch_kernel(embed_fwd_kernel<V>, (rows + 3) / 4, 128, 0, st, 1, tok, wte, wpe, x, rows, seq)));
     return cudaPeekAtLastError();
 }
 
@@ -649,17 +666,17 @@ cudaError_t embedding_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* dw
             cudaFuncSetAttribute(embed_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
-    embed_sort_kernel<<<1, 1024, smem, st>>>(tok, order, rows);
-    PTK_DISPATCH_V(h, (embed_bwd_runs_kernel<V><<<(rows + 7) / 8, 256, 0, st>>>(tok, order, dx, dwte, rows)));
+    launch_kernel(embed_sort_kernel, 1, 1024, smem, st, 1, tok, order, rows);
+    PTK_DISPATCH_V(h, (launch_kernel(embed_bwd_runs_kernel<V>, (rows + 7) / 8, 256, 0, st, 1, tok, order, dx, dwte, rows)));
     dim3 grid((h + 255) / 256, seq);
-    embed_bwd_wpe_kernel<<<grid, 256, 0, st>>>(dx, dwpe, seq, rows / seq, h);
+    launch_kernel(embed_bwd_wpe_kernel, grid, 256, 0, st, 1, dx, dwpe, seq, rows / seq, h);
     return cudaPeekAtLastError();
 }
 
 cudaError_t dgelu_mul(const __nv_bfloat16* dy, const __nv_bfloat16* pre, __nv_bfloat16* out, int64_t n,
                       cudaStream_t st) {
     if (n % 8) return cudaErrorInvalidValue;
-    dgelu_kernel<<<grid_for(n / 8, 256), 256, 0, st>>>(dy, pre, out, n / 8);
+    launch_kernel(dgelu_kernel, grid_for(n / 8, 256), 256, 0, st, 1, dy, pre, out, n / 8);
     return cudaPeekAtLastError();
 }
 
@@ -668,17 +685,17 @@ cudaError_t adamw_step(float* w, float* g, float* m, float* v, __nv_bfloat16* wb
     if (n % 4) return cudaErrorInvalidValue;
     const float bc1 = 1.f - powf(b1, static_cast<float>(step));
     const float bc2 = 1.f - powf(b2, static_cast<float>(step));
-    adamw_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(w, g, m, v, wb, n, lr, b1, b2, eps, wd, bc1, bc2);
+    launch_kernel(adamw_kernel, grid_for(n / 4, 256), 256, 0, st, 1, w, g, m, v, wb, n, lr, b1, b2, eps, wd, bc1, bc2);
     return cudaPeekAtLastError();
 }
 
 cudaError_t init_normal(float* w, int64_t n, uint64_t seed, float std, float mean, cudaStream_t st) {
-    init_normal_kernel<<<grid_for(n, 256), 256, 0, st>>>(w, n, seed, std, mean);
+    launch_kernel(init_normal_kernel, grid_for(n, 256), 256, 0, st, 1, w, n, seed, std, mean);
     return cudaPeekAtLastError();
 }
 
 cudaError_t cast_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t st) {
-    cast_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, dst, n);
+    launch_kernel(cast_bf16_kernel, grid_for(n, 256), 256, 0, st, 1, src, dst, n);
     return cudaPeekAtLastError();
 }
 

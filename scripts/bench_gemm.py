@@ -66,6 +66,12 @@ def main():
         ("x_out_aux", T, h, h, 0, 0, B_, 0, 1, 0),
         ("x_fc2wgrad_f32", h, f, T, 1, 1, L.EPI_F32, 0, 0, 0),
         ("x_fc2wgrad_bf16", h, f, T, 1, 1, B_, 0, 0, 0),
+        ("x_kk", T, f, h, 0, 0, B_, 0, 0, 0),
+        ("x_mk", T, f, h, 1, 0, B_, 0, 0, 0),
+        ("x_km", T, f, h, 0, 1, B_, 0, 0, 0),
+        ("x_mm", T, f, h, 1, 1, B_, 0, 0, 0),
+        ("x_kk_f32", T, f, h, 0, 0, L.EPI_F32, 0, 0, 0),
+        ("x_kk_acc", T, f, h, 0, 0, L.EPI_ACC_F32, 0, 0, 0),
     ]
     stream = torch.cuda.current_stream().cuda_stream
     out = []
