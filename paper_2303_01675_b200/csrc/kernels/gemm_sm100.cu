@@ -105,6 +105,7 @@ __device__ __forceinline__ uint4 pack_bf16x8(const float* f) {
 
 struct TileCoord {
     int z1, z2, m0, n0, kb0, kb1;
+    int ncols;  // output columns of this tile (BN, or 128 for a CTA-pair tail half)
 };
 
 // MC: a 2-CTA cluster owns a pair of m-tiles sharing one n-tile; t indexes
@@ -133,6 +134,7 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t, int r
     c.z2 = z / a.batch1;
     c.m0 = mb * kBM;
     c.n0 = nb * a.bn;
+    c.ncols = a.bn;
     const int kbs = (a.K + kBK - 1) / kBK;
     c.kb0 = 0;
     c.kb1 = kbs;
@@ -182,7 +184,7 @@ __device__ __forceinline__ void epi_fetch_aux64(const GemmArgs& args, const Tile
 template <int BN>
 __device__ __forceinline__ void epi_prefetch_tma(const GemmArgs& args, const TileCoord& tc, int quad, int half,
                                                  uint32_t lane, int et, __nv_bfloat16* bias_s, EpiTmaIn& in) {
-    if (epi_has_aux(args) && half < BN / 64) epi_fetch_aux64(args, tc, half, quad, lane, in.aux);
+    if (epi_has_aux(args) && half < tc.ncols / 64) epi_fetch_aux64(args, tc, half, quad, lane, in.aux);
     if (args.bias != nullptr) {
         if (et < BN / 8) {
             const int gn = tc.n0 + et * 8;
@@ -228,7 +230,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const CUtensorMap* tmC, const 
     if (args.epi == PTK_EPI_F32 || args.epi == PTK_EPI_ACC_F32) {
         const bool reduce = args.epi == PTK_EPI_ACC_F32;
 #pragma unroll 1
-        for (int c = half; c < BN / 32; c += 2) {
+        for (int c = half; c < tc.ncols / 32; c += 2) {
             float v[32];
             tmem_ld_32x32b_x32(tmem_col + lane_addr + static_cast<uint32_t>(c * 32), v);
             uint4 row[8];
@@ -241,7 +243,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const CUtensorMap* tmC, const 
         return;
     }
 #pragma unroll 1
-    for (int st = half; st < BN / 64; st += 2) {
+    for (int st = half; st < tc.ncols / 64; st += 2) {
         float v[64];
         tmem_ld_32x32b_x32_nw(tmem_col + lane_addr + static_cast<uint32_t>(st * 64), v);
         tmem_ld_32x32b_x32_nw(tmem_col + lane_addr + static_cast<uint32_t>(st * 64 + 32), v + 32);
@@ -269,7 +271,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const CUtensorMap* tmC, const 
             }
             out[j] = pack_bf16x8(f);
         }
-        if (epi_has_aux(args) && st + 2 < BN / 64) epi_fetch_aux64(args, tc, st + 2, quad, lane, in.aux);
+        if (epi_has_aux(args) && st + 2 < tc.ncols / 64) epi_fetch_aux64(args, tc, st + 2, quad, lane, in.aux);
         if (args.epi == PTK_EPI_BIAS_GELU) {
             // out holds the rounded pre-activation: store it (C2), then C = gelu(pre as stored)
             epi_stage_store(tmC2, stage, lane, out, tc.n0 + st * 64, row0, tc.z1, tc.z2, false);
@@ -470,18 +472,26 @@ constexpr int k2smStages = 6;
 constexpr int k2smStageBytes = 2 * 128 * kBK * 2;  // A half + B half
 constexpr int k2smSmem = k2smStages * k2smStageBytes + 1024 + 512 + 8 * 32 * 32 * 4 + 2 * 256 * 2;
 
+// Work item t: t < full_tiles is the 256 x 256 pair tile t; the tiles after
+// full_tiles (the last, partial wave) are split into two 256 x 128 halves,
+// items full_tiles + 2h and + 2h + 1, so the tail wave takes half as long.
 __device__ __forceinline__ TileCoord decode_pair_tile(const GemmArgs& a, int t, int rank) {
-    // t indexes 256 x 256 pair tiles; this CTA's rows are m0 + rank*128
+    int tile = t, nhalf = -1;
+    if (t >= a.full_tiles) {
+        tile = a.full_tiles + (t - a.full_tiles) / 2;
+        nhalf = (t - a.full_tiles) & 1;
+    }
     TileCoord c;
-    const int z = t / a.tiles_per_batch;
-    const int r = t - z * a.tiles_per_batch;
+    const int z = tile / a.tiles_per_batch;
+    const int r = tile - z * a.tiles_per_batch;
     const int mpairs = (a.tiles_m + 1) / 2;
     const int nb = r / mpairs;
     const int mp = r - nb * mpairs;
     c.z1 = z % a.batch1;
     c.z2 = z / a.batch1;
     c.m0 = mp * 256 + rank * 128;
-    c.n0 = nb * 256;
+    c.n0 = nb * 256 + (nhalf > 0 ? 128 : 0);
+    c.ncols = nhalf < 0 ? 256 : 128;
     c.kb0 = 0;
     c.kb1 = (a.K + kBK - 1) / kBK;
     return c;
@@ -490,11 +500,12 @@ __device__ __forceinline__ TileCoord decode_pair_tile(const GemmArgs& a, int t, 
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                         const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
-                         const __grid_constant__ GemmArgs args) {
+                         const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
+                         const __grid_constant__ CUtensorMap tmC2, const __grid_constant__ GemmArgs args) {
     constexpr int S = k2smStages;
     constexpr int kHalf = 128 * kBK * 2;  // 16 KiB
     constexpr uint32_t kIdesc = make_idesc_bf16(256, 256, A_MN, B_MN);
+    constexpr uint32_t kIdescHalf = make_idesc_bf16(256, 128, A_MN, B_MN);
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -539,10 +550,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             for (int t = t_begin; t < args.num_tiles; t += t_step) {
                 const TileCoord tc = decode_pair_tile(args, t, rank);
-                const int nrow = tc.n0 + rank * 128;  // this CTA's half of the B rows
+                const bool full_w = tc.ncols == 256;
+                const int nrow = tc.n0 + rank * (tc.ncols / 2);  // this CTA's half of the B rows
+                const uint32_t bytes = full_w ? 2 * k2smStageBytes : 2 * (kHalf + kHalf / 2);
                 for (int kb = tc.kb0; kb < tc.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2smStageBytes);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
                     uint8_t* sa = smem + stage * k2smStageBytes;
                     uint8_t* sb = sa + kHalf;
                     const int k0 = kb * kBK;
@@ -554,10 +567,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tma_load_4d_2sm(&tmA, &full[stage], sa + j * 64 * kBK * 2, tc.m0 + 64 * j, k0, tc.z1, tc.z2);
                     }
                     if (!B_MN) {
-                        tma_load_4d_2sm(&tmB, &full[stage], sb, k0, nrow, tc.z1, tc.z2);
+                        tma_load_4d_2sm(full_w ? &tmB : &tmB2, &full[stage], sb, k0, nrow, tc.z1, tc.z2);
                     } else {
-#pragma unroll
-                        for (int j = 0; j < 2; ++j)
+                        for (int j = 0; j < (full_w ? 2 : 1); ++j)
                             tma_load_4d_2sm(&tmB, &full[stage], sb + j * 64 * kBK * 2, nrow + 64 * j, k0, tc.z1, tc.z2);
                     }
                     if (++stage == S) {
@@ -589,7 +601,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  : make_sw128_desc(a_base + k * 32, 16, 1024);
                         const uint64_t db = B_MN ? make_sw128_desc(b_base + k * 2048, 64 * kBK * 2, 1024)
                                                  : make_sw128_desc(b_base + k * 32, 16, 1024);
-                        mma_bf16_ss_2sm(d_tmem, da, db, kIdesc, (kb > tc.kb0 || k > 0) ? 1u : 0u);
+                        mma_bf16_ss_2sm(d_tmem, da, db, tc.ncols == 256 ? kIdesc : kIdescHalf,
+                                        (kb > tc.kb0 || k > 0) ? 1u : 0u);
                     }
                     mma_commit_2sm_mc(&empty[stage], 0x3);
                     if (++stage == S) {
@@ -736,7 +749,8 @@ int launch_2sm(const GemmPlan& p, cudaStream_t stream) {
             return PTK_ERR_CUDA;
         attr_set = true;
     }
-    if (launch_kernel(kern, p.grid, kThreads, k2smSmem, stream, 2, p.tmA, p.tmB, p.tmC, p.tmC2, p.args) != cudaSuccess)
+    if (launch_kernel(kern, p.grid, kThreads, k2smSmem, stream, 2, p.tmA, p.tmB, p.tmB2, p.tmC, p.tmC2, p.args) !=
+        cudaSuccess)
         return PTK_ERR_CUDA;
     return cudaPeekAtLastError() == cudaSuccess ? PTK_OK : PTK_ERR_CUDA;
 }
@@ -813,6 +827,12 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     else
         rc = encode_operand(&p.tmB, d.b, d.n, d.k, kBK, b1, b2);
     if (rc != PTK_OK) return rc;
+    if (pair && !d.b.mn_major) {
+        rc = encode_operand(&p.tmB2, d.b, d.k, d.n, 64, b1, b2);  // tail halves: 64 B rows per CTA
+        if (rc != PTK_OK) return rc;
+    } else {
+        p.tmB2 = p.tmB;
+    }
 
     GemmArgs& a = p.args;
     a.M = d.m;
@@ -853,10 +873,20 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     const bool mc = mc_pre;
     p.flops = 2.0 * d.m * static_cast<double>(d.n) * d.k * b1 * b2;
     if (d.causal != PTK_CAUSAL_NONE) p.flops *= 0.5;
+    a.full_tiles = 1 << 30;
     if (pair) {
         a.tiles_per_batch = ((tiles_m + 1) / 2) * a.tiles_n;
-        a.num_tiles = a.tiles_per_batch * b1 * b2;
-        const int clusters = a.num_tiles < sms / 2 ? a.num_tiles : sms / 2;
+        const int tiles = a.tiles_per_batch * b1 * b2;
+        const int pairs = sms / 2;
+        a.num_tiles = tiles;
+        a.full_tiles = tiles;
+        const int rem = tiles % pairs;
+        if (tiles > pairs && rem > 0 && 2 * rem <= pairs && d.n % 256 == 0) {
+            // split the partial last wave into 256 x 128 halves: it then takes half as long
+            a.full_tiles = tiles - rem;
+            a.num_tiles = a.full_tiles + 2 * rem;
+        }
+        const int clusters = a.num_tiles < pairs ? a.num_tiles : pairs;
         p.grid = 2 * clusters;
         p.launch = pick_2sm(d.a.mn_major, d.b.mn_major);
     } else if (mc) {

@@ -20,13 +20,15 @@ struct GemmArgs {
     const void* aux;
     int64_t ld_aux, aux_bs1, aux_bs2;
     const void* bias;
-    int tma_store;  // 1: outputs leave through TMA stores (tmC / tmC2), else per-thread stores
+    int tma_store;   // outputs leave through TMA stores (tmC / tmC2)
+    int full_tiles;  // CTA-pair kernel: work items >= full_tiles are 256 x 128 halves of the tail tiles
 };
 
 struct GemmPlan {
     using Launcher = int (*)(const GemmPlan&, cudaStream_t);
     alignas(64) CUtensorMap tmA;
     alignas(64) CUtensorMap tmB;
+    alignas(64) CUtensorMap tmB2;  // CTA-pair kernel, K-major B: box of 64 rows (half-width tail tiles)
     alignas(64) CUtensorMap tmC;   // output C: box {64 bf16 | 32 fp32, 32 rows}, 128B swizzle
     alignas(64) CUtensorMap tmC2;  // BIAS_GELU pre-activation output
     GemmArgs args;
