@@ -11,7 +11,8 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libptk.so"
+# PTK_LIB_PATH: load another build of the same ABI (A/B performance comparisons only)
+LIB_PATH = Path(os.environ["PTK_LIB_PATH"]) if os.environ.get("PTK_LIB_PATH") else _PKG / "libptk.so"
 
 PTK_OK = 0
 STATUS_NAMES = {

@@ -46,6 +46,24 @@ __device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
     *reinterpret_cast<uint4*>(p) = u;
 }
 
+__device__ __forceinline__ void unpack_bf16x8(const uint4& u, float (&f)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 p = __bfloat1622float2(h[i]);
+        f[2 * i] = p.x;
+        f[2 * i + 1] = p.y;
+    }
+}
+
+__device__ __forceinline__ uint4 pack_bf16x8_f(const float (&f)[8]) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return u;
+}
+
 // --------------------------------------------------------------- LayerNorm
 // One warp per row; lane owns columns {j*256 + lane*8 .. +7}.  V = h / 256.
 template <int V>
@@ -94,125 +112,196 @@ __global__ void __launch_bounds__(128) ln_fwd_kernel(const __nv_bfloat16* __rest
     }
 }
 
-// dx = rstd * (dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)) + resid.  One warp
-// per row, two passes over the row (the second hits L1), so registers stay
-// bounded for any h.  The affine grads are a separate column reduction.
-template <int V>
-__global__ void __launch_bounds__(128) ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
-                                                     const __nv_bfloat16* __restrict__ x,
-                                                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
-                                                     const __nv_bfloat16* __restrict__ g,
-                                                     const __nv_bfloat16* __restrict__ resid,
-                                                     __nv_bfloat16* __restrict__ dx, int rows) {
+// Fused LayerNorm backward, column-slice layout: a block of h/8 threads owns
+// rows [p*R, (p+1)*R) of partial row p (R = ceil(rows/P), P = gridDim.x =
+// kVecParts); thread t owns columns [8t, 8t+8) of every row.  Per batch of 4
+// rows each thread loads its 16-byte slices of dy and x, the row sums
+// s1 = Σ dy·g, s2 = Σ dy·g·x̂ are reduced warp-then-block through smem (fixed
+// order), then
+//   dx = rstd (dy·g − s1/h − x̂ s2/h) (+ resid)          (bf16 out)
+// and the thread accumulates, in registers over its R rows,
+//   part_g += dy·x̂,  part_b += dy   (LayerNorm affine grads)
+//   part_o += dx (as stored)        (optional: the bias grad of the GEMM whose
+//                                    output gradient dx is — fused colsum)
+// written once per block with a plain += (each (p, c) has one owner; micro-
+// batches are stream-ordered), so the sums are deterministic.
+template <int NT>
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) ln_bwd_fused_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean_in,
+    const float* __restrict__ rstd_in, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ resid,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ part_g, float* __restrict__ part_b,
+    float* __restrict__ part_o, int rows) {
     pdl_begin();
-    constexpr int H = V * 256;
-    const int row = blockIdx.x * 4 + threadIdx.x / 32;
-    const int lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    const float mean = mean_in[row], rstd = rstd_in[row];
-    const __nv_bfloat16* xr = x + static_cast<int64_t>(row) * H;
-    const __nv_bfloat16* dr = dy + static_cast<int64_t>(row) * H;
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll 4
-    for (int j = 0; j < V; ++j) {
-        float xv[8], dv[8], gv[8];
-        load8(xr + j * 256 + lane * 8, xv);
-        load8(dr + j * 256 + lane * 8, dv);
-        load8(g + j * 256 + lane * 8, gv);
+    constexpr int H = NT * 8, NW = NT / 32;
+    constexpr int RB = 2;  // rows per batch, kept as packed bf16 (16-byte slices) until used
+    __shared__ float red[2][RB][NW][2];
+    const int t = threadIdx.x, warp = t / 32, lane = t & 31;
+    const int c0 = t * 8;
+    float gv[8];
+    load8(g + c0, gv);
+    float ag[8], ab[8], ao[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float dg = dv[i] * gv[i];
-            s1 += dg;
-            s2 += dg * (xv[i] - mean) * rstd;
+    for (int i = 0; i < 8; ++i) ag[i] = ab[i] = ao[i] = 0.f;
+    const int per = (rows + gridDim.x - 1) / gridDim.x;
+    const int r_begin = blockIdx.x * per;
+    const int r_end = min(rows, r_begin + per);
+    const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+    int batch = 0;
+    for (int r0 = r_begin; r0 < r_end; r0 += RB, ++batch) {
+        uint4 du[RB], xu[RB], ru[RB];
+        float mean[RB], rs[RB];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {  // every load of the batch in flight at once
+            const int row = r0 + rr;
+            const bool ok = row < r_end;
+            const int64_t off = static_cast<int64_t>(row) * H + c0;
+            du[rr] = ok ? *reinterpret_cast<const uint4*>(dy + off) : zero;
+            xu[rr] = ok ? *reinterpret_cast<const uint4*>(x + off) : zero;
+            ru[rr] = (ok && resid != nullptr) ? *reinterpret_cast<const uint4*>(resid + off) : zero;
+            mean[rr] = ok ? mean_in[row] : 0.f;
+            rs[rr] = ok ? rstd_in[row] : 0.f;
+        }
+        float (*rb)[NW][2] = red[batch & 1];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            float d[8], xv[8];
+            unpack_bf16x8(du[rr], d);
+            unpack_bf16x8(xu[rr], xv);
+            float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float dg = d[i] * gv[i];
+                s1 += dg;
+                s2 += dg * ((xv[i] - mean[rr]) * rs[rr]);
+            }
+            s1 = warp_sum(s1);
+            s2 = warp_sum(s2);
+            if (lane == 0) {
+                rb[rr][warp][0] = s1;
+                rb[rr][warp][1] = s2;
+            }
+        }
+        __syncthreads();  // red[batch & 1] complete (and red[(batch+1) & 1] no longer read)
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            const int row = r0 + rr;
+            if (row >= r_end) break;
+            float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                s1 += rb[rr][w][0];
+                s2 += rb[rr][w][1];
+            }
+            s1 *= 1.f / H;
+            s2 *= 1.f / H;
+            float d[8], xv[8], rv[8];
+            unpack_bf16x8(du[rr], d);
+            unpack_bf16x8(xu[rr], xv);
+            unpack_bf16x8(ru[rr], rv);
+            float o[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float xh = (xv[i] - mean[rr]) * rs[rr];
+                o[i] = rs[rr] * (d[i] * gv[i] - s1 - xh * s2) + rv[i];
+                ag[i] += d[i] * xh;
+                ab[i] += d[i];
+            }
+            const uint4 u = pack_bf16x8_f(o);
+            float q[8];
+            unpack_bf16x8(u, q);  // the bias grad sums dx as stored
+#pragma unroll
+            for (int i = 0; i < 8; ++i) ao[i] += q[i];
+            *reinterpret_cast<uint4*>(dx + static_cast<int64_t>(row) * H + c0) = u;
         }
     }
-    s1 = warp_sum(s1) * (1.f / H);
-    s2 = warp_sum(s2) * (1.f / H);
-#pragma unroll 4
-    for (int j = 0; j < V; ++j) {
-        float xv[8], dv[8], gv[8], o[8];
-        load8(xr + j * 256 + lane * 8, xv);
-        load8(dr + j * 256 + lane * 8, dv);
-        load8(g + j * 256 + lane * 8, gv);
-        float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (resid != nullptr) load8(resid + static_cast<int64_t>(row) * H + j * 256 + lane * 8, rv);
+    const int64_t o = static_cast<int64_t>(blockIdx.x) * H + c0;
+    float4* pg = reinterpret_cast<float4*>(part_g + o);
+    float4* pb = reinterpret_cast<float4*>(part_b + o);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = rstd * (dv[i] * gv[i] - s1 - (xv[i] - mean) * rstd * s2) + rv[i];
-        store8(dx + static_cast<int64_t>(row) * H + j * 256 + lane * 8, o);
+    for (int i = 0; i < 2; ++i) {
+        float4 a = pg[i], b = pb[i];
+        pg[i] = make_float4(a.x + ag[4 * i], a.y + ag[4 * i + 1], a.z + ag[4 * i + 2], a.w + ag[4 * i + 3]);
+        pb[i] = make_float4(b.x + ab[4 * i], b.y + ab[4 * i + 1], b.z + ab[4 * i + 2], b.w + ab[4 * i + 3]);
+    }
+    if (part_o != nullptr) {
+        float4* po = reinterpret_cast<float4*>(part_o + o);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            float4 a = po[i];
+            po[i] = make_float4(a.x + ao[4 * i], a.y + ao[4 * i + 1], a.z + ao[4 * i + 2], a.w + ao[4 * i + 3]);
+        }
     }
 }
 
-// Column sums into persistent per-parameter partials part[kVecParts][cols]
-// (+=).  Block (cx, p) owns rows [p*rows/P, (p+1)*rows/P) x 256 columns:
-// thread (rg, cg) accumulates every 8th row of the range over 8 columns with
-// 16-byte loads, the 8 row groups are combined in smem in a fixed order and
-// added to its own partial row.  Every (p, c) has one owner and micro-batches
-// run in stream order, so the sums are deterministic; vec_grad_finalize folds
-// the P partials into the gradient once per iteration (not per micro-batch).
-// AFFINE: part_g += dy * (x - mean) * rstd and part_b += dy (LayerNorm affine
-// grads); otherwise part_b += m (bias grads).
-template <bool AFFINE>
-__global__ void __launch_bounds__(256) colpart_kernel(const __nv_bfloat16* __restrict__ dy,
-                                                      const __nv_bfloat16* __restrict__ x,
-                                                      const float* __restrict__ mean_in,
-                                                      const float* __restrict__ rstd_in, float* __restrict__ part_g,
-                                                      float* __restrict__ part_b, int rows, int cols) {
+// Column sums into partial rows: block (cx, p) owns columns [2048 cx, +2048) of
+// rows [p*R, (p+1)*R); thread t accumulates columns 8t..8t+7 over the rows
+// (4 rows of 16-byte loads in flight) and adds them to part[p][c] (one owner).
+__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ m, float* __restrict__ part,
+                                                     int rows, int cols) {
     pdl_begin();
-    __shared__ float sg[AFFINE ? 8 : 1][257];
-    __shared__ float sb[8][257];
-    const int cg = threadIdx.x & 31, rg = threadIdx.x >> 5;
-    const int c0 = blockIdx.x * 256 + cg * 8;
-    const int per = rows / kVecParts;
-    const int r_end = (blockIdx.y + 1) * per;
-    float ag[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, ab[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-    for (int row = blockIdx.y * per + rg; row < r_end; row += 8) {
-        float d[8];
-        load8(dy + static_cast<int64_t>(row) * cols + c0, d);
-        if (AFFINE) {
-            float xv[8];
-            load8(x + static_cast<int64_t>(row) * cols + c0, xv);
-            const float mean = mean_in[row], rstd = rstd_in[row];
+    const int c0 = blockIdx.x * 2048 + threadIdx.x * 8;
+    if (c0 >= cols) return;
+    const int per = (rows + gridDim.y - 1) / gridDim.y;
+    const int r_begin = blockIdx.y * per;
+    const int r_end = min(rows, r_begin + per);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int row = r_begin;
+    for (; row + 4 <= r_end; row += 4) {
+        float v[4][8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) ag[i] += d[i] * ((xv[i] - mean) * rstd);
-        }
+        for (int rr = 0; rr < 4; ++rr) load8(m + static_cast<int64_t>(row + rr) * cols + c0, v[rr]);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) ab[i] += d[i];
+        for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] += v[rr][i];
     }
+    for (; row < r_end; ++row) {
+        float v[8];
+        load8(m + static_cast<int64_t>(row) * cols + c0, v);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        sb[rg][cg * 8 + i] = ab[i];
-        if (AFFINE) sg[rg][cg * 8 + i] = ag[i];
+        for (int i = 0; i < 8; ++i) acc[i] += v[i];
     }
-    __syncthreads();
-    const int c = threadIdx.x;
-    float tb = 0.f, tg = 0.f;
+    float* o = part + static_cast<int64_t>(blockIdx.y) * cols + c0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        tb += sb[k][c];
-        if (AFFINE) tg += sg[k][c];
-    }
-    const int64_t o = static_cast<int64_t>(blockIdx.y) * cols + blockIdx.x * 256 + c;
-    part_b[o] += tb;
-    if (AFFINE) part_g[o] += tg;
+    for (int i = 0; i < 8; ++i) o[i] += acc[i];
 }
 
-// grad[c] += sum_{p < P} part[p][c] (ascending p), part zeroed: one block row
-// per 1-D parameter of the stage, one launch per iteration.
+// grad[c] += sum_{p < P} part[p][c], part zeroed.  Block (cx, seg) owns columns
+// [256 cx, +256) of one 1-D parameter: warp w sums partial rows
+// [w P/8, (w+1) P/8) for 8 columns per lane (float4 loads, all rows in flight),
+// the 8 warp sums are combined in smem in warp order (deterministic).
 __global__ void __launch_bounds__(256) vec_finalize_kernel(const VecGradSeg* __restrict__ segs) {
     pdl_begin();
+    __shared__ float red[8][256];
     const VecGradSeg sg = segs[blockIdx.y];
-    for (int c = blockIdx.x * 256 + threadIdx.x; c < sg.cols; c += gridDim.x * 256) {
-        float v[kVecParts];
-#pragma unroll
-        for (int p = 0; p < kVecParts; ++p) v[p] = sg.part[static_cast<int64_t>(p) * sg.cols + c];
-        float acc = 0.f;
-#pragma unroll
-        for (int p = 0; p < kVecParts; ++p) {
-            acc += v[p];
-            sg.part[static_cast<int64_t>(p) * sg.cols + c] = 0.f;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int cbase = blockIdx.x * 256;
+    if (cbase >= sg.cols) return;
+    const int c = cbase + lane * 8;  // sg.cols % 8 == 0
+    constexpr int kRows = kVecParts / 8;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (c < sg.cols) {
+        float* q = sg.part + static_cast<int64_t>(warp * kRows) * sg.cols + c;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+        for (int r = 0; r < kRows; ++r) {
+            float4* p4 = reinterpret_cast<float4*>(q + static_cast<int64_t>(r) * sg.cols);
+            const float4 a = p4[0], b = p4[1];
+            acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+            acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+            p4[0] = z;
+            p4[1] = z;
         }
-        sg.grad[c] += acc;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[warp][lane * 8 + i] = acc[i];
+    __syncthreads();
+    const int cc = cbase + static_cast<int>(threadIdx.x);
+    if (cc < sg.cols) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+        sg.grad[cc] += t;
     }
 }
 
@@ -604,24 +693,33 @@ cudaError_t layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const 
 
 cudaError_t layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* mean, const float* rstd,
                           const __nv_bfloat16* g, const __nv_bfloat16* resid, __nv_bfloat16* dx, float* part_g,
-                          float* part_b, int rows, int h, cudaStream_t st) {
-    if (h % 256 || rows % kVecParts) return cudaErrorInvalidValue;
-    PTK_DISPATCH_V(h, (launch_kernel(ln_bwd_kernel<V>, (rows + 3) / 4, 128, 0, st, 1, dy, x, mean, rstd, g, resid, dx, rows)));
-    launch_kernel(colpart_kernel<true>, dim3(h / 256, kVecParts), 256, 0, st, 1, dy, x, mean, rstd, part_g, part_b, rows, h);
-    return cudaPeekAtLastError();
+                          float* part_b, float* part_out, int rows, int h, cudaStream_t st) {
+    switch (h) {
+        case 512: return launch_kernel(ln_bwd_fused_kernel<64>, kVecParts, 64, 0, st, 1, dy, x, mean, rstd, g, resid, dx,
+                                       part_g, part_b, part_out, rows);
+        case 768: return launch_kernel(ln_bwd_fused_kernel<96>, kVecParts, 96, 0, st, 1, dy, x, mean, rstd, g, resid, dx,
+                                       part_g, part_b, part_out, rows);
+        case 1024: return launch_kernel(ln_bwd_fused_kernel<128>, kVecParts, 128, 0, st, 1, dy, x, mean, rstd, g, resid,
+                                        dx, part_g, part_b, part_out, rows);
+        case 2048: return launch_kernel(ln_bwd_fused_kernel<256>, kVecParts, 256, 0, st, 1, dy, x, mean, rstd, g, resid,
+                                        dx, part_g, part_b, part_out, rows);
+        case 4096: return launch_kernel(ln_bwd_fused_kernel<512>, kVecParts, 512, 0, st, 1, dy, x, mean, rstd, g, resid,
+                                        dx, part_g, part_b, part_out, rows);
+        case 256: return launch_kernel(ln_bwd_fused_kernel<32>, kVecParts, 32, 0, st, 1, dy, x, mean, rstd, g, resid, dx,
+                                       part_g, part_b, part_out, rows);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t colsum_partial(const __nv_bfloat16* m, float* part, int rows, int cols, cudaStream_t st) {
-    if (cols % 256 || rows % kVecParts) return cudaErrorInvalidValue;
-    launch_kernel(colpart_kernel<false>, dim3(cols / 256, kVecParts), 256, 0, st, 1, m, nullptr, nullptr, nullptr, nullptr, part,
-                                                                      rows, cols);
-    return cudaPeekAtLastError();
+    if (cols % 8) return cudaErrorInvalidValue;
+    return launch_kernel(colsum_kernel, dim3((cols + 2047) / 2048, kVecParts), 256, 0, st, 1, m, part, rows, cols);
 }
 
 cudaError_t vec_grad_finalize(const VecGradSeg* segs_dev, int nseg, int max_cols, cudaStream_t st) {
     if (nseg <= 0) return cudaSuccess;
     if (nseg > 65535) return cudaErrorInvalidValue;
-    const int gx = std::min(16, (max_cols + 255) / 256);
+    const int gx = (max_cols + 255) / 256;
     launch_kernel(vec_finalize_kernel, dim3(gx, nseg), 256, 0, st, 1, segs_dev);
     return cudaPeekAtLastError();
 }

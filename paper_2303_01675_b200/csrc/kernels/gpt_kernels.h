@@ -14,17 +14,19 @@ cudaError_t layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const 
 // per-parameter partials float[kVecParts][cols] over the micro-batches of an
 // iteration; vec_grad_finalize adds them into the gradient (fixed order) and
 // clears them.  rows % kVecParts == 0.
-constexpr int kVecParts = 64;
+constexpr int kVecParts = 256;
 struct VecGradSeg {
     float* grad;
     float* part;
     int cols;
 };
-// dx = LN'(dy) (+ resid); part_g/part_b += the gamma/beta column partials.
+// dx = LN'(dy) (+ resid); part_g/part_b += the gamma/beta column partials;
+// part_out (optional) += the column partials of dx as stored (the bias grad
+// of the GEMM whose output gradient dx is).  h in {256, 512, 768, 1024, 2048, 4096}.
 cudaError_t layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* mean, const float* rstd,
                           const __nv_bfloat16* g, const __nv_bfloat16* resid, __nv_bfloat16* dx, float* part_g,
-                          float* part_b, int rows, int h, cudaStream_t st);
-// part[p][c] += sum over row block p of m[r][c].
+                          float* part_b, float* part_out, int rows, int h, cudaStream_t st);
+// part[p][c] += sum over row block p of m[r][c]  (cols % 8 == 0).
 cudaError_t colsum_partial(const __nv_bfloat16* m, float* part, int rows, int cols, cudaStream_t st);
 // segs_dev: device array of nseg segments; max_cols: the widest segment.
 cudaError_t vec_grad_finalize(const VecGradSeg* segs_dev, int nseg, int max_cols, cudaStream_t st);

@@ -353,8 +353,8 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
     const __nv_bfloat16* W = wbf_;
     float* G = grad_;
     // dz = LN2'(dy)
-    kl(2, layernorm_bwd(dy, s.ln2, s.mean2, s.rstd2, W + w.ln2_g, nullptr, d_ln_, vp(w.ln2_g), vp(w.ln2_b), T,
-                        h, st),
+    kl(1, layernorm_bwd(dy, s.ln2, s.mean2, s.rstd2, W + w.ln2_g, nullptr, d_ln_, vp(w.ln2_g), vp(w.ln2_b),
+                        vp(w.b_fc2) /* db2 = Σ dz, fused */, T, h, st),
        "ln2 bwd");
     {  // d_pre = dz W2 * gelu'(pre)
         ptk_gemm_desc g = desc(T, f, h, mat(d_ln_, h), mat(W + w.w_fc2, f, 1), mat(d_pre_, f), PTK_EPI_DGELU);
@@ -362,7 +362,6 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
         gemm(g, st);
     }
     gemm(desc(h, f, T, mat(d_ln_, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
-    kl(1, colsum_partial(d_ln_, vp(w.b_fc2), T, h, st), "db2");
     {  // d_xmid = d_pre W1 + dz   (residual around the FFN)
         ptk_gemm_desc g = desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(dx_mid_, h), PTK_EPI_BF16);
         g.aux = mat(d_ln_, h);
@@ -371,12 +370,11 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
     gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.x_mid, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
     kl(1, colsum_partial(d_pre_, vp(w.b_fc1), T, f, st), "db1");
     // dy_ = LN1'(d_xmid)
-    kl(2, layernorm_bwd(dx_mid_, s.ln1, s.mean1, s.rstd1, W + w.ln1_g, nullptr, dy_, vp(w.ln1_g), vp(w.ln1_b),
-                        T, h, st),
+    kl(1, layernorm_bwd(dx_mid_, s.ln1, s.mean1, s.rstd1, W + w.ln1_g, nullptr, dy_, vp(w.ln1_g), vp(w.ln1_b),
+                        vp(w.b_o) /* dbo = Σ dy_, fused */, T, h, st),
        "ln1 bwd");
     gemm(desc(T, h, h, mat(dy_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
     gemm(desc(h, h, T, mat(dy_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
-    kl(1, colsum_partial(dy_, vp(w.b_o), T, h, st), "dbo");
     attention_backward(s, st);
     gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.x_in, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
     kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
@@ -436,27 +434,28 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
         gemm(g, st);
     }
     gemm(desc(h, f, T, mat(dy, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
-    kl(1, colsum_partial(dy, vp(w.b_fc2), T, h, st), "db2");
+    // db2 = Σ dy: fused into the LayerNorm backward that produced dy (the next layer's LN1 or the
+    // head's final LN), except for the last layer of a stage whose dy arrives from the next stage
+    if (li == L_ - 1 && !c.has_head) kl(1, colsum_partial(dy, vp(w.b_fc2), T, h, st), "db2");
     // FC1: d_ln2 = d_pre W1; dW1 += d_preᵀ ln2; db1 += Σ d_pre
     gemm(desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
     gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.ln2, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
     kl(1, colsum_partial(d_pre_, vp(w.b_fc1), T, f, st), "db1");
     // LN2 backward + residual: dx_mid = LN2'(d_ln2) + dy
-    kl(2, layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, vp(w.ln2_g), vp(w.ln2_b), T, h,
-                     st),
+    kl(1, layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, vp(w.ln2_g), vp(w.ln2_b),
+                        vp(w.b_o) /* dbo = Σ dx_mid, fused */, T, h, st),
        "ln2 bwd");
     // out-proj: d_attn = dx_mid Wo; dWo += dx_midᵀ o; dbo += Σ dx_mid
     gemm(desc(T, h, h, mat(dx_mid_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
     gemm(desc(h, h, T, mat(dx_mid_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
-    kl(1, colsum_partial(dx_mid_, vp(w.b_o), T, h, st), "dbo");
     attention_backward(s, st);
     // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv += Σ dqkv
     gemm(desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
     gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
     kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
     // LN1 backward + residual: dx = LN1'(d_ln1) + dx_mid
-    kl(2, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, dx_mid_, dx, vp(w.ln1_g), vp(w.ln1_b), T, h,
-                     st),
+    kl(1, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, dx_mid_, dx, vp(w.ln1_g), vp(w.ln1_b),
+                        li > 0 ? vp(lw_[li - 1].b_fc2) : nullptr /* previous layer's db2 */, T, h, st),
        "ln1 bwd");
 }
 
@@ -523,16 +522,17 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
              st);
         if (bert()) {
             // dt = LN_h'(dxf); d_tpre = dt * gelu'(t_pre); dx_fin = d_tpre Wt; dWt += d_tpreᵀ x_fin
-            kl(2, layernorm_bwd(d_ln_, hs.t_act, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, dx_mid_, vp(lnf_g_),
-                                vp(lnf_b_), T, h, st),
+            kl(1, layernorm_bwd(d_ln_, hs.t_act, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, dx_mid_, vp(lnf_g_),
+                                vp(lnf_b_), nullptr, T, h, st),
                "lnh bwd");
             kl(1, dgelu_mul(dx_mid_, hs.t_pre, dy_, static_cast<int64_t>(T) * h, st), "dgelu");
             gemm(desc(T, h, h, mat(dy_, h), mat(W + w_t_, h, 1), mat(g_a_, h), PTK_EPI_BF16), st);
             gemm(desc(h, h, T, mat(dy_, h, 1), mat(hs.x_fin, h, 1), mat(G + w_t_, h), PTK_EPI_ACC_F32), st);
             kl(1, colsum_partial(dy_, vp(b_t_), T, h, st), "dbt");
         } else {
-            kl(2, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, vp(lnf_g_),
-                                vp(lnf_b_), T, h, st),
+            kl(1, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, vp(lnf_g_),
+                                vp(lnf_b_), L_ > 0 ? vp(lw_[L_ - 1].b_fc2) : nullptr /* last layer's db2 */, T, h,
+                                st),
                "lnf bwd");
         }
         g = g_a_;
@@ -548,8 +548,8 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
     if (c.has_embedding && bert()) {  // through the embedding LayerNorm
         EmbStash& e = emb_[static_cast<size_t>(slot)];
         __nv_bfloat16* dsum_bf = (g == g_a_) ? g_b_ : g_a_;
-        kl(2, layernorm_bwd(g, e.sum, e.mean, e.rstd, W + lne_g_, nullptr, dsum_bf, vp(lne_g_), vp(lne_b_), T, h,
-                            st),
+        kl(1, layernorm_bwd(g, e.sum, e.mean, e.rstd, W + lne_g_, nullptr, dsum_bf, vp(lne_g_), vp(lne_b_), nullptr, T,
+                            h, st),
            "emb ln bwd");
         g = dsum_bf;
     }
