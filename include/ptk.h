@@ -137,7 +137,9 @@ typedef struct ptk_gpt_config {
     int layer_begin, layer_end;
     int has_embedding, has_head;
     int micro_batch_size;  /* b */
-    int slots;             /* activation-stash slots = max in-flight micro-batches */
+    int slots;             /* activation-stash slots of micro_batch_size samples each; at a smaller b
+                              that divides it, each slot holds micro_batch_size / b micro-batches
+                              (virtual slots 0 .. slots * micro_batch_size / b - 1) */
     int micro_batches;     /* M: loss and gradients are the mean over M*b*seq tokens */
     int arch;              /* 0: GPT (pre-LN, causal, LM head); 1: BERT (post-LN, bidirectional,
                               embedding LayerNorm, MLM head = dense+GELU+LN+decoder over all positions) */

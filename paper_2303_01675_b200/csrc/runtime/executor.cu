@@ -116,8 +116,8 @@ void Executor::alloc_comm() {
     if (cfg_.stage > 0) {
         act_recv_ = static_cast<__nv_bfloat16*>(dalloc(block));
         act_flag_ = static_cast<uint32_t*>(dalloc(cfg_.global_batch * 4 + 256));
-        for (int s = 0; s < g.slots; ++s) {
-            grad_send_.push_back(static_cast<__nv_bfloat16*>(dalloc(tmax * g.hidden * 2)));
+        for (int s = 0; s < g.slots; ++s) grad_send_.push_back(static_cast<__nv_bfloat16*>(dalloc(tmax * g.hidden * 2)));
+        for (int s = 0; s < g.slots * g.micro_batch_size; ++s) {  // one per virtual slot at b = 1
             cudaEvent_t e;
             ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
             ck(cudaEventRecord(e, sendst_), "event");
@@ -127,8 +127,8 @@ void Executor::alloc_comm() {
     if (cfg_.stage + 1 < cfg_.stages) {
         grad_recv_ = static_cast<__nv_bfloat16*>(dalloc(block));
         grad_flag_ = static_cast<uint32_t*>(dalloc(cfg_.global_batch * 4 + 256));
-        for (int s = 0; s < g.slots; ++s) {
-            act_send_.push_back(static_cast<__nv_bfloat16*>(dalloc(tmax * g.hidden * 2)));
+        for (int s = 0; s < g.slots; ++s) act_send_.push_back(static_cast<__nv_bfloat16*>(dalloc(tmax * g.hidden * 2)));
+        for (int s = 0; s < g.slots * g.micro_batch_size; ++s) {
             cudaEvent_t e;
             ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
             ck(cudaEventRecord(e, sendst_), "event");
@@ -216,9 +216,11 @@ void Executor::set_plan(int k, int b) {
         if (kind == pipetune::TaskKind::ForwardCompute) peak = std::max(peak, ++live);
         if (kind == pipetune::TaskKind::BackwardCompute) --live;
     }
-    if (peak > g.slots)
-        throw pipetune::InfeasibleModel("set_plan: k=" + std::to_string(k) + " needs " + std::to_string(peak) +
-                                        " stash slots, stage has " + std::to_string(g.slots));
+    // slots are b_max samples wide: at b | b_max each holds b_max / b micro-batches
+    const int vslots = g.slots * ((g.micro_batch_size % b == 0) ? g.micro_batch_size / b : 1);
+    if (peak > vslots)
+        throw pipetune::InfeasibleModel("set_plan: k=" + std::to_string(k) + " b=" + std::to_string(b) + " needs " +
+                                        std::to_string(peak) + " stash slots, stage has " + std::to_string(vslots));
     k_ = k;
     b_ = b;
     M_ = cfg_.global_batch / b;
@@ -319,12 +321,15 @@ void Executor::run_iteration(int iter, const int32_t* host_tokens) {
     for (int id : plan_.per_device[static_cast<size_t>(s)]) {
         const pipetune::TaskNode& n = graph_->node(id);
         const int m = n.micro_batch;
-        const int slot = m >= 0 ? m % g.slots : 0;
+        const int slot = m >= 0 ? m % stage_->virtual_slots() : 0;
+        // this micro-batch's view of the b_max-wide send buffer of its physical slot
+        const int split = stage_->slot_split();
+        const int64_t sub = static_cast<int64_t>(slot % split) * T * g.hidden;
         GemmTiming& tm = stage_->gemm_timing();
         tm.enabled = tm.armed && m >= 0 && m % tm.stride == 0;
         if (n.kind == pipetune::TaskKind::ForwardCompute) {
             if (!first) wait_flag(comp_, act_flag_ + m, static_cast<uint32_t>(iter + 1));
-            __nv_bfloat16* out = last ? nullptr : act_send_[static_cast<size_t>(slot)];
+            __nv_bfloat16* out = last ? nullptr : act_send_[static_cast<size_t>(slot / split)] + sub;
             if (!last) ck(cudaStreamWaitEvent(comp_, act_sent_[static_cast<size_t>(slot)], 0), "wait");
             CompRecord r{id, 0, m, ev(), ev()};
             ck(cudaEventRecord(r.start, comp_), "event");
@@ -338,7 +343,7 @@ void Executor::run_iteration(int iter, const int32_t* host_tokens) {
             }
         } else if (n.kind == pipetune::TaskKind::BackwardCompute) {
             if (!last) wait_flag(comp_, grad_flag_ + m, static_cast<uint32_t>(iter + 1));
-            __nv_bfloat16* dx = first ? nullptr : grad_send_[static_cast<size_t>(slot)];
+            __nv_bfloat16* dx = first ? nullptr : grad_send_[static_cast<size_t>(slot / split)] + sub;
             if (!first) ck(cudaStreamWaitEvent(comp_, grad_sent_[static_cast<size_t>(slot)], 0), "wait");
             CompRecord r{id, 1, m, ev(), ev()};
             ck(cudaEventRecord(r.start, comp_), "event");

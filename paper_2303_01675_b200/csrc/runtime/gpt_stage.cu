@@ -239,6 +239,7 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
     order_ = static_cast<int32_t*>(alloc(T * 4));
     loss_acc_ = static_cast<float*>(alloc(64));
     ck(cudaMemset(loss_acc_, 0, 64), "memset");
+    build_virtual_slots();
     ck(cudaDeviceSynchronize(), "stage init");
 }
 
@@ -256,6 +257,63 @@ void GptStage::set_micro_batch(int b, int micro_batches) {
     if (b < 1 || b > b_max_) throw std::invalid_argument("set_micro_batch: b exceeds the allocated maximum");
     cfg_.micro_batch_size = b;
     cfg_.micro_batches = micro_batches;
+    build_virtual_slots();
+}
+
+// Virtual slot v = (physical slot v / r, sample offset (v % r)·b) with r = b_max / b:
+// every stash buffer is [b_max samples][per-sample extent], so a micro-batch of
+// b samples occupies a contiguous sub-range of a physical slot.
+void GptStage::build_virtual_slots() {
+    const ptk_gpt_config& c = cfg_;
+    const int b = c.micro_batch_size;
+    const int r = (b_max_ % b == 0) ? b_max_ / b : 1;
+    const int64_t s = c.seq, h = c.hidden, f = c.ffn;
+    const int phys = static_cast<int>(stash_.size());
+    vsplit_ = r;
+    vslots_ = phys * r;
+    vstash_.assign(vslots_, std::vector<LayerStash>(L_));
+    vhead_.assign(c.has_head ? vslots_ : 0, HeadStash{});
+    vemb_.assign(emb_.empty() ? 0 : vslots_, EmbStash{});
+    auto off = [](auto* p, int64_t n) { return p == nullptr ? p : p + n; };
+    for (int v = 0; v < vslots_; ++v) {
+        const int ps = v / r;
+        const int64_t j = static_cast<int64_t>(v % r) * b;  // first sample of this view
+        for (int i = 0; i < L_; ++i) {
+            const LayerStash& P = stash_[ps][i];
+            LayerStash& V = vstash_[v][i];
+            V.x_in = off(P.x_in, j * s * h);
+            V.ln1 = off(P.ln1, j * s * h);
+            V.qkv = off(P.qkv, j * s * 3 * h);
+            V.attn_o = off(P.attn_o, j * s * h);
+            V.x_mid = off(P.x_mid, j * s * h);
+            V.ln2 = off(P.ln2, j * s * h);
+            V.fc1_pre = off(P.fc1_pre, j * s * f);
+            V.fc1_act = off(P.fc1_act, j * s * f);
+            V.mean1 = off(P.mean1, j * s);
+            V.rstd1 = off(P.rstd1, j * s);
+            V.mean2 = off(P.mean2, j * s);
+            V.rstd2 = off(P.rstd2, j * s);
+            V.lse = off(P.lse, j * c.heads * s);
+        }
+        if (c.has_head) {
+            const HeadStash& P = head_[ps];
+            HeadStash& V = vhead_[v];
+            V.x_fin = off(P.x_fin, j * s * h);
+            V.xf = off(P.xf, j * s * h);
+            V.dlogits = off(P.dlogits, j * s * c.vocab);
+            V.meanf = off(P.meanf, j * s);
+            V.rstdf = off(P.rstdf, j * s);
+            V.t_pre = off(P.t_pre, j * s * h);
+            V.t_act = off(P.t_act, j * s * h);
+        }
+        if (!emb_.empty()) {
+            const EmbStash& P = emb_[ps];
+            EmbStash& V = vemb_[v];
+            V.sum = off(P.sum, j * s * h);
+            V.mean = off(P.mean, j * s);
+            V.rstd = off(P.rstd, j * s);
+        }
+    }
 }
 
 void GptStage::gemm(ptk_gemm_desc d, cudaStream_t st) {
@@ -463,13 +521,13 @@ void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, 
                        __nv_bfloat16* x_out, cudaStream_t st) {
     const ptk_gpt_config& c = cfg_;
     const int T = tokens(), h = c.hidden;
-    auto& S = stash_.at(static_cast<size_t>(slot));
+    auto& S = vstash_.at(static_cast<size_t>(slot));
     const __nv_bfloat16* W = wbf_;
     const __nv_bfloat16* cur = x_in;
     if (c.has_embedding && bert()) {  // BERT: LN(wte[tok] + wpe[pos])
-        EmbStash& e = emb_[static_cast<size_t>(slot)];
+        EmbStash& e = vemb_.at(static_cast<size_t>(slot));
         kl(1, embedding_fwd(tok, W + wte_, W + wpe_, e.sum, T, c.seq, h, st), "embedding");
-        __nv_bfloat16* dst = L_ > 0 ? S[0].x_in : head_[slot].x_fin;
+        __nv_bfloat16* dst = L_ > 0 ? S[0].x_in : vhead_.at(static_cast<size_t>(slot)).x_fin;
         kl(1, layernorm_fwd(e.sum, W + lne_g_, W + lne_b_, dst, e.mean, e.rstd, T, h, 1e-12f, st), "emb ln");
         cur = dst;
     } else if (c.has_embedding) {
@@ -479,7 +537,7 @@ void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, 
         S[0].x_in = const_cast<__nv_bfloat16*>(x_in);  // stage input stays live until this slot's backward
     }
     for (int i = 0; i < L_; ++i) {
-        __nv_bfloat16* out = (i + 1 < L_) ? S[i + 1].x_in : (c.has_head ? head_[slot].x_fin : x_out);
+        __nv_bfloat16* out = (i + 1 < L_) ? S[i + 1].x_in : (c.has_head ? vhead_.at(static_cast<size_t>(slot)).x_fin : x_out);
         if (bert())
             bert_layer_forward(i, S[i], cur, out, st);
         else
@@ -487,7 +545,7 @@ void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, 
         cur = out;
     }
     if (c.has_head) {
-        HeadStash& hs = head_[slot];
+        HeadStash& hs = vhead_.at(static_cast<size_t>(slot));
         if (L_ == 0 && cur != hs.x_fin)
             ck(cudaMemcpyAsync(hs.x_fin, cur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, st), "copy");
         if (bert()) {  // MLM transform: t = gelu(x Wtᵀ + b), xf = LN(t)
@@ -510,12 +568,12 @@ void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, 
 void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st) {
     const ptk_gpt_config& c = cfg_;
     const int T = tokens(), h = c.hidden;
-    auto& S = stash_.at(static_cast<size_t>(slot));
+    auto& S = vstash_.at(static_cast<size_t>(slot));
     const __nv_bfloat16* W = wbf_;
     float* G = grad_;
     const __nv_bfloat16* g = dy;
     if (c.has_head) {
-        HeadStash& hs = head_[slot];
+        HeadStash& hs = vhead_.at(static_cast<size_t>(slot));
         // dxf = dlogits W_head ; dW_head += dlogitsᵀ xf
         gemm(desc(T, h, c.vocab, mat(hs.dlogits, c.vocab), mat(W + w_head_, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
         gemm(desc(c.vocab, h, T, mat(hs.dlogits, c.vocab, 1), mat(hs.xf, h, 1), mat(G + w_head_, h), PTK_EPI_ACC_F32),
@@ -546,7 +604,7 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
         g = out;
     }
     if (c.has_embedding && bert()) {  // through the embedding LayerNorm
-        EmbStash& e = emb_[static_cast<size_t>(slot)];
+        EmbStash& e = vemb_.at(static_cast<size_t>(slot));
         __nv_bfloat16* dsum_bf = (g == g_a_) ? g_b_ : g_a_;
         kl(1, layernorm_bwd(g, e.sum, e.mean, e.rstd, W + lne_g_, nullptr, dsum_bf, vp(lne_g_), vp(lne_b_), nullptr, T,
                             h, st),

@@ -80,7 +80,11 @@ class GptStage {
     size_t stash_bytes_per_slot() const { return stash_per_slot_; }
 
     // Run subsequent micro-batches with b <= the allocated maximum (plan switch).
+    // When b divides the allocated maximum, every stash slot is split into
+    // b_max / b virtual slots (sample-granular stash): virtual_slots() grows.
     void set_micro_batch(int b, int micro_batches);
+    int virtual_slots() const { return vslots_; }
+    int slot_split() const { return vsplit_; }  // virtual slots per physical slot
     long launches() const { return launches_; }
     void reset_launches() { launches_ = 0; }
 
@@ -144,6 +148,12 @@ class GptStage {
 
     std::vector<std::vector<LayerStash>> stash_;  // [slot][layer]
     std::vector<HeadStash> head_;                 // [slot]
+    // views of the physical slots at the current micro-batch size
+    std::vector<std::vector<LayerStash>> vstash_;  // [virtual slot][layer]
+    std::vector<HeadStash> vhead_;
+    std::vector<EmbStash> vemb_;
+    int vslots_ = 0, vsplit_ = 1;
+    void build_virtual_slots();
     size_t stash_per_slot_ = 0;
 
     // scratch (one micro-batch in flight on the compute stream at a time)

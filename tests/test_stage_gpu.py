@@ -142,3 +142,24 @@ def test_optimizer_step_updates_and_zeroes(cuda):
     assert not torch.equal(before, st.master)
     assert float(st.grads.abs().max()) == 0.0
     assert torch.equal(st.weights, st.master.bfloat16())
+
+
+def test_sample_granular_stash_slots(cuda):
+    """A stage built for b_max=4 with ONE stash slot runs a b=1, k=2 plan (two
+    micro-batches in flight) by splitting the slot into four virtual slots, and
+    trains bit-identically to a stage built for b=1 with two slots."""
+    from paper_2303_01675_b200.executor import StageExecutor
+    shape = ModelShape(2, 256, 4, 1024, 128, 512)
+    digests = []
+    for b_max, slots in ((4, 1), (1, 2)):
+        ex = StageExecutor(shape, 0, 1, 8, b_max=b_max, slots=slots, layers=(0, 2))
+        ex.set_plan(2, 1)
+        for it in range(2):
+            ex.run_iteration(it)
+            ex.finish_iteration()
+        st = ex.stage_view()
+        torch.cuda.synchronize()
+        digests.append({n: st.param(n, "master").cpu().clone() for n in st.params})
+        ex.close()
+    for n in digests[0]:
+        assert torch.equal(digests[0][n], digests[1][n]), n
