@@ -104,6 +104,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def gemm_traffic():
+    """DRAM bytes per launch of the representative stage GEMM from the committed ncu capture
+    (profiles/gemm_traffic.json), or None when no capture is committed."""
+    try:
+        t = json.loads((ROOT / "profiles" / "gemm_traffic.json").read_text())
+        return {"bytes_per_launch": t["dram_read_bytes"] + t["dram_write_bytes"],
+                "algorithmic_bytes_per_launch": t["algorithmic_read_bytes"] + t["algorithmic_write_bytes"],
+                "kernel": t["kernel"], "source": t["source"]}
+    except Exception:
+        return None
+
+
 def trace_segments(args, link: int):
     """LinkTrace availability segments (ns from the arm's epoch)."""
     H = 10**13
@@ -351,7 +363,7 @@ def main():
                               "peak_tflops": peak_sus, "peak_kind": f"sustained bf16, {pk_kind}"},
         "roofline": {"bound": "tensor", "kernel": "gemm_bf16_kernel (tcgen05 + TMA, all stage GEMMs)",
                      "achieved": round(achieved, 1), "peak": peak_sus, "unit": "TFLOP/s",
-                     "frac": round(achieved / peak_sus, 4), "traffic": None,
+                     "frac": round(achieved / peak_sus, 4), "traffic": gemm_traffic(),
                      "launches": sum(g[2] for g in all_gemm),
                      "note": f"algorithmic GEMM FLOPs / summed CUDA-event GEMM durations over the timed steps; "
                              f"peak = sustained bf16 of {pk_kind} MEASURED_PEAKS.json"},
