@@ -328,7 +328,9 @@ __device__ __forceinline__ void mma_commit_2sm_mc(uint64_t* bar, uint16_t cta_ma
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
     uint32_t remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+    // relaxed: the caller's tcgen05.wait::ld + tcgen05.fence::before_thread_sync already order the
+    // TMEM reads this arrival publishes; a release at cluster scope costs a GPU-wide MEMBAR
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
 }  // namespace sm100
