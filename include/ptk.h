@@ -193,6 +193,9 @@ int ptk_exec_export(ptk_exec* ex, void* buf, size_t cap, size_t* written);
 int ptk_exec_import(ptk_exec* ex, int peer_stage, const void* buf, size_t n);
 int ptk_exec_connect_local(ptk_exec* ex, int peer_stage, ptk_exec* peer);
 int ptk_exec_set_plan(ptk_exec* ex, int k, int micro_batch_size);
+/* kFkB over explicit consecutive group sizes (sum = global_batch / micro_batch_size): k may change
+ * at every group boundary inside one iteration (pipetune::plan_groups). */
+int ptk_exec_set_plan_groups(ptk_exec* ex, int micro_batch_size, const int* group_sizes, int n_groups);
 /* Emulated-preemption trace for an outgoing link (times relative to the epoch). */
 int ptk_exec_set_trace(ptk_exec* ex, int link, double base_bytes_per_ns, int64_t latency_ns, int nseg,
                        const int64_t* start_ns, const int64_t* end_ns, const double* availability);

@@ -149,6 +149,19 @@ def make_plan(model, plan_req):
     M = gb // b
     g = Graph(stages, b, M)
     kind = plan_req.get("kind", "kfkb")
+    if kind == "groups":  # B200 extension: explicit consecutive group sizes
+        sizes = plan_req.get("groups")
+        if not sizes or any(n < 1 for n in sizes):
+            raise SpecError("ConfigError", "plan.groups sizes must be >= 1")
+        if sum(sizes) != M:
+            raise SpecError("PlanError", "groups must cover all micro-batches")
+        groups, first = [], 0
+        for n in sizes:
+            groups.append((first, first + n - 1))
+            first += n
+        return stages, g, kfkb_orders(g, 0, groups), (max(sizes), b, M)
+    if kind not in ("1f1b", "kfkb", "gpipe"):
+        raise SpecError("ConfigError", "plan.kind must be 1f1b, kfkb, gpipe or groups")
     k = 1 if kind == "1f1b" else (M if kind == "gpipe" else plan_req.get("k", 1))
     if k < 1 or k > M:
         raise SpecError("PlanError", "k out of range")

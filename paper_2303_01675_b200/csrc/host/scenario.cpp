@@ -2,6 +2,7 @@
 // one request object in, one result object out, through the C ABI
 // ptk_scenario_json().  Drives every spec-module operation so FFI callers and
 // the oracle parity tests exercise the C++ implementations directly.
+#include <algorithm>
 #include <cstring>
 #include <sstream>
 
@@ -120,7 +121,7 @@ TuningPolicy parse_policy(const Value* v) {
 }
 
 SchedulePlan parse_plan(const Value& v, const ModelSpec& model) {
-    json::require_keys(v, "plan", {"kind", "k", "micro_batch_size"});
+    json::require_keys(v, "plan", {"kind", "k", "micro_batch_size", "groups"});
     const std::string kind = v.get("kind") ? v.get("kind")->as_str("plan.kind") : "kfkb";
     const int b = v.get("micro_batch_size") ? static_cast<int>(v.get("micro_batch_size")->as_int("b")) : 1;
     const int k = v.get("k") ? static_cast<int>(v.get("k")->as_int("k")) : 1;
@@ -129,7 +130,21 @@ SchedulePlan parse_plan(const Value& v, const ModelSpec& model) {
     if (kind == "1f1b") return plan_1f1b(g);
     if (kind == "gpipe") return plan_gpipe(g);
     if (kind == "kfkb") return plan_kfkb(g, k);
-    throw ConfigError("plan.kind must be 1f1b, kfkb or gpipe");
+    if (kind == "groups") {  // kFkB over an explicit list of group sizes
+        const Value* gv = v.get("groups");
+        if (!gv) throw ConfigError("plan.groups (list of group sizes) is required for kind \"groups\"");
+        std::vector<MicroBatchGroup> groups;
+        int first = 0, kmax = 0;
+        for (const Value& x : gv->arr) {
+            const int n = static_cast<int>(x.as_int("plan.groups[]"));
+            if (n < 1) throw ConfigError("plan.groups: sizes must be >= 1");
+            groups.push_back({first, first + n - 1});
+            first += n;
+            kmax = std::max(kmax, n);
+        }
+        return plan_groups(g, kmax, groups);
+    }
+    throw ConfigError("plan.kind must be 1f1b, kfkb, gpipe or groups");
 }
 
 void write_config(json::Writer& w, const PlanConfig& c) {

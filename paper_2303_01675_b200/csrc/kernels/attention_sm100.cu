@@ -738,6 +738,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 mma_commit(pd_free);
                 ATRACE(1, na, 3);
+#ifdef PTK_ATTN_TRACE_MMA  // debug: accumulating-product latency as seen by the issuer (serialises)
+                mbar_wait(pd_free, na & 1);
+                ATRACE(1, na, 4);
+#endif
                 mma_commit(&ld_empty[st]);
                 if (ca.j == ca.nsteps - 1) mma_commit(&acc_full[ab]);
                 if (S == 1 && cx.valid) {

@@ -85,6 +85,13 @@ extern "C" int ptk_exec_set_plan(ptk_exec* ex, int k, int b) {
     return guarded("ptk_exec_set_plan", [&] { ex->impl.set_plan(k, b); });
 }
 
+extern "C" int ptk_exec_set_plan_groups(ptk_exec* ex, int b, const int* sizes, int n) {
+    EX_CHECK(ex);
+    if (n < 1 || sizes == nullptr) return ptk::set_error(PTK_ERR_ARG, "ptk_exec_set_plan_groups: empty group list");
+    return guarded("ptk_exec_set_plan_groups",
+                   [&] { ex->impl.set_plan_groups(b, std::vector<int>(sizes, sizes + n)); });
+}
+
 extern "C" int ptk_exec_set_trace(ptk_exec* ex, int link, double base, int64_t latency, int nseg, const int64_t* s,
                                   const int64_t* e, const double* a) {
     EX_CHECK(ex);

@@ -194,9 +194,24 @@ void Executor::connect_local(int peer, Executor& p) {
 }
 
 void Executor::set_plan(int k, int b) {
+    if (b < 1 || cfg_.global_batch % b) throw pipetune::ConfigError("set_plan: micro-batch size must divide the global batch");
+    const int M = cfg_.global_batch / b;
+    std::vector<int> sizes;
+    for (int first = 0; first < M; first += k) sizes.push_back(std::min(k, M - first));
+    install_plan(b, sizes, k);
+}
+
+void Executor::set_plan_groups(int b, const std::vector<int>& group_sizes) {
+    int kmax = 0;
+    for (int n : group_sizes) kmax = std::max(kmax, n);
+    install_plan(b, group_sizes, kmax);
+}
+
+void Executor::install_plan(int b, const std::vector<int>& group_sizes, int k) {
     const ptk_gpt_config& g = cfg_.gpt;
     if (b < 1 || b > g.micro_batch_size || cfg_.global_batch % b)
         throw pipetune::ConfigError("set_plan: micro-batch size must divide the global batch and be <= b_max");
+    if (k < 1) throw pipetune::ConfigError("set_plan: k must be >= 1");
     pipetune::ModelSpec spec;
     spec.global_batch = cfg_.global_batch;
     for (int s = 0; s < cfg_.stages; ++s) {
@@ -208,7 +223,14 @@ void Executor::set_plan(int k, int b) {
     }
     pipetune::PlanConfig pc{1, b, cfg_.global_batch / b};
     graph_ = std::make_shared<const pipetune::TaskGraph>(pipetune::build_task_graph(spec, pc));
-    plan_ = pipetune::plan_kfkb(graph_, k);
+    std::vector<pipetune::MicroBatchGroup> groups;
+    int first = 0;
+    for (int n : group_sizes) {
+        if (n < 1) throw pipetune::ConfigError("set_plan_groups: group sizes must be >= 1");
+        groups.push_back({first, first + n - 1});
+        first += n;
+    }
+    plan_ = pipetune::plan_groups(graph_, k, groups);  // throws PlanError unless the groups tile [0, M)
     // the stash must hold this stage's peak number of in-flight micro-batches
     int live = 0, peak = 0;
     for (int id : plan_.per_device[static_cast<size_t>(cfg_.stage)]) {

@@ -59,6 +59,9 @@ class Executor {
     void connect_local(int peer_stage, Executor& peer);
 
     void set_plan(int k, int micro_batch_size);
+    // kFkB over an explicit list of consecutive group sizes (sum = global_batch / b):
+    // group-boundary switching of k inside one iteration.
+    void set_plan_groups(int micro_batch_size, const std::vector<int>& group_sizes);
     int plan_k() const { return k_; }
     int plan_b() const { return b_; }
 
@@ -87,6 +90,7 @@ class Executor {
     long kernel_launches() const { return stage_->launches() + emu_launches_; }
 
   private:
+    void install_plan(int b, const std::vector<int>& group_sizes, int k);
     void alloc_comm();
     void send(bool forward, int mb, const __nv_bfloat16* src, int64_t bytes, cudaEvent_t ready);
     cudaEvent_t ev();

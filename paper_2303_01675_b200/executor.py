@@ -31,6 +31,7 @@ def _declare(lib):
     lib.ptk_exec_import.argtypes = [V, I, V, C.c_size_t]
     lib.ptk_exec_connect_local.argtypes = [V, I, V]
     lib.ptk_exec_set_plan.argtypes = [V, I, I]
+    lib.ptk_exec_set_plan_groups.argtypes = [V, I, C.POINTER(C.c_int), I]
     lib.ptk_exec_set_trace.argtypes = [V, I, C.c_double, C.c_int64, I, P(C.c_int64), P(C.c_int64), P(C.c_double)]
     lib.ptk_exec_set_epoch.argtypes = [V, C.c_int64]
     lib.ptk_exec_set_contender.argtypes = [V, I]
@@ -120,6 +121,11 @@ class StageExecutor:
     # ---- schedule / emulator
     def set_plan(self, k: int, b: int):
         L.check(self.lib.ptk_exec_set_plan(self.h, k, b))
+
+    def set_plan_groups(self, b: int, group_sizes):
+        """kFkB over explicit group sizes (k switches at group boundaries inside an iteration)."""
+        arr = (C.c_int * len(group_sizes))(*[int(x) for x in group_sizes])
+        L.check(self.lib.ptk_exec_set_plan_groups(self.h, b, arr, len(group_sizes)))
 
     def set_trace(self, link: int, base_bytes_per_ns: float, latency_ns: int, segments):
         n = len(segments)

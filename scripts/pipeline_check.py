@@ -33,7 +33,7 @@ def digests(ex):
 def run_pipeline(rank, S, k, group, trace=False, iters=2):
     M = GB // B
     layers = [(0, 2), (2, 4)] if S == 2 else [(i, i + 1) for i in range(4)]
-    slots = max(max_inflight(rank, S, M, kk) for kk in (1, 2, 4))
+    slots = max(max_inflight(rank, S, M, kk) for kk in (1, 2, 3, 4))
     ex = StageExecutor(SHAPE, rank, S, GB, b_max=B, slots=slots, layers=layers[rank], lr=1e-3)
     ex.connect_dist(group)
     if trace:
@@ -41,7 +41,10 @@ def run_pipeline(rank, S, k, group, trace=False, iters=2):
             ex.set_trace(link, 12.5 * 0.5, 2000, [])  # 50 Gb/s effective, 2 us latency
         dist.barrier(group=group)
         ex.set_epoch(ex.globaltimer())
-    ex.set_plan(k, B)
+    if isinstance(k, list):
+        ex.set_plan_groups(B, k)  # mixed group sizes: k switches at group boundaries
+    else:
+        ex.set_plan(k, B)
     ms, loss = [], None
     for it in range(iters):
         ex.run_iteration(it)
@@ -61,7 +64,7 @@ def main():
     dist.init_process_group("gloo")
     group = dist.group.WORLD
     res = {}
-    for name, k, tr in (("1f1b", 1, False), ("k2", 2, False), ("k2_paced", 2, True)):
+    for name, k, tr in (("1f1b", 1, False), ("k2", 2, False), ("k2_paced", 2, True), ("mixed", [1, 3, 2, 2], True)):
         d, loss, ms, tl = run_pipeline(rank, world, k, group, tr)
         allds = [None] * world
         dist.all_gather_object(allds, (d, loss, ms, len(tl["xfer"])), group=group)
@@ -82,14 +85,15 @@ def main():
         out = {
             "k1_vs_k2_bit_identical": res["1f1b"]["digest"] == res["k2"]["digest"],
             "paced_bit_identical": res["k2"]["digest"] == res["k2_paced"]["digest"],
+            "mixed_groups_bit_identical": res["k2"]["digest"] == res["mixed"]["digest"],
             "pipeline_vs_single_gpu_bit_identical": res["1f1b"]["digest"] == single,
             "loss": {"1f1b": res["1f1b"]["loss"], "k2": res["k2"]["loss"], "paced": res["k2_paced"]["loss"],
-                     "single": loss},
+                     "mixed": res["mixed"]["loss"], "single": loss},
             "ms": {k: v["ms"] for k, v in res.items()}, "xfers": {k: v["xfers"] for k, v in res.items()},
             "n_params": len(single),
         }
         out["ok"] = all([out["k1_vs_k2_bit_identical"], out["paced_bit_identical"],
-                         out["pipeline_vs_single_gpu_bit_identical"]])
+                         out["mixed_groups_bit_identical"], out["pipeline_vs_single_gpu_bit_identical"]])
         print(json.dumps(out), flush=True)
     dist.barrier(group=group)
     dist.destroy_process_group()

@@ -163,3 +163,27 @@ def test_sample_granular_stash_slots(cuda):
         ex.close()
     for n in digests[0]:
         assert torch.equal(digests[0][n], digests[1][n]), n
+
+
+def test_mixed_group_plan_bit_identical_to_uniform(cuda):
+    """Group-boundary k switching inside an iteration (pipetune::plan_groups through
+    ptk_exec_set_plan_groups) keeps micro-batches in ascending order on the device,
+    so training is bit-identical to any uniform k at the same micro-batch size."""
+    from paper_2303_01675_b200.executor import StageExecutor
+    shape = ModelShape(2, 256, 4, 1024, 128, 512)
+    digests = []
+    for groups in (None, [1, 2, 3, 2]):
+        ex = StageExecutor(shape, 0, 1, 8, b_max=1, slots=3, layers=(0, 2))
+        if groups is None:
+            ex.set_plan(1, 1)
+        else:
+            ex.set_plan_groups(1, groups)
+        for it in range(2):
+            ex.run_iteration(it)
+            ex.finish_iteration()
+        st = ex.stage_view()
+        torch.cuda.synchronize()
+        digests.append({n: st.param(n, "master").cpu().clone() for n in st.params})
+        ex.close()
+    for n in digests[0]:
+        assert torch.equal(digests[0][n], digests[1][n]), n
