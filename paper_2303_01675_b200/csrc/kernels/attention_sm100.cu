@@ -38,7 +38,8 @@ using namespace sm100;
 namespace {
 
 constexpr int kBlk = 128;      // query rows and key rows per block
-constexpr int kThreads = 384;  // 12 warps: TMA, MMA, 2 idle, 8 row-parallel elementwise warps
+constexpr int kThreads = 384;  // backward: 12 warps: TMA, MMA, 2 idle, 8 row-parallel elementwise warps
+constexpr int kFwdNQ = 2;      // forward: softmax rows split in kFwdNQ column parts (4 + 4·NQ warps)
 
 int sm_count() {
     static int n = 0;
@@ -59,7 +60,7 @@ struct FaCfg {
     static constexpr int kPBytes = kBlk * kBlk * 2;  // [2][128 rows x 128 B]
     static constexpr int kQBuf = D == 64 ? 2 : 1;
     static constexpr int kStages = D == 64 ? 3 : 2;
-    static constexpr int kXchg = (2 * 2 + 2 * 2) * kBlk * 4;  // row maxima [2][2][128], row sums [2][2][128]
+    static constexpr int kXchg = (2 * 4 + 2 * 4) * kBlk * 4;  // row maxima [2][NQ<=4][128], row sums [2][NQ][128]
     static constexpr int kSmem =
         kQBuf * kQBytes + kStages * (kKBytes + kVBytes) + kPBytes + kXchg + 1024 + 256;
     static constexpr uint32_t kTmemS0 = 0, kTmemS1 = 128, kTmemO = 256;  // O buffers at 256, 256 + D
@@ -94,12 +95,25 @@ __device__ __forceinline__ void fa_tile(const FaArgs& a, int k, FaCursor& c) {
     c.nkv = a.causal ? c.qb + 1 : nqb;
 }
 
+#ifdef PTK_ATTN_TRACE
+// Debug timeline of the forward kernel's CTA 0 (clock64): [role][key block][event].
+__device__ unsigned long long g_fwd_trace[2][64][8];
+#define FTRACE(role, step, ev)                                                  \
+    do {                                                                        \
+        if (blockIdx.x == 0 && (step) < 64) g_fwd_trace[role][step][ev] = clock64(); \
+    } while (0)
+#else
+#define FTRACE(role, step, ev) \
+    do {                       \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void fa_next(const FaArgs& a, FaCursor& c) {
     if (++c.j == c.nkv) fa_tile(a, c.k + 1, c);
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int D, int NQ>
+__global__ void __launch_bounds__(32 * (4 + 4 * NQ), 1)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
                      const __grid_constant__ FaArgs a) {
     using C = FaCfg<D>;
@@ -137,15 +151,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
             mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], 8);
+            mbar_init(&s_empty[i], 4 * NQ);
             mbar_init(&o_full[i], 1);
-            mbar_init(&o_empty[i], 8);
+            mbar_init(&o_empty[i], 4 * NQ);
         }
         for (int i = 0; i < S; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
         }
-        mbar_init(p_full, 8);
+        mbar_init(p_full, 4 * NQ);
         mbar_init(pv_done, 1);
         fence_barrier_init();
     }
@@ -204,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 kIdescS, k > 0 ? 1u : 0u);
                 }
                 mma_commit(&s_full[sb]);
+                FTRACE(1, n, 0);
                 if (c.j == c.nkv - 1) mma_commit(&q_empty[qbuf]);
             };
             FaCursor cs, cp;
@@ -221,6 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 const int st = np % S, ob = cp.k & 1;
                 mbar_wait(p_full, np & 1);
+                FTRACE(1, np, 1);
                 if (cp.j == 0) mbar_wait(&o_empty[ob], ((cp.k >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t p_base = smem_u32(sP);
@@ -234,124 +250,154 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 (cp.j > 0 || k > 0) ? 1u : 0u);
                 }
                 mma_commit(pv_done);
+                FTRACE(1, np, 2);
                 mma_commit(&kv_empty[st]);
                 if (cp.j == cp.nkv - 1) mma_commit(&o_full[ob]);
                 fa_next(a, cp);
                 ++np;
             }
         }
-    } else if (warp >= 4) {  // ---------------- softmax / epilogue: thread = (query row, column half)
+    } else if (warp >= 4) {  // ---------------- softmax / epilogue: thread = (query row, column part)
         const int quad = warp & 3;
-        const int half = (warp - 4) >> 2;  // columns [64*half, 64*half + 64) of S, [D/2*half, ..) of O
+        const int part = (warp - 4) >> 2;  // columns [kHc*part, +kHc) of S, [kOc*part, +kOc) of O
         const int r = quad * 32 + static_cast<int>(lane);
         const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
-        constexpr int kHc = kBlk / 2;  // S columns per thread
-        constexpr int kOc = D / 2;     // O columns per thread
-        int n = 0;                     // key blocks processed so far (all tiles)
+        constexpr int kHc = kBlk / NQ;  // S columns per thread
+        constexpr int kOc = D / NQ;     // O columns per thread
+        const uint32_t xbase = smem_u32(sX);
+        int n = 0;  // key blocks processed so far (all tiles)
         FaCursor c;
+        // O columns [col, col + kOc) of this thread's row scaled by `scale` (TMEM read-modify-write)
+        auto scale_o = [&](uint32_t col, float scale) {
+#pragma unroll
+            for (int cc = 0; cc < kOc; cc += 16) {
+                float v[16];
+                tmem_ld_32x32b_x16(col + cc, v);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] *= scale;
+                tmem_st_32x32b_x16(col + cc, v);
+            }
+        };
         for (fa_tile(a, 0, c); c.valid; fa_tile(a, c.k + 1, c)) {
             const int ob = c.k & 1;
-            const uint32_t o_cols = tmem + lane_base + C::kTmemO + ob * D + half * kOc;
-            float m = -INFINITY, l = 0.f;  // m in log2 units of the scaled scores; l = this half's row sum
+            const uint32_t o_cols = tmem + lane_base + C::kTmemO + ob * D + part * kOc;
+            float m = -INFINITY, l = 0.f;  // m in log2 units of the scaled scores; l = this part's row sum
             for (int j = 0; j < c.nkv; ++j, ++n) {
                 const int sb = n & 1;
                 mbar_wait(&s_full[sb], (n >> 1) & 1);
+                if (warp == 4 && lane == 0) FTRACE(0, n, 0);
                 tc_fence_after();
                 float x[kHc];
 #pragma unroll
                 for (int cc = 0; cc < kHc / 32; ++cc)
-                    tmem_ld_32x32b_x32_nw(tmem + lane_base + (sb ? C::kTmemS1 : C::kTmemS0) + half * kHc + cc * 32,
+                    tmem_ld_32x32b_x32_nw(tmem + lane_base + (sb ? C::kTmemS1 : C::kTmemS0) + part * kHc + cc * 32,
                                           x + cc * 32);
                 tmem_ld_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[sb]);
-                float mraw = -INFINITY;
-                if (a.causal && j == c.qb) {  // diagonal block: key > query masked
+                if (warp == 4 && lane == 0) FTRACE(0, n, 1);
+                // 8 independent max / sum chains (a single chain serialises on the ALU/MUFU latency)
+                float mr8[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mr8[i] = -INFINITY;
+                const bool diag = a.causal && j == c.qb;
+                if (diag) {  // diagonal block: key > query masked
 #pragma unroll
                     for (int e = 0; e < kHc; ++e) {
-                        if (half * kHc + e > r) x[e] = -INFINITY;
-                        mraw = fmaxf(mraw, x[e]);
+                        if (part * kHc + e > r) x[e] = -INFINITY;
+                        mr8[e & 7] = fmaxf(mr8[e & 7], x[e]);
                     }
                 } else {
 #pragma unroll
-                    for (int e = 0; e < kHc; ++e) mraw = fmaxf(mraw, x[e]);
+                    for (int e = 0; e < kHc; ++e) mr8[e & 7] = fmaxf(mr8[e & 7], x[e]);
                 }
-                // swap the half-row maxima with the partner warp (same rows, other half)
-                const uint32_t xb = smem_u32(sX) + (n & 1) * 2 * kBlk * 4;
-                sts32f(xb + (half * kBlk + r) * 4, mraw);
-                asm volatile("bar.sync %0, 64;" ::"r"(2 + quad) : "memory");
-                const float mx = fmaxf(m, fmaxf(lds32f(xb + r * 4), lds32f(xb + (kBlk + r) * 4)) * a.scale_log2);
-                const float alpha = ex2(m - mx);  // m = -inf on the first block -> 0
-                float sum = 0.f;
+                const float mraw = fmaxf(fmaxf(fmaxf(mr8[0], mr8[1]), fmaxf(mr8[2], mr8[3])),
+                                         fmaxf(fmaxf(mr8[4], mr8[5]), fmaxf(mr8[6], mr8[7])));
+                // swap the part maxima with the NQ-1 partner warps (same rows, other columns)
+                const uint32_t xb = xbase + (n & 1) * NQ * kBlk * 4;
+                sts32f(xb + (part * kBlk + r) * 4, mraw);
+                asm volatile("bar.sync %0, %1;" ::"r"(2 + quad), "r"(32 * NQ) : "memory");
+                if (warp == 4 && lane == 0) FTRACE(0, n, 2);
+                float pm = lds32f(xb + r * 4);
 #pragma unroll
-                for (int e = 0; e < kHc; ++e) {
-                    x[e] = ex2(fmaf(x[e], a.scale_log2, -mx));
-                    sum += x[e];
+                for (int q = 1; q < NQ; ++q) pm = fmaxf(pm, lds32f(xb + (q * kBlk + r) * 4));
+                const float mx = fmaxf(m, pm * a.scale_log2);
+                const float alpha = ex2(m - mx);  // m = -inf on the first block -> 0
+                float s8[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s8[i] = 0.f;
+                if (diag) {  // masked (-inf) entries: MUFU ex2 only
+#pragma unroll
+                    for (int e = 0; e < kHc; ++e) {
+                        x[e] = ex2(fmaf(x[e], a.scale_log2, -mx));
+                        s8[e & 7] += x[e];
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < kHc; ++e) {
+                        x[e] = ex2(fmaf(x[e], a.scale_log2, -mx));
+                        s8[e & 7] += x[e];
+                    }
                 }
+                const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
                 l = l * alpha + sum;
                 m = mx;
+                if (warp == 4 && lane == 0) FTRACE(0, n, 3);
                 if (n > 0) {
                     mbar_wait(pv_done, (n - 1) & 1);  // P buffer free (and O of this tile stable)
                     tc_fence_after();
                 }
-                // P half-row -> smem, K-major 128B-swizzled (16-byte chunk index ^= row % 8);
-                // columns [64*half, +64) are exactly swizzle atom `half`
-                const uint32_t prow = smem_u32(sP) + half * (kBlk * 128) + r * 128;
+                if (warp == 4 && lane == 0) FTRACE(0, n, 4);
+                // P row part -> smem, K-major 128B-swizzled (16-byte chunk index ^= row % 8)
 #pragma unroll
                 for (int q = 0; q < kHc / 8; ++q) {
+                    const int col = part * kHc + q * 8;
                     uint4 u;
                     u.x = pack_bf16(x[q * 8 + 0], x[q * 8 + 1]);
                     u.y = pack_bf16(x[q * 8 + 2], x[q * 8 + 3]);
                     u.z = pack_bf16(x[q * 8 + 4], x[q * 8 + 5]);
                     u.w = pack_bf16(x[q * 8 + 6], x[q * 8 + 7]);
-                    sts128(prow + ((q ^ (r & 7)) * 16), u);
+                    sts128(smem_u32(sP) + (col >> 6) * (kBlk * 128) + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) * 16),
+                           u);
                 }
-                if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rescale this thread's half of the O row
-#pragma unroll
-                    for (int cc = 0; cc < kOc / 32; ++cc) {
-                        float v[32];
-                        tmem_ld_32x32b_x32(o_cols + cc * 32, v);
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) v[e] *= alpha;
-                        tmem_st_32x32b_x32(o_cols + cc * 32, v);
-                    }
-                }
+                if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) scale_o(o_cols, alpha);
                 fence_proxy_async_smem();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full);
+                if (warp == 4 && lane == 0) FTRACE(0, n, 5);
             }
-            // total row sum = both halves (same m sequence, so the partial sums add)
-            const uint32_t lb = smem_u32(sX) + (4 * kBlk + (c.k & 1) * 2 * kBlk) * 4;
-            sts32f(lb + (half * kBlk + r) * 4, l);
-            asm volatile("bar.sync %0, 64;" ::"r"(2 + quad) : "memory");
-            const float lt = lds32f(lb + r * 4) + lds32f(lb + (kBlk + r) * 4);
+            // total row sum = all parts (same m sequence, so the partial sums add; fixed order)
+            const uint32_t lb = xbase + (2 * NQ * kBlk + (c.k & 1) * NQ * kBlk) * 4;
+            sts32f(lb + (part * kBlk + r) * 4, l);
+            asm volatile("bar.sync %0, %1;" ::"r"(2 + quad), "r"(32 * NQ) : "memory");
+            float lt = 0.f;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) lt += lds32f(lb + (q * kBlk + r) * 4);
             mbar_wait(&o_full[ob], (c.k >> 1) & 1);
             tc_fence_after();
             const float inv = 1.f / lt;
             const int q = c.qb * kBlk + r;
-            __nv_bfloat16* orow = a.o + (static_cast<int64_t>(c.bi) * a.s + q) * a.h + c.head * D + half * kOc;
+            __nv_bfloat16* orow = a.o + (static_cast<int64_t>(c.bi) * a.s + q) * a.h + c.head * D + part * kOc;
 #pragma unroll
-            for (int cc = 0; cc < kOc / 32; ++cc) {
-                float v[32];
-                tmem_ld_32x32b_x32(o_cols + cc * 32, v);
+            for (int cc = 0; cc < kOc; cc += 16) {
+                float v[16];
+                tmem_ld_32x32b_x16(o_cols + cc, v);
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
+                for (int g = 0; g < 2; ++g) {
                     uint4 u;
-                    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        __nv_bfloat162 hh = __floats2bfloat162_rn(v[g * 8 + 2 * e] * inv, v[g * 8 + 2 * e + 1] * inv);
-                        w[e] = *reinterpret_cast<uint32_t*>(&hh);
-                    }
-                    *reinterpret_cast<uint4*>(orow + cc * 32 + g * 8) = u;
+                    u.x = pack_bf16(v[g * 8 + 0] * inv, v[g * 8 + 1] * inv);
+                    u.y = pack_bf16(v[g * 8 + 2] * inv, v[g * 8 + 3] * inv);
+                    u.z = pack_bf16(v[g * 8 + 4] * inv, v[g * 8 + 5] * inv);
+                    u.w = pack_bf16(v[g * 8 + 6] * inv, v[g * 8 + 7] * inv);
+                    *reinterpret_cast<uint4*>(orow + cc + g * 8) = u;
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&o_empty[ob]);
-            if (half == 0) a.lse[(static_cast<int64_t>(c.bi) * a.H + c.head) * a.s + q] = m + __log2f(lt);
+            if (part == 0) a.lse[(static_cast<int64_t>(c.bi) * a.H + c.head) * a.s + q] = m + __log2f(lt);
         }
     }
     tc_fence_before();
@@ -401,14 +447,15 @@ cudaError_t launch_fwd(const FlashPlan& p, cudaStream_t st) {
     using C = FaCfg<D>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(flash_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        cudaError_t e =
+            cudaFuncSetAttribute(flash_fwd_kernel<D, kFwdNQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     FaArgs a{p.o, p.lse, p.s, p.H, p.H * p.d, p.b, p.scale_log2, p.causal};
     const int tiles = p.s / kBlk * p.H * p.b;
     const int grid = tiles < sm_count() ? tiles : sm_count();
-    return launch_kernel(flash_fwd_kernel<D>, grid, kThreads, C::kSmem, st, 1, p.tmQK, p.tmV, a);
+    return launch_kernel(flash_fwd_kernel<D, kFwdNQ>, grid, 32 * (4 + 4 * kFwdNQ), C::kSmem, st, 1, p.tmQK, p.tmV, a);
 }
 
 }  // namespace
@@ -521,16 +568,6 @@ __device__ __forceinline__ void bw_next(const BwArgs& a, BwCursor& c) {
     if (++c.j == c.nsteps) bw_tile<KV>(a, c.k + 1, c);
 }
 
-__device__ __forceinline__ void st_bf16_swz(uint32_t buf, int r, int c0, const float* v8) {
-    // 8 consecutive columns c0..c0+7 of row r into a [2][128 rows x 128 B] K-major swizzled buffer
-    uint4 u;
-    u.x = pack_bf16(v8[0], v8[1]);
-    u.y = pack_bf16(v8[2], v8[3]);
-    u.z = pack_bf16(v8[4], v8[5]);
-    u.w = pack_bf16(v8[6], v8[7]);
-    const int kb = c0 >> 6, c16 = (c0 & 63) >> 3;
-    sts128(buf + kb * (kBlk * 128) + r * 128 + ((c16 ^ (r & 7)) * 16), u);
-}
 
 __device__ __forceinline__ float4 lds128f(uint32_t addr) {
     float4 v;

@@ -36,12 +36,25 @@ int main(int argc, char** argv) {
     ptk::FlashBwdPlan bp;
     if (ptk::flash_prepare(qkv, o, lse, b, s, H, d, &fp, 1) != cudaSuccess) return 1;
     if (ptk::flash_bwd_prepare(qkv, o, dO, lse, dsum, dqkv, b, s, H, d, &bp, 1) != cudaSuccess) return 1;
-    ptk::flash_forward(fp, 0);
+    for (int i = 0; i < 3; ++i) ptk::flash_forward(fp, 0);
     for (int i = 0; i < 3; ++i) ptk::flash_backward(bp, 0);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         printf("error %s\n", cudaGetErrorString(e));
         return 1;
+    }
+    if (kv == 2) {  // forward kernel timeline
+        unsigned long long ft[2][64][8];
+        cudaMemcpyFromSymbol(ft, ptk::g_fwd_trace, sizeof ft);
+        const unsigned long long f0 = ft[1][0][0];
+        printf("forward kernel, CTA 0, cycles since S_0 was issued\n");
+        printf("blk | mma: S_issued p_full_seen PV_issued | sm: s_full s_loaded max_xchg exps_done pv_done_seen p_stored\n");
+        for (int n = 0; n < 24; ++n) {
+            auto f = [&](int r, int ev) { return static_cast<long long>(ft[r][n][ev] - f0); };
+            printf("%3d | %8lld %8lld %8lld | %8lld %8lld %8lld %8lld %8lld %8lld\n", n, f(1, 0), f(1, 1), f(1, 2),
+                   f(0, 0), f(0, 1), f(0, 2), f(0, 3), f(0, 4), f(0, 5));
+        }
+        return 0;
     }
     unsigned long long tr[2][64][8];
     cudaMemcpyFromSymbol(tr, ptk::g_attn_trace, sizeof tr);
