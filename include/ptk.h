@@ -219,6 +219,11 @@ int ptk_exec_profile_compute(ptk_exec* ex, int micro_batch_size, int repeats, in
 int ptk_exec_gemm_timing(ptk_exec* ex, int enable, double* total_flops, double* total_ms, long* launches);
 /* Non-owning view of the executor's stage (weights, grads, parameter table). */
 ptk_stage* ptk_exec_stage(ptk_exec* ex);
+/* Data-parallel replicas: with defer != 0 the GradAccum node only finalizes the
+ * stage gradients; the caller all-reduces them across replicas on ptk_exec_compute_stream() and then
+ * calls ptk_stage_optimizer_step on that stream (ptk_exec_stage gives the stage). */
+int ptk_exec_set_defer_optimizer(ptk_exec* ex, int defer);
+int ptk_exec_compute_stream(ptk_exec* ex, void** stream);
 
 #ifdef __cplusplus
 }

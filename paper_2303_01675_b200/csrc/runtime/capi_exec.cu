@@ -197,3 +197,15 @@ extern "C" int ptk_exec_gemm_timing(ptk_exec* ex, int enable, double* total_flop
 }
 
 extern "C" ptk_stage* ptk_exec_stage(ptk_exec* ex) { return ex ? &ex->stage_view : nullptr; }
+
+extern "C" int ptk_exec_set_defer_optimizer(ptk_exec* ex, int defer) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_set_defer_optimizer", [&] { ex->impl.set_defer_optimizer(defer != 0); });
+}
+
+extern "C" int ptk_exec_compute_stream(ptk_exec* ex, void** stream) {
+    EX_CHECK(ex);
+    if (stream == nullptr) return ptk::set_error(PTK_ERR_ARG, "ptk_exec_compute_stream: null output");
+    *stream = static_cast<void*>(ex->impl.compute_stream());
+    return PTK_OK;
+}

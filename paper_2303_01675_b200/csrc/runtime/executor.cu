@@ -379,7 +379,10 @@ void Executor::run_iteration(int iter, const int32_t* host_tokens) {
         } else if (n.kind == pipetune::TaskKind::GradAccum) {
             CompRecord r{id, 2, -1, ev(), ev()};
             ck(cudaEventRecord(r.start, comp_), "event");
-            stage_->optimizer_step(cfg_.lr, cfg_.weight_decay, comp_);
+            if (defer_optimizer_)
+                stage_->finalize_grads(comp_);  // the caller all-reduces, then steps the optimizer
+            else
+                stage_->optimizer_step(cfg_.lr, cfg_.weight_decay, comp_);
             ck(cudaEventRecord(r.end, comp_), "event");
             crec_.push_back(r);
         }

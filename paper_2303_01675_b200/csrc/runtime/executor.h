@@ -63,6 +63,10 @@ class Executor {
     // group-boundary switching of k inside one iteration.
     void set_plan_groups(int micro_batch_size, const std::vector<int>& group_sizes);
     int plan_k() const { return k_; }
+    // Data-parallel replicas: the GradAccum node leaves the
+    // optimizer to the caller, who all-reduces the finalized gradients first.
+    void set_defer_optimizer(bool on) { defer_optimizer_ = on; }
+    cudaStream_t compute_stream() const { return comp_; }
     int plan_b() const { return b_; }
 
     void set_trace(int link, const EmuTrace& trace);  // outgoing link pacing
@@ -104,6 +108,7 @@ class Executor {
     int iter_ = 0;
 
     cudaStream_t comp_ = nullptr, sendst_ = nullptr, contend_[2] = {nullptr, nullptr};
+    bool defer_optimizer_ = false;
     // receive blocks (owned; written by peers) and flags
     __nv_bfloat16 *act_recv_ = nullptr, *grad_recv_ = nullptr;
     uint32_t *act_flag_ = nullptr, *grad_flag_ = nullptr;

@@ -45,6 +45,8 @@ def _declare(lib):
     lib.ptk_exec_gemm_timing.argtypes = [V, I, P(C.c_double), P(C.c_double), P(C.c_long)]
     lib.ptk_exec_stage.argtypes = [V]
     lib.ptk_exec_stage.restype = C.c_void_p
+    lib.ptk_exec_set_defer_optimizer.argtypes = [V, I]
+    lib.ptk_exec_compute_stream.argtypes = [V, P(V)]
     lib._exec_declared = True
 
 
@@ -109,14 +111,39 @@ class StageExecutor:
         L.check(self.lib.ptk_exec_connect_local(self.h, peer_stage, peer.h))
 
     def connect_dist(self, group=None):
-        """Exchange IPC handles with the neighbouring ranks (rank == stage)."""
+        """Exchange IPC handles with the neighbouring ranks (rank in `group` == stage)."""
         import torch.distributed as dist
-        blobs = [None] * dist.get_world_size()
+        blobs = [None] * dist.get_world_size(group)
         dist.all_gather_object(blobs, self.export_handles(), group=group)
         if self.stage + 1 < self.stages:
             self.import_peer(self.stage + 1, blobs[self.stage + 1])
         if self.stage > 0:
             self.import_peer(self.stage - 1, blobs[self.stage - 1])
+
+    # ---- data-parallel replicas (SURVEY §8(f) #4)
+    def set_defer_optimizer(self, on: bool = True):
+        """GradAccum only finalizes the gradients; data_parallel_step() all-reduces and steps."""
+        L.check(self.lib.ptk_exec_set_defer_optimizer(self.h, int(bool(on))))
+
+    def compute_stream(self) -> int:
+        s = C.c_void_p()
+        L.check(self.lib.ptk_exec_compute_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def data_parallel_step(self, dp_group, step: bool = True):
+        """After run_iteration(): average this stage's gradients over its data-parallel replicas
+        (NCCL all-reduce, ordered on the executor's compute stream) and run AdamW there.
+        Replicas start from identical weights (same seed) and stay bit-identical."""
+        import torch
+        import torch.distributed as dist
+        if not hasattr(self, "_dp_view"):
+            self._dp_view = self.stage_view()
+        stream = torch.cuda.ExternalStream(self.compute_stream())
+        with torch.cuda.stream(stream):
+            dist.all_reduce(self._dp_view.grads, op=dist.ReduceOp.AVG, group=dp_group)
+        if step:
+            L.check(self.lib.ptk_stage_optimizer_step(self.lib.ptk_exec_stage(self.h), self.cfg.lr,
+                                                      self.cfg.weight_decay, C.c_void_p(stream.cuda_stream)))
 
     # ---- schedule / emulator
     def set_plan(self, k: int, b: int):
