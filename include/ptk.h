@@ -75,6 +75,8 @@ typedef struct ptk_gemm_desc {
     int bn_hint;       /* 0 = auto, else 64 / 128 / 256 */
     int multicast;     /* dense BN=256 only: 1 = 2-CTA cluster with B-tile multicast (K-major B);
                           2 = CTA-pair tcgen05.mma.cta_group::2 (256x256 pair tile) */
+    float* col_part;   /* optional, bf16 outputs, batch 1: fp32 [ceil(m/32)][n] += per-32-row-block column
+                          sums of C as stored (fused bias-gradient partials) */
 } ptk_gemm_desc;
 
 int ptk_gemm(const ptk_gemm_desc* desc, void* stream);

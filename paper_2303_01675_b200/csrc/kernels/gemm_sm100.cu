@@ -285,6 +285,27 @@ __device__ __forceinline__ void epilogue_tile_tma(const CUtensorMap* tmC, const 
             }
         }
         epi_stage_store(tmC, stage, lane, out, tc.n0 + st * 64, row0, tc.z1, tc.z2, false);
+        if (args.col_part != nullptr) {
+            // column sums of this warp's 32 rows of the step, read back from the swizzled staging
+            // buffer (lane l: columns 2l, 2l+1; conflict-free), into partial row (row0 / 32)
+            const uint32_t base = smem_u32(stage);
+            const int jc = static_cast<int>(lane >> 2), wc = static_cast<int>(lane & 3);
+            float s0 = 0.f, s1 = 0.f;
+            for (int r = 0; r < 32 && row0 + r < args.M; ++r) {
+                uint32_t v;
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v)
+                             : "r"(base + r * 128 + ((jc ^ (r & 7)) * 16) + wc * 4));
+                const float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
+                s0 += f.x;
+                s1 += f.y;
+            }
+            const int gn = tc.n0 + st * 64 + 2 * static_cast<int>(lane);
+            if (gn < args.N) {
+                float* pp = args.col_part + static_cast<int64_t>(row0 / 32) * args.N + gn;
+                pp[0] += s0;
+                pp[1] += s1;
+            }
+        }
     }
 }
 
@@ -858,6 +879,10 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     a.bias = d.bias;
     if ((a.epi == PTK_EPI_DGELU && a.aux == nullptr) || (a.epi == PTK_EPI_BIAS_GELU && (a.C2 == nullptr)))
         return PTK_ERR_ARG;
+    a.col_part = d.col_part;
+    if (a.col_part != nullptr && (b1 * b2 != 1 || a.epi == PTK_EPI_F32 || a.epi == PTK_EPI_ACC_F32 ||
+                                  d.causal != PTK_CAUSAL_NONE))
+        return PTK_ERR_ARG;  // column partials: dense, unbatched, bf16 output only
     {  // TMA-store epilogue when the output layout allows it (16-byte aligned rows and batches)
         const bool f32 = a.epi == PTK_EPI_F32 || a.epi == PTK_EPI_ACC_F32;
         bool ok = encode_output(&p.tmC, a.C, a.ldc, a.c_bs1, a.c_bs2, d.m, d.n, b1, b2, f32) == PTK_OK;

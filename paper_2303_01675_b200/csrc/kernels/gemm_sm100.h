@@ -21,6 +21,7 @@ struct GemmArgs {
     int64_t ld_aux, aux_bs1, aux_bs2;
     const void* bias;
     int tma_store;   // outputs leave through TMA stores (tmC / tmC2)
+    float* col_part;  // optional [ceil(M/32)][N] += column sums of C per 32-row block
     int full_tiles;  // CTA-pair kernel: work items >= full_tiles are 256 x 128 halves of the tail tiles
 };
 

@@ -96,6 +96,8 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
         throw std::invalid_argument("GptStage: bad layer range / slots / batch");
     L_ = c.layer_end - c.layer_begin;
     b_max_ = c.micro_batch_size;
+    if (static_cast<int64_t>(c.micro_batch_size) * c.seq > 32LL * kVecParts)
+        throw std::invalid_argument("GptStage: micro_batch_size * seq exceeds 32 * kVecParts tokens");
     const float proj_std = 0.02f / std::sqrt(2.f * c.n_layer);
     const uint64_t base = c.seed * 1000003ull;
 
@@ -414,9 +416,10 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
     kl(1, layernorm_bwd(dy, s.ln2, s.mean2, s.rstd2, W + w.ln2_g, nullptr, d_ln_, vp(w.ln2_g), vp(w.ln2_b),
                         vp(w.b_fc2) /* db2 = Σ dz, fused */, T, h, st),
        "ln2 bwd");
-    {  // d_pre = dz W2 * gelu'(pre)
+    {  // d_pre = dz W2 * gelu'(pre); db1 = Σ d_pre fused in the epilogue
         ptk_gemm_desc g = desc(T, f, h, mat(d_ln_, h), mat(W + w.w_fc2, f, 1), mat(d_pre_, f), PTK_EPI_DGELU);
         g.aux = mat(s.fc1_pre, f);
+        g.col_part = vp(w.b_fc1);
         gemm(g, st);
     }
     gemm(desc(h, f, T, mat(d_ln_, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
@@ -426,7 +429,6 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
         gemm(g, st);
     }
     gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.x_mid, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
-    kl(1, colsum_partial(d_pre_, vp(w.b_fc1), T, f, st), "db1");
     // dy_ = LN1'(d_xmid)
     kl(1, layernorm_bwd(dx_mid_, s.ln1, s.mean1, s.rstd1, W + w.ln1_g, nullptr, dy_, vp(w.ln1_g), vp(w.ln1_b),
                         vp(w.b_o) /* dbo = Σ dy_, fused */, T, h, st),
@@ -489,6 +491,7 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
     {
         ptk_gemm_desc g = desc(T, f, h, mat(dy, h), mat(W + w.w_fc2, f, 1), mat(d_pre_, f), PTK_EPI_DGELU);
         g.aux = mat(s.fc1_pre, f);
+        g.col_part = vp(w.b_fc1);  // db1 = Σ d_pre, fused in the epilogue
         gemm(g, st);
     }
     gemm(desc(h, f, T, mat(dy, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
@@ -498,7 +501,6 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
     // FC1: d_ln2 = d_pre W1; dW1 += d_preᵀ ln2; db1 += Σ d_pre
     gemm(desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
     gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.ln2, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
-    kl(1, colsum_partial(d_pre_, vp(w.b_fc1), T, f, st), "db1");
     // LN2 backward + residual: dx_mid = LN2'(d_ln2) + dy
     kl(1, layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, vp(w.ln2_g), vp(w.ln2_b),
                         vp(w.b_o) /* dbo = Σ dx_mid, fused */, T, h, st),

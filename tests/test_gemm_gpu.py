@@ -193,3 +193,23 @@ def test_gemm_pair_epilogues_and_wgrad(cuda, mc):
     _run(_desc(m, n, k, L.matrix(Ad.data_ptr(), m, 1), L.matrix(Bd.data_ptr(), n, 1), L.matrix(G.data_ptr(), n),
                epi=L.EPI_BIAS_GELU, bias=bias.data_ptr(), c2=P.data_ptr(), mc=mc))
     _close(P, (acc + bias.double().cpu()).float())
+
+
+@pytest.mark.parametrize("epi,mc", [(L.EPI_BF16, 2), (L.EPI_DGELU, 2), (L.EPI_BF16, 0)])
+def test_gemm_fused_column_partials(cuda, epi, mc):
+    """col_part: per-32-row-block column sums of C as stored (the fused bias gradient)."""
+    m, n, k = 1024, 1536, 256
+    torch.manual_seed(21)
+    A = torch.randn(m, k).bfloat16().to(cuda)
+    B = (torch.randn(n, k) * 0.1).bfloat16().to(cuda)
+    aux = torch.randn(m, n).bfloat16().to(cuda)
+    C = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    part = torch.ones(m // 32 + 3, n, dtype=torch.float32, device=cuda)  # += semantics; spare rows untouched
+    d = _desc(m, n, k, L.matrix(A.data_ptr(), k), L.matrix(B.data_ptr(), k), L.matrix(C.data_ptr(), n), epi=epi,
+              aux=L.matrix(aux.data_ptr(), n) if epi == L.EPI_DGELU else None, mc=mc)
+    d.col_part = part.data_ptr()
+    _run(d)
+    torch.cuda.synchronize()
+    ref = C.float().view(m // 32, 32, n).sum(1) + 1.0
+    assert torch.allclose(part[: m // 32], ref, rtol=1e-5, atol=1e-4)
+    assert torch.equal(part[m // 32:], torch.ones(3, n, device=cuda))
