@@ -146,21 +146,36 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) ln_bwd_fused_ker
     const int r_begin = blockIdx.x * per;
     const int r_end = min(rows, r_begin + per);
     const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+    // software pipeline: the next batch's loads are in flight while this batch is reduced and stored
+    uint4 nd[RB], nx[RB], nr[RB];
+    float nm[RB], ns[RB];
+    auto fetch = [&](int r0) {
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            const int row = r0 + rr;
+            const bool ok = row < r_end;
+            const int64_t off = static_cast<int64_t>(row) * H + c0;
+            nd[rr] = ok ? *reinterpret_cast<const uint4*>(dy + off) : zero;
+            nx[rr] = ok ? *reinterpret_cast<const uint4*>(x + off) : zero;
+            nr[rr] = (ok && resid != nullptr) ? *reinterpret_cast<const uint4*>(resid + off) : zero;
+            nm[rr] = ok ? mean_in[row] : 0.f;
+            ns[rr] = ok ? rstd_in[row] : 0.f;
+        }
+    };
+    if (r_begin < r_end) fetch(r_begin);
     int batch = 0;
     for (int r0 = r_begin; r0 < r_end; r0 += RB, ++batch) {
         uint4 du[RB], xu[RB], ru[RB];
         float mean[RB], rs[RB];
 #pragma unroll
-        for (int rr = 0; rr < RB; ++rr) {  // every load of the batch in flight at once
-            const int row = r0 + rr;
-            const bool ok = row < r_end;
-            const int64_t off = static_cast<int64_t>(row) * H + c0;
-            du[rr] = ok ? *reinterpret_cast<const uint4*>(dy + off) : zero;
-            xu[rr] = ok ? *reinterpret_cast<const uint4*>(x + off) : zero;
-            ru[rr] = (ok && resid != nullptr) ? *reinterpret_cast<const uint4*>(resid + off) : zero;
-            mean[rr] = ok ? mean_in[row] : 0.f;
-            rs[rr] = ok ? rstd_in[row] : 0.f;
+        for (int rr = 0; rr < RB; ++rr) {
+            du[rr] = nd[rr];
+            xu[rr] = nx[rr];
+            ru[rr] = nr[rr];
+            mean[rr] = nm[rr];
+            rs[rr] = ns[rr];
         }
+        if (r0 + RB < r_end) fetch(r0 + RB);
         float (*rb)[NW][2] = red[batch & 1];
 #pragma unroll
         for (int rr = 0; rr < RB; ++rr) {
@@ -246,14 +261,17 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
     const int r_end = min(rows, r_begin + per);
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     int row = r_begin;
-    for (; row + 4 <= r_end; row += 4) {
-        float v[4][8];
+    for (; row + 8 <= r_end; row += 8) {  // 8 rows of 16-byte loads in flight
+        uint4 u[8];
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) load8(m + static_cast<int64_t>(row + rr) * cols + c0, v[rr]);
+        for (int rr = 0; rr < 8; ++rr) u[rr] = *reinterpret_cast<const uint4*>(m + static_cast<int64_t>(row + rr) * cols + c0);
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr)
+        for (int rr = 0; rr < 8; ++rr) {
+            float v[8];
+            unpack_bf16x8(u[rr], v);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] += v[rr][i];
+            for (int i = 0; i < 8; ++i) acc[i] += v[i];
+        }
     }
     for (; row < r_end; ++row) {
         float v[8];
