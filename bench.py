@@ -173,7 +173,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2303_01675_b200.executor import StageExecutor, max_inflight, partition_layers
+    from paper_2303_01675_b200.executor import StageExecutor, max_inflight, partition_halves
     from paper_2303_01675_b200.stage import BERT_LARGE, GPT_1_3B, GPT_6_7B
     from paper_2303_01675_b200.tuning import OnlineTuner, candidate_set, outgoing_links
 
@@ -196,14 +196,17 @@ def main():
     shape = {"6.7b": GPT_6_7B, "bert-large": BERT_LARGE}.get(args.model, GPT_1_3B)
     GB = args.global_batch
     S = world
-    layers = partition_layers(shape.n_layer, S, head_weight=2.3 if shape.arch == "bert" else 2.0)
+    # half-layer stage cuts (attention | MLP blocks), weights measured on B200
+    halves = partition_halves(shape.n_layer, S, head_weight=2.3 if shape.arch == "bert" else 1.6,
+                              attn_weight=0.42 if shape.arch == "bert" else 0.47)
+    layers = halves
     cap = args.mem_cap_gb * 1e9 if args.mem_cap_gb > 0 else None
-    cands = candidate_set(shape, layers, S, GB, cap, fixed_b=args.micro_batch) if S > 1 else \
+    cands = candidate_set(shape, halves, S, GB, cap, fixed_b=args.micro_batch, halves=True) if S > 1 else \
         [[1, args.micro_batch, GB // args.micro_batch]]
     b_max = max(c[1] for c in cands)
     slots = max(max_inflight(rank, S, c[2], c[0]) * c[1] for c in cands) // b_max
     slots = max(slots, max(max_inflight(rank, S, c[2], c[0]) for c in cands if c[1] == b_max))
-    ex = StageExecutor(shape, rank, S, GB, b_max=b_max, slots=slots, layers=layers[rank])
+    ex = StageExecutor(shape, rank, S, GB, b_max=b_max, slots=slots, halves=halves[rank])
     ks = [c[0] for c in cands]
     b = cands[0][1]  # plan micro-batch size before tuning (the k=1 candidate)
     M = GB // b
@@ -333,9 +336,7 @@ def main():
     achieved = gf / gt / 1e12 if gt > 0 else 0.0
     flops_sample = shape.flops_per_sample()
     # ideal pipeline roofline: T* = sum_s T_s + (M-1) max_s T_s, T_s = b*FLOPs_s/P
-    per_layer = flops_sample / (shape.n_layer + 2.0)  # head ≈ 2 layer-equivalents (H7) for the split
-    Ts = [b * per_layer * ((e - s_) + (2.0 if i == S - 1 else 0.0)) / (peak_sus * 1e12) for i, (s_, e) in
-          enumerate(layers)]
+    Ts = [b * shape.flops_halves(s_, e, i == S - 1) / (peak_sus * 1e12) for i, (s_, e) in enumerate(halves)]
     t_star = sum(Ts) + (M - 1) * max(Ts)
     ideal = M * b / t_star
     out = {
@@ -348,7 +349,8 @@ def main():
                                               "V30528, post-LN, bidirectional)"}[args.model],
                    "global_batch": GB, "micro_batch": b, "micro_batches": M, "seq_len": shape.seq,
                    "candidates_kbM": cands, "memory_cap_gb": args.mem_cap_gb or None,
-                   "stages": S, "layers_per_stage": [e - s_ for s_, e in layers],
+                   "stages": S, "layers_per_stage": [(e - s_) / 2 for s_, e in halves],
+                   "half_layer_ranges": [list(x) for x in halves],
                    "parallelism": f"pp{S}" if S > 1 else "single stage (no pipeline)",
                    "schedule": (f"Ada-Grouper adaptive kFkB ((k, b) per step {plans_run})" if S > 1 else "1F1B (S=1)"),
                    "emulated_preemption": trace_desc, "l2": "working set (weights + activations) >> 126 MB L2"},

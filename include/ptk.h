@@ -146,6 +146,9 @@ typedef struct ptk_gpt_config {
     int arch;              /* 0: GPT (pre-LN, causal, LM head); 1: BERT (post-LN, bidirectional,
                               embedding LayerNorm, MLM head = dense+GELU+LN+decoder over all positions) */
     uint64_t seed;
+    /* half-layer stage boundaries (a layer = attention block + MLP block): */
+    int skip_first_attn;   /* layer_begin's attention block is on the previous stage (input = its x_mid) */
+    int skip_last_mlp;     /* layer_end-1's MLP block is on the next stage (output = its x_mid) */
 } ptk_gpt_config;
 
 typedef struct ptk_stage ptk_stage;

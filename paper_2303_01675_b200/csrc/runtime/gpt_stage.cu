@@ -96,6 +96,10 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
         throw std::invalid_argument("GptStage: bad layer range / slots / batch");
     L_ = c.layer_end - c.layer_begin;
     b_max_ = c.micro_batch_size;
+    if ((c.skip_first_attn && (c.has_embedding || L_ < 1)) || (c.skip_last_mlp && (c.has_head || L_ < 1)) ||
+        (L_ == 1 && c.skip_first_attn && c.skip_last_mlp))
+        throw std::invalid_argument("GptStage: half-layer boundaries need a layer block on this stage, no "
+                                    "attention-less embedding stage and no MLP-less head stage");
     if (static_cast<int64_t>(c.micro_batch_size) * c.seq > 32LL * kVecParts)
         throw std::invalid_argument("GptStage: micro_batch_size * seq exceeds 32 * kVecParts tokens");
     const float proj_std = 0.02f / std::sqrt(2.f * c.n_layer);
@@ -116,18 +120,22 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
         const uint64_t s = base + 100 + 16ull * l;
         const std::string p = "h" + std::to_string(l) + ".";
         LayerW w;
-        w.ln1_g = add_param(p + "ln1_g", 1, h, 0.f, 1.f, s + 0);
-        w.ln1_b = add_param(p + "ln1_b", 1, h, 0.f, 0.f, s + 1);
-        w.w_qkv = add_param(p + "w_qkv", 3 * h, h, 0.02f, 0.f, s + 2);
-        w.b_qkv = add_param(p + "b_qkv", 1, 3 * h, 0.f, 0.f, s + 3);
-        w.w_o = add_param(p + "w_o", h, h, proj_std, 0.f, s + 4);
-        w.b_o = add_param(p + "b_o", 1, h, 0.f, 0.f, s + 5);
-        w.ln2_g = add_param(p + "ln2_g", 1, h, 0.f, 1.f, s + 6);
-        w.ln2_b = add_param(p + "ln2_b", 1, h, 0.f, 0.f, s + 7);
-        w.w_fc1 = add_param(p + "w_fc1", f, h, 0.02f, 0.f, s + 8);
-        w.b_fc1 = add_param(p + "b_fc1", 1, f, 0.f, 0.f, s + 9);
-        w.w_fc2 = add_param(p + "w_fc2", h, f, proj_std, 0.f, s + 10);
-        w.b_fc2 = add_param(p + "b_fc2", 1, h, 0.f, 0.f, s + 11);
+        if (!(i == 0 && c.skip_first_attn)) {  // attention block
+            w.ln1_g = add_param(p + "ln1_g", 1, h, 0.f, 1.f, s + 0);
+            w.ln1_b = add_param(p + "ln1_b", 1, h, 0.f, 0.f, s + 1);
+            w.w_qkv = add_param(p + "w_qkv", 3 * h, h, 0.02f, 0.f, s + 2);
+            w.b_qkv = add_param(p + "b_qkv", 1, 3 * h, 0.f, 0.f, s + 3);
+            w.w_o = add_param(p + "w_o", h, h, proj_std, 0.f, s + 4);
+            w.b_o = add_param(p + "b_o", 1, h, 0.f, 0.f, s + 5);
+        }
+        if (!(i == L_ - 1 && c.skip_last_mlp)) {  // MLP block
+            w.ln2_g = add_param(p + "ln2_g", 1, h, 0.f, 1.f, s + 6);
+            w.ln2_b = add_param(p + "ln2_b", 1, h, 0.f, 0.f, s + 7);
+            w.w_fc1 = add_param(p + "w_fc1", f, h, 0.02f, 0.f, s + 8);
+            w.b_fc1 = add_param(p + "b_fc1", 1, f, 0.f, 0.f, s + 9);
+            w.w_fc2 = add_param(p + "w_fc2", h, f, proj_std, 0.f, s + 10);
+            w.b_fc2 = add_param(p + "b_fc2", 1, h, 0.f, 0.f, s + 11);
+        }
         lw_.push_back(w);
     }
     if (c.has_head) {
@@ -167,19 +175,26 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
                 bytes += n * 4;
                 return static_cast<float*>(alloc(n * 4));
             };
-            s.x_in = (i == 0 && !c.has_embedding) ? nullptr : bf(T * h);  // layer 0 reads the stage input
-            s.ln1 = bf(T * h);
-            s.qkv = bf(T * 3 * h);
-            s.attn_o = bf(T * h);
-            s.x_mid = bf(T * h);
-            s.ln2 = bf(T * h);
-            s.fc1_pre = bf(T * f);
-            s.fc1_act = bf(T * f);
-            s.mean1 = fl(T);
-            s.rstd1 = fl(T);
-            s.mean2 = fl(T);
-            s.rstd2 = fl(T);
-            s.lse = fl(static_cast<int64_t>(c.micro_batch_size) * c.heads * c.seq);
+            const bool A = has_attn(i), M = has_mlp(i);
+            if (A) {
+                s.x_in = (i == 0 && !c.has_embedding) ? nullptr : bf(T * h);  // layer 0 reads the stage input
+                s.ln1 = bf(T * h);
+                s.qkv = bf(T * 3 * h);
+                s.attn_o = bf(T * h);
+                s.mean1 = fl(T);
+                s.rstd1 = fl(T);
+                s.lse = fl(static_cast<int64_t>(c.micro_batch_size) * c.heads * c.seq);
+            }
+            // x_mid: the attention block's output; an MLP-only first layer reads the stage input
+            // there, an attention-only last layer writes it straight to the stage output
+            if (A && M) s.x_mid = bf(T * h);
+            if (M) {
+                s.ln2 = bf(T * h);
+                s.fc1_pre = bf(T * f);
+                s.fc1_act = bf(T * f);
+                s.mean2 = fl(T);
+                s.rstd2 = fl(T);
+            }
         }
         if (c.has_head) {
             HeadStash& hs = head_[sl];
@@ -377,32 +392,41 @@ void GptStage::bert_layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_
     const LayerW& w = lw_[li];
     const int T = tokens(), h = c.hidden, f = c.ffn;
     const __nv_bfloat16* W = wbf_;
-    {
-        ptk_gemm_desc g = desc(T, 3 * h, h, mat(x_in, h), mat(W + w.w_qkv, h), mat(s.qkv, 3 * h), PTK_EPI_BF16);
-        g.bias = W + w.b_qkv;
-        gemm(g, st);
+    const bool A = has_attn(li), M = has_mlp(li);
+    // attention block (input x_in) -> x_mid; MLP block (input x_mid) -> x_out
+    const __nv_bfloat16* xm = A ? (M ? s.x_mid : x_out) : x_in;
+    if (A) {
+        {
+            ptk_gemm_desc g = desc(T, 3 * h, h, mat(x_in, h), mat(W + w.w_qkv, h), mat(s.qkv, 3 * h), PTK_EPI_BF16);
+            g.bias = W + w.b_qkv;
+            gemm(g, st);
+        }
+        attention_forward(s, st);
+        {
+            ptk_gemm_desc g = desc(T, h, h, mat(s.attn_o, h), mat(W + w.w_o, h), mat(s.ln1, h), PTK_EPI_BF16);
+            g.bias = W + w.b_o;
+            g.aux = mat(x_in, h);
+            gemm(g, st);
+        }
+        kl(1, layernorm_fwd(s.ln1, W + w.ln1_g, W + w.ln1_b, const_cast<__nv_bfloat16*>(xm), s.mean1, s.rstd1, T, h,
+                            1e-12f, st),
+           "ln1");
     }
-    attention_forward(s, st);
-    {
-        ptk_gemm_desc g = desc(T, h, h, mat(s.attn_o, h), mat(W + w.w_o, h), mat(s.ln1, h), PTK_EPI_BF16);
-        g.bias = W + w.b_o;
-        g.aux = mat(x_in, h);
-        gemm(g, st);
+    if (M) {
+        {
+            ptk_gemm_desc g = desc(T, f, h, mat(xm, h), mat(W + w.w_fc1, h), mat(s.fc1_act, f), PTK_EPI_BIAS_GELU);
+            g.bias = W + w.b_fc1;
+            g.c2 = s.fc1_pre;
+            gemm(g, st);
+        }
+        {
+            ptk_gemm_desc g = desc(T, h, f, mat(s.fc1_act, f), mat(W + w.w_fc2, f), mat(s.ln2, h), PTK_EPI_BF16);
+            g.bias = W + w.b_fc2;
+            g.aux = mat(xm, h);
+            gemm(g, st);
+        }
+        kl(1, layernorm_fwd(s.ln2, W + w.ln2_g, W + w.ln2_b, x_out, s.mean2, s.rstd2, T, h, 1e-12f, st), "ln2");
     }
-    kl(1, layernorm_fwd(s.ln1, W + w.ln1_g, W + w.ln1_b, s.x_mid, s.mean1, s.rstd1, T, h, 1e-12f, st), "ln1");
-    {
-        ptk_gemm_desc g = desc(T, f, h, mat(s.x_mid, h), mat(W + w.w_fc1, h), mat(s.fc1_act, f), PTK_EPI_BIAS_GELU);
-        g.bias = W + w.b_fc1;
-        g.c2 = s.fc1_pre;
-        gemm(g, st);
-    }
-    {
-        ptk_gemm_desc g = desc(T, h, f, mat(s.fc1_act, f), mat(W + w.w_fc2, f), mat(s.ln2, h), PTK_EPI_BF16);
-        g.bias = W + w.b_fc2;
-        g.aux = mat(s.x_mid, h);
-        gemm(g, st);
-    }
-    kl(1, layernorm_fwd(s.ln2, W + w.ln2_g, W + w.ln2_b, x_out, s.mean2, s.rstd2, T, h, 1e-12f, st), "ln2");
 }
 
 void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __nv_bfloat16* dx,
@@ -412,36 +436,46 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
     const int T = tokens(), h = c.hidden, f = c.ffn;
     const __nv_bfloat16* W = wbf_;
     float* G = grad_;
-    // dz = LN2'(dy)
-    kl(1, layernorm_bwd(dy, s.ln2, s.mean2, s.rstd2, W + w.ln2_g, nullptr, d_ln_, vp(w.ln2_g), vp(w.ln2_b),
-                        vp(w.b_fc2) /* db2 = Σ dz, fused */, T, h, st),
-       "ln2 bwd");
-    {  // d_pre = dz W2 * gelu'(pre); db1 = Σ d_pre fused in the epilogue
-        ptk_gemm_desc g = desc(T, f, h, mat(d_ln_, h), mat(W + w.w_fc2, f, 1), mat(d_pre_, f), PTK_EPI_DGELU);
-        g.aux = mat(s.fc1_pre, f);
-        g.col_part = vp(w.b_fc1);
-        gemm(g, st);
+    const bool A = has_attn(li), M = has_mlp(li);
+    // gradient w.r.t. x_mid: from the MLP block, or the incoming gradient of an attention-only layer
+    const __nv_bfloat16* gxm = dy;
+    if (M) {
+        const __nv_bfloat16* xm = s.x_mid;  // an MLP-only first layer: the stage input (set by forward)
+        // dz = LN2'(dy)
+        kl(1, layernorm_bwd(dy, s.ln2, s.mean2, s.rstd2, W + w.ln2_g, nullptr, d_ln_, vp(w.ln2_g), vp(w.ln2_b),
+                            vp(w.b_fc2) /* db2 = Σ dz, fused */, T, h, st),
+           "ln2 bwd");
+        {  // d_pre = dz W2 * gelu'(pre); db1 = Σ d_pre fused in the epilogue
+            ptk_gemm_desc g = desc(T, f, h, mat(d_ln_, h), mat(W + w.w_fc2, f, 1), mat(d_pre_, f), PTK_EPI_DGELU);
+            g.aux = mat(s.fc1_pre, f);
+            g.col_part = vp(w.b_fc1);
+            gemm(g, st);
+        }
+        gemm(desc(h, f, T, mat(d_ln_, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
+        __nv_bfloat16* out = A ? dx_mid_ : dx;  // an MLP-only first layer hands d(x_mid) to the previous stage
+        {  // d_xmid = d_pre W1 + dz   (residual around the FFN)
+            ptk_gemm_desc g = desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(out, h), PTK_EPI_BF16);
+            g.aux = mat(d_ln_, h);
+            gemm(g, st);
+        }
+        gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(xm, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
+        gxm = out;
     }
-    gemm(desc(h, f, T, mat(d_ln_, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
-    {  // d_xmid = d_pre W1 + dz   (residual around the FFN)
-        ptk_gemm_desc g = desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(dx_mid_, h), PTK_EPI_BF16);
-        g.aux = mat(d_ln_, h);
-        gemm(g, st);
-    }
-    gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.x_mid, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
-    // dy_ = LN1'(d_xmid)
-    kl(1, layernorm_bwd(dx_mid_, s.ln1, s.mean1, s.rstd1, W + w.ln1_g, nullptr, dy_, vp(w.ln1_g), vp(w.ln1_b),
-                        vp(w.b_o) /* dbo = Σ dy_, fused */, T, h, st),
-       "ln1 bwd");
-    gemm(desc(T, h, h, mat(dy_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
-    gemm(desc(h, h, T, mat(dy_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
-    attention_backward(s, st);
-    gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.x_in, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
-    kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
-    {  // dx = dqkv Wqkv + dy_   (residual around attention)
-        ptk_gemm_desc g = desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(dx, h), PTK_EPI_BF16);
-        g.aux = mat(dy_, h);
-        gemm(g, st);
+    if (A) {
+        // dy_ = LN1'(d_xmid)
+        kl(1, layernorm_bwd(gxm, s.ln1, s.mean1, s.rstd1, W + w.ln1_g, nullptr, dy_, vp(w.ln1_g), vp(w.ln1_b),
+                            vp(w.b_o) /* dbo = Σ dy_, fused */, T, h, st),
+           "ln1 bwd");
+        gemm(desc(T, h, h, mat(dy_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
+        gemm(desc(h, h, T, mat(dy_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
+        attention_backward(s, st);
+        gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.x_in, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
+        kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
+        {  // dx = dqkv Wqkv + dy_   (residual around attention)
+            ptk_gemm_desc g = desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(dx, h), PTK_EPI_BF16);
+            g.aux = mat(dy_, h);
+            gemm(g, st);
+        }
     }
 }
 
@@ -449,74 +483,94 @@ void GptStage::layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, _
                              cudaStream_t st) {
     const ptk_gpt_config& c = cfg_;
     const LayerW& w = lw_[li];
-    const int T = tokens(), h = c.hidden, f = c.ffn, H = c.heads, d = h / H, n = c.seq, b = c.micro_batch_size;
+    const int T = tokens(), h = c.hidden, f = c.ffn;
     const __nv_bfloat16* W = wbf_;
-
-    kl(1, layernorm_fwd(x_in, W + w.ln1_g, W + w.ln1_b, s.ln1, s.mean1, s.rstd1, T, h, 1e-5f, st), "ln1");
-    {
-        ptk_gemm_desc g = desc(T, 3 * h, h, mat(s.ln1, h), mat(W + w.w_qkv, h), mat(s.qkv, 3 * h), PTK_EPI_BF16);
-        g.bias = W + w.b_qkv;
-        gemm(g, st);
+    const bool A = has_attn(li), M = has_mlp(li);
+    // attention block: x_mid = x + attn(LN1(x)); MLP block: x_out = x_mid + mlp(LN2(x_mid)).
+    // An MLP-only first layer reads x_mid = the stage input; an attention-only last layer
+    // writes x_mid straight to the stage output.
+    const __nv_bfloat16* xm = A ? (M ? s.x_mid : x_out) : x_in;
+    if (A) {
+        kl(1, layernorm_fwd(x_in, W + w.ln1_g, W + w.ln1_b, s.ln1, s.mean1, s.rstd1, T, h, 1e-5f, st), "ln1");
+        {
+            ptk_gemm_desc g = desc(T, 3 * h, h, mat(s.ln1, h), mat(W + w.w_qkv, h), mat(s.qkv, 3 * h), PTK_EPI_BF16);
+            g.bias = W + w.b_qkv;
+            gemm(g, st);
+        }
+        attention_forward(s, st);
+        {  // x_mid = o Woᵀ + b + x
+            ptk_gemm_desc g = desc(T, h, h, mat(s.attn_o, h), mat(W + w.w_o, h), mat(xm, h), PTK_EPI_BF16);
+            g.bias = W + w.b_o;
+            g.aux = mat(x_in, h);
+            gemm(g, st);
+        }
     }
-    attention_forward(s, st);
-    {  // x_mid = o Woᵀ + b + x
-        ptk_gemm_desc g = desc(T, h, h, mat(s.attn_o, h), mat(W + w.w_o, h), mat(s.x_mid, h), PTK_EPI_BF16);
-        g.bias = W + w.b_o;
-        g.aux = mat(x_in, h);
-        gemm(g, st);
-    }
-    kl(1, layernorm_fwd(s.x_mid, W + w.ln2_g, W + w.ln2_b, s.ln2, s.mean2, s.rstd2, T, h, 1e-5f, st), "ln2");
-    {
-        ptk_gemm_desc g = desc(T, f, h, mat(s.ln2, h), mat(W + w.w_fc1, h), mat(s.fc1_act, f), PTK_EPI_BIAS_GELU);
-        g.bias = W + w.b_fc1;
-        g.c2 = s.fc1_pre;
-        gemm(g, st);
-    }
-    {
-        ptk_gemm_desc g = desc(T, h, f, mat(s.fc1_act, f), mat(W + w.w_fc2, f), mat(x_out, h), PTK_EPI_BF16);
-        g.bias = W + w.b_fc2;
-        g.aux = mat(s.x_mid, h);
-        gemm(g, st);
+    if (M) {
+        kl(1, layernorm_fwd(xm, W + w.ln2_g, W + w.ln2_b, s.ln2, s.mean2, s.rstd2, T, h, 1e-5f, st), "ln2");
+        {
+            ptk_gemm_desc g = desc(T, f, h, mat(s.ln2, h), mat(W + w.w_fc1, h), mat(s.fc1_act, f), PTK_EPI_BIAS_GELU);
+            g.bias = W + w.b_fc1;
+            g.c2 = s.fc1_pre;
+            gemm(g, st);
+        }
+        {
+            ptk_gemm_desc g = desc(T, h, f, mat(s.fc1_act, f), mat(W + w.w_fc2, f), mat(x_out, h), PTK_EPI_BF16);
+            g.bias = W + w.b_fc2;
+            g.aux = mat(xm, h);
+            gemm(g, st);
+        }
     }
 }
 
 void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st) {
     const ptk_gpt_config& c = cfg_;
     const LayerW& w = lw_[li];
-    const int T = tokens(), h = c.hidden, f = c.ffn, H = c.heads, d = h / H, n = c.seq, b = c.micro_batch_size;
+    const int T = tokens(), h = c.hidden, f = c.ffn;
     const __nv_bfloat16* W = wbf_;
     float* G = grad_;
-
-    // FC2: d_pre = (dy W2) * gelu'(pre); dW2 += dyᵀ a; db2 += Σ dy
-    {
-        ptk_gemm_desc g = desc(T, f, h, mat(dy, h), mat(W + w.w_fc2, f, 1), mat(d_pre_, f), PTK_EPI_DGELU);
-        g.aux = mat(s.fc1_pre, f);
-        g.col_part = vp(w.b_fc1);  // db1 = Σ d_pre, fused in the epilogue
-        gemm(g, st);
+    const bool A = has_attn(li), M = has_mlp(li);
+    // gradient w.r.t. x_mid: from the MLP block, or the incoming gradient of an attention-only layer
+    const __nv_bfloat16* gxm = dy;
+    if (M) {
+        // FC2: d_pre = (dy W2) * gelu'(pre); dW2 += dyᵀ a; db1 = Σ d_pre fused in the epilogue
+        {
+            ptk_gemm_desc g = desc(T, f, h, mat(dy, h), mat(W + w.w_fc2, f, 1), mat(d_pre_, f), PTK_EPI_DGELU);
+            g.aux = mat(s.fc1_pre, f);
+            g.col_part = vp(w.b_fc1);
+            gemm(g, st);
+        }
+        gemm(desc(h, f, T, mat(dy, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
+        // db2 = Σ dy: fused into the LayerNorm backward that produced dy (the next layer's LN1 or the
+        // head's final LN), except for the last layer of a stage whose dy arrives from the next stage
+        if (li == L_ - 1 && !c.has_head) kl(1, colsum_partial(dy, vp(w.b_fc2), T, h, st), "db2");
+        // FC1: d_ln2 = d_pre W1; dW1 += d_preᵀ ln2
+        gemm(desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
+        gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.ln2, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
+        // LN2 backward + residual: d(x_mid) = LN2'(d_ln2) + dy; an MLP-only first layer hands it to the
+        // previous stage, whose attention block then owns db_o
+        __nv_bfloat16* out = A ? dx_mid_ : dx;
+        kl(1, layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, out, vp(w.ln2_g), vp(w.ln2_b),
+                            A ? vp(w.b_o) : nullptr /* dbo = Σ d(x_mid), fused */, T, h, st),
+           "ln2 bwd");
+        gxm = out;
+    } else {
+        // attention-only last layer: dy is d(x_mid) from the next stage; db_o = Σ dy here
+        kl(1, colsum_partial(dy, vp(w.b_o), T, h, st), "dbo");
     }
-    gemm(desc(h, f, T, mat(dy, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
-    // db2 = Σ dy: fused into the LayerNorm backward that produced dy (the next layer's LN1 or the
-    // head's final LN), except for the last layer of a stage whose dy arrives from the next stage
-    if (li == L_ - 1 && !c.has_head) kl(1, colsum_partial(dy, vp(w.b_fc2), T, h, st), "db2");
-    // FC1: d_ln2 = d_pre W1; dW1 += d_preᵀ ln2; db1 += Σ d_pre
-    gemm(desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
-    gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.ln2, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
-    // LN2 backward + residual: dx_mid = LN2'(d_ln2) + dy
-    kl(1, layernorm_bwd(d_ln_, s.x_mid, s.mean2, s.rstd2, W + w.ln2_g, dy, dx_mid_, vp(w.ln2_g), vp(w.ln2_b),
-                        vp(w.b_o) /* dbo = Σ dx_mid, fused */, T, h, st),
-       "ln2 bwd");
-    // out-proj: d_attn = dx_mid Wo; dWo += dx_midᵀ o; dbo += Σ dx_mid
-    gemm(desc(T, h, h, mat(dx_mid_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
-    gemm(desc(h, h, T, mat(dx_mid_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
-    attention_backward(s, st);
-    // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv += Σ dqkv
-    gemm(desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
-    gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
-    kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
-    // LN1 backward + residual: dx = LN1'(d_ln1) + dx_mid
-    kl(1, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, dx_mid_, dx, vp(w.ln1_g), vp(w.ln1_b),
-                        li > 0 ? vp(lw_[li - 1].b_fc2) : nullptr /* previous layer's db2 */, T, h, st),
-       "ln1 bwd");
+    if (A) {
+        // out-proj: d_attn = d(x_mid) Wo; dWo += d(x_mid)ᵀ o
+        gemm(desc(T, h, h, mat(gxm, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
+        gemm(desc(h, h, T, mat(gxm, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
+        attention_backward(s, st);
+        // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv += Σ dqkv
+        gemm(desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
+        gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
+        kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
+        // LN1 backward + residual: dx = LN1'(d_ln1) + d(x_mid)
+        kl(1, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, gxm, dx, vp(w.ln1_g), vp(w.ln1_b),
+                            li > 0 ? vp(lw_[li - 1].b_fc2) : nullptr /* previous layer's db2 */, T, h, st),
+           "ln1 bwd");
+    }
 }
 
 void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, const int32_t* labels,
@@ -536,7 +590,11 @@ void GptStage::forward(int slot, const int32_t* tok, const __nv_bfloat16* x_in, 
         kl(1, embedding_fwd(tok, W + wte_, W + wpe_, S[0].x_in, T, c.seq, h, st), "embedding");
         cur = S[0].x_in;
     } else if (L_ > 0) {
-        S[0].x_in = const_cast<__nv_bfloat16*>(x_in);  // stage input stays live until this slot's backward
+        // the stage input stays live until this slot's backward
+        if (has_attn(0))
+            S[0].x_in = const_cast<__nv_bfloat16*>(x_in);
+        else
+            S[0].x_mid = const_cast<__nv_bfloat16*>(x_in);
     }
     for (int i = 0; i < L_; ++i) {
         __nv_bfloat16* out = (i + 1 < L_) ? S[i + 1].x_in : (c.has_head ? vhead_.at(static_cast<size_t>(slot)).x_fin : x_out);

@@ -93,12 +93,14 @@ class GptStage {
     void collect_timing();
 
   private:
-    struct LayerW {  // element offsets
-        int64_t ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_fc1, b_fc1, w_fc2, b_fc2;
+    struct LayerW {  // element offsets (-1: block on another stage)
+        int64_t ln1_g = -1, ln1_b = -1, w_qkv = -1, b_qkv = -1, w_o = -1, b_o = -1;
+        int64_t ln2_g = -1, ln2_b = -1, w_fc1 = -1, b_fc1 = -1, w_fc2 = -1, b_fc2 = -1;
     };
     struct LayerStash {
-        __nv_bfloat16 *x_in, *ln1, *qkv, *attn_o, *x_mid, *ln2, *fc1_pre, *fc1_act;
-        float *mean1, *rstd1, *mean2, *rstd2, *lse;
+        __nv_bfloat16 *x_in = nullptr, *ln1 = nullptr, *qkv = nullptr, *attn_o = nullptr, *x_mid = nullptr,
+                      *ln2 = nullptr, *fc1_pre = nullptr, *fc1_act = nullptr;
+        float *mean1 = nullptr, *rstd1 = nullptr, *mean2 = nullptr, *rstd2 = nullptr, *lse = nullptr;
     };
     // GPT: ln1/ln2 hold the pre-LN outputs, x_mid the post-attention residual.
     // BERT (post-LN): ln1 holds y = attn + x (pre-LN1), x_mid = LN1(y),
@@ -113,6 +115,9 @@ class GptStage {
         float *mean, *rstd;
     };
     bool bert() const { return cfg_.arch == 1; }
+    // half-layer stage boundaries: the first layer may lack its attention block, the last its MLP block
+    bool has_attn(int li) const { return !(li == 0 && cfg_.skip_first_attn); }
+    bool has_mlp(int li) const { return !(li == L_ - 1 && cfg_.skip_last_mlp); }
     void bert_layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, __nv_bfloat16* x_out, cudaStream_t st);
     void bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st);
     void attention_forward(LayerStash& s, cudaStream_t st);

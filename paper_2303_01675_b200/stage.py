@@ -19,8 +19,14 @@ class GptConfig(C.Structure):
         ("n_layer", C.c_int), ("hidden", C.c_int), ("heads", C.c_int), ("ffn", C.c_int), ("seq", C.c_int),
         ("vocab", C.c_int), ("layer_begin", C.c_int), ("layer_end", C.c_int), ("has_embedding", C.c_int),
         ("has_head", C.c_int), ("micro_batch_size", C.c_int), ("slots", C.c_int), ("micro_batches", C.c_int),
-        ("arch", C.c_int), ("seed", C.c_uint64),
+        ("arch", C.c_int), ("seed", C.c_uint64), ("skip_first_attn", C.c_int), ("skip_last_mlp", C.c_int),
     ]
+
+
+def halves_to_layers(hb: int, he: int) -> tuple[int, int, int, int]:
+    """Half-layer range [hb, he) (2l = attention block of layer l, 2l+1 = its MLP block) ->
+    (layer_begin, layer_end, skip_first_attn, skip_last_mlp) of ptk_gpt_config."""
+    return hb // 2, (he + 1) // 2, hb % 2, he % 2
 
 
 @dataclass(frozen=True)
@@ -49,6 +55,33 @@ class ModelShape:
         head = 2 * h * V + (2 * h * h if self.arch == "bert" else 0)  # BERT MLM transform
         return 3.0 * s * (l * per_tok_layer + head)
 
+
+    def half_params(self) -> tuple[int, int]:
+        """(attention block, MLP block) parameter counts of one layer."""
+        h, f = self.hidden, self.ffn
+        return 4 * h * h + 6 * h, 2 * h * f + f + 3 * h
+
+    def param_count_halves(self, hb: int, he: int, has_embedding: bool, has_head: bool) -> int:
+        pa, pm = self.half_params()
+        n = sum(pa if u % 2 == 0 else pm for u in range(hb, he))
+        return n + self.param_count(0, has_embedding, has_head)
+
+    def stash_bytes_halves(self, hb: int, he: int, has_head: bool) -> int:
+        s, h, f, H = self.seq, self.hidden, self.ffn, self.heads
+        attn = 7 * s * h * 2 + 2 * s * 4 + H * s * 4  # x_in, ln1, qkv, attn_o, x_mid; LN stats; lse
+        mlp = (s * h + 2 * s * f) * 2 + 2 * s * 4     # ln2, fc1 pre/act; LN stats
+        out = sum(attn if u % 2 == 0 else mlp for u in range(hb, he))
+        return out + self.stash_bytes_per_sample(0, has_head)
+
+    def flops_halves(self, hb: int, he: int, has_head: bool) -> float:
+        """Training FLOPs per sample of half-layer blocks [hb, he) (+ the head)."""
+        h, f, s, V = self.hidden, self.ffn, self.seq, self.vocab
+        att = 2 * s * h if self.arch == "gpt" else 4 * s * h
+        fa, fm = 2 * 4 * h * h + att, 2 * 2 * h * f
+        n = sum(fa if u % 2 == 0 else fm for u in range(hb, he))
+        if has_head:
+            n += 2 * h * V + (2 * h * h if self.arch == "bert" else 0)
+        return 3.0 * s * n
 
     def param_count(self, n_layers: int, has_embedding: bool, has_head: bool) -> int:
         h, V = self.hidden, self.vocab
@@ -117,13 +150,14 @@ def _ptr(t) -> int:
 
 class GptStage:
     def __init__(self, shape: ModelShape, layer_begin: int, layer_end: int, has_embedding: bool, has_head: bool,
-                 micro_batch_size: int, slots: int, micro_batches: int, seed: int = 42):
+                 micro_batch_size: int, slots: int, micro_batches: int, seed: int = 42, skip_first_attn: bool = False,
+                 skip_last_mlp: bool = False):
         self.lib = L.lib()
         _declare(self.lib)
         self.shape = shape
         self.cfg = GptConfig(shape.n_layer, shape.hidden, shape.heads, shape.ffn, shape.seq, shape.vocab,
                              layer_begin, layer_end, int(has_embedding), int(has_head), micro_batch_size, slots,
-                             micro_batches, shape.arch_id, seed)
+                             micro_batches, shape.arch_id, seed, int(skip_first_attn), int(skip_last_mlp))
         h = C.c_void_p()
         L.check(self.lib.ptk_stage_create(C.byref(self.cfg), C.byref(h)))
         self.h = h

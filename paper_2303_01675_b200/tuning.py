@@ -92,28 +92,31 @@ class OnlineTuner:
         return self.decide(current, clock)
 
 
-def memory_model(shape, layers, stages: int, global_batch: int) -> dict:
+def memory_model(shape, layers, stages: int, global_batch: int, halves: bool = False) -> dict:
     """pipetune ModelSpec with the real per-stage byte model: weights = fp32 master +
-    grad + AdamW m, v + bf16 copy (18 B/param); activations = the stash per sample."""
+    grad + AdamW m, v + bf16 copy (18 B/param); activations = the stash per sample.
+    `layers`: per-stage layer ranges, or half-layer ranges when `halves`."""
     st = []
     for s_, (lb, le) in enumerate(layers):
         first, last = s_ == 0, s_ == stages - 1
+        params = shape.param_count_halves(lb, le, first, last) if halves else shape.param_count(le - lb, first, last)
+        stash = shape.stash_bytes_halves(lb, le, last) if halves else shape.stash_bytes_per_sample(le - lb, last)
         st.append(pt.StageProfile(
-            stage_id=s_, weight_bytes=18 * shape.param_count(le - lb, first, last),
-            activation_bytes_per_sample=shape.stash_bytes_per_sample(le - lb, last),
+            stage_id=s_, weight_bytes=18 * params,
+            activation_bytes_per_sample=stash,
             output_bytes_per_sample_fwd=shape.seq * shape.hidden * 2,
             output_bytes_per_sample_bwd=shape.seq * shape.hidden * 2))
     return pt.model_dict(pt.ModelSpec(st, global_batch))
 
 
 def candidate_set(shape, layers, stages: int, global_batch: int, mem_cap_bytes: int | None, k_max: int = 8,
-                  fixed_b: int = 2) -> list[list[int]]:
+                  fixed_b: int = 2, halves: bool = False) -> list[list[int]]:
     """Ada-Grouper candidates: the (k, b) memory-limit frontier via the C++
     enumerate_candidates under an imposed per-GPU cap; without a cap, k in {1,2,4,8} at b."""
     if mem_cap_bytes is None:
         M = global_batch // fixed_b
         return [[k, fixed_b, M] for k in (1, 2, 4, 8) if k <= M]
-    model = memory_model(shape, layers, stages, global_batch)
+    model = memory_model(shape, layers, stages, global_batch, halves)
     out = pt.scenario({"op": "enumerate", "model": model, "k_max": k_max,
                        "cluster": {"device_memory_limit": int(mem_cap_bytes), "devices": stages}})
     return [e[:3] for e in out["entries"]]

@@ -30,11 +30,16 @@ def digests(ex):
     return {n: hashlib.sha256(st.param(n, "master").cpu().numpy().tobytes()).hexdigest()[:16] for n in st.params}
 
 
-def run_pipeline(rank, S, k, group, trace=False, iters=2):
+def run_pipeline(rank, S, k, group, trace=False, iters=2, half_cuts=False):
     M = GB // B
     layers = [(0, 2), (2, 4)] if S == 2 else [(i, i + 1) for i in range(4)]
+    # half-layer cuts (attention | MLP of a layer on adjacent stages)
+    halves = [(0, 5), (5, 8)] if S == 2 else [(0, 3), (3, 4), (4, 7), (7, 8)]
     slots = max(max_inflight(rank, S, M, kk) for kk in (1, 2, 3, 4))
-    ex = StageExecutor(SHAPE, rank, S, GB, b_max=B, slots=slots, layers=layers[rank], lr=1e-3)
+    if half_cuts:
+        ex = StageExecutor(SHAPE, rank, S, GB, b_max=B, slots=slots, halves=halves[rank], lr=1e-3)
+    else:
+        ex = StageExecutor(SHAPE, rank, S, GB, b_max=B, slots=slots, layers=layers[rank], lr=1e-3)
     ex.connect_dist(group)
     if trace:
         for link in outgoing_links(rank, S):
@@ -64,8 +69,9 @@ def main():
     dist.init_process_group("gloo")
     group = dist.group.WORLD
     res = {}
-    for name, k, tr in (("1f1b", 1, False), ("k2", 2, False), ("k2_paced", 2, True), ("mixed", [1, 3, 2, 2], True)):
-        d, loss, ms, tl = run_pipeline(rank, world, k, group, tr)
+    for name, k, tr, hc in (("1f1b", 1, False, False), ("k2", 2, False, False), ("k2_paced", 2, True, False),
+                            ("mixed", [1, 3, 2, 2], True, False), ("half_cuts", 2, False, True)):
+        d, loss, ms, tl = run_pipeline(rank, world, k, group, tr, half_cuts=hc)
         allds = [None] * world
         dist.all_gather_object(allds, (d, loss, ms, len(tl["xfer"])), group=group)
         merged = {}
@@ -86,6 +92,7 @@ def main():
             "k1_vs_k2_bit_identical": res["1f1b"]["digest"] == res["k2"]["digest"],
             "paced_bit_identical": res["k2"]["digest"] == res["k2_paced"]["digest"],
             "mixed_groups_bit_identical": res["k2"]["digest"] == res["mixed"]["digest"],
+            "half_layer_cuts_bit_identical": res["k2"]["digest"] == res["half_cuts"]["digest"],
             "pipeline_vs_single_gpu_bit_identical": res["1f1b"]["digest"] == single,
             "loss": {"1f1b": res["1f1b"]["loss"], "k2": res["k2"]["loss"], "paced": res["k2_paced"]["loss"],
                      "mixed": res["mixed"]["loss"], "single": loss},
@@ -93,7 +100,8 @@ def main():
             "n_params": len(single),
         }
         out["ok"] = all([out["k1_vs_k2_bit_identical"], out["paced_bit_identical"],
-                         out["mixed_groups_bit_identical"], out["pipeline_vs_single_gpu_bit_identical"]])
+                         out["mixed_groups_bit_identical"], out["half_layer_cuts_bit_identical"],
+                         out["pipeline_vs_single_gpu_bit_identical"]])
         print(json.dumps(out), flush=True)
     dist.barrier(group=group)
     dist.destroy_process_group()

@@ -64,12 +64,20 @@ def test_toy_single_stage_matches_oracle(cuda, shape):
     assert worst[0] <= GRAD_TOL, worst
 
 
+@pytest.mark.parametrize("half", [False, True], ids=["layer_cut", "half_layer_cut"])
 @pytest.mark.parametrize("shape", [TOY, TOY_BERT], ids=["gpt", "bert"])
-def test_two_stage_split_bit_identical(cuda, shape):
+def test_two_stage_split_bit_identical(cuda, shape, half):
+    """A 2-stage split reproduces the 1-stage gradients exactly — also when the cut falls
+    between layer 2's attention block (stage 0) and its MLP block (stage 1)."""
     b, M = 2, 2
     full = GptStage(shape, 0, 4, True, True, b, slots=1, micro_batches=M)
-    s0 = GptStage(shape, 0, 2, True, False, b, slots=1, micro_batches=M)
-    s1 = GptStage(shape, 2, 4, False, True, b, slots=1, micro_batches=M)
+    if half:
+        s0 = GptStage(shape, 0, 3, True, False, b, slots=1, micro_batches=M, skip_last_mlp=True)
+        s1 = GptStage(shape, 2, 4, False, True, b, slots=1, micro_batches=M, skip_first_attn=True)
+    else:
+        s0 = GptStage(shape, 0, 2, True, False, b, slots=1, micro_batches=M)
+        s1 = GptStage(shape, 2, 4, False, True, b, slots=1, micro_batches=M)
+    assert not (set(s0.params) & set(s1.params)) and set(s0.params) | set(s1.params) == set(full.params)
     batches = _batches(shape, b, M, seed=7)
     T, h = b * TOY.seq, TOY.hidden
     act = torch.empty(T, h, dtype=torch.bfloat16, device="cuda")
