@@ -92,18 +92,21 @@ def partition_halves(n_layer: int, stages: int, head_weight: float = 1.6, attn_w
 
     @lru_cache(None)
     def solve(start: int, k: int):
+        # minimise the bottleneck, then the sum of squared stage costs (spreads the slack)
         extra_first = embed_weight if start == 0 else 0.0
         if k == 1:
-            return (pre[n] - pre[start] + head_weight + extra_first, ((start, n),))
+            c = pre[n] - pre[start] + head_weight + extra_first
+            return (c, c * c, ((start, n),))
         best = None
         for end in range(start + 1, n - k + 2):
             rest = solve(end, k - 1)
-            cost = max(pre[end] - pre[start] + extra_first, rest[0])
-            if best is None or cost < best[0] - 1e-12:
-                best = (cost, ((start, end),) + rest[1])
+            c = pre[end] - pre[start] + extra_first
+            key = (round(max(c, rest[0]), 9), round(c * c + rest[1], 9))
+            if best is None or key < (round(best[0], 9), round(best[1], 9)):
+                best = (max(c, rest[0]), c * c + rest[1], ((start, end),) + rest[2])
         return best
 
-    return list(solve(0, stages)[1])
+    return list(solve(0, stages)[2])
 
 
 def max_inflight(stage: int, stages: int, micro_batches: int, k: int) -> int:
