@@ -827,7 +827,17 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
             const long waves = (tiles + sms - 1) / sms;
             return static_cast<double>(tiles) / static_cast<double>(waves * sms);
         };
-        bn = eff(128) > eff(256) + 0.15 ? 128 : 256;
+        double e256 = eff(256);
+        if (d.multicast == 2 && tiles_m >= 2 && d.causal == PTK_CAUSAL_NONE) {
+            // CTA-pair 256 x 256 tiles on sms/2 pairs, partial last wave split into halves
+            const long t = static_cast<long>((tiles_m + 1) / 2) * ((d.n + 255) / 256) * b1 * b2;
+            const long p = sms / 2;
+            const long rem = t % p;
+            double rounds = static_cast<double>(t / p);
+            if (rem > 0) rounds += (t > p && 2 * rem <= p && d.n % 256 == 0) ? 0.5 : 1.0;
+            e256 = static_cast<double>(t) / (static_cast<double>(p) * rounds) + 0.1;  // pair kernel: faster per SM
+        }
+        bn = eff(128) > e256 + 0.15 ? 128 : 256;
     }
     if (d.causal == PTK_CAUSAL_TILES && (bn != kBM || d.m != d.n)) return PTK_ERR_ARG;
 

@@ -22,6 +22,7 @@ def gemm_desc(m, n, k, A, a_mn, B, b_mn, Cm, epi):
     d.aux = L.matrix(0, 0)
     d.epilogue = epi
     d.multicast = MC
+    d.bn_hint = int(__import__("os").environ.get("PTK_BN", "0"))
     return d
 
 
@@ -66,6 +67,14 @@ def main():
         ("x_out_aux", T, h, h, 0, 0, B_, 0, 1, 0),
         ("x_fc2wgrad_f32", h, f, T, 1, 1, L.EPI_F32, 0, 0, 0),
         ("x_fc2wgrad_bf16", h, f, T, 1, 1, B_, 0, 0, 0),
+        # BERT-large b=4 shapes (T=2048, h=1024, f=4096) under the GEMM modes (PTK_MC env: 0/1/2/3)
+        ("bert_qkv", T, 3072, 1024, 0, 0, B_, 1, 0, 0),
+        ("bert_out", T, 1024, 1024, 0, 0, B_, 1, 1, 0),
+        ("bert_fc1", T, 4096, 1024, 0, 0, L.EPI_BIAS_GELU, 1, 0, 1),
+        ("bert_fc2", T, 1024, 4096, 0, 0, B_, 1, 1, 0),
+        ("bert_fc1_wgrad", 4096, 1024, T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
+        ("bert_fc2_dgrad", T, 4096, 1024, 0, 1, L.EPI_DGELU, 0, 1, 0),
+        ("bert_out_wgrad", 1024, 1024, T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
         ("x_kk", T, f, h, 0, 0, B_, 0, 0, 0),
         ("x_mk", T, f, h, 1, 0, B_, 0, 0, 0),
         ("x_km", T, f, h, 0, 1, B_, 0, 0, 0),
@@ -102,7 +111,7 @@ def main():
         Bb = B if b_mn else B.T
         tc = timeit(lambda: torch.matmul(Ab, Bb))
         fl = 2.0 * m * n * k
-        if not name.startswith("head") and not name.startswith("x_"):
+        if not name.startswith(("head", "x_", "bert_")):
             tot_ptk += t
             tot_cub += tc
             tot_fl += fl
