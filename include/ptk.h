@@ -80,6 +80,9 @@ typedef struct ptk_gemm_desc {
 } ptk_gemm_desc;
 
 int ptk_gemm(const ptk_gemm_desc* desc, void* stream);
+/* The launch ptk_gemm would make for desc (no launch): info[0] tile width BN, info[1] grid
+ * (CTAs), info[2] work items, info[3] 1 = 2-CTA cluster (B multicast or CTA pair). */
+int ptk_gemm_plan_info(const ptk_gemm_desc* desc, int* info);
 
 /* Fused attention forward (causal = 1: key <= query; 0: bidirectional): qkv bf16 [b][s][3][H][d] -> o bf16 [b*s][H*d],
  * lse fp32 [b][H][s] = log2(sum_k 2^(S_qk * log2(e)/sqrt(d))) (row max included). */

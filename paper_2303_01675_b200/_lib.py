@@ -63,6 +63,8 @@ def _declare(L: C.CDLL) -> None:
     L.ptk_version.restype = C.c_char_p
     L.ptk_gemm.argtypes = [C.POINTER(GemmDesc), C.c_void_p]
     L.ptk_gemm.restype = C.c_int
+    L.ptk_gemm_plan_info.argtypes = [C.POINTER(GemmDesc), C.POINTER(C.c_int)]
+    L.ptk_gemm_plan_info.restype = C.c_int
     L.ptk_flash_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int] * 5 + [C.c_void_p]
     L.ptk_flash_backward.argtypes = [C.c_void_p] * 6 + [C.c_int] * 5 + [C.c_void_p]
     L.ptk_plan_json.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t,

@@ -19,6 +19,18 @@ extern "C" int ptk_gemm(const ptk_gemm_desc* desc, void* stream) {
     return PTK_OK;
 }
 
+extern "C" int ptk_gemm_plan_info(const ptk_gemm_desc* desc, int* info) {
+    if (desc == nullptr || info == nullptr) return ptk::set_error(PTK_ERR_ARG, "ptk_gemm_plan_info: null argument");
+    ptk::GemmPlan plan;
+    const int rc = ptk::gemm_prepare(*desc, &plan);
+    if (rc != PTK_OK) return ptk::set_error(rc, "ptk_gemm_plan_info: prepare failed (shape/alignment)");
+    info[0] = plan.args.bn;
+    info[1] = plan.grid;
+    info[2] = plan.args.num_tiles;
+    info[3] = plan.multicast ? 1 : 0;
+    return PTK_OK;
+}
+
 extern "C" int ptk_flash_forward(const void* qkv, void* o, float* lse, int b, int s, int H, int d, int causal,
                                  void* stream) {
     ptk::FlashPlan p;

@@ -213,3 +213,26 @@ def test_gemm_fused_column_partials(cuda, epi, mc):
     ref = C.float().view(m // 32, 32, n).sum(1) + 1.0
     assert torch.allclose(part[: m // 32], ref, rtol=1e-5, atol=1e-4)
     assert torch.equal(part[m // 32:], torch.ones(3, n, device=cuda))
+
+
+def test_gemm_plan_info(cuda):
+    """ptk_gemm_plan_info reports the launch ptk_gemm makes: the CTA-pair kernel for the wide dense
+    stage GEMMs, a partial last wave split into half tiles, plain 1-CTA tiles for narrow outputs."""
+    import ctypes
+    A = torch.empty(2048, 8192, dtype=torch.bfloat16, device=cuda)
+    B = torch.empty(8192, 8192, dtype=torch.bfloat16, device=cuda)
+    C = torch.empty(2048, 8192, dtype=torch.bfloat16, device=cuda)
+    info = (ctypes.c_int * 4)()
+
+    def plan(m, n, k, mc):
+        d = _desc(m, n, k, L.matrix(A.data_ptr(), k), L.matrix(B.data_ptr(), k), L.matrix(C.data_ptr(), n), mc=mc)
+        L.check(L.lib().ptk_gemm_plan_info(d, info))
+        return list(info)
+    bn, grid, items, pair = plan(2048, 8192, 2048, 2)  # fc1 fwd: 8 x 32 = 256 pair tiles
+    sms = torch.cuda.get_device_properties(cuda).multi_processor_count
+    assert (bn, pair) == (256, 1) and grid == 2 * (sms // 2)
+    tiles = 256
+    rem = tiles % (sms // 2)
+    assert items == (tiles - rem + 2 * rem if 2 * rem <= sms // 2 else tiles)
+    assert plan(2048, 64, 512, 0)[0] == 64
+    assert plan(256, 128, 512, 0)[:2] == [128, 2]
