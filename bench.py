@@ -52,6 +52,9 @@ def parse():
     p.add_argument("--mem-cap-gb", type=float, default=0.0,
                    help="imposed per-GPU memory limit: candidates = the (k, b) frontier under it (config 4)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--ref-stages", type=int, default=1,
+                   help="--impl reference: S > 1 runs the CPU-thread pipeline executor (S stage threads, "
+                        "S micro-batches per step, oracle/cpu_pipeline.py); 1 = the whole model on all cores")
     p.add_argument("--timeline", type=str, default="")
     return p.parse_args()
 
@@ -142,9 +145,11 @@ def reference_arm(args):
     if rank != 0:
         return
     from oracle.cpu_baseline import CpuTrainer
+    from oracle.cpu_pipeline import CpuPipeline
     from paper_2303_01675_b200.stage import BERT_LARGE, GPT_1_3B, GPT_6_7B
     shape = {"6.7b": GPT_6_7B, "bert-large": BERT_LARGE}.get(args.model, GPT_1_3B)
-    trainer = CpuTrainer(shape, 1, 1)
+    S = max(1, args.ref_stages)
+    trainer = CpuTrainer(shape, 1, 1) if S == 1 else CpuPipeline(shape, S, 1, S, k=1)
     for _ in range(min(args.warmup, 1)):  # one untimed warm-up sample (allocator, thread pool)
         trainer.step()
     vals = []
@@ -158,8 +163,10 @@ def reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.model} training step on the CPU path (fp32), bounded sample of 1 sample/step",
-                   "global_batch": args.global_batch, "seq_len": shape.seq, "parallelism": "none (host cores)"},
+        "config": {"workload": f"{args.model} training step on the CPU path (fp32), bounded sample of "
+                               f"{S} sample(s)/step",
+                   "global_batch": args.global_batch, "seq_len": shape.seq,
+                   "parallelism": "none (host cores)" if S == 1 else f"pp{S} stage threads (host cores)"},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)

@@ -126,6 +126,9 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t, int r
         while ((mb + 1) * (mb + 2) / 2 <= r) ++mb;
         while (mb * (mb + 1) / 2 > r) --mb;
         nb = r - mb * (mb + 1) / 2;
+    } else if (a.n_fast) {
+        mb = r / a.tiles_n;
+        nb = r - mb * a.tiles_n;
     } else {
         nb = r / a.tiles_m;
         mb = r - nb * a.tiles_m;
@@ -506,8 +509,14 @@ __device__ __forceinline__ TileCoord decode_pair_tile(const GemmArgs& a, int t, 
     const int z = tile / a.tiles_per_batch;
     const int r = tile - z * a.tiles_per_batch;
     const int mpairs = (a.tiles_m + 1) / 2;
-    const int nb = r / mpairs;
-    const int mp = r - nb * mpairs;
+    int nb, mp;
+    if (a.n_fast) {
+        mp = r / a.tiles_n;
+        nb = r - mp * a.tiles_n;
+    } else {
+        nb = r / mpairs;
+        mp = r - nb * mpairs;
+    }
     c.z1 = z % a.batch1;
     c.z2 = z / a.batch1;
     c.m0 = mp * 256 + rank * 128;
@@ -902,6 +911,18 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
         a.tma_store = 1;
     }
 
+    // Raster order: the ~150 concurrent tiles share the operand block of the
+    // fastest-varying index's partner through L2.  m-fastest streams B once but
+    // re-reads A once per n-tile column unless A stays L2-resident; n-fastest is
+    // the mirror image.  Pick the order with less HBM operand traffic (the
+    // vocabulary-head weight gradient: A = dlogits^T, 206 MB, 8 n-tiles).
+    if (b1 * b2 == 1 && d.causal == PTK_CAUSAL_NONE) {
+        const double l2 = 60e6;  // bytes of operand that stay resident in the 126 MB L2 under streaming
+        const double ab = 2.0 * d.m * d.k, bb = 2.0 * d.n * d.k;
+        const double m_fast = (ab <= l2 ? ab : ab * a.tiles_n) + bb;
+        const double n_fast = (bb <= l2 ? bb : bb * ((tiles_m + 1) / 2)) + ab;
+        a.n_fast = n_fast < 0.8 * m_fast ? 1 : 0;
+    }
     const int sms = num_sms();
     // B-tile multicast across a 2-CTA cluster halves the L2 -> SM operand
     // traffic per FLOP (dense, non-causal GEMMs with at least two m-tiles).

@@ -23,6 +23,7 @@ struct GemmArgs {
     int tma_store;   // outputs leave through TMA stores (tmC / tmC2)
     float* col_part;  // optional [ceil(M/32)][N] += column sums of C per 32-row block
     int full_tiles;  // CTA-pair kernel: work items >= full_tiles are 256 x 128 halves of the tail tiles
+    int n_fast;      // tile raster: 0 = m-tiles fastest (B tile shared), 1 = n-tiles fastest (A tile shared)
 };
 
 struct GemmPlan {

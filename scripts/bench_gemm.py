@@ -81,6 +81,9 @@ def main():
         ("x_mm", T, f, h, 1, 1, B_, 0, 0, 0),
         ("x_kk_f32", T, f, h, 0, 0, L.EPI_F32, 0, 0, 0),
         ("x_kk_acc", T, f, h, 0, 0, L.EPI_ACC_F32, 0, 0, 0),
+        ("x_headw_f32", V, h, T, 1, 1, L.EPI_F32, 0, 0, 0),
+        ("x_headw_bf16", V, h, T, 1, 1, B_, 0, 0, 0),
+        ("x_headw_kk_acc", V, h, T, 0, 0, L.EPI_ACC_F32, 0, 0, 0),
     ]
     stream = torch.cuda.current_stream().cuda_stream
     out = []
