@@ -271,7 +271,8 @@ def main():
     chosen, decisions, tune_s = cands[0], [], 0.0
     arm_reset()
     with ClockSampler(local) as clk:
-        ex.gemm_timing(1)
+        if os.environ.get("PTK_BENCH_GEMM_TIMING", "1") != "0":  # 0: diagnostics, no per-GEMM events
+            ex.gemm_timing(1)
         t0 = time.perf_counter()
         ms, plans_run = [], []
         for step in range(args.steps):
