@@ -189,10 +189,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
+    # PTK_OVERSUBSCRIBE=1 (dry runs only): more ranks than GPUs, rank -> GPU local % count, gloo only
+    oversub = os.environ.get("PTK_OVERSUBSCRIBE") == "1"
+    if oversub:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.new_group(backend="gloo")
 
     def barrier():
