@@ -40,6 +40,7 @@ namespace {
 constexpr int kBlk = 128;      // query rows and key rows per block
 constexpr int kThreads = 384;  // backward: 12 warps: TMA, MMA, 2 idle, 8 row-parallel elementwise warps
 constexpr int kFwdNQ = 2;      // forward: softmax rows split in kFwdNQ column parts (4 + 4·NQ warps)
+constexpr float kLazyRescaleLog2 = 8.f;  // forward: move the running max only when it grows by > 2^8
 
 int sm_count() {
     static int n = 0;
@@ -322,7 +323,11 @@ __global__ void __launch_bounds__(32 * (4 + 4 * NQ), 1)
                 float pm = lds32f(xb + r * 4);
 #pragma unroll
                 for (int q = 1; q < NQ; ++q) pm = fmaxf(pm, lds32f(xb + (q * kBlk + r) * 4));
-                const float mx = fmaxf(m, pm * a.scale_log2);
+                // lazy rescaling: the running max m only moves when the block max exceeds it by more
+                // than 2^8 (P <= 256 stays exact enough in bf16, l and O share the same stale m), so
+                // the O rescale (a TMEM read-modify-write on the P -> PV critical path) is rare
+                const float pmx = pm * a.scale_log2;
+                const float mx = pmx > m + kLazyRescaleLog2 ? pmx : m;
                 const float alpha = ex2(m - mx);  // m = -inf on the first block -> 0
                 float s8[8];
 #pragma unroll
