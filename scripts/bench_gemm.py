@@ -26,7 +26,28 @@ def gemm_desc(m, n, k, A, a_mn, B, b_mn, Cm, epi):
     return d
 
 
+FLUSH = __import__("os").environ.get("PTK_FLUSH", "0") == "1"
+_flush_buf = None
+
+
 def timeit(fn, iters=20):
+    """Mean time per call. PTK_FLUSH=1: cold L2 — a 512 MB write between calls, each call timed alone."""
+    global _flush_buf
+    if FLUSH:
+        if _flush_buf is None:
+            _flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+        for _ in range(2):
+            fn()
+        tot = 0.0
+        for _ in range(iters):
+            _flush_buf.fill_(1)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize()
+            tot += s.elapsed_time(e)
+        return tot / iters * 1e-3
     for _ in range(3):
         fn()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -94,7 +115,7 @@ def main():
             continue
         A = torch.randn((k, m) if a_mn else (m, k), device=dev).bfloat16()
         B = torch.randn((k, n) if b_mn else (n, k), device=dev).bfloat16()
-        Cm = torch.zeros(m, n, device=dev, dtype=torch.float32 if epi == L.EPI_ACC_F32 else torch.bfloat16)
+        Cm = torch.zeros(m, n, device=dev, dtype=torch.float32 if epi in (L.EPI_F32, L.EPI_ACC_F32) else torch.bfloat16)
         d = gemm_desc(m, n, k, A, a_mn, B, b_mn, Cm, epi)
         keep = []
         if bias:
