@@ -52,6 +52,9 @@ def parse():
     p.add_argument("--mem-cap-gb", type=float, default=0.0,
                    help="imposed per-GPU memory limit: candidates = the (k, b) frontier under it (config 4)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-wgrad-pairs", action="store_true",
+                   help="one weight-gradient GEMM per micro-batch (default: two-K-segment pairs; always off "
+                        "under --mem-cap-gb, whose candidate frontier does not budget the pairing buffers)")
     p.add_argument("--ref-stages", type=int, default=1,
                    help="--impl reference: S > 1 runs the CPU-thread pipeline executor (S stage threads, "
                         "S micro-batches per step, oracle/cpu_pipeline.py); 1 = the whole model on all cores")
@@ -177,6 +180,9 @@ def main():
     if args.impl == "reference":
         return reference_arm(args)
 
+    # rank 0 prints exactly one JSON line on stdout: keep NCCL's version banner off it
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     import torch
     import torch.distributed as dist
 
@@ -220,7 +226,8 @@ def main():
     b_max = max(c[1] for c in cands)
     slots = max(max_inflight(rank, S, c[2], c[0]) * c[1] for c in cands) // b_max
     slots = max(slots, max(max_inflight(rank, S, c[2], c[0]) for c in cands if c[1] == b_max))
-    ex = StageExecutor(shape, rank, S, GB, b_max=b_max, slots=slots, halves=halves[rank])
+    wgrad_pairs = not args.no_wgrad_pairs and cap is None
+    ex = StageExecutor(shape, rank, S, GB, b_max=b_max, slots=slots, halves=halves[rank], wgrad_pairs=wgrad_pairs)
     ks = [c[0] for c in cands]
     b = cands[0][1]  # plan micro-batch size before tuning (the k=1 candidate)
     M = GB // b
@@ -269,6 +276,14 @@ def main():
             if k in by_k:
                 arm_reset()
                 fixed[k] = run(args.steps, by_k[k])
+        if wgrad_pairs and 1 in by_k:
+            # 1F1B also with one weight-gradient GEMM per micro-batch: pairing alternates short and
+            # long backwards, which 1F1B's strict F/B alternation cannot absorb; the arm reports the
+            # faster of the two (decided on the max-over-ranks times below)
+            ex.set_wgrad_pairs(False)
+            arm_reset()
+            fixed["1_unpaired"] = run(args.steps, by_k[1])
+            ex.set_wgrad_pairs(True)
 
     # ---- timed region: Ada-Grouper (tuning round at start, re-tune every `retune` steps)
     tuner = OnlineTuner(ex, rank, S, GB, [(c[0], c[1]) for c in cands], shape.seq * shape.hidden * 2,
@@ -327,6 +342,7 @@ def main():
 
     all_ms = gather(sum(ms) + tune_s * 1e3)
     all_1f1b = gather(sum(ms_1f1b))
+    all_1f1b_u = gather(sum(fixed["1_unpaired"])) if "1_unpaired" in fixed else None
     all_k2 = gather(sum(fixed.get(2, ms)))
     all_loss = gather(loss)
     all_e2e = gather(e2e_s)
@@ -342,6 +358,10 @@ def main():
     T = max(all_ms) / 1e3
     value = GB * args.steps / T
     v1f1b = GB * args.steps / (max(all_1f1b) / 1e3)
+    v1f1b_paired = v1f1b
+    v1f1b_unpaired = GB * args.steps / (max(all_1f1b_u) / 1e3) if all_1f1b_u else None
+    if v1f1b_unpaired is not None:
+        v1f1b = max(v1f1b, v1f1b_unpaired)
     vk2 = GB * args.steps / (max(all_k2) / 1e3)
     loss = all_loss[-1]
     pk, pk_kind = peaks()
@@ -367,11 +387,14 @@ def main():
                    "stages": S, "layers_per_stage": [(e - s_) / 2 for s_, e in halves],
                    "half_layer_ranges": [list(x) for x in halves],
                    "parallelism": f"pp{S}" if S > 1 else "single stage (no pipeline)",
+                   "wgrad_pairs": wgrad_pairs,
                    "schedule": (f"Ada-Grouper adaptive kFkB ((k, b) per step {plans_run})" if S > 1 else "1F1B (S=1)"),
                    "emulated_preemption": trace_desc, "l2": "working set (weights + activations) >> 126 MB L2"},
         "schedules": {"ada_grouper": {"kb_per_step": plans_run, "samples_per_s": round(value, 3),
                                       "tuning_overhead_s": round(tune_s, 4)},
-                      "1f1b": {"kbM": by_k.get(1), "samples_per_s": round(v1f1b, 3)},
+                      "1f1b": {"kbM": by_k.get(1), "samples_per_s": round(v1f1b, 3),
+                               "paired_wgrads_samples_per_s": round(v1f1b_paired, 3),
+                               "unpaired_wgrads_samples_per_s": round(v1f1b_unpaired, 3) if v1f1b_unpaired else None},
                       "kfkb_k2": {"kbM": by_k.get(2), "samples_per_s": round(vk2, 3)},
                       "speedup_vs_1f1b": round(value / v1f1b, 4)},
         "tuner_decisions": [{"chosen": d["chosen"], "switched": d["switched"],

@@ -77,6 +77,11 @@ typedef struct ptk_gemm_desc {
                           2 = CTA-pair tcgen05.mma.cta_group::2 (256x256 pair tile) */
     float* col_part;   /* optional, bf16 outputs, batch 1: fp32 [ceil(m/32)][n] += per-32-row-block column
                           sums of C as stored (fused bias-gradient partials) */
+    /* optional second K segment (k2 > 0): D = A Bᵀ + A2 B2ᵀ, one fp32 accumulation over k + k2
+     * (k % 64 == 0; same majors, batch 1, dense): the weight gradients of two micro-batches in one
+     * launch, so the fp32 gradient is read and written once per pair */
+    ptk_matrix a2, b2;
+    int k2;
 } ptk_gemm_desc;
 
 int ptk_gemm(const ptk_gemm_desc* desc, void* stream);
@@ -152,6 +157,12 @@ typedef struct ptk_gpt_config {
     /* half-layer stage boundaries (a layer = attention block + MLP block): */
     int skip_first_attn;   /* layer_begin's attention block is on the previous stage (input = its x_mid) */
     int skip_last_mlp;     /* layer_end-1's MLP block is on the next stage (output = its x_mid) */
+    /* 1: weight gradients of consecutive backward micro-batches are computed in pairs, one GEMM with
+     * two K segments per weight (the fp32 gradient is read and written once per pair).  The first
+     * micro-batch of a pair keeps its gradient-side operands in per-layer buffers and its stash slot
+     * stays live until the second one's backward, so the caller provides one more slot than the plan's
+     * in-flight peak.  An unpaired last micro-batch is flushed by finalize (GradAccum). */
+    int wgrad_pairs;
 } ptk_gpt_config;
 
 typedef struct ptk_stage ptk_stage;
@@ -232,6 +243,9 @@ ptk_stage* ptk_exec_stage(ptk_exec* ex);
  * calls ptk_stage_optimizer_step on that stream (ptk_exec_stage gives the stage). */
 int ptk_exec_set_defer_optimizer(ptk_exec* ex, int defer);
 int ptk_exec_compute_stream(ptk_exec* ex, void** stream);
+/* Paired weight gradients on/off for the following iterations (the stage must have been created
+ * with ptk_gpt_config.wgrad_pairs = 1; off = one weight-gradient GEMM per micro-batch). */
+int ptk_exec_set_wgrad_pairs(ptk_exec* ex, int on);
 
 #ifdef __cplusplus
 }

@@ -39,7 +39,7 @@ class GemmDesc(C.Structure):
         ("m", C.c_int), ("n", C.c_int), ("k", C.c_int), ("batch", C.c_int * 2),
         ("a", Matrix), ("b", Matrix), ("c", Matrix), ("c2", C.c_void_p), ("aux", Matrix),
         ("bias", C.c_void_p), ("epilogue", C.c_int), ("causal", C.c_int), ("bn_hint", C.c_int),
-        ("multicast", C.c_int), ("col_part", C.c_void_p),
+        ("multicast", C.c_int), ("col_part", C.c_void_p), ("a2", Matrix), ("b2", Matrix), ("k2", C.c_int),
     ]
 
 

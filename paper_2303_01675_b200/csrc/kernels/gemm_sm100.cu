@@ -531,7 +531,8 @@ template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
-                         const __grid_constant__ CUtensorMap tmC2, const __grid_constant__ GemmArgs args) {
+                         const __grid_constant__ CUtensorMap tmC2, const __grid_constant__ CUtensorMap tmA2,
+                         const __grid_constant__ CUtensorMap tmB2s, const __grid_constant__ GemmArgs args) {
     constexpr int S = k2smStages;
     constexpr int kHalf = 128 * kBK * 2;  // 16 KiB
     constexpr uint32_t kIdesc = make_idesc_bf16(256, 256, A_MN, B_MN);
@@ -588,19 +589,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
                     uint8_t* sa = smem + stage * k2smStageBytes;
                     uint8_t* sb = sa + kHalf;
-                    const int k0 = kb * kBK;
+                    // second K segment: the other micro-batch's operands (tmA2 / tmB2s)
+                    const bool seg2 = args.kb_split > 0 && kb >= args.kb_split;
+                    const int k0 = (seg2 ? kb - args.kb_split : kb) * kBK;
+                    const CUtensorMap* ma = seg2 ? &tmA2 : &tmA;
+                    const CUtensorMap* mb = seg2 ? &tmB2s : &tmB;
                     if (!A_MN) {
-                        tma_load_4d_2sm(&tmA, &full[stage], sa, k0, tc.m0, tc.z1, tc.z2);
+                        tma_load_4d_2sm(ma, &full[stage], sa, k0, tc.m0, tc.z1, tc.z2);
                     } else {
 #pragma unroll
                         for (int j = 0; j < 2; ++j)
-                            tma_load_4d_2sm(&tmA, &full[stage], sa + j * 64 * kBK * 2, tc.m0 + 64 * j, k0, tc.z1, tc.z2);
+                            tma_load_4d_2sm(ma, &full[stage], sa + j * 64 * kBK * 2, tc.m0 + 64 * j, k0, tc.z1, tc.z2);
                     }
                     if (!B_MN) {
-                        tma_load_4d_2sm(full_w ? &tmB : &tmB2, &full[stage], sb, k0, nrow, tc.z1, tc.z2);
+                        tma_load_4d_2sm(full_w ? mb : &tmB2, &full[stage], sb, k0, nrow, tc.z1, tc.z2);
                     } else {
                         for (int j = 0; j < (full_w ? 2 : 1); ++j)
-                            tma_load_4d_2sm(&tmB, &full[stage], sb + j * 64 * kBK * 2, nrow + 64 * j, k0, tc.z1, tc.z2);
+                            tma_load_4d_2sm(mb, &full[stage], sb + j * 64 * kBK * 2, nrow + 64 * j, k0, tc.z1, tc.z2);
                     }
                     if (++stage == S) {
                         stage = 0;
@@ -779,8 +784,8 @@ int launch_2sm(const GemmPlan& p, cudaStream_t stream) {
             return PTK_ERR_CUDA;
         attr_set = true;
     }
-    if (launch_kernel(kern, p.grid, kThreads, k2smSmem, stream, 2, p.tmA, p.tmB, p.tmB2, p.tmC, p.tmC2, p.args) !=
-        cudaSuccess)
+    if (launch_kernel(kern, p.grid, kThreads, k2smSmem, stream, 2, p.tmA, p.tmB, p.tmB2, p.tmC, p.tmC2, p.tmA2, p.tmB2s,
+                      p.args) != cudaSuccess)
         return PTK_ERR_CUDA;
     return cudaPeekAtLastError() == cudaSuccess ? PTK_OK : PTK_ERR_CUDA;
 }
@@ -820,7 +825,13 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     const int tiles_m = (d.m + kBM - 1) / kBM;
 
     int bn;
-    if (d.bn_hint == 64 || d.bn_hint == 128 || d.bn_hint == 256) {
+    if (d.k2 > 0) {
+        // two K segments: CTA-pair kernel only, dense, unbatched, segment boundary on a k-block
+        if (d.k % kBK != 0 || b1 * b2 != 1 || d.causal != PTK_CAUSAL_NONE || d.multicast != 2 || tiles_m < 2 ||
+            d.a2.mn_major != d.a.mn_major || d.b2.mn_major != d.b.mn_major || d.col_part != nullptr)
+            return PTK_ERR_ARG;
+        bn = 256;
+    } else if (d.bn_hint == 64 || d.bn_hint == 128 || d.bn_hint == 256) {
         bn = d.bn_hint;
     } else if (d.causal == PTK_CAUSAL_TILES) {
         bn = 128;
@@ -873,11 +884,22 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     } else {
         p.tmB2 = p.tmB;
     }
+    p.tmA2 = p.tmA;
+    p.tmB2s = p.tmB;
+    if (d.k2 > 0) {  // the second K segment's operands (same majors and boxes)
+        rc = !d.a2.mn_major ? encode_operand(&p.tmA2, d.a2, d.k2, d.m, kBM, 1, 1)
+                            : encode_operand(&p.tmA2, d.a2, d.m, d.k2, kBK, 1, 1);
+        if (rc != PTK_OK) return rc;
+        rc = !d.b2.mn_major ? encode_operand(&p.tmB2s, d.b2, d.k2, d.n, bn / 2, 1, 1)
+                            : encode_operand(&p.tmB2s, d.b2, d.n, d.k2, kBK, 1, 1);
+        if (rc != PTK_OK) return rc;
+    }
 
     GemmArgs& a = p.args;
     a.M = d.m;
     a.N = d.n;
-    a.K = d.k;
+    a.K = d.k + (d.k2 > 0 ? d.k2 : 0);
+    a.kb_split = d.k2 > 0 ? d.k / kBK : 0;
     a.batch1 = b1;
     a.bn = bn;
     a.tiles_m = tiles_m;
@@ -927,7 +949,7 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     // B-tile multicast across a 2-CTA cluster halves the L2 -> SM operand
     // traffic per FLOP (dense, non-causal GEMMs with at least two m-tiles).
     const bool mc = mc_pre;
-    p.flops = 2.0 * d.m * static_cast<double>(d.n) * d.k * b1 * b2;
+    p.flops = 2.0 * d.m * static_cast<double>(d.n) * a.K * b1 * b2;
     if (d.causal != PTK_CAUSAL_NONE) p.flops *= 0.5;
     a.full_tiles = 1 << 30;
     if (pair) {
@@ -937,7 +959,7 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
         a.num_tiles = tiles;
         a.full_tiles = tiles;
         const int rem = tiles % pairs;
-        if (tiles > pairs && rem > 0 && 2 * rem <= pairs && d.n % 256 == 0) {
+        if (tiles > pairs && rem > 0 && 2 * rem <= pairs && d.n % 256 == 0 && d.k2 <= 0) {
             // split the partial last wave into 256 x 128 halves: it then takes half as long
             a.full_tiles = tiles - rem;
             a.num_tiles = a.full_tiles + 2 * rem;

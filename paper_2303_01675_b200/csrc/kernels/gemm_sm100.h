@@ -23,7 +23,8 @@ struct GemmArgs {
     int tma_store;   // outputs leave through TMA stores (tmC / tmC2)
     float* col_part;  // optional [ceil(M/32)][N] += column sums of C per 32-row block
     int full_tiles;  // CTA-pair kernel: work items >= full_tiles are 256 x 128 halves of the tail tiles
-    int n_fast;      // tile raster: 0 = m-tiles fastest (B tile shared), 1 = n-tiles fastest (A tile shared)
+    int n_fast;
+    int kb_split;    // CTA-pair kernel: k-blocks >= kb_split come from the second K segment (tmA2 / tmB2s)      // tile raster: 0 = m-tiles fastest (B tile shared), 1 = n-tiles fastest (A tile shared)
 };
 
 struct GemmPlan {
@@ -33,6 +34,8 @@ struct GemmPlan {
     alignas(64) CUtensorMap tmB2;  // CTA-pair kernel, K-major B: box of 64 rows (half-width tail tiles)
     alignas(64) CUtensorMap tmC;   // output C: box {64 bf16 | 32 fp32, 32 rows}, 128B swizzle
     alignas(64) CUtensorMap tmC2;  // BIAS_GELU pre-activation output
+    alignas(64) CUtensorMap tmA2;  // second K segment (k2 > 0), CTA-pair kernel
+    alignas(64) CUtensorMap tmB2s;
     GemmArgs args;
     int grid = 0;
     double flops = 0.0;  // algorithmic FLOPs of one launch

@@ -198,6 +198,11 @@ extern "C" int ptk_exec_gemm_timing(ptk_exec* ex, int enable, double* total_flop
 
 extern "C" ptk_stage* ptk_exec_stage(ptk_exec* ex) { return ex ? &ex->stage_view : nullptr; }
 
+extern "C" int ptk_exec_set_wgrad_pairs(ptk_exec* ex, int on) {
+    if (ex == nullptr) return ptk::set_error(PTK_ERR_ARG, "ptk_exec_set_wgrad_pairs: null executor");
+    return guarded("ptk_exec_set_wgrad_pairs", [&] { ex->impl.stage().set_wgrad_pairs(on != 0); });
+}
+
 extern "C" int ptk_exec_set_defer_optimizer(ptk_exec* ex, int defer) {
     EX_CHECK(ex);
     return guarded("ptk_exec_set_defer_optimizer", [&] { ex->impl.set_defer_optimizer(defer != 0); });

@@ -238,6 +238,8 @@ void Executor::install_plan(int b, const std::vector<int>& group_sizes, int k) {
         if (kind == pipetune::TaskKind::ForwardCompute) peak = std::max(peak, ++live);
         if (kind == pipetune::TaskKind::BackwardCompute) --live;
     }
+    // paired weight gradients keep the previous micro-batch's slot live one backward longer
+    if (g.wgrad_pairs) ++peak;
     // slots are b_max samples wide: at b | b_max each holds b_max / b micro-batches
     const int vslots = g.slots * ((g.micro_batch_size % b == 0) ? g.micro_batch_size / b : 1);
     if (peak > vslots)
@@ -456,6 +458,10 @@ void Executor::profile_compute(int b, int repeats, int64_t* fwd_ns, int64_t* bwd
     ck(cudaEventCreate(&e1), "event");
     ck(cudaEventCreate(&e2), "event");
     double f = 0, bw = 0;
+    // one micro-batch at a time in one slot: profile with per-micro-batch weight gradients
+    const bool pairs = stage_->wgrad_pairs_on();
+    stage_->flush_wgrads(comp_);
+    stage_->set_wgrad_pairs(false);
     for (int r = 0; r < repeats + 1; ++r) {  // first round is warm-up
         ck(cudaEventRecord(e0, comp_), "event");
         stage_->forward(0, tok_dev_, xin, lab_dev_, xout, comp_);
@@ -476,6 +482,7 @@ void Executor::profile_compute(int b, int repeats, int64_t* fwd_ns, int64_t* bwd
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
     stage_->zero_grads(comp_);
+    stage_->set_wgrad_pairs(pairs);
     ck(cudaMemsetAsync(stage_->loss_accumulator(), 0, 4, comp_), "memset");
     ck(cudaStreamSynchronize(comp_), "sync");
     *fwd_ns = static_cast<int64_t>(f / repeats * 1e6 + 0.5);

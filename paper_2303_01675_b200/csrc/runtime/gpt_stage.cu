@@ -234,6 +234,29 @@ GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
     dqkv_ = static_cast<__nv_bfloat16*>(alloc(T * 3 * h * 2));
     dx_mid_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
     dy_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+    s_d_pre_ = d_pre_;
+    s_d_ln_ = d_ln_;
+    s_dqkv_ = dqkv_;
+    s_dx_mid_ = dx_mid_;
+    s_dy_ = dy_;
+    pairs_on_ = c.wgrad_pairs != 0;
+    if (c.wgrad_pairs) {
+        dbuf_.resize(L_);
+        for (int i = 0; i < L_; ++i) {
+            DeferBufs& d = dbuf_[i];
+            auto bf = [&](int64_t n) { return static_cast<__nv_bfloat16*>(alloc(n * 2)); };
+            d.out = bf(T * h);
+            d.d_pre = bf(T * f);
+            d.dx_mid = bf(T * h);
+            d.dqkv = bf(T * 3 * h);
+            d.d_ln = bf(T * h);
+            d.dy = bf(T * h);
+        }
+        if (c.has_head) {
+            dhead_g_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+            dhead_dy_ = static_cast<__nv_bfloat16*>(alloc(T * h * 2));
+        }
+    }
     // 1-D parameter gradient partials (see vec_grad_finalize)
     {
         std::vector<VecGradSeg> segs;
@@ -355,6 +378,61 @@ void GptStage::gemm(ptk_gemm_desc d, cudaStream_t st) {
     if (gemm_run(p, st) != PTK_OK) throw std::runtime_error("gemm launch failed");
 }
 
+// Weight-gradient GEMM (fp32 accumulate into the gradient buffer).  With paired weight
+// gradients, the first micro-batch of a pair only records the descriptor (its operands stay
+// live: stash slot + per-layer deferral buffers); the second launches ONE GEMM with two K
+// segments, deferred micro-batch first, so the fp32 gradient is read and written once per
+// pair.  Pairs are (0,1), (2,3), ... in backward order, which is ascending for every plan, so
+// gradients stay bit-identical across k and stage splits.
+void GptStage::wgrad(const ptk_gemm_desc& d, cudaStream_t st) {
+    if (wg_mode_ == 1) {
+        wg_pending_.push_back(d);
+        return;
+    }
+    if (wg_mode_ == 2) {
+        for (size_t i = 0; i < wg_pending_.size(); ++i) {
+            const ptk_gemm_desc& p = wg_pending_[i];
+            if (p.c.ptr != d.c.ptr) continue;
+            ptk_gemm_desc two = p;
+            two.a2 = d.a;
+            two.b2 = d.b;
+            two.k2 = d.k;
+            wg_pending_.erase(wg_pending_.begin() + static_cast<std::ptrdiff_t>(i));
+            gemm(two, st);
+            return;
+        }
+    }
+    gemm(d, st);
+}
+
+void GptStage::set_wgrad_pairs(bool on) {
+    if (on && !cfg_.wgrad_pairs) throw std::invalid_argument("set_wgrad_pairs: stage created without wgrad_pairs");
+    if (!wg_pending_.empty()) throw std::logic_error("set_wgrad_pairs: a deferred micro-batch is pending");
+    pairs_on_ = on;
+}
+
+void GptStage::flush_wgrads(cudaStream_t st) {
+    for (const ptk_gemm_desc& d : wg_pending_) gemm(d, st);
+    wg_pending_.clear();
+}
+
+void GptStage::use_scratch(int layer) {
+    if (layer < 0) {
+        d_pre_ = s_d_pre_;
+        d_ln_ = s_d_ln_;
+        dqkv_ = s_dqkv_;
+        dx_mid_ = s_dx_mid_;
+        dy_ = s_dy_;
+        return;
+    }
+    const DeferBufs& b = dbuf_[static_cast<size_t>(layer)];
+    d_pre_ = b.d_pre;
+    d_ln_ = b.d_ln;
+    dqkv_ = b.dqkv;
+    dx_mid_ = b.dx_mid;
+    dy_ = b.dy;
+}
+
 void GptStage::attention_forward(LayerStash& s, cudaStream_t st) {
     // fused attention (tcgen05): o = softmax(QKᵀ/√d [causal for GPT]) V, lse for the backward
     const ptk_gpt_config& c = cfg_;
@@ -373,7 +451,8 @@ void GptStage::attention_backward(LayerStash& s, cudaStream_t st) {
     // dqkv = flash backward (dK/dV per key block, dQ per query block; deterministic)
     const ptk_gpt_config& c = cfg_;
     const int b = c.micro_batch_size, d = c.hidden / c.heads;
-    const std::string key = std::to_string(reinterpret_cast<uintptr_t>(s.qkv)) + "." + std::to_string(b);
+    const std::string key = std::to_string(reinterpret_cast<uintptr_t>(s.qkv)) + "." + std::to_string(b) + "." +
+                            std::to_string(reinterpret_cast<uintptr_t>(dqkv_));
     auto it = flash_bwd_.find(key);
     if (it == flash_bwd_.end()) {
         auto p = std::make_unique<FlashBwdPlan>();
@@ -451,14 +530,14 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
             g.col_part = vp(w.b_fc1);
             gemm(g, st);
         }
-        gemm(desc(h, f, T, mat(d_ln_, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
+        wgrad(desc(h, f, T, mat(d_ln_, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
         __nv_bfloat16* out = A ? dx_mid_ : dx;  // an MLP-only first layer hands d(x_mid) to the previous stage
         {  // d_xmid = d_pre W1 + dz   (residual around the FFN)
             ptk_gemm_desc g = desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(out, h), PTK_EPI_BF16);
             g.aux = mat(d_ln_, h);
             gemm(g, st);
         }
-        gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(xm, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
+        wgrad(desc(f, h, T, mat(d_pre_, f, 1), mat(xm, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
         gxm = out;
     }
     if (A) {
@@ -467,9 +546,9 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
                             vp(w.b_o) /* dbo = Σ dy_, fused */, T, h, st),
            "ln1 bwd");
         gemm(desc(T, h, h, mat(dy_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
-        gemm(desc(h, h, T, mat(dy_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
+        wgrad(desc(h, h, T, mat(dy_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
         attention_backward(s, st);
-        gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.x_in, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
+        wgrad(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.x_in, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
         kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
         {  // dx = dqkv Wqkv + dy_   (residual around attention)
             ptk_gemm_desc g = desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(dx, h), PTK_EPI_BF16);
@@ -539,13 +618,13 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
             g.col_part = vp(w.b_fc1);
             gemm(g, st);
         }
-        gemm(desc(h, f, T, mat(dy, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
+        wgrad(desc(h, f, T, mat(dy, h, 1), mat(s.fc1_act, f, 1), mat(G + w.w_fc2, f), PTK_EPI_ACC_F32), st);
         // db2 = Σ dy: fused into the LayerNorm backward that produced dy (the next layer's LN1 or the
         // head's final LN), except for the last layer of a stage whose dy arrives from the next stage
         if (li == L_ - 1 && !c.has_head) kl(1, colsum_partial(dy, vp(w.b_fc2), T, h, st), "db2");
         // FC1: d_ln2 = d_pre W1; dW1 += d_preᵀ ln2
         gemm(desc(T, h, f, mat(d_pre_, f), mat(W + w.w_fc1, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
-        gemm(desc(f, h, T, mat(d_pre_, f, 1), mat(s.ln2, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
+        wgrad(desc(f, h, T, mat(d_pre_, f, 1), mat(s.ln2, h, 1), mat(G + w.w_fc1, h), PTK_EPI_ACC_F32), st);
         // LN2 backward + residual: d(x_mid) = LN2'(d_ln2) + dy; an MLP-only first layer hands it to the
         // previous stage, whose attention block then owns db_o
         __nv_bfloat16* out = A ? dx_mid_ : dx;
@@ -560,11 +639,11 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
     if (A) {
         // out-proj: d_attn = d(x_mid) Wo; dWo += d(x_mid)ᵀ o
         gemm(desc(T, h, h, mat(gxm, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
-        gemm(desc(h, h, T, mat(gxm, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
+        wgrad(desc(h, h, T, mat(gxm, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
         attention_backward(s, st);
         // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv += Σ dqkv
         gemm(desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
-        gemm(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
+        wgrad(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
         kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
         // LN1 backward + residual: dx = LN1'(d_ln1) + d(x_mid)
         kl(1, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, gxm, dx, vp(w.ln1_g), vp(w.ln1_b),
@@ -632,37 +711,46 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
     const __nv_bfloat16* W = wbf_;
     float* G = grad_;
     const __nv_bfloat16* g = dy;
+    wg_mode_ = pairs_on_ ? (wg_pending_.empty() ? 1 : 2) : 0;
+    const bool defer = wg_mode_ == 1;
+    // deferring: the head's gradient-side operands go to their own buffers
+    __nv_bfloat16* head_g = defer ? dhead_g_ : g_a_;
+    if (defer) dy_ = dhead_dy_;
     if (c.has_head) {
         HeadStash& hs = vhead_.at(static_cast<size_t>(slot));
         // dxf = dlogits W_head ; dW_head += dlogitsᵀ xf
         gemm(desc(T, h, c.vocab, mat(hs.dlogits, c.vocab), mat(W + w_head_, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
-        gemm(desc(c.vocab, h, T, mat(hs.dlogits, c.vocab, 1), mat(hs.xf, h, 1), mat(G + w_head_, h), PTK_EPI_ACC_F32),
-             st);
+        wgrad(desc(c.vocab, h, T, mat(hs.dlogits, c.vocab, 1), mat(hs.xf, h, 1), mat(G + w_head_, h), PTK_EPI_ACC_F32), st);
         if (bert()) {
             // dt = LN_h'(dxf); d_tpre = dt * gelu'(t_pre); dx_fin = d_tpre Wt; dWt += d_tpreᵀ x_fin
             kl(1, layernorm_bwd(d_ln_, hs.t_act, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, dx_mid_, vp(lnf_g_),
                                 vp(lnf_b_), nullptr, T, h, st),
                "lnh bwd");
             kl(1, dgelu_mul(dx_mid_, hs.t_pre, dy_, static_cast<int64_t>(T) * h, st), "dgelu");
-            gemm(desc(T, h, h, mat(dy_, h), mat(W + w_t_, h, 1), mat(g_a_, h), PTK_EPI_BF16), st);
-            gemm(desc(h, h, T, mat(dy_, h, 1), mat(hs.x_fin, h, 1), mat(G + w_t_, h), PTK_EPI_ACC_F32), st);
+            gemm(desc(T, h, h, mat(dy_, h), mat(W + w_t_, h, 1), mat(head_g, h), PTK_EPI_BF16), st);
+            wgrad(desc(h, h, T, mat(dy_, h, 1), mat(hs.x_fin, h, 1), mat(G + w_t_, h), PTK_EPI_ACC_F32), st);
             kl(1, colsum_partial(dy_, vp(b_t_), T, h, st), "dbt");
         } else {
-            kl(1, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, g_a_, vp(lnf_g_),
+            kl(1, layernorm_bwd(d_ln_, hs.x_fin, hs.meanf, hs.rstdf, W + lnf_g_, nullptr, head_g, vp(lnf_g_),
                                 vp(lnf_b_), L_ > 0 ? vp(lw_[L_ - 1].b_fc2) : nullptr /* last layer's db2 */, T, h,
                                 st),
                "lnf bwd");
         }
-        g = g_a_;
+        g = head_g;
     }
     for (int i = L_ - 1; i >= 0; --i) {
-        __nv_bfloat16* out = (i == 0 && !c.has_embedding) ? dx : (g == g_a_ ? g_b_ : g_a_);
+        __nv_bfloat16* out = (i == 0 && !c.has_embedding) ? dx
+                             : defer                        ? dbuf_[static_cast<size_t>(i)].out
+                                                            : (g == g_a_ ? g_b_ : g_a_);
+        if (defer) use_scratch(i);
         if (bert())
             bert_layer_backward(i, S[i], g, out, st);
         else
             layer_backward(i, S[i], g, out, st);
         g = out;
     }
+    if (defer) use_scratch(-1);
+    wg_mode_ = 0;
     if (c.has_embedding && bert()) {  // through the embedding LayerNorm
         EmbStash& e = vemb_.at(static_cast<size_t>(slot));
         __nv_bfloat16* dsum_bf = (g == g_a_) ? g_b_ : g_a_;
@@ -685,6 +773,7 @@ float* GptStage::vp(int64_t offset) {
 }
 
 void GptStage::finalize_grads(cudaStream_t st) {
+    flush_wgrads(st);
     kl(1, vec_grad_finalize(vsegs_, nvseg_, vseg_max_cols_, st), "finalize grads");
 }
 
@@ -708,6 +797,7 @@ void GptStage::collect_timing() {
 }
 
 void GptStage::zero_grads(cudaStream_t st) {
+    wg_pending_.clear();
     ck(cudaMemsetAsync(grad_, 0, total_ * 4, st), "zero grads");
     for (const auto& kv : vparts_) {
         const ParamInfo* p = nullptr;

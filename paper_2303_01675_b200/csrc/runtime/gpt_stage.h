@@ -68,6 +68,11 @@ class GptStage {
     // Folds the 1-D parameter partials of the micro-batches run so far into
     // grads() (one launch; idempotent).  optimizer_step() calls it first.
     void finalize_grads(cudaStream_t st);
+    // Paired weight gradients: runs the deferred micro-batch's weight-gradient GEMMs alone.
+    void flush_wgrads(cudaStream_t st);
+    // Runtime switch (buffers exist only if the stage was created with cfg.wgrad_pairs).
+    void set_wgrad_pairs(bool on);
+    bool wgrad_pairs_on() const { return pairs_on_; }
     void optimizer_step(float lr, float wd, cudaStream_t st);
     void zero_grads(cudaStream_t st);
 
@@ -166,6 +171,21 @@ class GptStage {
     float *dsum_ = nullptr, *loss_rows_ = nullptr, *loss_acc_ = nullptr;
     __nv_bfloat16 *g_a_ = nullptr, *g_b_ = nullptr, *d_pre_ = nullptr, *d_ln_ = nullptr,
                   *d_attn_ = nullptr, *dqkv_ = nullptr, *dx_mid_ = nullptr, *dy_ = nullptr;
+    // paired weight gradients (cfg.wgrad_pairs): the deferred micro-batch's gradient-side
+    // operands live in per-layer buffers (the scratch pointers are switched to them while it runs)
+    struct DeferBufs {
+        __nv_bfloat16 *out = nullptr, *d_pre = nullptr, *dx_mid = nullptr, *dqkv = nullptr, *d_ln = nullptr,
+                      *dy = nullptr;
+    };
+    std::vector<DeferBufs> dbuf_;
+    __nv_bfloat16 *dhead_g_ = nullptr, *dhead_dy_ = nullptr;
+    bool pairs_on_ = false;
+    int wg_mode_ = 0;                        // 0 direct, 1 deferring (first of a pair), 2 pairing (second)
+    std::vector<ptk_gemm_desc> wg_pending_;  // the deferred micro-batch's weight-gradient GEMMs
+    void wgrad(const ptk_gemm_desc& d, cudaStream_t st);
+    void use_scratch(int layer);             // layer >= 0: deferral buffers of that layer; -1: shared scratch
+    __nv_bfloat16 *s_d_pre_ = nullptr, *s_d_ln_ = nullptr, *s_dqkv_ = nullptr, *s_dx_mid_ = nullptr,
+                  *s_dy_ = nullptr;  // the shared scratch set
 
     // 1-D parameter gradient partials: grad offset -> float[kVecParts][cols]
     std::unordered_map<int64_t, float*> vparts_;

@@ -46,6 +46,7 @@ def _declare(lib):
     lib.ptk_exec_stage.argtypes = [V]
     lib.ptk_exec_stage.restype = C.c_void_p
     lib.ptk_exec_set_defer_optimizer.argtypes = [V, I]
+    lib.ptk_exec_set_wgrad_pairs.argtypes = [V, I]
     lib.ptk_exec_compute_stream.argtypes = [V, P(V)]
     lib._exec_declared = True
 
@@ -117,9 +118,10 @@ def max_inflight(stage: int, stages: int, micro_batches: int, k: int) -> int:
 class StageExecutor:
     def __init__(self, shape: ModelShape, stage: int, stages: int, global_batch: int, b_max: int, slots: int,
                  layers: tuple[int, int] | None = None, seed: int = 42, data_seed: int = 1234, lr: float = 1e-4,
-                 weight_decay: float = 0.0, halves: tuple[int, int] | None = None):
+                 weight_decay: float = 0.0, halves: tuple[int, int] | None = None, wgrad_pairs: bool = False):
         """`layers` = whole-layer range [lb, le); or `halves` = half-layer range [hb, he) (stage
-        boundaries may fall between a layer's attention and MLP blocks)."""
+        boundaries may fall between a layer's attention and MLP blocks).  `wgrad_pairs`: weight
+        gradients of consecutive micro-batches in one two-segment GEMM (one more stash slot)."""
         self.lib = L.lib()
         _declare(self.lib)
         from .stage import halves_to_layers
@@ -128,9 +130,11 @@ class StageExecutor:
         else:
             lb, le = layers if layers is not None else partition_layers(shape.n_layer, stages)[stage]
             sfa = slm = 0
+        if wgrad_pairs:
+            slots += 1  # the deferred micro-batch's stash stays live until its partner's backward
         gpt = GptConfig(shape.n_layer, shape.hidden, shape.heads, shape.ffn, shape.seq, shape.vocab, lb, le,
                         int(stage == 0), int(stage == stages - 1), b_max, slots, global_batch // b_max,
-                        shape.arch_id, seed, sfa, slm)
+                        shape.arch_id, seed, sfa, slm, int(wgrad_pairs))
         self.cfg = ExecConfig(gpt, stage, stages, global_batch, lr, weight_decay, data_seed)
         self.shape, self.stage, self.stages, self.global_batch = shape, stage, stages, global_batch
         h = C.c_void_p()
@@ -164,6 +168,10 @@ class StageExecutor:
     def set_defer_optimizer(self, on: bool = True):
         """GradAccum only finalizes the gradients; data_parallel_step() all-reduces and steps."""
         L.check(self.lib.ptk_exec_set_defer_optimizer(self.h, int(bool(on))))
+
+    def set_wgrad_pairs(self, on: bool):
+        """Paired weight gradients on/off from the next iteration (needs wgrad_pairs=True at creation)."""
+        L.check(self.lib.ptk_exec_set_wgrad_pairs(self.h, int(bool(on))))
 
     def compute_stream(self) -> int:
         s = C.c_void_p()

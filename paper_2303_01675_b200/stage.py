@@ -20,6 +20,7 @@ class GptConfig(C.Structure):
         ("vocab", C.c_int), ("layer_begin", C.c_int), ("layer_end", C.c_int), ("has_embedding", C.c_int),
         ("has_head", C.c_int), ("micro_batch_size", C.c_int), ("slots", C.c_int), ("micro_batches", C.c_int),
         ("arch", C.c_int), ("seed", C.c_uint64), ("skip_first_attn", C.c_int), ("skip_last_mlp", C.c_int),
+        ("wgrad_pairs", C.c_int),
     ]
 
 

@@ -103,6 +103,11 @@ def main():
         ("x_kk_f32", T, f, h, 0, 0, L.EPI_F32, 0, 0, 0),
         ("x_kk_acc", T, f, h, 0, 0, L.EPI_ACC_F32, 0, 0, 0),
         ("x_headw_f32", V, h, T, 1, 1, L.EPI_F32, 0, 0, 0),
+        # wgrads of two micro-batches fused along K (K = 2T): vs 2x the K = T launches
+        ("x_fc2_wgrad_2T", h, f, 2 * T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
+        ("x_fc1_wgrad_2T", f, h, 2 * T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
+        ("x_out_wgrad_2T", h, h, 2 * T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
+        ("x_qkv_wgrad_2T", 3 * h, h, 2 * T, 1, 1, L.EPI_ACC_F32, 0, 0, 0),
         ("x_headw_bf16", V, h, T, 1, 1, B_, 0, 0, 0),
         ("x_headw_kk_acc", V, h, T, 0, 0, L.EPI_ACC_F32, 0, 0, 0),
     ]

@@ -24,6 +24,9 @@ SHAPE = ModelShape(4, 1024, 16, 4096, 512, 8192)
 GB, B = 16, 2
 
 
+PAIRS = os.environ.get("PTK_WGRAD_PAIRS", "0") == "1"  # paired weight gradients on every arm
+
+
 def digests(ex):
     st = ex.stage_view()
     torch.cuda.synchronize()
@@ -37,9 +40,9 @@ def run_pipeline(rank, S, k, group, trace=False, iters=2, half_cuts=False):
     halves = [(0, 5), (5, 8)] if S == 2 else [(0, 3), (3, 4), (4, 7), (7, 8)]
     slots = max(max_inflight(rank, S, M, kk) for kk in (1, 2, 3, 4))
     if half_cuts:
-        ex = StageExecutor(SHAPE, rank, S, GB, b_max=B, slots=slots, halves=halves[rank], lr=1e-3)
+        ex = StageExecutor(SHAPE, rank, S, GB, b_max=B, slots=slots, halves=halves[rank], lr=1e-3, wgrad_pairs=PAIRS)
     else:
-        ex = StageExecutor(SHAPE, rank, S, GB, b_max=B, slots=slots, layers=layers[rank], lr=1e-3)
+        ex = StageExecutor(SHAPE, rank, S, GB, b_max=B, slots=slots, layers=layers[rank], lr=1e-3, wgrad_pairs=PAIRS)
     ex.connect_dist(group)
     if trace:
         for link in outgoing_links(rank, S):
@@ -80,7 +83,7 @@ def main():
         res[name] = {"digest": merged, "loss": allds[-1][1], "ms": [x[2] for x in allds],
                      "xfers": [x[3] for x in allds]}
     if rank == 0:
-        ref = StageExecutor(SHAPE, 0, 1, GB, b_max=B, slots=1, layers=(0, 4), lr=1e-3)
+        ref = StageExecutor(SHAPE, 0, 1, GB, b_max=B, slots=1, layers=(0, 4), lr=1e-3, wgrad_pairs=PAIRS)
         ref.set_plan(1, B)
         loss = None
         for it in range(2):
@@ -97,7 +100,7 @@ def main():
             "loss": {"1f1b": res["1f1b"]["loss"], "k2": res["k2"]["loss"], "paced": res["k2_paced"]["loss"],
                      "mixed": res["mixed"]["loss"], "single": loss},
             "ms": {k: v["ms"] for k, v in res.items()}, "xfers": {k: v["xfers"] for k, v in res.items()},
-            "n_params": len(single),
+            "n_params": len(single), "wgrad_pairs": PAIRS,
         }
         out["ok"] = all([out["k1_vs_k2_bit_identical"], out["paced_bit_identical"],
                          out["mixed_groups_bit_identical"], out["half_layer_cuts_bit_identical"],

@@ -19,12 +19,13 @@ p.add_argument("--mb", type=int, default=2)
 p.add_argument("--iters", type=int, default=2)
 p.add_argument("--model", choices=["gpt", "bert"], default="gpt")
 p.add_argument("--b", type=int, default=0, help="micro-batch size (default 2 GPT / 4 BERT)")
+p.add_argument("--pairs", type=int, default=1, help="paired weight gradients (two-segment wgrad GEMMs)")
 a = p.parse_args()
 if a.model == "bert":
     shape, b = ModelShape(a.layers, 1024, 16, 4096, 512, 30528, "bert"), a.b or 4
 else:
     shape, b = ModelShape(a.layers, 2048, 32, 8192, 1024, 50304), a.b or 2
-ex = StageExecutor(shape, 0, 1, b * a.mb, b_max=b, slots=1, layers=(0, a.layers))
+ex = StageExecutor(shape, 0, 1, b * a.mb, b_max=b, slots=1, layers=(0, a.layers), wgrad_pairs=bool(a.pairs))
 for i in range(a.iters):
     t0 = time.perf_counter()
     ex.run_iteration(i)

@@ -236,3 +236,29 @@ def test_gemm_plan_info(cuda):
     assert items == (tiles - rem + 2 * rem if 2 * rem <= sms // 2 else tiles)
     assert plan(2048, 64, 512, 0)[0] == 64
     assert plan(256, 128, 512, 0)[:2] == [128, 2]
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(1, 1), (0, 0), (0, 1)])
+@pytest.mark.parametrize("epi", [L.EPI_ACC_F32, L.EPI_BF16])
+def test_gemm_two_k_segments(cuda, a_mn, b_mn, epi):
+    """k2 > 0: D = A Bᵀ + A2 B2ᵀ in one fp32 accumulation (the paired weight gradients of two
+    micro-batches: MN-major [T][m] / [T][n] operands from two separate buffers)."""
+    m, n, k, k2 = 1024, 1536, 512, 768
+    torch.manual_seed(a_mn * 4 + b_mn + epi)
+    mats = []
+    for kk in (k, k2):
+        A = torch.randn(m, kk).bfloat16()
+        B = torch.randn(n, kk).bfloat16()
+        mats.append((A, B, (A.T.contiguous() if a_mn else A).to(cuda), (B.T.contiguous() if b_mn else B).to(cuda)))
+    ref = sum(A.double() @ B.double().T for A, B, _, _ in mats).float()
+    f32 = epi == L.EPI_ACC_F32
+    C = torch.ones(m, n, device=cuda) if f32 else torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    (_, _, A1, B1), (_, _, A2, B2) = mats
+    d = _desc(m, n, k, L.matrix(A1.data_ptr(), m if a_mn else k, a_mn), L.matrix(B1.data_ptr(), n if b_mn else k, b_mn),
+              L.matrix(C.data_ptr(), n), epi=epi, mc=2)
+    d.a2 = L.matrix(A2.data_ptr(), m if a_mn else k2, a_mn)
+    d.b2 = L.matrix(B2.data_ptr(), n if b_mn else k2, b_mn)
+    d.k2 = k2
+    _run(d)
+    torch.cuda.synchronize()
+    _close(C, ref + 1.0 if f32 else ref, tol=1e-4 if f32 else 1.5e-2)

@@ -195,3 +195,49 @@ def test_mixed_group_plan_bit_identical_to_uniform(cuda):
         ex.close()
     for n in digests[0]:
         assert torch.equal(digests[0][n], digests[1][n]), n
+
+
+def _first_iteration_grads(shape, M, k, pairs, b=1, groups=None, layers=None):
+    from paper_2303_01675_b200.executor import StageExecutor, max_inflight
+    slots = max_inflight(0, 1, M, k)
+    ex = StageExecutor(shape, 0, 1, M * b, b_max=b, slots=max(slots, 3), layers=layers or (0, shape.n_layer),
+                       wgrad_pairs=pairs)
+    if groups is None:
+        ex.set_plan(k, b)
+    else:
+        ex.set_plan_groups(b, groups)
+    ex.set_defer_optimizer(True)  # GradAccum only finalizes: the accumulated gradients stay readable
+    ex.run_iteration(0)
+    ex.finish_iteration()
+    st = ex.stage_view()
+    torch.cuda.synchronize()
+    g = {n: st.param(n, "grads").cpu().clone() for n in st.params}
+    ex.close()
+    return g
+
+
+@pytest.mark.parametrize("shape", [ModelShape(2, 256, 4, 1024, 128, 512),
+                                   ModelShape(2, 256, 4, 1024, 128, 512, "bert")], ids=["gpt", "bert"])
+@pytest.mark.parametrize("M", [4, 5])
+def test_wgrad_pairs_match_unpaired(cuda, shape, M):
+    """Paired weight gradients (two micro-batches per two-K-segment GEMM, the odd one flushed at
+    GradAccum) equal the per-micro-batch accumulation up to fp32 summation order, and leave the
+    1-D (bias / LayerNorm) gradients bit-identical."""
+    g0 = _first_iteration_grads(shape, M, 1, False)
+    g1 = _first_iteration_grads(shape, M, 1, True)
+    for n in g0:
+        if g0[n].dim() == 1 or g0[n].shape[0] == 1:
+            assert torch.equal(g0[n], g1[n]), n
+        else:
+            assert _rel(g1[n], g0[n]) < 1e-5, n
+
+
+def test_wgrad_pairs_bit_identical_across_k(cuda):
+    """Pairs are formed in backward order, ascending for every plan: with paired weight gradients
+    the accumulated gradients are still bit-identical across k and mixed group plans."""
+    shape = ModelShape(2, 256, 4, 1024, 128, 512)
+    ref = _first_iteration_grads(shape, 6, 1, True)
+    for k, groups in ((2, None), (3, None), (6, None), (1, [1, 2, 3])):
+        g = _first_iteration_grads(shape, 6, k, True, groups=groups)
+        for n in ref:
+            assert torch.equal(ref[n], g[n]), (k, groups, n)
