@@ -409,11 +409,13 @@ void GptStage::set_wgrad_pairs(bool on) {
     if (on && !cfg_.wgrad_pairs) throw std::invalid_argument("set_wgrad_pairs: stage created without wgrad_pairs");
     if (!wg_pending_.empty()) throw std::logic_error("set_wgrad_pairs: a deferred micro-batch is pending");
     pairs_on_ = on;
+    wg_count_ = 0;
 }
 
 void GptStage::flush_wgrads(cudaStream_t st) {
     for (const ptk_gemm_desc& d : wg_pending_) gemm(d, st);
     wg_pending_.clear();
+    wg_count_ = 0;
 }
 
 void GptStage::use_scratch(int layer) {
@@ -711,11 +713,24 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
     const __nv_bfloat16* W = wbf_;
     float* G = grad_;
     const __nv_bfloat16* g = dy;
-    wg_mode_ = pairs_on_ ? (wg_pending_.empty() ? 1 : 2) : 0;
-    const bool defer = wg_mode_ == 1;
-    // deferring: the head's gradient-side operands go to their own buffers
-    __nv_bfloat16* head_g = defer ? dhead_g_ : g_a_;
-    if (defer) dy_ = dhead_dy_;
+    // Paired weight gradients, balanced: layers of even global index pair backwards (0,1), (2,3),
+    // ... and layers of odd index (1,2), (3,4), ... (0 and an unpaired last one run alone), the head
+    // counting as layer n_layer.  Every backward then defers about half of the weight gradients and
+    // runs the other half as pairs, so consecutive backwards cost the same (1F1B's strict F/B
+    // alternation would otherwise see alternating short and long backwards).  Pairs depend only on
+    // the backward count, ascending for every plan: bit-identical across k and stage splits.
+    const int n = wg_count_++;
+    auto mode_of = [&](int global_layer) -> int {
+        if (!pairs_on_) return 0;
+        const bool odd = (global_layer & 1) != 0;
+        if (odd ? (n & 1) != 0 : (n & 1) == 0) return 1;  // this backward defers the layer
+        return (!odd || n >= 2) ? 2 : 0;                   // pair with the deferred one (odd layers: none at n = 0)
+    };
+    wg_mode_ = mode_of(c.n_layer);
+    // the top layer's input gradient is an operand of its (deferred) FC2 weight gradient
+    const bool top_defers = L_ > 0 && mode_of(c.layer_begin + L_ - 1) == 1;
+    __nv_bfloat16* head_g = top_defers ? dhead_g_ : g_a_;
+    if (wg_mode_ == 1) dy_ = dhead_dy_;  // the head's own deferred operand (BERT transform)
     if (c.has_head) {
         HeadStash& hs = vhead_.at(static_cast<size_t>(slot));
         // dxf = dlogits W_head ; dW_head += dlogitsᵀ xf
@@ -738,18 +753,22 @@ void GptStage::backward(int slot, const int32_t* tok, const __nv_bfloat16* dy, _
         }
         g = head_g;
     }
+    if (pairs_on_) use_scratch(-1);
     for (int i = L_ - 1; i >= 0; --i) {
+        wg_mode_ = mode_of(c.layer_begin + i);
+        // layer i's output gradient feeds layer i-1's FC2 weight gradient: persistent if that one defers
+        const bool consumer_defers = i > 0 && mode_of(c.layer_begin + i - 1) == 1;
         __nv_bfloat16* out = (i == 0 && !c.has_embedding) ? dx
-                             : defer                        ? dbuf_[static_cast<size_t>(i)].out
+                             : consumer_defers              ? dbuf_[static_cast<size_t>(i)].out
                                                             : (g == g_a_ ? g_b_ : g_a_);
-        if (defer) use_scratch(i);
+        if (pairs_on_) use_scratch(wg_mode_ == 1 ? i : -1);
         if (bert())
             bert_layer_backward(i, S[i], g, out, st);
         else
             layer_backward(i, S[i], g, out, st);
         g = out;
     }
-    if (defer) use_scratch(-1);
+    if (pairs_on_) use_scratch(-1);
     wg_mode_ = 0;
     if (c.has_embedding && bert()) {  // through the embedding LayerNorm
         EmbStash& e = vemb_.at(static_cast<size_t>(slot));
@@ -798,6 +817,7 @@ void GptStage::collect_timing() {
 
 void GptStage::zero_grads(cudaStream_t st) {
     wg_pending_.clear();
+    wg_count_ = 0;
     ck(cudaMemsetAsync(grad_, 0, total_ * 4, st), "zero grads");
     for (const auto& kv : vparts_) {
         const ParamInfo* p = nullptr;

@@ -181,6 +181,7 @@ class GptStage {
     __nv_bfloat16 *dhead_g_ = nullptr, *dhead_dy_ = nullptr;
     bool pairs_on_ = false;
     int wg_mode_ = 0;                        // 0 direct, 1 deferring (first of a pair), 2 pairing (second)
+    int wg_count_ = 0;                       // backwards since the last flush (pairing phase)
     std::vector<ptk_gemm_desc> wg_pending_;  // the deferred micro-batch's weight-gradient GEMMs
     void wgrad(const ptk_gemm_desc& d, cudaStream_t st);
     void use_scratch(int layer);             // layer >= 0: deferral buffers of that layer; -1: shared scratch
