@@ -523,6 +523,7 @@ struct BwCfg {
 
 struct BwArgs {
     __nv_bfloat16* dqkv;  // [b*s][3h]
+    float* col_part;      // optional [b*s/32][3h] += column sums of dqkv per 32 rows
     const float* lse;     // [b][H][s]
     const float* dsum;    // [b][H][s]
     int s, H, h, b;
@@ -908,6 +909,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                     u.w = pack_bf16(v[g * 8 + 6], v[g * 8 + 7]);
                     *reinterpret_cast<uint4*>(dst + cc * 32 + g * 8) = u;
                 }
+                if (a.col_part != nullptr) {
+                    // QKV bias gradient: column sums of the warp's 32 rows of dqkv as stored.  A
+                    // reduce-scatter over the lanes (fixed xor order) leaves column `lane` in x[0].
+                    float x[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) x[e] = __bfloat162float(__float2bfloat16(v[e]));
+#pragma unroll
+                    for (int k = 16; k >= 1; k >>= 1) {
+                        const bool upper = (lane & static_cast<uint32_t>(k)) != 0;
+#pragma unroll
+                        for (int i = 0; i < k; ++i) {
+                            const float send = upper ? x[i] : x[i + k];
+                            const float keep = upper ? x[i + k] : x[i];
+                            x[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+                        }
+                    }
+                    const int64_t prow = (static_cast<int64_t>(c.bi) * a.s + c.blk * kBlk + (r & ~31)) / 32;
+                    const int64_t col = (dst - base) + c.head * D + cc * 32 + lane;
+                    a.col_part[prow * (3 * a.h) + col] += x[0];
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -988,7 +1009,7 @@ cudaError_t launch_bwd(const FlashBwdPlan& p, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    BwArgs a{p.dqkv, p.lse, p.dsum, p.s, p.H, p.H * p.d, p.b, p.scale_log2, 1.f / sqrtf(static_cast<float>(p.d)),
+    BwArgs a{p.dqkv, p.col_part, p.lse, p.dsum, p.s, p.H, p.H * p.d, p.b, p.scale_log2, 1.f / sqrtf(static_cast<float>(p.d)),
              p.causal};
     const int tiles = p.s / kBlk * p.H * p.b;
     const int grid = tiles < sm_count() ? tiles : sm_count();

@@ -33,6 +33,9 @@ struct FlashBwdPlan {
     int b = 0, s = 0, H = 0, d = 0;
     float scale_log2 = 0.f;
     int causal = 1;
+    // optional fp32 [b*s/32][3*H*d]: += per-32-row column sums of dqkv as stored (the QKV bias
+    // gradient, fused into the dQ / dK / dV epilogues; one owner per entry, fixed order)
+    float* col_part = nullptr;
 };
 
 // dqkv (all three sections) from qkv, the forward output o, its gradient dO and lse.

@@ -449,7 +449,7 @@ void GptStage::attention_forward(LayerStash& s, cudaStream_t st) {
     kl(1, flash_forward(*it->second, st), "flash fwd");
 }
 
-void GptStage::attention_backward(LayerStash& s, cudaStream_t st) {
+void GptStage::attention_backward(LayerStash& s, float* bqkv_part, cudaStream_t st) {
     // dqkv = flash backward (dK/dV per key block, dQ per query block; deterministic)
     const ptk_gpt_config& c = cfg_;
     const int b = c.micro_batch_size, d = c.hidden / c.heads;
@@ -461,6 +461,7 @@ void GptStage::attention_backward(LayerStash& s, cudaStream_t st) {
         ck(flash_bwd_prepare(s.qkv, s.attn_o, d_attn_, s.lse, dsum_, dqkv_, b, c.seq, c.heads, d, p.get(),
                              bert() ? 0 : 1),
            "flash bwd prep");
+        p->col_part = bqkv_part;  // dbqkv = column sums of dqkv, fused into the dQ/dK/dV epilogues
         it = flash_bwd_.emplace(key, std::move(p)).first;
     }
     kl(3, flash_backward(*it->second, st), "flash bwd");
@@ -549,9 +550,8 @@ void GptStage::bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* d
            "ln1 bwd");
         gemm(desc(T, h, h, mat(dy_, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
         wgrad(desc(h, h, T, mat(dy_, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
-        attention_backward(s, st);
+        attention_backward(s, vp(w.b_qkv), st);
         wgrad(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.x_in, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
-        kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
         {  // dx = dqkv Wqkv + dy_   (residual around attention)
             ptk_gemm_desc g = desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(dx, h), PTK_EPI_BF16);
             g.aux = mat(dy_, h);
@@ -642,11 +642,10 @@ void GptStage::layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __
         // out-proj: d_attn = d(x_mid) Wo; dWo += d(x_mid)ᵀ o
         gemm(desc(T, h, h, mat(gxm, h), mat(W + w.w_o, h, 1), mat(d_attn_, h), PTK_EPI_BF16), st);
         wgrad(desc(h, h, T, mat(gxm, h, 1), mat(s.attn_o, h, 1), mat(G + w.w_o, h), PTK_EPI_ACC_F32), st);
-        attention_backward(s, st);
-        // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv += Σ dqkv
+        attention_backward(s, vp(w.b_qkv), st);
+        // QKV: d_ln1 = dqkv Wqkv; dWqkv += dqkvᵀ ln1; dbqkv = Σ dqkv (fused in the flash backward)
         gemm(desc(T, h, 3 * h, mat(dqkv_, 3 * h), mat(W + w.w_qkv, h, 1), mat(d_ln_, h), PTK_EPI_BF16), st);
         wgrad(desc(3 * h, h, T, mat(dqkv_, 3 * h, 1), mat(s.ln1, h, 1), mat(G + w.w_qkv, h), PTK_EPI_ACC_F32), st);
-        kl(1, colsum_partial(dqkv_, vp(w.b_qkv), T, 3 * h, st), "dbqkv");
         // LN1 backward + residual: dx = LN1'(d_ln1) + d(x_mid)
         kl(1, layernorm_bwd(d_ln_, s.x_in, s.mean1, s.rstd1, W + w.ln1_g, gxm, dx, vp(w.ln1_g), vp(w.ln1_b),
                             li > 0 ? vp(lw_[li - 1].b_fc2) : nullptr /* previous layer's db2 */, T, h, st),

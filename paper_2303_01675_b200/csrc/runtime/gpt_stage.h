@@ -126,7 +126,7 @@ class GptStage {
     void bert_layer_forward(int li, LayerStash& s, const __nv_bfloat16* x_in, __nv_bfloat16* x_out, cudaStream_t st);
     void bert_layer_backward(int li, LayerStash& s, const __nv_bfloat16* dy, __nv_bfloat16* dx, cudaStream_t st);
     void attention_forward(LayerStash& s, cudaStream_t st);
-    void attention_backward(LayerStash& s, cudaStream_t st);
+    void attention_backward(LayerStash& s, float* bqkv_part, cudaStream_t st);
 
     struct InitSpec {
         int64_t offset, numel;
