@@ -27,6 +27,7 @@
 
 #include <mutex>
 
+#include "../runtime/preload.h"
 #include "attention_sm100.h"
 #include "launch.cuh"
 #include "sm100_ptx.cuh"
@@ -1050,6 +1051,10 @@ cudaError_t flash_backward(const FlashBwdPlan& p, cudaStream_t st) {
     e = p.d == 64 ? launch_bwd<64, true>(p, st) : launch_bwd<128, true>(p, st);
     if (e != cudaSuccess) return e;
     return p.d == 64 ? launch_bwd<64, false>(p, st) : launch_bwd<128, false>(p, st);
+}
+
+void preload_attention_kernels() {
+    preload_module_of(reinterpret_cast<const void*>(&flash_fwd_kernel<64, kFwdNQ>));
 }
 
 }  // namespace ptk

@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <mutex>
 
+#include "../runtime/preload.h"
 #include "../../../include/ptk.h"
 #include "gemm_sm100.h"
 #include "launch.cuh"
@@ -987,5 +988,7 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
 }
 
 int gemm_run(const GemmPlan& p, cudaStream_t stream) { return p.launch(p, stream); }
+
+void preload_gemm_kernels() { preload_module_of(reinterpret_cast<const void*>(&gemm_bf16_2sm_kernel<false, false>)); }
 
 }  // namespace ptk

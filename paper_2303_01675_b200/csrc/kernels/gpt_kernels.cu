@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "../runtime/preload.h"
 #include "gpt_kernels.h"
 #include "launch.cuh"
 
@@ -814,5 +815,7 @@ cudaError_t cast_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaSt
     launch_kernel(cast_bf16_kernel, grid_for(n, 256), 256, 0, st, 1, src, dst, n);
     return cudaPeekAtLastError();
 }
+
+void preload_gpt_kernels() { preload_module_of(reinterpret_cast<const void*>(&colsum_kernel)); }
 
 }  // namespace ptk

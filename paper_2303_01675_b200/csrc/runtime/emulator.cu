@@ -1,4 +1,5 @@
 // Preemption emulator: trace-paced transfers + contender traffic (emulator.h).
+#include "preload.h"
 #include "emulator.h"
 
 #include <algorithm>
@@ -220,5 +221,7 @@ int64_t device_globaltimer(cudaStream_t st) {
     cudaFree(d);
     return h;
 }
+
+void preload_emulator_kernels() { preload_module_of(reinterpret_cast<const void*>(&gate_kernel)); }
 
 }  // namespace ptk

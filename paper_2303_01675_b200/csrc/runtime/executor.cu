@@ -1,5 +1,6 @@
 // kFkB stage executor — see executor.h.
 #include "executor.h"
+#include "preload.h"
 
 #include <cuda.h>
 
@@ -69,8 +70,10 @@ constexpr size_t kHandle = sizeof(cudaIpcMemHandle_t);
 Executor::Executor(const ptk_exec_config& c) : cfg_(c) {
     if (c.stages < 1 || c.stage < 0 || c.stage >= c.stages || c.global_batch < 1)
         throw std::invalid_argument("Executor: bad stage / global batch");
+    preload_all_kernels();  // no lazy module loading behind another stage's waiting streams
     int lo = 0, hi = 0;
     ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priorities");
+    if (std::getenv("PTK_FLAT_PRIORITY") != nullptr) hi = lo;  // diagnostics: all streams at one priority
     ck(cudaStreamCreateWithPriority(&comp_, cudaStreamNonBlocking, hi), "stream");
     ck(cudaStreamCreateWithPriority(&sendst_, cudaStreamNonBlocking, lo), "stream");
     ck(cudaStreamCreateWithPriority(&contend_[0], cudaStreamNonBlocking, lo), "stream");

@@ -10,6 +10,7 @@
 // place (fp32, β = 1) in the order micro-batches are run — ascending on every
 // device for every k, so gradients are bit-identical across k at fixed b.
 #include "gpt_stage.h"
+#include "preload.h"
 
 #include <cmath>
 #include <cstring>
@@ -87,6 +88,7 @@ int64_t GptStage::add_param(const std::string& name, int64_t rows, int64_t cols,
 }
 
 GptStage::GptStage(const ptk_gpt_config& c) : cfg_(c) {
+    preload_all_kernels();
     const int h = c.hidden, f = c.ffn, V = c.vocab;
     if (h % 256 || c.heads <= 0 || h % c.heads || (h / c.heads) % 64 || c.seq % 128 || f % 64 || V % 64)
         throw std::invalid_argument("GptStage: unsupported shape (h%256, d%64, seq%128, ffn%64, vocab%64)");

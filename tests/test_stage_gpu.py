@@ -241,3 +241,32 @@ def test_wgrad_pairs_bit_identical_across_k(cuda):
         g = _first_iteration_grads(shape, 6, k, True, groups=groups)
         for n in ref:
             assert torch.equal(ref[n], g[n]), (k, groups, n)
+
+
+@pytest.mark.timeout(180)
+def test_two_stages_one_process_one_gpu(cuda):
+    """Two pipeline stages in one process on one GPU (same-process peers), each waiting on the
+    other's arrival flags.  Regression: with CUDA's lazy module loading the first launch of a
+    kernel serialised behind the other stage's waiting stream and the iteration deadlocked;
+    the library now loads all its kernels eagerly (runtime/preload.cu).  Stage 1 is enqueued
+    first on purpose.  The result must equal the one-stage run bit for bit."""
+    from paper_2303_01675_b200.executor import StageExecutor
+    from paper_2303_01675_b200.stage import TOY
+    e0 = StageExecutor(TOY, 0, 2, 8, b_max=2, slots=4, layers=(0, 2))
+    e1 = StageExecutor(TOY, 1, 2, 8, b_max=2, slots=4, layers=(2, 4))
+    e0.connect_local(1, e1)
+    e1.connect_local(0, e0)
+    for e in (e0, e1):
+        e.set_plan(2, 2)
+    e1.run_iteration(0)
+    e0.run_iteration(0)
+    e1.finish_iteration()
+    e0.finish_iteration()
+    loss = e1.read_loss()
+    ref = StageExecutor(TOY, 0, 1, 8, b_max=2, slots=4, layers=(0, 4))
+    ref.set_plan(2, 2)
+    ref.run_iteration(0)
+    ref.finish_iteration()
+    assert loss == ref.read_loss()
+    for e in (e0, e1, ref):
+        e.close()
