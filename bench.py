@@ -224,7 +224,8 @@ def main():
     cands = candidate_set(shape, halves, S, GB, cap, fixed_b=args.micro_batch, halves=True) if S > 1 else \
         [[1, args.micro_batch, GB // args.micro_batch]]
     b_max = max(c[1] for c in cands)
-    slots = max(max_inflight(rank, S, c[2], c[0]) * c[1] for c in cands) // b_max
+    # physical slots are b_max samples wide: enough of them for every candidate's in-flight samples
+    slots = -(-max(max_inflight(rank, S, c[2], c[0]) * c[1] for c in cands) // b_max)
     slots = max(slots, max(max_inflight(rank, S, c[2], c[0]) for c in cands if c[1] == b_max))
     wgrad_pairs = not args.no_wgrad_pairs and cap is None
     ex = StageExecutor(shape, rank, S, GB, b_max=b_max, slots=slots, halves=halves[rank], wgrad_pairs=wgrad_pairs)
