@@ -41,7 +41,11 @@ namespace {
 constexpr int kBlk = 128;      // query rows and key rows per block
 constexpr int kThreads = 384;  // backward: 12 warps: TMA, MMA, 2 idle, 8 row-parallel elementwise warps
 constexpr int kFwdNQ = 2;      // forward: softmax rows split in kFwdNQ column parts (4 + 4·NQ warps)
-constexpr float kLazyRescaleLog2 = 8.f;  // forward: move the running max only when it grows by > 2^8
+constexpr float kLazyRescaleLog2 = 8.f;
+#ifndef PTK_BW_POLY
+#define PTK_BW_POLY 2
+#endif
+constexpr int kBwPoly = PTK_BW_POLY;  // backward: exponentials per 32 on the FMA pipe (0, 1, 2, 4 or 8)  // forward: move the running max only when it grows by > 2^8
 
 int sm_count() {
     static int n = 0;
@@ -612,7 +616,9 @@ __device__ __forceinline__ void bw_pass(const float (&x)[32], const float (&y)[3
                 const int col = cb + u;
                 if (KV ? col < r : col > r) xs = -INFINITY;  // exp2(-inf) = 0
             }
-            pv[u] = ex2(fmaf(xs, sc, -l2[u]));
+            // a share of the exponentials on the FMA pipe (the pass is MUFU-bound; kBwPoly of 8)
+            const bool poly = !MASK && kBwPoly > 0 && u == 3 && (e4 % (8 / kBwPoly)) == 0;
+            pv[u] = poly ? ex2_poly(fmaf(xs, sc, -l2[u])) : ex2(fmaf(xs, sc, -l2[u]));
             dv4[u] = pv[u] * fmaf(tau, y[e4 * 4 + u], -dd[u]);
         }
         pk_p[e4 * 2] = pack_bf16(pv[0], pv[1]);
