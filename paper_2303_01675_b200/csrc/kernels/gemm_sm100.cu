@@ -941,7 +941,8 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
     // vocabulary-head weight gradient: A = dlogits^T, 206 MB, 8 n-tiles).
     if (b1 * b2 == 1 && d.causal == PTK_CAUSAL_NONE) {
         const double l2 = 60e6;  // bytes of operand that stay resident in the 126 MB L2 under streaming
-        const double ab = 2.0 * d.m * d.k, bb = 2.0 * d.n * d.k;
+        const double kt = static_cast<double>(d.k) + (d.k2 > 0 ? d.k2 : 0);  // both K segments
+        const double ab = 2.0 * d.m * kt, bb = 2.0 * d.n * kt;
         const double m_fast = (ab <= l2 ? ab : ab * a.tiles_n) + bb;
         const double n_fast = (bb <= l2 ? bb : bb * ((tiles_m + 1) / 2)) + ab;
         a.n_fast = n_fast < 0.8 * m_fast ? 1 : 0;
