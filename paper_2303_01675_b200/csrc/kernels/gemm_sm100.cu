@@ -859,6 +859,10 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
             e256 = static_cast<double>(t) / (static_cast<double>(p) * rounds) + 0.1;  // pair kernel: faster per SM
         }
         bn = eff(128) > e256 + 0.15 ? 128 : 256;
+        // narrow tiles only when the machine is otherwise mostly idle (small M x N, e.g. BERT-large's
+        // 1024 x 1024 out-proj weight gradient: 16 pair tiles on 74 pairs); a 128 x 64 tile is
+        // smem-operand bound at ~2/3 of the wide tiles' per-SM rate
+        if (0.67 * eff(64) > std::max(e256, eff(128) - 0.15)) bn = 64;
     }
     if (d.causal == PTK_CAUSAL_TILES && (bn != kBM || d.m != d.n)) return PTK_ERR_ARG;
 

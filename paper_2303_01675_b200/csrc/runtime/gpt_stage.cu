@@ -387,6 +387,15 @@ void GptStage::gemm(ptk_gemm_desc d, cudaStream_t st) {
 // pair.  Pairs are (0,1), (2,3), ... in backward order, which is ascending for every plan, so
 // gradients stay bit-identical across k and stage splits.
 void GptStage::wgrad(const ptk_gemm_desc& d, cudaStream_t st) {
+    // only GEMMs that run on the CTA-pair kernel anyway are paired (a two-segment GEMM needs it);
+    // a narrow-tile weight gradient (BERT-large's 1024 x 1024 out-proj) stays per micro-batch
+    if (wg_mode_ != 0) {
+        const GemmPlan& p = cache_.get(d);
+        if (!(p.multicast && p.args.bn == 256 && d.multicast == 2)) {
+            gemm(d, st);
+            return;
+        }
+    }
     if (wg_mode_ == 1) {
         wg_pending_.push_back(d);
         return;
