@@ -966,25 +966,37 @@ __global__ void __launch_bounds__(256) attn_bwd_dot_kernel(const __nv_bfloat16* 
     const int chunks = H * kLanesPerHead;  // 16-byte chunks per row
     const int64_t off = static_cast<int64_t>(row) * H * D;
     const int bi = row / s, q = row % s;
-    for (int c0 = 0; c0 < chunks; c0 += 32) {
-        const int ci = c0 + lane;
-        float acc = 0.f;
-        if (ci < chunks) {
-            const uint4 ua = *reinterpret_cast<const uint4*>(dO + off + ci * 8);
-            const uint4 ub = *reinterpret_cast<const uint4*>(O + off + ci * 8);
-            const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&ua);
-            const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&ub);
+    constexpr int kIn = 8;  // 16-byte chunk pairs per lane in flight (all loads first, then the math)
+    for (int base = 0; base < chunks; base += 32 * kIn) {
+        uint4 ua[kIn], ub[kIn];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float2 x = __bfloat1622float2(ha[e]), y = __bfloat1622float2(hb[e]);
-                acc += x.x * y.x + x.y * y.y;
+        for (int u = 0; u < kIn; ++u) {
+            const int ci = base + u * 32 + lane;
+            if (ci < chunks) {
+                ua[u] = *reinterpret_cast<const uint4*>(dO + off + ci * 8);
+                ub[u] = *reinterpret_cast<const uint4*>(O + off + ci * 8);
             }
         }
 #pragma unroll
-        for (int o = 1; o < kLanesPerHead; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (ci < chunks && (lane % kLanesPerHead) == 0) {
-            const int head = ci / kLanesPerHead;
-            dsum[(static_cast<int64_t>(bi) * H + head) * s + q] = acc;
+        for (int u = 0; u < kIn; ++u) {
+            const int ci = base + u * 32 + lane;
+            if (base + u * 32 >= chunks) break;  // warp-uniform
+            float acc = 0.f;
+            if (ci < chunks) {
+                const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&ua[u]);
+                const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&ub[u]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 x = __bfloat1622float2(ha[e]), y = __bfloat1622float2(hb[e]);
+                    acc += x.x * y.x + x.y * y.y;
+                }
+            }
+#pragma unroll
+            for (int o = 1; o < kLanesPerHead; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (ci < chunks && (lane % kLanesPerHead) == 0) {
+                const int head = ci / kLanesPerHead;
+                dsum[(static_cast<int64_t>(bi) * H + head) * s + q] = acc;
+            }
         }
     }
 }
