@@ -183,15 +183,19 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) ln_bwd_fused_ker
             float d[8], xv[8];
             unpack_bf16x8(du[rr], d);
             unpack_bf16x8(xu[rr], xv);
-            float s1 = 0.f, s2 = 0.f;
+            // packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2): half the FP issue slots
+            const float2 mr = make_float2(-mean[rr] * rs[rr], -mean[rr] * rs[rr]);
+            const float2 r2 = make_float2(rs[rr], rs[rr]);
+            float2 s1v = make_float2(0.f, 0.f), s2v = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float dg = d[i] * gv[i];
-                s1 += dg;
-                s2 += dg * ((xv[i] - mean[rr]) * rs[rr]);
+            for (int i = 0; i < 8; i += 2) {
+                const float2 dg = __fmul2_rn(make_float2(d[i], d[i + 1]), make_float2(gv[i], gv[i + 1]));
+                const float2 xh = __ffma2_rn(make_float2(xv[i], xv[i + 1]), r2, mr);
+                s1v = __fadd2_rn(s1v, dg);
+                s2v = __ffma2_rn(dg, xh, s2v);
             }
-            s1 = warp_sum(s1);
-            s2 = warp_sum(s2);
+            float s1 = warp_sum(s1v.x + s1v.y);
+            float s2 = warp_sum(s2v.x + s2v.y);
             if (lane == 0) {
                 rb[rr][warp][0] = s1;
                 rb[rr][warp][1] = s2;
@@ -215,18 +219,30 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) ln_bwd_fused_ker
             unpack_bf16x8(xu[rr], xv);
             unpack_bf16x8(ru[rr], rv);
             float o[8];
+            const float2 mr = make_float2(-mean[rr] * rs[rr], -mean[rr] * rs[rr]);
+            const float2 r2 = make_float2(rs[rr], rs[rr]);
+            const float2 ms1 = make_float2(-s1, -s1), ms2 = make_float2(-s2, -s2);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float xh = (xv[i] - mean[rr]) * rs[rr];
-                o[i] = rs[rr] * (d[i] * gv[i] - s1 - xh * s2) + rv[i];
-                ag[i] += d[i] * xh;
-                ab[i] += d[i];
+            for (int i = 0; i < 8; i += 2) {
+                const float2 dv = make_float2(d[i], d[i + 1]);
+                const float2 xh = __ffma2_rn(make_float2(xv[i], xv[i + 1]), r2, mr);
+                // rs (d g - s1 - xh s2) + resid
+                const float2 t = __ffma2_rn(xh, ms2, __ffma2_rn(dv, make_float2(gv[i], gv[i + 1]), ms1));
+                const float2 ov = __ffma2_rn(r2, t, make_float2(rv[i], rv[i + 1]));
+                o[i] = ov.x;
+                o[i + 1] = ov.y;
+                const float2 agv = __ffma2_rn(dv, xh, make_float2(ag[i], ag[i + 1]));
+                const float2 abv = __fadd2_rn(make_float2(ab[i], ab[i + 1]), dv);
+                ag[i] = agv.x, ag[i + 1] = agv.y, ab[i] = abv.x, ab[i + 1] = abv.y;
             }
             const uint4 u = pack_bf16x8_f(o);
             float q[8];
             unpack_bf16x8(u, q);  // the bias grad sums dx as stored
 #pragma unroll
-            for (int i = 0; i < 8; ++i) ao[i] += q[i];
+            for (int i = 0; i < 8; i += 2) {
+                const float2 aov = __fadd2_rn(make_float2(ao[i], ao[i + 1]), make_float2(q[i], q[i + 1]));
+                ao[i] = aov.x, ao[i + 1] = aov.y;
+            }
             *reinterpret_cast<uint4*>(dx + static_cast<int64_t>(row) * H + c0) = u;
         }
     }
