@@ -344,10 +344,16 @@ __global__ void __launch_bounds__(32 * (4 + 4 * NQ), 1)
                         s8[e & 7] += x[e];
                     }
                 } else {
+                    // packed fp32x2 scale-and-subtract and sums (FFMA2 / FADD2; same per-lane
+                    // operations and the same 8 sum chains, so bit-identical to the scalar form)
+                    const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), mm2 = make_float2(-mx, -mx);
+                    float2* s2 = reinterpret_cast<float2*>(s8);
 #pragma unroll
-                    for (int e = 0; e < kHc; ++e) {
-                        x[e] = ex2(fmaf(x[e], a.scale_log2, -mx));
-                        s8[e & 7] += x[e];
+                    for (int e = 0; e < kHc; e += 2) {
+                        const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, mm2);
+                        x[e] = ex2(t.x);
+                        x[e + 1] = ex2(t.y);
+                        s2[(e >> 1) & 3] = __fadd2_rn(s2[(e >> 1) & 3], make_float2(x[e], x[e + 1]));
                     }
                 }
                 const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
@@ -608,18 +614,30 @@ __device__ __forceinline__ void bw_pass(const float (&x)[32], const float (&y)[3
             for (int u = 0; u < 4; ++u) l2[u] = my_lse, dd[u] = my_d;
         }
         float pv[4], dv4[4];
+        float xs[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            float xs = x[e4 * 4 + u];
+            xs[u] = x[e4 * 4 + u];
             if (MASK) {
                 // KV: row = key, col = query -> valid iff query >= key ; Q: row = query, col = key
                 const int col = cb + u;
-                if (KV ? col < r : col > r) xs = -INFINITY;  // exp2(-inf) = 0
+                if (KV ? col < r : col > r) xs[u] = -INFINITY;  // exp2(-inf) = 0
             }
+        }
+        // packed fp32x2 (FFMA2 / FMUL2): the same per-lane operations as the scalar form
+        const float2 sc2 = make_float2(sc, sc), tau2 = make_float2(tau, tau);
+#pragma unroll
+        for (int u = 0; u < 4; u += 2) {
+            const float2 t = __ffma2_rn(make_float2(xs[u], xs[u + 1]), sc2, make_float2(-l2[u], -l2[u + 1]));
             // a share of the exponentials on the FMA pipe (the pass is MUFU-bound; kBwPoly of 8)
-            const bool poly = !MASK && kBwPoly > 0 && u == 3 && (e4 % (8 / kBwPoly)) == 0;
-            pv[u] = poly ? ex2_poly(fmaf(xs, sc, -l2[u])) : ex2(fmaf(xs, sc, -l2[u]));
-            dv4[u] = pv[u] * fmaf(tau, y[e4 * 4 + u], -dd[u]);
+            const bool poly = !MASK && kBwPoly > 0 && (e4 % (8 / kBwPoly)) == 0;
+            pv[u] = ex2(t.x);
+            pv[u + 1] = (poly && u + 1 == 3) ? ex2_poly(t.y) : ex2(t.y);
+            const float2 g = __ffma2_rn(tau2, make_float2(y[e4 * 4 + u], y[e4 * 4 + u + 1]),
+                                        make_float2(-dd[u], -dd[u + 1]));
+            const float2 ds = __fmul2_rn(make_float2(pv[u], pv[u + 1]), g);
+            dv4[u] = ds.x;
+            dv4[u + 1] = ds.y;
         }
         pk_p[e4 * 2] = pack_bf16(pv[0], pv[1]);
         pk_p[e4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
