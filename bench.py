@@ -59,6 +59,9 @@ def parse():
                    help="--impl reference: S > 1 runs the CPU-thread pipeline executor (S stage threads, "
                         "S micro-batches per step, oracle/cpu_pipeline.py); 1 = the whole model on all cores")
     p.add_argument("--timeline", type=str, default="")
+    p.add_argument("--k-sweep", action="store_true",
+                   help="configs[2]: also time a fixed-plan kFkB arm for every candidate k (1/2/4/8 ...), "
+                        "reported under schedules.kfkb_sweep")
     return p.parse_args()
 
 
@@ -273,7 +276,7 @@ def main():
     # ---- fixed-plan arms (same kernels, same trace from t=0)
     fixed = {}
     if S > 1:
-        for k in (1, 2):
+        for k in (sorted(by_k) if args.k_sweep else (1, 2)):
             if k in by_k:
                 arm_reset()
                 fixed[k] = run(args.steps, by_k[k])
@@ -345,6 +348,7 @@ def main():
     all_1f1b = gather(sum(ms_1f1b))
     all_1f1b_u = gather(sum(fixed["1_unpaired"])) if "1_unpaired" in fixed else None
     all_k2 = gather(sum(fixed.get(2, ms)))
+    all_sweep = {k: gather(sum(fixed[k])) for k in sorted(by_k) if k in fixed} if args.k_sweep else None
     all_loss = gather(loss)
     all_e2e = gather(e2e_s)
     all_launch = gather(tl["launches"] * args.steps)
@@ -398,6 +402,8 @@ def main():
                                "unpaired_wgrads_samples_per_s": round(v1f1b_unpaired, 3) if v1f1b_unpaired else None},
                       "kfkb_k2": {"kbM": by_k.get(2), "samples_per_s": round(vk2, 3)},
                       "speedup_vs_1f1b": round(value / v1f1b, 4)},
+        **({"kfkb_sweep": {str(k): {"kbM": by_k[k], "samples_per_s": round(GB * args.steps / (max(v) / 1e3), 3)}
+                            for k, v in all_sweep.items()}} if all_sweep else {}),
         "tuner_decisions": [{"chosen": d["chosen"], "switched": d["switched"],
                              "estimates_ns": [e[3] for e in d["estimates"]]} for d in decisions],
         "pipeline_roofline": {"ideal_samples_per_s": round(ideal, 2), "frac": round(value / ideal, 4),
