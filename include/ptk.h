@@ -185,7 +185,8 @@ int ptk_stage_buffers(ptk_stage* st, float** master, void** weights_bf16, float*
                       int64_t* numel);
 /* Parameter i: name (copied into name_buf), element offset and shape; PTK_ERR_ARG past the end. */
 int ptk_stage_param(ptk_stage* st, int i, char* name_buf, size_t cap, int64_t* offset, int64_t* rows, int64_t* cols);
-/* GEMM event timing inside the stage's launches (roofline evidence). */
+/* GEMM event timing inside the stage's launches (roofline evidence). enable: -1 read only, 0 off,
+   1 on (the executor samples one micro-batch in 8), > 1 on with that sampling stride. */
 int ptk_stage_gemm_timing(ptk_stage* st, int enable, double* total_flops, double* total_ms, long* launches);
 size_t ptk_stage_stash_bytes(ptk_stage* st);
 

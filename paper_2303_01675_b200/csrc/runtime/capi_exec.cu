@@ -190,6 +190,7 @@ extern "C" int ptk_exec_gemm_timing(ptk_exec* ex, int enable, double* total_flop
         if (enable >= 0) {
             t.armed = enable != 0;
             t.enabled = t.armed;
+            if (t.armed) t.stride = enable > 1 ? enable : 8;  // executor: time one micro-batch in `stride`
             t.total_flops = t.total_ms = 0.0;
             t.launches = 0;
         }

@@ -109,6 +109,7 @@ extern "C" int ptk_stage_gemm_timing(ptk_stage* st, int enable, double* total_fl
         if (enable >= 0) {
             t.armed = enable != 0;
             t.enabled = t.armed;
+            if (t.armed) t.stride = enable > 1 ? enable : 8;  // executor: time one micro-batch in `stride`
             t.total_flops = t.total_ms = 0.0;
             t.launches = 0;
         }
