@@ -38,7 +38,9 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--link-gbps", type=float, default=100.0, help="emulated link bandwidth (Gb/s)")
     p.add_argument("--availability", type=float, default=0.5, help="availability while preempted")
-    p.add_argument("--trace", choices=["constant", "two-regime", "bursty", "none"], default="constant")
+    p.add_argument("--trace", choices=["constant", "two-regime", "bursty", "square", "none"], default="constant")
+    p.add_argument("--period-ms", type=float, default=1000.0,
+                   help="square: preempted (availability) for period-ms, free for period-ms, repeating")
     p.add_argument("--regime-ms", type=float, default=2000.0, help="two-regime: preempted for the first X ms")
     p.add_argument("--on-ms", type=float, default=200.0, help="bursty: mean preempted (ON) burst")
     p.add_argument("--off-ms", type=float, default=300.0, help="bursty: mean idle (OFF) gap")
@@ -135,6 +137,9 @@ def trace_segments(args, link: int):
         return [(0, H, a)]
     if args.trace == "two-regime":
         return [(0, int(args.regime_ms * 1e6), a)]
+    if args.trace == "square":  # regime changes every period: preempted, free, preempted, ...
+        P = int(args.period_ms * 1e6)
+        return [(2 * i * P, (2 * i + 1) * P, a) for i in range(int(600e9 // (2 * P)) + 1)]
     import random
     rng = random.Random(args.trace_seed * 1000 + link)  # seeded two-state Markov ON/OFF
     segs, t = [], 0.0
@@ -178,14 +183,31 @@ def reference_arm(args):
     }), flush=True)
 
 
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` (N > 1) without torchrun: re-launch this script under
+    torch.distributed.run, one rank per GPU / pipeline stage, and pass its exit code through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         return reference_arm(args)
 
-    # rank 0 prints exactly one JSON line on stdout: keep NCCL's version banner off it
-    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
-        os.environ["NCCL_DEBUG"] = "WARN"
+    # rank 0 prints exactly one JSON line on stdout: NCCL's communicator-init lines (which name
+    # nRanks) go to stderr, nothing else of NCCL's is printed
+    if "NCCL_DEBUG" not in os.environ:
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import torch
     import torch.distributed as dist
 
@@ -245,14 +267,18 @@ def main():
         ex.set_contender(args.contender)
         trace_desc = {"emulated_link_gbps": args.link_gbps, "trace": args.trace, "availability": args.availability,
                       "regime_ms": args.regime_ms if args.trace == "two-regime" else None,
+                      "period_ms": args.period_ms if args.trace == "square" else None,
                       "bursty_mean_on_off_ms": [args.on_ms, args.off_ms] if args.trace == "bursty" else None,
                       "seed": args.trace_seed, "retune_every": args.retune, "contender_kernels": args.contender}
+
+    sync_gt = [0]
 
     def arm_reset():
         """Every arm replays the trace from t=0 (per-rank globaltimer epoch after a barrier)."""
         barrier()
         if S > 1:
-            ex.set_epoch(ex.globaltimer())
+            sync_gt[0] = ex.globaltimer()
+            ex.set_epoch(sync_gt[0])
 
     it = 0
 
@@ -317,6 +343,11 @@ def main():
         wall = time.perf_counter() - t0
         gemm_flops, gemm_ms, gemm_n = ex.gemm_timing(0)
     tl = ex.timeline()
+    # achieved transfer / forward ratio of the last timed iteration (the paper's regime is ~0.5,
+    # PAPER.md:102): mean paced transfer vs mean forward of this stage
+    fwd_ns = [r[4] - r[3] for r in tl["compute"] if r[1] == 0]
+    xfer_ns = [r[4] - r[3] for r in tl["xfer"]]
+    xf_ratio = round(statistics.mean(xfer_ns) / statistics.mean(fwd_ns), 4) if fwd_ns and xfer_ns else None
     loss = ex.read_loss() if rank == S - 1 else None
     if tuner is not None and rank == 0 and args.tuner_log:
         Path(args.tuner_log).write_text(json.dumps({"trace": trace_desc, "candidates": cands, "rounds": tuner.log}))
@@ -357,6 +388,9 @@ def main():
     all_h2d = gather(tl["h2d_bytes"])
     all_gemm = gather((gemm_flops, gemm_ms, gemm_n))
     all_clk = gather(clk.summary())
+    all_xf = gather(xf_ratio)
+    all_tl = gather(tl) if S > 1 else None
+    all_sync = gather(sync_gt[0]) if S > 1 else None
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -419,14 +453,34 @@ def main():
         "e2e": {"value": round(GB * args.steps / max(all_e2e), 3), "unit": "samples/s",
                 "h2d_bytes_per_step": int(sum(all_h2d)), "d2h_bytes_per_step": 4},
         "gpu_launches": int(sum(all_launch)),
+        "transfer_forward_ratio": ({"per_stage": all_xf, "mean": round(statistics.mean(x for x in all_xf if x), 4),
+                                    "what": "mean paced inter-stage transfer / mean stage forward, last timed "
+                                            "iteration (paper regime ~0.5, PAPER.md:102)"}
+                                   if world > 1 and any(all_xf) else None),
         "loss": loss,
         "clocks": all_clk[0],
         "wall_s_timed": round(wall, 3),
     }
+    if S > 1:
+        # bubble_report / queue_analysis of the last timed iteration from the GPU timestamps, and the
+        # cost model's simulate() of the same plan fed that iteration's mean durations
+        try:
+            from paper_2303_01675_b200.report import pipeline_report
+            from paper_2303_01675_b200.tuning import pipeline_model
+            out["hardware_report"] = pipeline_report(all_tl, pipeline_model(S, GB, shape.seq * shape.hidden * 2),
+                                                     [g - all_sync[0] for g in all_sync])
+            out["hardware_report"].pop("queue_analysis", None)
+        except Exception as e:
+            out["hardware_report"] = {"error": str(e)[:300]}
     if not args.no_cpu_baseline and world == 1:
         from oracle.cpu_baseline import time_cpu_training
         torch.cuda.empty_cache()
         out["cpu_baseline"] = time_cpu_training(shape, 1, 1)
+    try:
+        from oracle.cpu_baseline import planner_cost_us
+        out["reference_planner_cpu"] = planner_cost_us(S, M, b, chosen[0])
+    except Exception as e:  # the compiled reference planner is test infrastructure; report, never fail
+        out["reference_planner_cpu"] = {"error": str(e)[:200]}
     if args.timeline:
         Path(args.timeline).write_text(json.dumps(tl))
     print(json.dumps(out), flush=True)

@@ -68,6 +68,28 @@ SimResult simulate_with(const SchedulePlan& plan, const ModelSpec& model, const 
 // True traces: compute_duration_ticks + transfer_duration.
 SimResult simulate(const SchedulePlan& plan, const ModelSpec& model, const LinkTraces& traces, Tick start = 0);
 
+// Measured execution (the B200 executor's records, on one clock) as a SimResult,
+// so bubble_report / queue_analysis apply unchanged to hardware runs
+// (SPEC.md:351-361).  A compute record is (device, compute node id, start, end);
+// a transfer record is (link, micro-batch, start, end): link 2s carries F(s, m)'s
+// output to stage s+1, link 2s-1 carries B(s, m)'s to stage s-1 (model.hpp link
+// ids).  Busy = summed compute durations, bubble = active span - busy; a launch
+// with an input is pre-buffered when that input landed strictly before the device
+// was free (its previous compute ended; `start` before the first).  Throws
+// ConfigError on records that do not belong to the plan.
+struct HwCompute {
+    int device = -1;
+    int node = -1;
+    Tick start = 0, end = 0;
+};
+struct HwTransfer {
+    LinkId link = -1;
+    int micro_batch = -1;
+    Tick start = 0, end = 0;
+};
+SimResult result_from_records(const SchedulePlan& plan, const std::vector<HwCompute>& compute,
+                              const std::vector<HwTransfer>& transfers, Tick start);
+
 // bubble / (busy + bubble) per device (0 for an idle device).
 std::vector<double> bubble_report(const SimResult& result);
 

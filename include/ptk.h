@@ -228,7 +228,27 @@ int64_t ptk_globaltimer(void);
  * labels, or NULL for the built-in synthetic corpus); finish blocks and
  * returns the stage's device milliseconds for it. */
 int ptk_exec_run_iteration(ptk_exec* ex, int iter, const int32_t* host_tokens);
+/* ptk_exec_run_iteration one plan node at a time: begin stages the data, each enqueue_next
+ * enqueues the next node of the stage's order and sets *more = 0 once the iteration is fully
+ * enqueued (then call finish).  `iter` only seeds the synthetic corpus: arrival flags carry an
+ * internal per-executor epoch, so reusing or restarting `iter` is safe. */
+int ptk_exec_begin_iteration(ptk_exec* ex, int iter, const int32_t* host_tokens);
+int ptk_exec_enqueue_next(ptk_exec* ex, int* more);
+/* All n stages of one pipeline in this process (stages[s] = stage s, wired with
+ * ptk_exec_connect_local): one iteration enqueued in a global order where each node follows the
+ * nodes it receives from, so it completes even when launches are serialised (ncu).  A plan whose
+ * per-device orders cannot be merged returns PTK_ERR_DEADLOCK.  Finish each stage afterwards. */
+int ptk_exec_run_local(ptk_exec* const* stages, int n, int iter, const int32_t* host_tokens);
+/* Blocks until the stage's iteration (compute and sends) finished.  After the deadlock timeout
+ * (default 600 s, env PTK_DEADLOCK_TIMEOUT_S) it returns PTK_ERR_DEADLOCK
+ * (pipetune::DeadlockDetected, proj/include/pipetune/errors.hpp:38-40): the stage's arrival flags
+ * are forced open so its streams drain, and the executor is poisoned (destroy it). */
 int ptk_exec_finish_iteration(ptk_exec* ex, double* ms);
+int ptk_exec_set_deadlock_timeout(ptk_exec* ex, double seconds);
+/* 1: one dedicated copy stream per outgoing link (activations and gradients of a middle stage
+ * never queue behind each other); 0 (default): one send stream per stage for both directions,
+ * the spec simulator's model the cost model predicts.  Env PTK_SEND_STREAMS=per_link. */
+int ptk_exec_set_send_streams(ptk_exec* ex, int per_link);
 int ptk_exec_read_loss(ptk_exec* ex, float* loss);
 /* Records of the last finished iteration, ns from its start:
  * {"compute": [[node, kind(0F/1B/2GA), mb, start, end]...], "xfer": [[link, mb, bytes, start, end]...],

@@ -70,10 +70,36 @@ class CpuTrainer:
                 stash.pop(m).backward()
         dt = time.perf_counter() - t0
         samples = b * self.M
-        return {"value": samples / dt, "unit": "samples/s", "cores": self.threads, "kind": self.kind,
+        return {"value": samples / dt, "unit": "samples/s", "cores": self.threads, "kind": "port",
+                "order_source": self.kind, **host_info(),
                 "sample": f"{shape.n_layer}-layer h={shape.hidden} s={shape.seq} {shape.arch.upper()} fp32 fwd+bwd "
-                          f"of {samples} sample(s) (b={b}) on the host cores in the reference planner's order; "
-                          f"{dt:.1f} s"}
+                          f"of {samples} sample(s) (b={b}) by the oracle port (oracle/gpt_oracle.py) on the host "
+                          f"cores, in the order of the {self.kind} planner; {dt:.1f} s"}
+
+
+def host_info() -> dict:
+    """CPU model and core count of the host the CPU path ran on."""
+    model = "unknown"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def planner_cost_us(stages: int, micro_batches: int, b: int, k: int, reps: int = 200) -> dict | None:
+    """Mean µs of the COMPILED REFERENCE planner (build_task_graph + plan_kfkb, reference
+    taskgraph.cpp:35 / plan.cpp:75) for this configuration, 1 core — the reference's own CPU cost
+    of the path, timed beside the GPU run (oracle/ref_dump --time)."""
+    if not REF_BIN.exists():
+        return None
+    out = subprocess.run([str(REF_BIN), "--time", str(reps)], input=f"{stages} {micro_batches} {b} 1 {k} 1 1\n",
+                         capture_output=True, text=True, check=True).stdout.split()
+    return {"us": float(out[0]), "config": [stages, micro_batches, b, k], "reps": reps,
+            "what": "reference build_task_graph + plan_kfkb, g++ -O2, 1 core"}
 
 
 def init_weights(shape):

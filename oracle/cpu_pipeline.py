@@ -117,7 +117,9 @@ class CpuPipeline:
         self.loss = sum(losses)
         samples = self.b * self.M
         shape = self.shape
-        return {"value": samples / dt, "unit": "samples/s", "cores": self.threads, "kind": self.kind,
+        from .cpu_baseline import host_info
+        return {"value": samples / dt, "unit": "samples/s", "cores": self.threads, "kind": "port",
+                "order_source": self.kind, **host_info(),
                 "sample": f"{shape.n_layer}-layer h={shape.hidden} s={shape.seq} {shape.arch.upper()} fp32, "
                           f"{S} stage thread(s) x {max(1, self.threads // S)} intra-op threads, one iteration of "
                           f"{self.M} micro-batch(es) of b={self.b} in the reference planner's k={self.k} order; "

@@ -19,6 +19,26 @@ namespace pipetune {
 
 using json::Value;
 
+// Mandatory request fields: a missing key is a ConfigError (exit code 2 through
+// the CLI), never a null dereference.
+const Value& need(const Value& o, const char* k) {
+    const Value* v = o.get(k);
+    if (v == nullptr) throw ConfigError(std::string("missing required key \"") + k + "\"");
+    return *v;
+}
+
+const Value& need_arr(const Value& o, const char* k) {
+    const Value& v = need(o, k);
+    if (v.kind != Value::Array) throw ConfigError(std::string("\"") + k + "\" must be an array");
+    return v;
+}
+
+// Fixed-length array entries ([k, b, M], [link, bytes] ...).
+const Value& entry(const Value& a, size_t i, const char* what) {
+    if (a.kind != Value::Array || i >= a.arr.size()) throw ConfigError(std::string("malformed ") + what);
+    return a.arr[i];
+}
+
 ModelSpec parse_model(const Value& v) {
     json::require_keys(v, "model", {"global_batch", "stages"});
     ModelSpec m;
@@ -220,7 +240,7 @@ std::string run_scenario(const std::string& request) {
     json::require_keys(req, "scenario",
                        {"schema_version", "op", "model", "cluster", "traces", "plan", "policy", "horizon", "start",
                         "bytes", "trace", "buckets", "clock", "repeats", "window", "samples", "query", "k_max",
-                        "compute_profile", "current", "hysteresis", "candidates"});
+                        "compute_profile", "current", "hysteresis", "candidates", "records"});
     if (const Value* sv = req.get("schema_version"))
         if (sv->as_int("schema_version") != 1) throw ConfigError("unsupported schema_version");
     const Value* opv = req.get("op");
@@ -230,20 +250,20 @@ std::string run_scenario(const std::string& request) {
     w.begin_obj();
 
     if (op == "transfer") {
-        const LinkTrace t = parse_trace(*req.get("trace"));
+        const LinkTrace t = parse_trace(need(req, "trace"));
         const Tick start = req.get("start") ? req.get("start")->as_int("start") : 0;
-        w.key("duration").num(transfer_duration(t, req.get("bytes")->as_int("bytes"), start));
+        w.key("duration").num(transfer_duration(t, need(req, "bytes").as_int("bytes"), start));
     } else if (op == "estimate") {
         ProfileStore store(req.get("window") ? static_cast<int>(req.get("window")->as_int("window")) : 8);
-        fill_store(*req.get("samples"), store);
-        const Value& q = *req.get("query");
-        w.key("estimate").num(store.estimate(static_cast<int>(q.arr.at(0).as_int("link")), q.arr.at(1).as_int("bytes")));
+        fill_store(need_arr(req, "samples"), store);
+        const Value& q = need(req, "query");
+        w.key("estimate").num(store.estimate(static_cast<int>(entry(q, 0, "query").as_int("link")), entry(q, 1, "query").as_int("bytes")));
     } else {
         const Value* mv = req.get("model");
         if (!mv) throw ConfigError("scenario: model is required for op " + op);
         const ModelSpec model = parse_model(*mv);
         if (op == "peak_memory" || op == "simulate") {
-            const SchedulePlan plan = parse_plan(*req.get("plan"), model);
+            const SchedulePlan plan = parse_plan(need(req, "plan"), model);
             if (op == "peak_memory") {
                 const PeakMemoryReport r = peak_memory(plan, model);
                 w.key("per_device_peak").ints(r.per_device_peak);
@@ -254,8 +274,35 @@ std::string run_scenario(const std::string& request) {
                 w.key("result");
                 write_sim(w, simulate(plan, model, traces, start));
             }
+        } else if (op == "hardware_report") {
+            // SimResult of a measured GPU run (bubble_report / queue_analysis on hardware)
+            const SchedulePlan plan = parse_plan(need(req, "plan"), model);
+            const Value& rec = need(req, "records");
+            std::vector<HwCompute> comp;
+            std::vector<HwTransfer> xfer;
+            for (const Value& e : need_arr(rec, "compute").arr)
+                comp.push_back({static_cast<int>(entry(e, 0, "compute record").as_int("device")),
+                                static_cast<int>(entry(e, 1, "compute record").as_int("node")),
+                                entry(e, 2, "compute record").as_int("start"), entry(e, 3, "compute record").as_int("end")});
+            for (const Value& e : need_arr(rec, "xfer").arr)
+                xfer.push_back({static_cast<int>(entry(e, 0, "xfer record").as_int("link")),
+                                static_cast<int>(entry(e, 1, "xfer record").as_int("mb")),
+                                entry(e, 2, "xfer record").as_int("start"), entry(e, 3, "xfer record").as_int("end")});
+            const Tick start = req.get("start") ? req.get("start")->as_int("start") : 0;
+            w.key("result");
+            write_sim(w, result_from_records(plan, comp, xfer, start));
+        } else if (op == "estimate_sim") {
+            // the cost model's full simulation of one plan over constant profiled durations
+            const SchedulePlan plan = parse_plan(need(req, "plan"), model);
+            const ComputeProfile comp = parse_compute_profile(need_arr(req, "compute_profile"));
+            ProfileStore store(req.get("window") ? static_cast<int>(req.get("window")->as_int("window")) : 8);
+            fill_store(need_arr(req, "samples"), store);
+            auto cf = [&comp](int s, int bb, Direction dir) { return comp.get(s, bb, dir); };
+            auto xf = [&store](LinkId l, Bytes bytes, Tick) { return store.estimate(l, bytes); };
+            w.key("result");
+            write_sim(w, simulate_with(plan, model, cf, xf, 0));
         } else if (op == "enumerate") {
-            const ClusterSpec cluster = parse_cluster(*req.get("cluster"));
+            const ClusterSpec cluster = parse_cluster(need(req, "cluster"));
             const int k_max = req.get("k_max") ? static_cast<int>(req.get("k_max")->as_int("k_max"))
                                                : default_k_max(model);
             const CandidateSet set = enumerate_candidates(model, cluster, k_max);
@@ -267,7 +314,7 @@ std::string run_scenario(const std::string& request) {
             w.end_arr();
         } else if (op == "profile") {
             const LinkTraces traces = parse_traces(req.get("traces"), model.stage_count());
-            const SchedulePlan plan = parse_plan(*req.get("plan"), model);
+            const SchedulePlan plan = parse_plan(need(req, "plan"), model);
             ProfileStore store(req.get("window") ? static_cast<int>(req.get("window")->as_int("window")) : 8);
             const Tick clock = req.get("clock") ? req.get("clock")->as_int("clock") : 0;
             const int reps = req.get("repeats") ? static_cast<int>(req.get("repeats")->as_int("repeats")) : 3;
@@ -277,7 +324,7 @@ std::string run_scenario(const std::string& request) {
             for (const auto& [l, b] : plan_buckets(plan)) w.begin_arr().v(l).v(b).v(store.estimate(l, b)).end_arr();
             w.end_arr();
         } else if (op == "compare") {
-            const ClusterSpec cluster = parse_cluster(*req.get("cluster"));
+            const ClusterSpec cluster = parse_cluster(need(req, "cluster"));
             const LinkTraces traces = parse_traces(req.get("traces"), model.stage_count());
             const TuningPolicy pol = parse_policy(req.get("policy"));
             const CandidateSet set = enumerate_candidates(model, cluster, pol.k_max);
@@ -294,27 +341,27 @@ std::string run_scenario(const std::string& request) {
         } else if (op == "decide") {
             // the GPU tuner's decision, replayed from recorded int64-ns samples
             CandidateSet set;
-            for (const Value& c : req.get("candidates")->arr)
-                set.entries.push_back({PlanConfig{static_cast<int>(c.arr.at(0).as_int("k")),
-                                                  static_cast<int>(c.arr.at(1).as_int("b")),
-                                                  static_cast<int>(c.arr.at(2).as_int("M"))},
+            for (const Value& c : need_arr(req, "candidates").arr)
+                set.entries.push_back({PlanConfig{static_cast<int>(entry(c, 0, "candidate").as_int("k")),
+                                                  static_cast<int>(entry(c, 1, "candidate").as_int("b")),
+                                                  static_cast<int>(entry(c, 2, "candidate").as_int("M"))},
                                        {}});
-            const ComputeProfile comp = parse_compute_profile(*req.get("compute_profile"));
+            const ComputeProfile comp = parse_compute_profile(need_arr(req, "compute_profile"));
             ProfileStore store(req.get("window") ? static_cast<int>(req.get("window")->as_int("window")) : 8);
-            fill_store(*req.get("samples"), store);
+            fill_store(need_arr(req, "samples"), store);
             PlanConfig cur{0, 0, 0};
             if (const Value* c = req.get("current"))
-                cur = {static_cast<int>(c->arr.at(0).as_int("k")), static_cast<int>(c->arr.at(1).as_int("b")),
-                       static_cast<int>(c->arr.at(2).as_int("M"))};
+                cur = {static_cast<int>(entry(*c, 0, "current").as_int("k")), static_cast<int>(entry(*c, 1, "current").as_int("b")),
+                       static_cast<int>(entry(*c, 2, "current").as_int("M"))};
             const double h = req.get("hysteresis") ? req.get("hysteresis")->as_double("hysteresis") : 0.02;
             const Tick t = req.get("clock") ? req.get("clock")->as_int("clock") : 0;
             w.key("decision");
             write_decision(w, tuning_round(set, model, comp, store, cur, h, t));
         } else if (op == "tune") {
-            const ClusterSpec cluster = parse_cluster(*req.get("cluster"));
+            const ClusterSpec cluster = parse_cluster(need(req, "cluster"));
             const LinkTraces traces = parse_traces(req.get("traces"), model.stage_count());
             const TuningPolicy pol = parse_policy(req.get("policy"));
-            const AdaptiveResult r = run_adaptive(model, cluster, traces, pol, req.get("horizon")->as_double("horizon"));
+            const AdaptiveResult r = run_adaptive(model, cluster, traces, pol, need(req, "horizon").as_double("horizon"));
             w.key("rounds").begin_arr();
             for (const TuningDecision& d : r.log.rounds) write_decision(w, d);
             w.end_arr();

@@ -179,6 +179,81 @@ SimResult simulate(const SchedulePlan& plan, const ModelSpec& model, const LinkT
     return simulate_with(plan, model, comp, xfer, start);
 }
 
+SimResult result_from_records(const SchedulePlan& plan, const std::vector<HwCompute>& compute,
+                              const std::vector<HwTransfer>& transfers, Tick start) {
+    const TaskGraph& g = *plan.graph;
+    const int S = plan.device_count();
+    SimResult res;
+    res.start = start;
+    res.queue_depth_trace.resize(static_cast<size_t>(S));
+    res.launches.resize(static_cast<size_t>(S));
+    std::vector<Tick> arrival(g.nodes.size(), -1);  // Recv id -> landing time
+    Tick end = start;
+    for (const HwTransfer& x : transfers) {
+        if (x.link < 0 || x.link >= link_count(S) || x.micro_batch < 0 || x.micro_batch >= plan.config.micro_batch_count)
+            throw ConfigError("result_from_records: transfer outside the plan");
+        const bool fwd = x.link % 2 == 0;
+        const int producer = fwd ? x.link / 2 : (x.link + 1) / 2;
+        int cid = -1;
+        for (int id : plan.per_device[static_cast<size_t>(producer)]) {
+            const TaskNode& t = g.node(id);
+            if (t.micro_batch == x.micro_batch &&
+                t.kind == (fwd ? TaskKind::ForwardCompute : TaskKind::BackwardCompute)) {
+                cid = id;
+                break;
+            }
+        }
+        const int sid = cid < 0 ? -1 : g.send_of_compute[static_cast<size_t>(cid)];
+        if (sid < 0) throw ConfigError("result_from_records: no Send for a transfer record");
+        const int rid = g.pair_of[static_cast<size_t>(sid)];
+        arrival[static_cast<size_t>(rid)] = x.end;
+        res.timeline.push_back({sid, producer, Stream::Send, x.start, x.end});
+        res.timeline.push_back({rid, g.node(rid).device, Stream::Recv, x.start, x.end});
+        end = std::max(end, x.end);
+    }
+    std::vector<std::vector<const HwCompute*>> per(static_cast<size_t>(S));
+    for (const HwCompute& c : compute) {
+        if (c.device < 0 || c.device >= S || c.node < 0 || static_cast<size_t>(c.node) >= g.nodes.size() ||
+            g.node(c.node).device != c.device)
+            throw ConfigError("result_from_records: compute record outside the plan");
+        per[static_cast<size_t>(c.device)].push_back(&c);
+    }
+    for (int d = 0; d < S; ++d) {
+        auto& v = per[static_cast<size_t>(d)];
+        std::stable_sort(v.begin(), v.end(), [](const HwCompute* a, const HwCompute* b) { return a->start < b->start; });
+        Tick busy = 0, first = -1, last = -1, prev_end = start;
+        std::vector<std::tuple<Tick, int, int>> qev;  // (time, 0 arrival / 1 launch, node)
+        for (const HwCompute* c : v) {
+            busy += c->end - c->start;
+            if (first < 0) first = c->start;
+            last = std::max(last, c->end);
+            res.timeline.push_back({c->node, d, Stream::Compute, c->start, c->end});
+            const int recv = g.recv_of_compute[static_cast<size_t>(c->node)];
+            if (recv >= 0) {
+                const Tick a = arrival[static_cast<size_t>(recv)];
+                if (a < 0) throw ConfigError("result_from_records: a compute's input transfer is missing");
+                res.launches[static_cast<size_t>(d)].push_back({c->node, a < prev_end});
+                qev.emplace_back(a, 0, recv);
+                qev.emplace_back(c->start, 1, c->node);
+            }
+            prev_end = c->end;
+            end = std::max(end, c->end);
+        }
+        std::sort(qev.begin(), qev.end());
+        int depth = 0;
+        for (const auto& [t, kind, node] : qev) {
+            (void)node;
+            depth += kind == 0 ? 1 : -1;
+            res.queue_depth_trace[static_cast<size_t>(d)].push_back({t, depth});
+        }
+        res.per_device_busy.push_back(busy);
+        res.per_device_bubble.push_back(first < 0 ? 0 : (last - first) - busy);
+        res.observed_peak_bytes.push_back(0);
+    }
+    res.pipeline_length = end - start;
+    return res;
+}
+
 std::vector<double> bubble_report(const SimResult& r) {
     std::vector<double> out;
     for (size_t d = 0; d < r.per_device_busy.size(); ++d) {

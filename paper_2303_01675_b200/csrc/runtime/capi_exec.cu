@@ -28,9 +28,11 @@ int guarded(const char* what, F&& f) {
         return ptk::set_error(PTK_ERR_ARG, std::string(what) + ": " + e.what());
     } catch (const pipetune::PlanError& e) {
         return ptk::set_error(PTK_ERR_PLAN, std::string(what) + ": " + e.what());
+    } catch (const pipetune::DeadlockDetected& e) {
+        return ptk::set_error(PTK_ERR_DEADLOCK, std::string(what) + ": " + e.what());
     } catch (const pipetune::InfeasibleModel& e) {
         return ptk::set_error(PTK_ERR_INFEASIBLE, std::string(what) + ": " + e.what());
-    } catch (const std::invalid_argument& e) {
+    } catch (const std::logic_error& e) {  // invalid_argument, out-of-order calls
         return ptk::set_error(PTK_ERR_ARG, std::string(what) + ": " + e.what());
     } catch (const std::exception& e) {
         return ptk::set_error(PTK_ERR_CUDA, std::string(what) + ": " + e.what());
@@ -128,6 +130,44 @@ extern "C" int ptk_exec_run_iteration(ptk_exec* ex, int iter, const int32_t* hos
     return guarded("ptk_exec_run_iteration", [&] { ex->impl.run_iteration(iter, host_tokens); });
 }
 
+extern "C" int ptk_exec_begin_iteration(ptk_exec* ex, int iter, const int32_t* host_tokens) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_begin_iteration", [&] { ex->impl.begin_iteration(iter, host_tokens); });
+}
+
+extern "C" int ptk_exec_enqueue_next(ptk_exec* ex, int* more) {
+    EX_CHECK(ex);
+    return guarded("ptk_exec_enqueue_next", [&] {
+        const bool m = ex->impl.enqueue_next();
+        if (more) *more = m ? 1 : 0;
+    });
+}
+
+extern "C" int ptk_exec_run_local(ptk_exec* const* stages, int n, int iter, const int32_t* host_tokens) {
+    if (stages == nullptr || n < 1) return ptk::set_error(PTK_ERR_ARG, "ptk_exec_run_local: empty stage list");
+    return guarded("ptk_exec_run_local", [&] {
+        std::vector<ptk::Executor*> v;
+        for (int i = 0; i < n; ++i) {
+            if (stages[i] == nullptr) throw std::invalid_argument("null stage");
+            v.push_back(&stages[i]->impl);
+        }
+        ptk::run_local_pipeline(v, iter, host_tokens);
+    });
+}
+
+extern "C" int ptk_exec_set_deadlock_timeout(ptk_exec* ex, double seconds) {
+    EX_CHECK(ex);
+    if (!(seconds > 0.0)) return ptk::set_error(PTK_ERR_ARG, "ptk_exec_set_deadlock_timeout: seconds must be > 0");
+    ex->impl.set_deadlock_timeout(seconds);
+    return PTK_OK;
+}
+
+extern "C" int ptk_exec_set_send_streams(ptk_exec* ex, int per_link) {
+    EX_CHECK(ex);
+    ex->impl.set_send_streams_per_link(per_link != 0);
+    return PTK_OK;
+}
+
 extern "C" int ptk_exec_finish_iteration(ptk_exec* ex, double* ms) {
     EX_CHECK(ex);
     return guarded("ptk_exec_finish_iteration", [&] {
@@ -158,6 +198,11 @@ extern "C" int ptk_exec_timeline_json(ptk_exec* ex, char* buf, size_t cap, size_
         w.key("h2d_bytes").num(ex->impl.h2d_bytes());
         w.key("k").num(ex->impl.plan_k());
         w.key("b").num(ex->impl.plan_b());
+        w.key("groups").begin_arr();
+        for (int n : ex->impl.plan_groups()) w.v(n);
+        w.end_arr();
+        w.key("t0_globaltimer").num(ex->impl.iteration_start_globaltimer());
+        w.key("stage").num(ex->impl.cfg().stage);
         w.end_obj();
         if (written) *written = w.out.size() + 1;
         if (!buf || cap < w.out.size() + 1) throw std::invalid_argument("buffer too small");

@@ -211,6 +211,11 @@ void Emulator::stop_contender() {
     if (stop_host_) *stop_host_ = 1;
 }
 
+cudaError_t record_globaltimer(int64_t* dst, cudaStream_t st) {
+    timer_kernel<<<1, 1, 0, st>>>(dst);
+    return cudaPeekAtLastError();
+}
+
 int64_t device_globaltimer(cudaStream_t st) {
     int64_t* d = nullptr;
     int64_t h = 0;

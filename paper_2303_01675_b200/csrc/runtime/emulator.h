@@ -62,5 +62,7 @@ class Emulator {
 
 // Reads %globaltimer on the device (ns) — used to align trace epochs.
 int64_t device_globaltimer(cudaStream_t st);
+// Enqueues a one-thread kernel writing %globaltimer to *dst (device memory) on `st`.
+cudaError_t record_globaltimer(int64_t* dst, cudaStream_t st);
 
 }  // namespace ptk

@@ -5,9 +5,13 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <cstring>
 #include <mutex>
+#include <chrono>
 #include <stdexcept>
+#include <thread>
 
 #include "pipetune/errors.hpp"
 
@@ -76,6 +80,9 @@ Executor::Executor(const ptk_exec_config& c) : cfg_(c) {
     if (std::getenv("PTK_FLAT_PRIORITY") != nullptr) hi = lo;  // diagnostics: all streams at one priority
     ck(cudaStreamCreateWithPriority(&comp_, cudaStreamNonBlocking, hi), "stream");
     ck(cudaStreamCreateWithPriority(&sendst_, cudaStreamNonBlocking, lo), "stream");
+    ck(cudaStreamCreateWithPriority(&sendst_bwd_, cudaStreamNonBlocking, lo), "stream");
+    if (const char* v = std::getenv("PTK_DEADLOCK_TIMEOUT_S")) deadlock_timeout_s_ = std::atof(v);
+    if (const char* v = std::getenv("PTK_SEND_STREAMS")) per_link_send_ = std::string(v) == "per_link";
     ck(cudaStreamCreateWithPriority(&contend_[0], cudaStreamNonBlocking, lo), "stream");
     ck(cudaStreamCreateWithPriority(&contend_[1], cudaStreamNonBlocking, lo), "stream");
     stage_ = std::make_unique<GptStage>(c.gpt);
@@ -89,7 +96,16 @@ Executor::Executor(const ptk_exec_config& c) : cfg_(c) {
 
 Executor::~Executor() {
     emu_.stop_contender();
-    cudaDeviceSynchronize();
+    if (in_iteration_) {  // destroyed half-enqueued: open this stage's flags so nothing waits forever
+        poisoned_ = true;
+        if (act_flag_) cudaMemsetAsync(act_flag_, 0xff, cfg_.global_batch * 4, rescue_stream());
+        if (grad_flag_) cudaMemsetAsync(grad_flag_, 0xff, cfg_.global_batch * 4, rescue_stream());
+    }
+    cudaStreamSynchronize(comp_);
+    cudaStreamSynchronize(sendst_);
+    cudaStreamSynchronize(sendst_bwd_);
+    cudaStreamSynchronize(contend_[0]);
+    cudaStreamSynchronize(contend_[1]);
     for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
     for (cudaEvent_t e : pool_) cudaEventDestroy(e);
     for (cudaEvent_t e : act_sent_) cudaEventDestroy(e);
@@ -101,6 +117,8 @@ Executor::~Executor() {
     if (host_stage_) cudaFreeHost(host_stage_);
     cudaStreamDestroy(comp_);
     cudaStreamDestroy(sendst_);
+    cudaStreamDestroy(sendst_bwd_);
+    if (rescue_) cudaStreamDestroy(rescue_);
     cudaStreamDestroy(contend_[0]);
     cudaStreamDestroy(contend_[1]);
 }
@@ -139,6 +157,7 @@ void Executor::alloc_comm() {
         }
     }
     if (cfg_.stages > 1) scratch_ = dalloc(kScratch);
+    gt_start_ = static_cast<int64_t*>(dalloc(64));
     const int64_t toks = static_cast<int64_t>(cfg_.global_batch) * g.seq;
     tok_dev_ = static_cast<int32_t*>(dalloc(toks * 4));
     lab_dev_ = static_cast<int32_t*>(dalloc(toks * 4));
@@ -251,6 +270,7 @@ void Executor::install_plan(int b, const std::vector<int>& group_sizes, int k) {
     k_ = k;
     b_ = b;
     M_ = cfg_.global_batch / b;
+    groups_ = group_sizes;
     stage_->set_micro_batch(b, M_);
 }
 
@@ -296,24 +316,34 @@ void Executor::send(bool fwd, int mb, const __nv_bfloat16* src, int64_t bytes, c
     uint32_t* flag = fwd ? peer_act_flag_ : peer_grad_flag_;
     if (!dst_block || !flag) throw std::runtime_error("send: peer not connected");
     const int64_t off = static_cast<int64_t>(mb) * b_ * g.seq * g.hidden;
-    ck(cudaStreamWaitEvent(sendst_, ready, 0), "wait");
+    cudaStream_t st = send_stream(fwd);
+    ck(cudaStreamWaitEvent(st, ready, 0), "wait");
     XferRecord r{fwd ? 2 * cfg_.stage : 2 * cfg_.stage - 1, mb, bytes, ev(), ev()};
-    ck(cudaEventRecord(r.start, sendst_), "event");
-    ck(emu_.paced_copy(fwd ? 0 : 1, dst_block + off, src, bytes, sendst_), "peer copy");
+    ck(cudaEventRecord(r.start, st), "event");
+    ck(emu_.paced_copy(fwd ? 0 : 1, dst_block + off, src, bytes, st), "peer copy");
     if (emu_.active(fwd ? 0 : 1)) emu_launches_ += Emulator::kChunks + 1;
-    write_flag(sendst_, flag + mb, static_cast<uint32_t>(iter_ + 1));
-    ck(cudaEventRecord(r.end, sendst_), "event");
+    write_flag(st, flag + mb, epoch_);
+    ck(cudaEventRecord(r.end, st), "event");
     xrec_.push_back(r);
 }
 
 void Executor::run_iteration(int iter, const int32_t* host_tokens) {
+    begin_iteration(iter, host_tokens);
+    while (enqueue_next()) {
+    }
+}
+
+void Executor::begin_iteration(int iter, const int32_t* host_tokens) {
+    if (poisoned_) throw pipetune::DeadlockDetected("executor poisoned by an earlier deadlock; destroy it");
+    if (in_iteration_) throw std::logic_error("begin_iteration: the previous iteration is still being enqueued");
     const ptk_gpt_config& g = cfg_.gpt;
     const int S = cfg_.stages, s = cfg_.stage;
     const bool first = s == 0, last = s == S - 1;
-    const int64_t T = static_cast<int64_t>(b_) * g.seq;
-    const int64_t act_bytes = T * g.hidden * 2;
     const int64_t toks = static_cast<int64_t>(cfg_.global_batch) * g.seq;
     iter_ = iter;
+    ++epoch_;
+    cursor_ = 0;
+    in_iteration_ = true;
     pool_used_ = 0;
     crec_.clear();
     xrec_.clear();
@@ -327,7 +357,9 @@ void Executor::run_iteration(int iter, const int32_t* host_tokens) {
     else
         synth_tokens(iter, host_stage_);
     ck(cudaEventRecord(it_start_, comp_), "event");
+    ck(record_globaltimer(gt_start_, comp_), "globaltimer");  // the iteration start on the device clock
     ck(cudaStreamWaitEvent(sendst_, it_start_, 0), "wait");
+    ck(cudaStreamWaitEvent(sendst_bwd_, it_start_, 0), "wait");
     h2d_bytes_ = 0;
     if (first) {
         ck(cudaMemcpyAsync(tok_dev_, host_stage_, toks * 4, cudaMemcpyHostToDevice, comp_), "h2d");
@@ -339,65 +371,153 @@ void Executor::run_iteration(int iter, const int32_t* host_tokens) {
     }
     ck(cudaEventRecord(h2d_done_, comp_), "event");
     if (last) ck(cudaMemsetAsync(stage_->loss_accumulator(), 0, 4, comp_), "memset");
-    if (contender_on_) {  // real competing NVLink stores while a trace is in a preempted segment
+    if (contender_on_) {  // competing NVLink stores while a trace is in a preempted segment
         if (peer_scratch_fwd_) ck(emu_.start_contender(0, peer_scratch_fwd_, kScratch, contend_[0]), "contender");
         if (peer_scratch_bwd_) ck(emu_.start_contender(1, peer_scratch_bwd_, kScratch, contend_[1]), "contender");
     }
     emu_launches_ = 0;
+}
 
-    for (int id : plan_.per_device[static_cast<size_t>(s)]) {
-        const pipetune::TaskNode& n = graph_->node(id);
-        const int m = n.micro_batch;
-        const int slot = m >= 0 ? m % stage_->virtual_slots() : 0;
-        // this micro-batch's view of the b_max-wide send buffer of its physical slot
-        const int split = stage_->slot_split();
-        const int64_t sub = static_cast<int64_t>(slot % split) * T * g.hidden;
-        GemmTiming& tm = stage_->gemm_timing();
-        tm.enabled = tm.armed && m >= 0 && m % tm.stride == 0;
-        if (n.kind == pipetune::TaskKind::ForwardCompute) {
-            if (!first) wait_flag(comp_, act_flag_ + m, static_cast<uint32_t>(iter + 1));
-            __nv_bfloat16* out = last ? nullptr : act_send_[static_cast<size_t>(slot / split)] + sub;
-            if (!last) ck(cudaStreamWaitEvent(comp_, act_sent_[static_cast<size_t>(slot)], 0), "wait");
-            CompRecord r{id, 0, m, ev(), ev()};
-            ck(cudaEventRecord(r.start, comp_), "event");
-            stage_->forward(slot, tok_dev_ + m * T, first ? nullptr : act_recv_ + m * T * g.hidden, lab_dev_ + m * T,
-                            out, comp_);
-            ck(cudaEventRecord(r.end, comp_), "event");
-            crec_.push_back(r);
-            if (!last) {
-                send(true, m, out, act_bytes, r.end);
-                ck(cudaEventRecord(act_sent_[static_cast<size_t>(slot)], sendst_), "event");
-            }
-        } else if (n.kind == pipetune::TaskKind::BackwardCompute) {
-            if (!last) wait_flag(comp_, grad_flag_ + m, static_cast<uint32_t>(iter + 1));
-            __nv_bfloat16* dx = first ? nullptr : grad_send_[static_cast<size_t>(slot / split)] + sub;
-            if (!first) ck(cudaStreamWaitEvent(comp_, grad_sent_[static_cast<size_t>(slot)], 0), "wait");
-            CompRecord r{id, 1, m, ev(), ev()};
-            ck(cudaEventRecord(r.start, comp_), "event");
-            stage_->backward(slot, tok_dev_ + m * T, last ? nullptr : grad_recv_ + m * T * g.hidden, dx, comp_);
-            ck(cudaEventRecord(r.end, comp_), "event");
-            crec_.push_back(r);
-            if (!first) {
-                send(false, m, dx, act_bytes, r.end);
-                ck(cudaEventRecord(grad_sent_[static_cast<size_t>(slot)], sendst_), "event");
-            }
-        } else if (n.kind == pipetune::TaskKind::GradAccum) {
-            CompRecord r{id, 2, -1, ev(), ev()};
-            ck(cudaEventRecord(r.start, comp_), "event");
-            if (defer_optimizer_)
-                stage_->finalize_grads(comp_);  // the caller all-reduces, then steps the optimizer
-            else
-                stage_->optimizer_step(cfg_.lr, cfg_.weight_decay, comp_);
-            ck(cudaEventRecord(r.end, comp_), "event");
-            crec_.push_back(r);
-        }
+void Executor::peek_next(int* kind, int* mb) const {
+    const auto& order = plan_.per_device[static_cast<size_t>(cfg_.stage)];
+    if (!in_iteration_ || cursor_ >= order.size()) {
+        *kind = -1;
+        *mb = -1;
+        return;
     }
+    const pipetune::TaskNode& n = graph_->node(order[cursor_]);
+    *kind = n.kind == pipetune::TaskKind::ForwardCompute ? 0 : n.kind == pipetune::TaskKind::BackwardCompute ? 1 : 2;
+    *mb = n.micro_batch;
+}
+
+bool Executor::enqueue_next() {
+    if (!in_iteration_) return false;
+    const auto& order = plan_.per_device[static_cast<size_t>(cfg_.stage)];
+    if (cursor_ < order.size()) enqueue_node(order[cursor_++]);
+    if (cursor_ < order.size()) return true;
     ck(cudaEventRecord(it_end_, comp_), "event");
+    in_iteration_ = false;
+    return false;
+}
+
+void Executor::enqueue_node(int id) {
+    const ptk_gpt_config& g = cfg_.gpt;
+    const int S = cfg_.stages, s = cfg_.stage;
+    const bool first = s == 0, last = s == S - 1;
+    const int64_t T = static_cast<int64_t>(b_) * g.seq;
+    const int64_t act_bytes = T * g.hidden * 2;
+    const pipetune::TaskNode& n = graph_->node(id);
+    const int m = n.micro_batch;
+    const int slot = m >= 0 ? m % stage_->virtual_slots() : 0;
+    // this micro-batch's view of the b_max-wide send buffer of its physical slot
+    const int split = stage_->slot_split();
+    const int64_t sub = static_cast<int64_t>(slot % split) * T * g.hidden;
+    GemmTiming& tm = stage_->gemm_timing();
+    tm.enabled = tm.armed && m >= 0 && m % tm.stride == 0;
+    if (n.kind == pipetune::TaskKind::ForwardCompute) {
+        if (!first) wait_flag(comp_, act_flag_ + m, epoch_);
+        __nv_bfloat16* out = last ? nullptr : act_send_[static_cast<size_t>(slot / split)] + sub;
+        if (!last) ck(cudaStreamWaitEvent(comp_, act_sent_[static_cast<size_t>(slot)], 0), "wait");
+        CompRecord r{id, 0, m, ev(), ev()};
+        ck(cudaEventRecord(r.start, comp_), "event");
+        stage_->forward(slot, tok_dev_ + m * T, first ? nullptr : act_recv_ + m * T * g.hidden, lab_dev_ + m * T,
+                        out, comp_);
+        ck(cudaEventRecord(r.end, comp_), "event");
+        crec_.push_back(r);
+        if (!last) {
+            send(true, m, out, act_bytes, r.end);
+            ck(cudaEventRecord(act_sent_[static_cast<size_t>(slot)], send_stream(true)), "event");
+        }
+    } else if (n.kind == pipetune::TaskKind::BackwardCompute) {
+        if (!last) wait_flag(comp_, grad_flag_ + m, epoch_);
+        __nv_bfloat16* dx = first ? nullptr : grad_send_[static_cast<size_t>(slot / split)] + sub;
+        if (!first) ck(cudaStreamWaitEvent(comp_, grad_sent_[static_cast<size_t>(slot)], 0), "wait");
+        CompRecord r{id, 1, m, ev(), ev()};
+        ck(cudaEventRecord(r.start, comp_), "event");
+        stage_->backward(slot, tok_dev_ + m * T, last ? nullptr : grad_recv_ + m * T * g.hidden, dx, comp_);
+        ck(cudaEventRecord(r.end, comp_), "event");
+        crec_.push_back(r);
+        if (!first) {
+            send(false, m, dx, act_bytes, r.end);
+            ck(cudaEventRecord(grad_sent_[static_cast<size_t>(slot)], send_stream(false)), "event");
+        }
+    } else if (n.kind == pipetune::TaskKind::GradAccum) {
+        CompRecord r{id, 2, -1, ev(), ev()};
+        ck(cudaEventRecord(r.start, comp_), "event");
+        if (defer_optimizer_)
+            stage_->finalize_grads(comp_);  // the caller all-reduces, then steps the optimizer
+        else
+            stage_->optimizer_step(cfg_.lr, cfg_.weight_decay, comp_);
+        ck(cudaEventRecord(r.end, comp_), "event");
+        crec_.push_back(r);
+    }
+}
+
+void run_local_pipeline(const std::vector<Executor*>& st, int iter, const int32_t* host_tokens) {
+    const int S = static_cast<int>(st.size());
+    for (int s = 0; s < S; ++s)
+        if (!st[s] || st[s]->cfg().stage != s || st[s]->cfg().stages != S)
+            throw std::invalid_argument("run_local_pipeline: stages[s] must be stage s of an S-stage pipeline");
+    for (Executor* e : st) e->begin_iteration(iter, host_tokens);
+    // enqueued forwards / backwards per stage (both ascending in every plan)
+    std::vector<int> nf(static_cast<size_t>(S), 0), nb(static_cast<size_t>(S), 0);
+    std::vector<bool> done(static_cast<size_t>(S), false);
+    int left = S;
+    while (left > 0) {
+        bool progress = false;
+        for (int s = 0; s < S; ++s) {
+            for (;;) {
+                if (done[s]) break;
+                int kind = -1, mb = -1;
+                st[s]->peek_next(&kind, &mb);
+                const bool ready = kind == 2 || (kind == 0 && (s == 0 || nf[s - 1] > mb)) ||
+                                   (kind == 1 && (s == S - 1 || nb[s + 1] > mb));
+                if (!ready) break;
+                if (kind == 0) ++nf[s];
+                if (kind == 1) ++nb[s];
+                if (!st[s]->enqueue_next()) {
+                    done[s] = true;
+                    --left;
+                }
+                progress = true;
+            }
+        }
+        if (!progress)
+            throw pipetune::DeadlockDetected("run_local_pipeline: no stage can enqueue its next node");
+    }
 }
 
 double Executor::finish_iteration() {
-    ck(cudaStreamSynchronize(comp_), "sync compute");
-    ck(cudaStreamSynchronize(sendst_), "sync send");
+    if (in_iteration_) throw std::logic_error("finish_iteration: the iteration is not fully enqueued");
+    // Poll instead of blocking: a stage whose peer never sends waits forever in
+    // cuStreamWaitValue32; SPEC's DeadlockDetected (errors.hpp) is raised instead.
+    cudaEvent_t send_done = ev(), send_bwd_done = ev();
+    ck(cudaEventRecord(send_done, sendst_), "event");
+    ck(cudaEventRecord(send_bwd_done, sendst_bwd_), "event");
+    const auto t0 = std::chrono::steady_clock::now();
+    auto finished = [&] {
+        for (cudaEvent_t e : {it_end_, send_done, send_bwd_done}) {
+            const cudaError_t q = cudaEventQuery(e);
+            if (q == cudaErrorNotReady) return false;
+            ck(q, "event query");
+        }
+        return true;
+    };
+    int spins = 0;
+    while (!finished()) {
+        const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (waited > deadlock_timeout_s_) {
+            poisoned_ = true;
+            // open every flag this stage waits on so its streams drain (inputs are garbage from here)
+            if (act_flag_) ck(cudaMemsetAsync(act_flag_, 0xff, cfg_.global_batch * 4, rescue_stream()), "rescue");
+            if (grad_flag_) ck(cudaMemsetAsync(grad_flag_, 0xff, cfg_.global_batch * 4, rescue_stream()), "rescue");
+            emu_.stop_contender();
+            cudaStreamSynchronize(rescue_stream());
+            throw pipetune::DeadlockDetected("stage " + std::to_string(cfg_.stage) + ": iteration not finished after " +
+                                             std::to_string(deadlock_timeout_s_) + " s (a peer never delivered)");
+        }
+        if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(spins > 4096 ? 1000 : 50));
+    }
     if (contender_on_) {
         emu_.stop_contender();
         ck(cudaStreamSynchronize(contend_[0]), "sync contender");
@@ -406,6 +526,17 @@ double Executor::finish_iteration() {
     float ms = 0.f;
     ck(cudaEventElapsedTime(&ms, it_start_, it_end_), "elapsed");
     return ms;
+}
+
+cudaStream_t Executor::rescue_stream() {
+    if (!rescue_) ck(cudaStreamCreateWithFlags(&rescue_, cudaStreamNonBlocking), "stream");
+    return rescue_;
+}
+
+int64_t Executor::iteration_start_globaltimer() {
+    int64_t v = 0;
+    ck(cudaMemcpy(&v, gt_start_, 8, cudaMemcpyDeviceToHost), "d2h");
+    return v;
 }
 
 float Executor::read_loss() {
@@ -418,18 +549,21 @@ float Executor::read_loss() {
 std::vector<int64_t> Executor::probe_link(int link, int64_t bytes, int repeats) {
     const bool fwd = link == 2 * cfg_.stage;
     if (!fwd && link != 2 * cfg_.stage - 1) throw std::invalid_argument("probe_link: not an outgoing link");
-    __nv_bfloat16* dst = fwd ? peer_act_recv_ : peer_grad_recv_;
+    // probes land in the peer's scratch block, never in its live receive slots
+    void* dst = fwd ? peer_scratch_fwd_ : peer_scratch_bwd_;
     const __nv_bfloat16* src = fwd ? act_send_.at(0) : grad_send_.at(0);
     const int64_t cap = static_cast<int64_t>(cfg_.gpt.micro_batch_size) * cfg_.gpt.seq * cfg_.gpt.hidden * 2;
-    if (!dst || bytes > cap) throw std::invalid_argument("probe_link: peer not connected or payload too large");
+    if (!dst || bytes > cap || bytes > static_cast<int64_t>(kScratch))
+        throw std::invalid_argument("probe_link: peer not connected or payload too large");
+    cudaStream_t st = send_stream(fwd);
     std::vector<int64_t> out;
     cudaEvent_t a, b;
     ck(cudaEventCreate(&a), "event");
     ck(cudaEventCreate(&b), "event");
     for (int r = 0; r < repeats; ++r) {
-        ck(cudaEventRecord(a, sendst_), "event");
-        ck(emu_.paced_copy(fwd ? 0 : 1, dst, src, bytes, sendst_), "probe copy");
-        ck(cudaEventRecord(b, sendst_), "event");
+        ck(cudaEventRecord(a, st), "event");
+        ck(emu_.paced_copy(fwd ? 0 : 1, dst, src, bytes, st), "probe copy");
+        ck(cudaEventRecord(b, st), "event");
         ck(cudaEventSynchronize(b), "sync");
         float ms = 0.f;
         ck(cudaEventElapsedTime(&ms, a, b), "elapsed");

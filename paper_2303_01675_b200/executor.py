@@ -38,6 +38,11 @@ def _declare(lib):
     lib.ptk_globaltimer.restype = C.c_int64
     lib.ptk_exec_run_iteration.argtypes = [V, I, V]
     lib.ptk_exec_finish_iteration.argtypes = [V, P(C.c_double)]
+    lib.ptk_exec_begin_iteration.argtypes = [V, I, V]
+    lib.ptk_exec_enqueue_next.argtypes = [V, P(I)]
+    lib.ptk_exec_run_local.argtypes = [P(V), I, I, V]
+    lib.ptk_exec_set_deadlock_timeout.argtypes = [V, C.c_double]
+    lib.ptk_exec_set_send_streams.argtypes = [V, I]
     lib.ptk_exec_read_loss.argtypes = [V, P(C.c_float)]
     lib.ptk_exec_timeline_json.argtypes = [V, C.c_char_p, C.c_size_t, P(C.c_size_t)]
     lib.ptk_exec_probe_link.argtypes = [V, I, C.c_int64, I, P(C.c_int64)]
@@ -222,6 +227,20 @@ class StageExecutor:
     def run_iteration(self, it: int, host_tokens=None):
         L.check(self.lib.ptk_exec_run_iteration(self.h, it, host_tokens if host_tokens is not None else None))
 
+    def begin_iteration(self, it: int, host_tokens=None):
+        L.check(self.lib.ptk_exec_begin_iteration(self.h, it, host_tokens if host_tokens is not None else None))
+
+    def enqueue_next(self) -> bool:
+        more = C.c_int()
+        L.check(self.lib.ptk_exec_enqueue_next(self.h, C.byref(more)))
+        return bool(more.value)
+
+    def set_deadlock_timeout(self, seconds: float):
+        L.check(self.lib.ptk_exec_set_deadlock_timeout(self.h, float(seconds)))
+
+    def set_send_streams(self, per_link: bool):
+        L.check(self.lib.ptk_exec_set_send_streams(self.h, int(bool(per_link))))
+
     def finish_iteration(self) -> float:
         ms = C.c_double()
         L.check(self.lib.ptk_exec_finish_iteration(self.h, C.byref(ms)))
@@ -256,6 +275,16 @@ class StageExecutor:
     def stage_view(self):
         from .stage import GptStage
         return GptStage.view(self.lib, self.lib.ptk_exec_stage(self.h), self.shape, self.cfg.gpt.micro_batch_size)
+
+    @staticmethod
+    def run_local(stages: "list[StageExecutor]", it: int, host_tokens=None) -> list[float]:
+        """One iteration of a whole same-process pipeline (stages[s] = stage s, connect_local-wired),
+        enqueued in a global dependency-respecting order (ptk_exec_run_local), then finished stage by
+        stage; returns each stage's device ms."""
+        lib = stages[0].lib
+        arr = (C.c_void_p * len(stages))(*[e.h.value for e in stages])
+        L.check(lib.ptk_exec_run_local(arr, len(stages), it, host_tokens if host_tokens is not None else None))
+        return [e.finish_iteration() for e in stages]
 
     def close(self):
         if getattr(self, "h", None):

@@ -67,12 +67,33 @@ class ModelShape:
         n = sum(pa if u % 2 == 0 else pm for u in range(hb, he))
         return n + self.param_count(0, has_embedding, has_head)
 
-    def stash_bytes_halves(self, hb: int, he: int, has_head: bool) -> int:
+    def stash_bytes_halves(self, hb: int, he: int, has_head: bool, has_embedding: bool | None = None) -> int:
+        """Activation-stash bytes per in-flight sample of half-layer blocks [hb, he), exactly what
+        GptStage allocates per slot divided by b (gpt_stage.cu, "activation stash"): per attention
+        block x_in (not on a stage's first layer without the embedding: it reads the receive block),
+        ln1, qkv, attn_o, its LayerNorm stats and lse; x_mid when the layer has both blocks; per MLP
+        block ln2, fc1 pre-activation and activation and stats; the head's final LN input/output,
+        bf16 dlogits and stats (+ BERT's transform), BERT's embedding sum and stats."""
+        if has_embedding is None:
+            has_embedding = hb == 0
         s, h, f, H = self.seq, self.hidden, self.ffn, self.heads
-        attn = 7 * s * h * 2 + 2 * s * 4 + H * s * 4  # x_in, ln1, qkv, attn_o, x_mid; LN stats; lse
-        mlp = (s * h + 2 * s * f) * 2 + 2 * s * 4     # ln2, fc1 pre/act; LN stats
-        out = sum(attn if u % 2 == 0 else mlp for u in range(hb, he))
-        return out + self.stash_bytes_per_sample(0, has_head)
+        lb, le, sfa, slm = halves_to_layers(hb, he)
+        out = 0
+        for i in range(lb, le):
+            A = not (i == lb and sfa)
+            M = not (i == le - 1 and slm)
+            if A:
+                out += (0 if (i == lb and not has_embedding) else s * h * 2)  # x_in
+                out += (s * h + 3 * s * h + s * h) * 2 + 2 * s * 4 + H * s * 4  # ln1, qkv, attn_o; stats; lse
+            if A and M:
+                out += s * h * 2  # x_mid
+            if M:
+                out += (s * h + 2 * s * f) * 2 + 2 * s * 4  # ln2, fc1 pre/act; stats
+        if has_head:
+            out += 2 * s * h * 2 + s * self.vocab * 2 + 2 * s * 4 + (2 * s * h * 2 if self.arch == "bert" else 0)
+        if has_embedding and self.arch == "bert":
+            out += s * h * 2 + 2 * s * 4
+        return out
 
     def flops_halves(self, hb: int, he: int, has_head: bool) -> float:
         """Training FLOPs per sample of half-layer blocks [hb, he) (+ the head)."""
@@ -93,15 +114,10 @@ class ModelShape:
             n += V * h + 2 * h + (h * h + h if self.arch == "bert" else 0)
         return n
 
-    def stash_bytes_per_sample(self, n_layers: int, has_head: bool) -> int:
-        """Activation bytes one in-flight sample keeps on a stage until its backward
-        (mirrors GptStage's stash: bf16 activations, fp32 LN stats and attention lse)."""
-        s, h, f, H = self.seq, self.hidden, self.ffn, self.heads
-        per_layer = (5 * s * h + 3 * s * h + 2 * s * f) * 2 + 4 * s * 4 + H * s * 4
-        out = n_layers * per_layer
-        if has_head:
-            out += 2 * s * h * 2 + s * self.vocab * 2 + 2 * s * 4
-        return out
+    def stash_bytes_per_sample(self, n_layers: int, has_head: bool, has_embedding: bool = True) -> int:
+        """Activation bytes one in-flight sample keeps on a stage of `n_layers` whole layers until
+        its backward (stash_bytes_halves over whole layers; exact against ptk_stage_stash_bytes)."""
+        return self.stash_bytes_halves(0, 2 * n_layers, has_head, has_embedding)
 
 
 GPT_1_3B = ModelShape(24, 2048, 32, 8192, 1024, 50304)

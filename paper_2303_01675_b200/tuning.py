@@ -100,7 +100,8 @@ def memory_model(shape, layers, stages: int, global_batch: int, halves: bool = F
     for s_, (lb, le) in enumerate(layers):
         first, last = s_ == 0, s_ == stages - 1
         params = shape.param_count_halves(lb, le, first, last) if halves else shape.param_count(le - lb, first, last)
-        stash = shape.stash_bytes_halves(lb, le, last) if halves else shape.stash_bytes_per_sample(le - lb, last)
+        stash = shape.stash_bytes_halves(lb, le, last, first) if halves else \
+            shape.stash_bytes_per_sample(le - lb, last, first)
         st.append(pt.StageProfile(
             stage_id=s_, weight_bytes=18 * params,
             activation_bytes_per_sample=stash,

@@ -16,6 +16,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[2]
 REF = ROOT / "oracle" / "_ref" / "ref_dump"
 OUT = Path(__file__).with_name("planner_ref.json")
+C1 = Path(__file__).with_name("c1_sequences.json")
 
 
 def grid():
@@ -53,6 +54,12 @@ def main():
         out["cases"].append(e)
     OUT.write_text(json.dumps(out, separators=(",", ":")) + "\n")
     print(f"wrote {len(cases)} cases to {OUT}")
+    # configs[0] (C1 toy: S=4, M=16, b=1) per-device sequences for k = 1, 2, 4, 16 (GPipe-equivalent):
+    # what the GPU executor's recorded order must equal (tests/test_pipeline_gpu.py)
+    c1 = [(4, 16, 1, 1, k) for k in (1, 2, 4, 16)] + [(2, 8, 1, 1, k) for k in (1, 2, 4)]
+    seqs = {f"S{S}_M{M}_b{b}_k{k}": json.loads(line)["sequences"] for (S, M, b, _, k), line in zip(c1, run(c1))}
+    C1.write_text(json.dumps({"generator": out["generator"], "sequences": seqs}, indent=1) + "\n")
+    print(f"wrote {len(seqs)} C1 sequence sets to {C1}")
 
 
 if __name__ == "__main__":

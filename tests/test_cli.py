@@ -40,3 +40,29 @@ def test_exit_codes(tmp_path):
     inf.write_text(json.dumps({"model": {"global_batch": 4, "stages": [{"weight_bytes": 1000}]},
                                "cluster": {"device_memory_limit": 10, "devices": 1}}))
     assert cli.main(["enumerate", "--config", str(inf)]) == 3      # InfeasibleModel
+
+
+def test_missing_required_fields_are_config_errors(tmp_path):
+    """Mandatory request fields missing -> ConfigError / exit code 2, never a crash
+    (enumerate without a cluster, tune without a horizon, simulate without a plan)."""
+    model = {"global_batch": 4, "stages": [{}, {}]}
+    cases = [("enumerate", {"model": model}),
+             ("tune", {"model": model, "cluster": {"device_memory_limit": 10**12, "devices": 2},
+                       "traces": [{"link": 0}, {"link": 1}]}),
+             ("compare", {"model": model})]
+    for cmd, cfg in cases:
+        p = tmp_path / f"{cmd}.json"
+        p.write_text(json.dumps(cfg))
+        assert cli.main([cmd, "--config", str(p)]) == 2, cmd
+
+
+def test_abi_missing_keys_return_config_error():
+    from paper_2303_01675_b200 import pipetune as pt
+    import pytest
+    model = {"global_batch": 4, "stages": [{}]}
+    for req in ({"op": "decide", "model": model}, {"op": "transfer"}, {"op": "estimate", "samples": []},
+                {"op": "simulate", "model": model}, {"op": "decide", "model": model, "candidates": [[1]],
+                                                    "compute_profile": [], "samples": []}):
+        with pytest.raises(pt.PipetuneError) as e:
+            pt.scenario(req)
+        assert e.value.kind == "ConfigError", (req, e.value.kind)

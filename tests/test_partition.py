@@ -42,5 +42,6 @@ def test_halves_to_layers():
 def test_half_memory_model_matches_whole_layers():
     s = GPT_1_3B
     assert s.param_count_halves(0, 48, True, True) == s.param_count(24, True, True)
-    assert s.stash_bytes_halves(4, 10, False) == s.stash_bytes_per_sample(3, False)
+    assert s.stash_bytes_halves(4, 10, False) == s.stash_bytes_per_sample(3, False, has_embedding=False)
+    assert s.stash_bytes_halves(0, 6, False) == s.stash_bytes_per_sample(3, False)
     assert abs(s.flops_halves(0, 48, True) - s.flops_per_sample()) < 1e-3 * s.flops_per_sample()

@@ -109,3 +109,23 @@ def test_errors_are_typed():
     with pytest.raises(pt.PipetuneError) as e:
         pt.plan_kfkb(pt.uniform_model(2, 4), 3, 1)  # b=3 does not divide 4
     assert e.value.kind == "ConfigError"
+
+
+def test_reference_harness_source_compatible_with_our_headers(tmp_path):
+    """Drop-in at the C++ source level: the SAME harness source that links the reference planner
+    (oracle/ref_dump.cpp) compiles against OUR include/pipetune headers, links libptk.so instead of
+    the reference objects, and prints byte-identical output over the whole golden grid."""
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    from paper_2303_01675_b200 import _lib as L
+    exe = tmp_path / "ref_dump_ptk"
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", str(ROOT / "oracle" / "ref_dump.cpp"),
+                    f"-L{L.LIB_PATH.parent}", "-lptk", f"-Wl,-rpath,{L.LIB_PATH.parent}", "-o", str(exe)],
+                   check=True, capture_output=True)
+    fwd, bwd = GOLDEN["payload"]["fwd_base"], GOLDEN["payload"]["bwd_base"]
+    inp = "".join(f"{S} {M} {b} {kind} {k} {fwd} {bwd}\n" for S, M, b, kind, k in (e["case"] for e in GOLDEN["cases"]))
+    out = subprocess.run([str(exe)], input=inp, capture_output=True, text=True, check=True).stdout.splitlines()
+    assert len(out) == len(GOLDEN["cases"])
+    bad = [e["case"] for e, line in zip(GOLDEN["cases"], out)
+           if hashlib.sha256(line.encode()).hexdigest() != e["sha256"]]
+    assert not bad, bad[:5]
