@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "../runtime/preload.h"
@@ -108,8 +109,18 @@ __device__ unsigned long long g_fwd_trace[2][64][8];
     do {                                                                        \
         if (blockIdx.x == 0 && (step) < 64) g_fwd_trace[role][step][ev] = clock64(); \
     } while (0)
+// ping-pong forward: [0 lane A softmax, 1 lane B softmax, 2 MMA][lane block][event]
+__device__ unsigned long long g_pp_trace[3][64][8];
+__device__ unsigned long long g_pp_cta[160][4];  // per CTA: globaltimer at entry, first S issue, MMA done, exit
+#define PTRACE(role, step, ev)                                                  \
+    do {                                                                        \
+        if (blockIdx.x == 0 && (step) < 64) g_pp_trace[role][step][ev] = clock64(); \
+    } while (0)
 #else
 #define FTRACE(role, step, ev) \
+    do {                       \
+    } while (0)
+#define PTRACE(role, step, ev) \
     do {                       \
     } while (0)
 #endif
@@ -424,6 +435,408 @@ __global__ void __launch_bounds__(32 * (4 + 4 * NQ), 1)
     }
 }
 
+// ============================================================================
+// Forward, d = 64, two-tile ping-pong (the default for GPT-1.3B / BERT-large).
+//
+// The single-tile kernel above is bound by its softmax phase (MUFU ex2 plus
+// the non-exponential work of the same warps, all phase-locked on one S
+// buffer and one P buffer).  Here a CTA works on a PAIR of 128-query tiles of
+// one (head, sample) — lane A = query block 2p, lane B = 2p+1 — which share
+// every K/V block.  Each lane has its own S (TMEM), P (smem), O (TMEM,
+// double-buffered across pairs) and four softmax warps with ONE THREAD PER
+// QUERY ROW (all 128 columns of the row in registers: the row max needs no
+// cross-warp exchange and no named barrier).  The MMA warp keeps each lane one
+// score product ahead (S_L(j+1) is issued as soon as lane L has read S_L(j)
+// into registers) and issues PV_L(j) when lane L's P is in smem, so while one
+// lane's warps do their non-exponential work (TMEM loads, max, P stores, O
+// rescale) the other lane's exponentials keep the MUFU busy.
+// ============================================================================
+struct Fa2Cfg {
+    static constexpr int D = 64;
+    static constexpr int kQBytes = kBlk * D * 2;     // 16 KiB, K-major sw128
+    static constexpr int kKVBytes = 2 * kBlk * D * 2;  // K then V
+    static constexpr int kStages = 4;
+    static constexpr int kSmem = 4 * kQBytes + kStages * kKVBytes + 1024 + 768;
+    // TMEM: S_L at 128 L (fp32 128x128); P_L at 256 + 64 L (bf16x2-packed 128x128, the A operand of
+    // P·V read straight from TMEM); O_L at 384 + 64 L (fp32 128x64)
+    static constexpr uint32_t kTmemS = 0, kTmemP = 256, kTmemO = 384;
+};
+static_assert(Fa2Cfg::kSmem <= 232448, "ping-pong forward smem");
+
+
+constexpr int kFa2MaxItems = 24;  // pair items per CTA (launch_fwd_pp enforces it)
+
+// Pair cursor: item k of this CTA -> (pair p, head, sample); lane L's tile is query block 2p + L.
+struct Fa2Item {
+    int p, head, bi;
+    bool valid;
+};
+
+__device__ __forceinline__ Fa2Item fa2_item(const FaArgs& a, int k) {
+    const int G = gridDim.x, i = blockIdx.x;
+    const int npair = a.s / (2 * kBlk);
+    const int per = a.H * a.b;
+    const int t = (k & 1) ? (k + 1) * G - 1 - i : k * G + i;
+    Fa2Item it;
+    it.valid = t < npair * per;
+    const int rank = t / per, rem = t % per;
+    it.p = npair - 1 - rank;  // heaviest first
+    it.head = rem % a.H;
+    it.bi = rem / a.H;
+    return it;
+}
+
+__device__ __forceinline__ int fa2_nkv(const FaArgs& a, int p, int lane) {
+    return a.causal ? 2 * p + lane + 1 : a.s / kBlk;
+}
+
+// kFwdPoly: of every 16 unmasked exponentials, this many on the FMA pipe (ex2_poly) instead of MUFU
+template <int kFwdPoly>
+__global__ void __launch_bounds__(384, 1)
+    flash_fwd_pp_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
+                        const __grid_constant__ FaArgs a) {
+    using C = Fa2Cfg;
+    constexpr int D = C::D, NS = C::kStages;
+    constexpr uint32_t kIdescS = make_idesc_bf16(kBlk, kBlk, false, false);
+    constexpr uint32_t kIdescO = make_idesc_bf16(kBlk, D, false, true);
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;                        // [lane][qbuf] 16 KiB each
+    uint8_t* sKV = sQ + 4 * C::kQBytes;        // [stage] K 16 KiB, V 16 KiB
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NS * C::kKVBytes);
+    uint64_t* q_full = bars + 0;     // [lane][qbuf]
+    uint64_t* q_empty = bars + 4;    // [lane][qbuf]
+    uint64_t* kv_full = bars + 8;    // [NS]
+    uint64_t* kv_empty = bars + 12;  // [NS]
+    uint64_t* s_full = bars + 16;    // [lane]
+    uint64_t* s_empty = bars + 18;   // [lane]
+    uint64_t* p_full = bars + 20;    // [lane]
+    uint64_t* pv_done = bars + 22;   // [lane]
+    uint64_t* o_full = bars + 24;    // [lane]
+    uint64_t* o_empty = bars + 28;   // [lane]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+    // this CTA's pair items, decoded once (the role loops never divide: integer division runs on
+    // the MUFU, which the softmax warps saturate)
+    int4* items = reinterpret_cast<int4*>(bars + 34);  // {p, head, bi, kvbase}
+    int* n_items = reinterpret_cast<int*>(bars + 34 + 2 * kFa2MaxItems);
+
+    const int warp = threadIdx.x / 32;
+    const uint32_t lane_id_ = lane_id();
+#ifdef PTK_ATTN_TRACE
+    auto gt = [] {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return t;
+    };
+    if (threadIdx.x == 0 && blockIdx.x < 160) g_pp_cta[blockIdx.x][0] = gt();
+#endif
+
+    if (warp == 0 && lane_id_ == 0) {
+        tma_prefetch_desc(&tmQK);
+        tma_prefetch_desc(&tmV);
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+            mbar_init(&o_full[i], 1);
+            mbar_init(&o_empty[i], 4);
+        }
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int l = 0; l < 2; ++l) {
+            mbar_init(&s_full[l], 1);
+            mbar_init(&s_empty[l], 4);
+            mbar_init(&p_full[l], 4);
+            mbar_init(&pv_done[l], 1);
+        }
+        fence_barrier_init();
+        int kvb = 0, n = 0;
+        for (; n < kFa2MaxItems; ++n) {
+            const Fa2Item it = fa2_item(a, n);
+            if (!it.valid) break;
+            items[n] = make_int4(it.p, it.head, it.bi, kvb);
+            kvb += fa2_nkv(a, it.p, 1);
+        }
+        *n_items = n;
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_begin();
+    // registers: 3 warps per SM sub-partition at 168 each at launch; the producer / MMA warpgroup
+    // (warps 0-3) gives its share to the softmax warpgroups (a thread holds a 128-column row)
+
+    if (warp == 0) {
+        reg_dealloc<72>();
+        if (lane_id_ == 0) {  // ---------------- TMA producer
+            int n = 0;
+            const int nit = *n_items;
+            for (int k = 0; k < nit; ++k) {
+                const int4 itv = items[k];
+                const Fa2Item it{itv.x, itv.y, itv.z, true};
+                const int qbuf = k & 1;
+                for (int l = 0; l < 2; ++l) {
+                    mbar_wait(&q_empty[l * 2 + qbuf], ((k >> 1) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&q_full[l * 2 + qbuf], C::kQBytes);
+                    tma_load_4d(&tmQK, &q_full[l * 2 + qbuf], sQ + (l * 2 + qbuf) * C::kQBytes, 0,
+                                (2 * it.p + l) * kBlk, it.head, it.bi);
+                }
+                const int nkv = fa2_nkv(a, it.p, 1);
+                for (int j = 0; j < nkv; ++j, ++n) {
+                    const int st = n % NS;
+                    mbar_wait(&kv_empty[st], ((n / NS) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&kv_full[st], C::kKVBytes);
+                    uint8_t* kk = sKV + st * C::kKVBytes;
+                    uint8_t* vv = kk + kBlk * D * 2;
+                    tma_load_4d(&tmQK, &kv_full[st], kk, 0, j * kBlk, a.H + it.head, it.bi);
+                    tma_load_4d(&tmV, &kv_full[st], vv, 0, j * kBlk, 2 * a.H + it.head, it.bi);
+                    tma_load_4d(&tmV, &kv_full[st], vv + 8192, 0, j * kBlk + 64, 2 * a.H + it.head, it.bi);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        reg_dealloc<72>();
+        if (lane_id_ == 0) {  // ---------------- MMA issuer
+            // Per lane: the block stream (item k, key block j) over all items; the KV stage of a
+            // block is the producer's running block counter.  S is issued one block ahead of PV.
+            struct LaneCur {
+                int k, j, n, nkv, kvbase;  // n = blocks of this lane so far; kvbase = KV counter at item start
+                bool valid;
+            };
+            const int nit = *n_items;
+            auto lane_start = [&](LaneCur& c, int l, int k, int) {
+                c.k = k;
+                c.j = 0;
+                c.valid = k < nit;
+                const int4 itv = c.valid ? items[k] : make_int4(0, 0, 0, 0);
+                c.nkv = c.valid ? fa2_nkv(a, itv.x, l) : 0;
+                c.kvbase = itv.w;
+            };
+            // KV users of the current item's stages: 2 where both lanes use the block, else 1
+            uint8_t kv_users[NS];
+            for (int i = 0; i < NS; ++i) kv_users[i] = 0;
+            LaneCur cs[2], cp[2];  // S-issue and PV-issue cursors per lane
+            for (int l = 0; l < 2; ++l) {
+                lane_start(cs[l], l, 0, 0);
+                cs[l].n = 0;
+                lane_start(cp[l], l, 0, 0);
+                cp[l].n = 0;
+            }
+            auto advance = [&](LaneCur& c, int l) {
+                ++c.n;
+                if (++c.j == c.nkv) {
+                    const int n = c.n;
+                    lane_start(c, l, c.k + 1, 0);
+                    c.n = n;
+                }
+            };
+            auto issue_s = [&](int l) {
+                LaneCur& c = cs[l];
+                const int st = (c.kvbase + c.j) % NS, qbuf = c.k & 1;
+                if (c.j == 0) mbar_wait(&q_full[l * 2 + qbuf], (c.k >> 1) & 1);
+                mbar_wait(&kv_full[st], ((c.kvbase + c.j) / NS) & 1);
+                mbar_wait(&s_empty[l], (c.n & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t q_base = smem_u32(sQ + (l * 2 + qbuf) * C::kQBytes);
+                const uint32_t k_base = smem_u32(sKV + st * C::kKVBytes);
+                const uint32_t d_tmem = tmem + C::kTmemS + 128 * l;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    mma_bf16_ss(d_tmem, make_sw128_desc(q_base + kk * 32, 16, 1024),
+                                make_sw128_desc(k_base + kk * 32, 16, 1024), kIdescS, kk > 0 ? 1u : 0u);
+                mma_commit(&s_full[l]);
+                PTRACE(2, c.n, l * 4 + 0);
+                if (c.j == c.nkv - 1) mma_commit(&q_empty[l * 2 + qbuf]);
+                advance(c, l);
+            };
+            auto issue_pv = [&](int l) {
+                LaneCur& c = cp[l];
+                const int g = c.kvbase + c.j, st = g % NS;
+                mbar_wait(&p_full[l], c.n & 1);
+                PTRACE(2, c.n, l * 4 + 1);
+                // single O buffer per lane: the epilogue of the previous pair always read it before
+                // the same warps produced this pair's first P, so this wait never stalls
+                if (c.j == 0) mbar_wait(&o_empty[l], (c.k & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t p_tmem = tmem + C::kTmemP + 64 * l;
+                const uint32_t v_base = smem_u32(sKV + st * C::kKVBytes + kBlk * D * 2);
+                const uint32_t o_tmem = tmem + C::kTmemO + 64 * l;
+#pragma unroll
+                for (int kk = 0; kk < kBlk / 16; ++kk) {
+                    const uint32_t vb = v_base + (kk / 4) * 8192 + (kk % 4) * 2048;
+                    mma_bf16_ts(o_tmem, p_tmem + kk * 8, make_sw128_desc(vb, 8192, 1024), kIdescO,
+                                (c.j > 0 || kk > 0) ? 1u : 0u);
+                }
+                mma_commit(&pv_done[l]);
+                PTRACE(2, c.n, l * 4 + 2);
+                // the KV stage is free once every lane that uses this block has issued its PV
+                if (kv_users[st] == 0) kv_users[st] = (c.j < fa2_nkv(a, items[c.k].x, 0)) ? 2 : 1;
+                if (--kv_users[st] == 0) mma_commit(&kv_empty[st]);
+                if (c.j == c.nkv - 1) mma_commit(&o_full[l]);
+                advance(c, l);
+            };
+            for (int l = 0; l < 2; ++l)
+                if (cs[l].valid) issue_s(l);
+#ifdef PTK_ATTN_TRACE
+            if (blockIdx.x < 160) g_pp_cta[blockIdx.x][1] = gt();
+#endif
+            while (cp[0].valid || cp[1].valid) {
+                for (int l = 0; l < 2; ++l) {
+                    if (!cp[l].valid) continue;
+                    if (cs[l].valid) issue_s(l);  // one block ahead
+                    issue_pv(l);
+                }
+            }
+        }
+    } else if (warp < 4) {
+        reg_dealloc<72>();
+    } else {  // ---------------- softmax / epilogue: thread = query row of lane L
+        reg_alloc<208>();
+        // warps 4-7 = lane A, 8-11 = lane B; each set covers the four TMEM lane quarters (warp % 4)
+        const int L = (warp - 4) >> 2;
+        const int quad = warp & 3;
+        const int r = quad * 32 + static_cast<int>(lane_id_);
+        const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+        const uint32_t s_cols = tmem + lane_base + C::kTmemS + 128 * L;
+        const uint32_t p_cols = tmem + lane_base + C::kTmemP + 64 * L;
+        int n = 0;
+        const int nit = *n_items;
+        for (int k = 0; k < nit; ++k) {
+            const int4 itv = items[k];
+            const Fa2Item it{itv.x, itv.y, itv.z, true};
+            const int qb = 2 * it.p + L, nkv = fa2_nkv(a, it.p, L);
+            const uint32_t o_cols = tmem + lane_base + C::kTmemO + 64 * L;
+            float m = -INFINITY, l = 0.f;
+            const bool tr = (warp & 3) == 0 && lane_id_ == 0;
+            for (int j = 0; j < nkv; ++j, ++n) {
+                mbar_wait(&s_full[L], n & 1);
+                if (tr) PTRACE(L, n, 0);
+                tc_fence_after();
+                float x[kBlk];
+#pragma unroll
+                for (int cc = 0; cc < kBlk / 32; ++cc) tmem_ld_32x32b_x32_nw(s_cols + cc * 32, x + cc * 32);
+                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane_id_ == 0) mbar_arrive(&s_empty[L]);
+                if (tr) PTRACE(L, n, 1);
+                const bool diag = a.causal && j == qb;
+                float mr8[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mr8[i] = -INFINITY;
+                if (diag) {
+#pragma unroll
+                    for (int e = 0; e < kBlk; ++e) {
+                        if (e > r) x[e] = -INFINITY;
+                        mr8[e & 7] = fmaxf(mr8[e & 7], x[e]);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < kBlk; ++e) mr8[e & 7] = fmaxf(mr8[e & 7], x[e]);
+                }
+                const float mraw = fmaxf(fmaxf(fmaxf(mr8[0], mr8[1]), fmaxf(mr8[2], mr8[3])),
+                                         fmaxf(fmaxf(mr8[4], mr8[5]), fmaxf(mr8[6], mr8[7])));
+                const float pmx = mraw * a.scale_log2;
+                const float mx = pmx > m + kLazyRescaleLog2 ? pmx : m;
+                const float alpha = ex2(m - mx);
+                float s8[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s8[i] = 0.f;
+                const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), mm2 = make_float2(-mx, -mx);
+                float2* s2 = reinterpret_cast<float2*>(s8);
+                if (diag) {
+#pragma unroll
+                    for (int e = 0; e < kBlk; e += 2) {
+                        const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, mm2);
+                        x[e] = ex2(t.x);
+                        x[e + 1] = ex2(t.y);
+                        s2[(e >> 1) & 3] = __fadd2_rn(s2[(e >> 1) & 3], make_float2(x[e], x[e + 1]));
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < kBlk; e += 2) {
+                        const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, mm2);
+                        if (kFwdPoly > 0 && ((e >> 1) & 7) < kFwdPoly / 2) {  // first kFwdPoly of every 16
+                            x[e] = ex2_poly(t.x);
+                            x[e + 1] = ex2_poly(t.y);
+                        } else {
+                            x[e] = ex2(t.x);
+                            x[e + 1] = ex2(t.y);
+                        }
+                        s2[(e >> 1) & 3] = __fadd2_rn(s2[(e >> 1) & 3], make_float2(x[e], x[e + 1]));
+                    }
+                }
+                const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+                l = l * alpha + sum;
+                m = mx;
+                if (tr) PTRACE(L, n, 2);
+                if (n > 0) {
+                    mbar_wait(&pv_done[L], (n - 1) & 1);  // P buffer free, O of this pair stable
+                    tc_fence_after();
+                }
+                if (tr) PTRACE(L, n, 3);
+                // P (bf16, two per 32-bit column) -> TMEM: the A operand of this lane's P·V
+                // packed in place: x[q] = bf16x2(x[2q], x[2q+1]) (x[2q..] not yet overwritten)
+#pragma unroll
+                for (int q = 0; q < kBlk / 2; ++q) x[q] = __uint_as_float(pack_bf16(x[2 * q], x[2 * q + 1]));
+                tmem_st_32x32b_x32_f_nw(p_cols, x);
+                tmem_st_32x32b_x32_f_nw(p_cols + 32, x + 32);
+                if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+                    for (int cc = 0; cc < D; cc += 16) {
+                        float v[16];
+                        tmem_ld_32x32b_x16(o_cols + cc, v);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] *= alpha;
+                        tmem_st_32x32b_x16(o_cols + cc, v);
+                    }
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane_id_ == 0) mbar_arrive(&p_full[L]);
+                if (tr) PTRACE(L, n, 4);
+            }
+            mbar_wait(&o_full[L], k & 1);
+            tc_fence_after();
+            const float inv = 1.f / l;
+            const int q = qb * kBlk + r;
+            __nv_bfloat16* orow = a.o + (static_cast<int64_t>(it.bi) * a.s + q) * a.h + it.head * D;
+#pragma unroll
+            for (int cc = 0; cc < D; cc += 16) {
+                float v[16];
+                tmem_ld_32x32b_x16(o_cols + cc, v);
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    uint4 u;
+                    u.x = pack_bf16(v[g * 8 + 0] * inv, v[g * 8 + 1] * inv);
+                    u.y = pack_bf16(v[g * 8 + 2] * inv, v[g * 8 + 3] * inv);
+                    u.z = pack_bf16(v[g * 8 + 4] * inv, v[g * 8 + 5] * inv);
+                    u.w = pack_bf16(v[g * 8 + 6] * inv, v[g * 8 + 7] * inv);
+                    *reinterpret_cast<uint4*>(orow + cc + g * 8) = u;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id_ == 0) mbar_arrive(&o_empty[L]);
+            a.lse[(static_cast<int64_t>(it.bi) * a.H + it.head) * a.s + q] = m + __log2f(l);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+#ifdef PTK_ATTN_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 160) g_pp_cta[blockIdx.x][3] = gt();
+#endif
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -458,8 +871,52 @@ cudaError_t qkv_map(CUtensorMap* m, const void* qkv, int b, int s, int H, int d,
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+bool fwd_pp_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("PTK_FWD_PP");
+        return v == nullptr || v[0] != '0';
+    }();
+    return on;
+}
+
+int fwd_poly() {
+    static const int v = [] {
+        const char* e = std::getenv("PTK_FWD_POLY");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <int D>
-cudaError_t launch_fwd(const FlashPlan& p, cudaStream_t st) {
+cudaError_t launch_fwd_single(const FlashPlan& p, cudaStream_t st);
+
+template <int POLY>
+cudaError_t launch_fwd_pp_t(const FlashPlan& p, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(flash_fwd_pp_kernel<POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Fa2Cfg::kSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    FaArgs a{p.o, p.lse, p.s, p.H, p.H * p.d, p.b, p.scale_log2, p.causal};
+    const int items = p.s / (2 * kBlk) * p.H * p.b;
+    const int grid = items < sm_count() ? items : sm_count();
+    if ((items + grid - 1) / grid > kFa2MaxItems) return launch_fwd_single<64>(p, st);
+    return launch_kernel(flash_fwd_pp_kernel<POLY>, grid, 384, Fa2Cfg::kSmem, st, 1, p.tmQK, p.tmV, a);
+}
+
+cudaError_t launch_fwd_pp(const FlashPlan& p, cudaStream_t st) {
+    switch (fwd_poly()) {
+        case 2: return launch_fwd_pp_t<2>(p, st);
+        case 4: return launch_fwd_pp_t<4>(p, st);
+        case 6: return launch_fwd_pp_t<6>(p, st);
+        default: return launch_fwd_pp_t<0>(p, st);
+    }
+}
+
+template <int D>
+cudaError_t launch_fwd_single(const FlashPlan& p, cudaStream_t st) {
     using C = FaCfg<D>;
     static bool attr = false;
     if (!attr) {
@@ -472,6 +929,12 @@ cudaError_t launch_fwd(const FlashPlan& p, cudaStream_t st) {
     const int tiles = p.s / kBlk * p.H * p.b;
     const int grid = tiles < sm_count() ? tiles : sm_count();
     return launch_kernel(flash_fwd_kernel<D, kFwdNQ>, grid, 32 * (4 + 4 * kFwdNQ), C::kSmem, st, 1, p.tmQK, p.tmV, a);
+}
+
+template <int D>
+cudaError_t launch_fwd(const FlashPlan& p, cudaStream_t st) {
+    if (D == 64 && p.s % (2 * kBlk) == 0 && fwd_pp_enabled()) return launch_fwd_pp(p, st);
+    return launch_fwd_single<D>(p, st);
 }
 
 }  // namespace

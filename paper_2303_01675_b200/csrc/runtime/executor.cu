@@ -96,10 +96,12 @@ Executor::Executor(const ptk_exec_config& c) : cfg_(c) {
 
 Executor::~Executor() {
     emu_.stop_contender();
-    if (in_iteration_) {  // destroyed half-enqueued: open this stage's flags so nothing waits forever
+    if (in_iteration_ || poisoned_) {  // half-enqueued or deadlocked: open this stage's flags so nothing waits forever
         poisoned_ = true;
-        if (act_flag_) cudaMemsetAsync(act_flag_, 0xff, cfg_.global_batch * 4, rescue_stream());
-        if (grad_flag_) cudaMemsetAsync(grad_flag_, 0xff, cfg_.global_batch * 4, rescue_stream());
+        try {
+            open_flags();
+        } catch (...) {
+        }
     }
     cudaStreamSynchronize(comp_);
     cudaStreamSynchronize(sendst_);
@@ -508,11 +510,8 @@ double Executor::finish_iteration() {
         const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (waited > deadlock_timeout_s_) {
             poisoned_ = true;
-            // open every flag this stage waits on so its streams drain (inputs are garbage from here)
-            if (act_flag_) ck(cudaMemsetAsync(act_flag_, 0xff, cfg_.global_batch * 4, rescue_stream()), "rescue");
-            if (grad_flag_) ck(cudaMemsetAsync(grad_flag_, 0xff, cfg_.global_batch * 4, rescue_stream()), "rescue");
+            open_flags();  // this stage's streams drain (their inputs are garbage from here)
             emu_.stop_contender();
-            cudaStreamSynchronize(rescue_stream());
             throw pipetune::DeadlockDetected("stage " + std::to_string(cfg_.stage) + ": iteration not finished after " +
                                              std::to_string(deadlock_timeout_s_) + " s (a peer never delivered)");
         }
@@ -526,6 +525,15 @@ double Executor::finish_iteration() {
     float ms = 0.f;
     ck(cudaEventElapsedTime(&ms, it_start_, it_end_), "elapsed");
     return ms;
+}
+
+void Executor::open_flags() {
+    // cuStreamWaitValue32 GEQ is a cyclic comparison ((int32)(*flag - value) >= 0): a value half the
+    // counter range ahead of the current epoch satisfies every wait of this and later epochs
+    std::vector<uint32_t> v(static_cast<size_t>(cfg_.global_batch), epoch_ + (1u << 30));
+    for (uint32_t* f : {act_flag_, grad_flag_})
+        if (f) ck(cudaMemcpyAsync(f, v.data(), v.size() * 4, cudaMemcpyHostToDevice, rescue_stream()), "rescue");
+    ck(cudaStreamSynchronize(rescue_stream()), "rescue sync");
 }
 
 cudaStream_t Executor::rescue_stream() {

@@ -126,6 +126,7 @@ class Executor {
     void send(bool forward, int mb, const __nv_bfloat16* src, int64_t bytes, cudaEvent_t ready);
     cudaEvent_t ev();
     cudaStream_t rescue_stream();
+    void open_flags();
     cudaStream_t rescue_ = nullptr;
     void synth_tokens(int iter, int32_t* dst) const;
 

@@ -1,11 +1,16 @@
 // Debug tool: per-step timeline (SM clock cycles) of CTA 0 of the flash
 // attention backward kernels at the GPT-1.3B shape.  Not part of the library.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DPTK_ATTN_TRACE \
-//        -o scripts/attn_trace scripts/attn_trace.cu
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr -DPTK_ATTN_TRACE \
+//        -Iinclude -Ipaper_2303_01675_b200/csrc -o scripts/attn_trace scripts/attn_trace.cu -lcuda
+//   scripts/attn_trace 3    (ping-pong forward; 2 single-tile forward; 1 / 0 backward KV / Q)
 #include <cstdio>
 #include <vector>
 
 #include "../paper_2303_01675_b200/csrc/kernels/attention_sm100.cu"
+
+namespace ptk {  // the library's eager-load hook is not needed in this standalone tool
+void preload_module_of(const void*) {}
+}  // namespace ptk
 
 __global__ void fill(__nv_bfloat16* p, size_t n, unsigned seed) {
     for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -42,6 +47,33 @@ int main(int argc, char** argv) {
     if (e != cudaSuccess) {
         printf("error %s\n", cudaGetErrorString(e));
         return 1;
+    }
+    if (kv == 3) {  // ping-pong forward kernel timeline
+        unsigned long long pt[3][64][8];
+        cudaMemcpyFromSymbol(pt, ptk::g_pp_trace, sizeof pt);
+        const unsigned long long p0 = pt[2][0][0];
+        printf("ping-pong forward, CTA 0, cycles since S_A(0) was issued; per lane block n\n");
+        printf("  n | lane A: s_full loaded exps pv_ok p_full | lane B: same | mma: S_A pA_seen PV_A S_B pB_seen PV_B\n");
+        for (int n = 0; n < 20; ++n) {
+            auto f = [&](int r, int ev) { return static_cast<long long>(pt[r][n][ev] - p0); };
+            printf("%3d | %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld %7lld\n",
+                   n, f(0, 0), f(0, 1), f(0, 2), f(0, 3), f(0, 4), f(1, 0), f(1, 1), f(1, 2), f(1, 3), f(1, 4),
+                   f(2, 0), f(2, 1), f(2, 2), f(2, 4), f(2, 5), f(2, 6));
+        }
+        unsigned long long ct[160][4];
+        cudaMemcpyFromSymbol(ct, ptk::g_pp_cta, sizeof ct);
+        unsigned long long t0 = ~0ull, t1 = 0;
+        int grid = 0;
+        for (int i = 0; i < 160 && ct[i][0]; ++i, ++grid) {
+            t0 = ct[i][0] < t0 ? ct[i][0] : t0;
+            t1 = ct[i][3] > t1 ? ct[i][3] : t1;
+        }
+        printf("CTAs %d, kernel span %.2f us (first entry to last exit)\n", grid, (t1 - t0) * 1e-3);
+        printf("cta: entry first_S exit (us from the first entry)\n");
+        for (int i = 0; i < grid; i += 8)
+            printf("%3d: %6.2f %6.2f %6.2f\n", i, (ct[i][0] - t0) * 1e-3, (ct[i][1] - t0) * 1e-3,
+                   (ct[i][3] - t0) * 1e-3);
+        return 0;
     }
     if (kv == 2) {  // forward kernel timeline
         unsigned long long ft[2][64][8];

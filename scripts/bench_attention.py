@@ -29,6 +29,8 @@ def main():
     dev = torch.device("cuda:0")
     lib = L.lib()
     st = torch.cuda.current_stream().cuda_stream
+    only = sys.argv[1] if len(sys.argv) > 1 else None
+    iters = int(sys.argv[2]) if len(sys.argv) > 2 else 50
     for name, b, s, H, d, causal in [("gpt-1.3b", 2, 1024, 32, 64, 1), ("bert-large", 4, 512, 16, 64, 0),
                                      ("bert-large b16", 16, 512, 16, 64, 0), ("gpt-6.7b", 2, 1024, 32, 128, 1)]:
         h = H * d
@@ -45,8 +47,10 @@ def main():
         def bwd():
             L.check(lib.ptk_flash_backward(qkv.data_ptr(), o.data_ptr(), dO.data_ptr(), lse.data_ptr(),
                                            dsum.data_ptr(), dqkv.data_ptr(), b, s, H, d, causal, st))
-        tf = timeit(fwd)
-        tb = timeit(bwd)
+        if only and name != only:
+            continue
+        tf = timeit(fwd, iters)
+        tb = timeit(bwd, iters)
         flops = 4.0 * b * H * s * s * d * (0.5 if causal else 1.0)
         print(f"{name:16s} fwd {tf * 1e6:7.1f} us {flops / tf / 1e12:6.0f} TF/s   "
               f"bwd {tb * 1e6:7.1f} us {2.5 * flops / tb / 1e12:6.0f} TF/s", flush=True)
