@@ -55,8 +55,12 @@ def parse():
                    help="imposed per-GPU memory limit: candidates = the (k, b) frontier under it (config 4)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-wgrad-pairs", action="store_true",
-                   help="one weight-gradient GEMM per micro-batch (default: two-K-segment pairs; always off "
-                        "under --mem-cap-gb, whose candidate frontier does not budget the pairing buffers)")
+                   help="one weight-gradient GEMM per micro-batch (default: two-K-segment pairs, whose "
+                        "buffers the --mem-cap-gb frontier budgets)")
+    p.add_argument("--tuner-repeats", type=int, default=3, help="active link probes per payload (SPEC default 3)")
+    p.add_argument("--passive-profile", action="store_true",
+                   help="feed every re-tuning round the last iteration's own transfers as link samples and probe "
+                        "only the other candidates' payloads")
     p.add_argument("--ref-stages", type=int, default=1,
                    help="--impl reference: S > 1 runs the CPU-thread pipeline executor (S stage threads, "
                         "S micro-batches per step, oracle/cpu_pipeline.py); 1 = the whole model on all cores")
@@ -204,10 +208,12 @@ def main():
 
     # rank 0 prints exactly one JSON line on stdout: NCCL's communicator-init lines (which name
     # nRanks) go to stderr, nothing else of NCCL's is printed
+    nccl_log = None
     if "NCCL_DEBUG" not in os.environ:
+        nccl_log = f"/tmp/ptk_nccl_{os.getpid()}.log"
         os.environ["NCCL_DEBUG"] = "INFO"
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        os.environ["NCCL_DEBUG_FILE"] = nccl_log
     import torch
     import torch.distributed as dist
 
@@ -231,7 +237,15 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            # create the NCCL communicator now, then copy NCCL's INIT lines (they name nRanks) to stderr
+            dist.all_reduce(torch.ones(1, device="cuda"))
+            torch.cuda.synchronize()
+            if nccl_log and os.path.exists(nccl_log):
+                sys.stderr.write(Path(nccl_log).read_text())
+                sys.stderr.flush()
         group = dist.new_group(backend="gloo")
+    log = lambda msg: print(f"[bench rank {rank}] {msg}", file=sys.stderr, flush=True)  # noqa: E731
+    log(f"world {world}, device {local}")
 
     def barrier():
         torch.cuda.synchronize()
@@ -246,13 +260,13 @@ def main():
                               attn_weight=0.42 if shape.arch == "bert" else 0.47)
     layers = halves
     cap = args.mem_cap_gb * 1e9 if args.mem_cap_gb > 0 else None
-    cands = candidate_set(shape, halves, S, GB, cap, fixed_b=args.micro_batch, halves=True) if S > 1 else \
-        [[1, args.micro_batch, GB // args.micro_batch]]
+    wgrad_pairs = not args.no_wgrad_pairs
+    cands = candidate_set(shape, halves, S, GB, cap, fixed_b=args.micro_batch, halves=True,
+                          wgrad_pairs=wgrad_pairs) if S > 1 else [[1, args.micro_batch, GB // args.micro_batch]]
     b_max = max(c[1] for c in cands)
     # physical slots are b_max samples wide: enough of them for every candidate's in-flight samples
     slots = -(-max(max_inflight(rank, S, c[2], c[0]) * c[1] for c in cands) // b_max)
     slots = max(slots, max(max_inflight(rank, S, c[2], c[0]) for c in cands if c[1] == b_max))
-    wgrad_pairs = not args.no_wgrad_pairs and cap is None
     ex = StageExecutor(shape, rank, S, GB, b_max=b_max, slots=slots, halves=halves[rank], wgrad_pairs=wgrad_pairs)
     ks = [c[0] for c in cands]
     b = cands[0][1]  # plan micro-batch size before tuning (the k=1 candidate)
@@ -269,7 +283,8 @@ def main():
                       "regime_ms": args.regime_ms if args.trace == "two-regime" else None,
                       "period_ms": args.period_ms if args.trace == "square" else None,
                       "bursty_mean_on_off_ms": [args.on_ms, args.off_ms] if args.trace == "bursty" else None,
-                      "seed": args.trace_seed, "retune_every": args.retune, "contender_kernels": args.contender}
+                      "seed": args.trace_seed, "retune_every": args.retune, "contender_kernels": args.contender,
+                      "tuner_repeats": args.tuner_repeats, "passive_profile": args.passive_profile}
 
     sync_gt = [0]
 
@@ -293,8 +308,10 @@ def main():
         return ms
 
     by_k = {c[0]: c for c in cands}
+    log(f"candidates {cands}, slots {slots}, b_max {b_max}")
     arm_reset()
     run(args.warmup, cands[0])
+    log("warm-up done")
     if S > 1:
         for c in cands[1:]:
             run(1, c)  # every candidate plan warmed (GEMM / attention plans cached)
@@ -306,6 +323,7 @@ def main():
             if k in by_k:
                 arm_reset()
                 fixed[k] = run(args.steps, by_k[k])
+                log(f"fixed arm k={k}: {sum(fixed[k]):.1f} ms")
         if wgrad_pairs and 1 in by_k:
             # 1F1B also with one weight-gradient GEMM per micro-batch: pairing alternates short and
             # long backwards, which 1F1B's strict F/B alternation cannot absorb; the arm reports the
@@ -317,7 +335,7 @@ def main():
 
     # ---- timed region: Ada-Grouper (tuning round at start, re-tune every `retune` steps)
     tuner = OnlineTuner(ex, rank, S, GB, [(c[0], c[1]) for c in cands], shape.seq * shape.hidden * 2,
-                        group=group) if S > 1 else None
+                        group=group, repeats=args.tuner_repeats, passive=args.passive_profile) if S > 1 else None
     if tuner is not None:
         tuner.profile_compute()  # once, before the timed region
     chosen, decisions, tune_s = cands[0], [], 0.0
@@ -332,6 +350,8 @@ def main():
         for step in range(args.steps):
             if tuner is not None and (step == 0 or (args.retune > 0 and step % args.retune == 0)):
                 tr0 = time.perf_counter()
+                if step > 0 and args.passive_profile:
+                    tuner.observe_iteration(ex.timeline(), clock=step)
                 d = tuner.round(None if step == 0 else list(chosen), clock=step)
                 decisions.append(d)
                 chosen = d["chosen"]
@@ -342,6 +362,7 @@ def main():
         barrier()
         wall = time.perf_counter() - t0
         gemm_flops, gemm_ms, gemm_n = ex.gemm_timing(0)
+    log("timed Ada-Grouper arm done")
     tl = ex.timeline()
     # achieved transfer / forward ratio of the last timed iteration (the paper's regime is ~0.5,
     # PAPER.md:102): mean paced transfer vs mean forward of this stage

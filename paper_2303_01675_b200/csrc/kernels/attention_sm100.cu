@@ -684,9 +684,15 @@ __global__ void __launch_bounds__(384, 1)
 #ifdef PTK_ATTN_TRACE
             if (blockIdx.x < 160) g_pp_cta[blockIdx.x][1] = gt();
 #endif
+            // Causal pairs give lane A one block fewer per pair than lane B, so lane A's cursor would
+            // drift ahead in the shared KV stream; a lane only advances while its next P·V is not past
+            // the other lane's, which keeps every S it issues within the producer's NS loaded stages
+            // (otherwise the producer waits on a stage only the starved lane can free).
+            auto gpv = [&](int l) { return cp[l].kvbase + cp[l].j; };
             while (cp[0].valid || cp[1].valid) {
                 for (int l = 0; l < 2; ++l) {
                     if (!cp[l].valid) continue;
+                    if (cp[l ^ 1].valid && gpv(l) > gpv(l ^ 1)) continue;
                     if (cs[l].valid) issue_s(l);  // one block ahead
                     issue_pv(l);
                 }

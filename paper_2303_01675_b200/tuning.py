@@ -46,12 +46,13 @@ def all_gather(obj, group=None, world: int = 1):
 class OnlineTuner:
     def __init__(self, ex, rank: int, stages: int, global_batch: int, candidates: list[tuple[int, int]],
                  act_bytes_per_sample: int, hysteresis: float = 0.02, repeats: int = 3, window: int = 8,
-                 group=None):
+                 group=None, passive: bool = False):
         self.ex, self.rank, self.S = ex, rank, stages
         self.gb = global_batch
         self.cands = [[k, b, global_batch // b] for k, b in candidates]
         self.act = act_bytes_per_sample
         self.h, self.repeats, self.window, self.group = hysteresis, repeats, window, group
+        self.passive = passive  # use observe_iteration() samples for the current payload
         self.compute = None
         self.samples: list[list[int]] = []
         self.log: list[dict] = []
@@ -65,15 +66,40 @@ class OnlineTuner:
             mine += [[self.rank, b, 0, f], [self.rank, b, 1, bw]]
         self.compute = sorted(x for r in all_gather(mine, self.group, self.S) for x in r)
 
+    def _add_samples(self, gathered):
+        """Append in recording order, keeping only the last `window` per (link, payload) bucket —
+        all the ProfileStore ever reads, so the request stays bounded."""
+        self.samples += gathered
+        keep, seen = [], {}
+        for x in reversed(self.samples):
+            key = (x[0], x[1])
+            if seen.get(key, 0) < self.window:
+                seen[key] = seen.get(key, 0) + 1
+                keep.append(x)
+        self.samples = keep[::-1]
+
+    def observe_iteration(self, timeline: dict, clock: int = 0):
+        """Passive link profile: every transfer the last iteration made on this rank's outgoing links
+        is a sample of its exact payload under the live contention (no pipeline suspension).
+        Collective: every rank calls it after the same iteration."""
+        mine = [[int(link), int(nbytes), clock, int(end) - int(start)]
+                for link, mb, nbytes, start, end in timeline.get("xfer", [])]
+        self._add_samples(sorted(x for r in all_gather(mine, self.group, self.S) for x in r))
+        self.passive_bytes = {x[1] for x in mine}
+
     def profile_links(self, clock: int = 0):
+        """Active probes (pipeline suspended): every candidate payload not already
+        measured passively in the last iteration, `repeats` times per outgoing link."""
         mine = []
+        skip = getattr(self, "passive_bytes", set()) if self.passive else set()
         for b in sorted({c[1] for c in self.cands}):
             nbytes = b * self.act
+            if nbytes in skip:
+                continue
             for link in outgoing_links(self.rank, self.S):
                 for d in self.ex.probe_link(link, nbytes, self.repeats):
                     mine.append([link, nbytes, clock, d])
-        gathered = sorted(x for r in all_gather(mine, self.group, self.S) for x in r)
-        self.samples += gathered  # ProfileStore keeps the last `window` per bucket
+        self._add_samples(sorted(x for r in all_gather(mine, self.group, self.S) for x in r))
 
     def decide(self, current, clock: int = 0) -> dict:
         req = {"op": "decide", "model": self.model, "candidates": self.cands, "compute_profile": self.compute,
@@ -92,18 +118,33 @@ class OnlineTuner:
         return self.decide(current, clock)
 
 
-def memory_model(shape, layers, stages: int, global_batch: int, halves: bool = False) -> dict:
+def pair_bytes_per_sample(shape, hb: int, he: int, has_head: bool) -> int:
+    """Per-sample bytes of the paired-weight-gradient buffers GptStage allocates at b_max
+    (gpt_stage.cu, `wgrad_pairs`: per layer of the stage out, d(x_mid), d_ln, dy [T,h], d_pre [T,f],
+    dqkv [T,3h]; on the head stage the head's g and dy [T,h])."""
+    from .stage import halves_to_layers
+    lb, le, _, _ = halves_to_layers(hb, he)
+    s, h, f = shape.seq, shape.hidden, shape.ffn
+    return (le - lb) * (7 * s * h + s * f) * 2 + (2 * s * h * 2 if has_head else 0)
+
+
+def memory_model(shape, layers, stages: int, global_batch: int, halves: bool = False,
+                 pairs_b_max: int = 0) -> dict:
     """pipetune ModelSpec with the real per-stage byte model: weights = fp32 master +
     grad + AdamW m, v + bf16 copy (18 B/param); activations = the stash per sample.
-    `layers`: per-stage layer ranges, or half-layer ranges when `halves`."""
+    `layers`: per-stage layer ranges, or half-layer ranges when `halves`.  pairs_b_max > 0 budgets
+    paired weight gradients allocated at that b_max as a fixed per-stage cost: their buffers plus
+    the one extra stash slot of b_max samples the executor keeps (SPEC.md:218-226 liveness + it)."""
     st = []
     for s_, (lb, le) in enumerate(layers):
         first, last = s_ == 0, s_ == stages - 1
         params = shape.param_count_halves(lb, le, first, last) if halves else shape.param_count(le - lb, first, last)
         stash = shape.stash_bytes_halves(lb, le, last, first) if halves else \
             shape.stash_bytes_per_sample(le - lb, last, first)
+        hb, he = (lb, le) if halves else (2 * lb, 2 * le)
+        fixed = pairs_b_max * (stash + pair_bytes_per_sample(shape, hb, he, last)) if pairs_b_max else 0
         st.append(pt.StageProfile(
-            stage_id=s_, weight_bytes=18 * params,
+            stage_id=s_, weight_bytes=18 * params + fixed,
             activation_bytes_per_sample=stash,
             output_bytes_per_sample_fwd=shape.seq * shape.hidden * 2,
             output_bytes_per_sample_bwd=shape.seq * shape.hidden * 2))
@@ -111,13 +152,29 @@ def memory_model(shape, layers, stages: int, global_batch: int, halves: bool = F
 
 
 def candidate_set(shape, layers, stages: int, global_batch: int, mem_cap_bytes: int | None, k_max: int = 8,
-                  fixed_b: int = 2, halves: bool = False) -> list[list[int]]:
+                  fixed_b: int = 2, halves: bool = False, wgrad_pairs: bool = False) -> list[list[int]]:
     """Ada-Grouper candidates: the (k, b) memory-limit frontier via the C++
-    enumerate_candidates under an imposed per-GPU cap; without a cap, k in {1,2,4,8} at b."""
+    enumerate_candidates under an imposed per-GPU cap; without a cap, k in {1,2,4,8} at b.
+    With wgrad_pairs the pairing buffers of the allocation (sized by the largest candidate b) are
+    budgeted too: b_max is iterated to a fixed point (it can only shrink)."""
     if mem_cap_bytes is None:
         M = global_batch // fixed_b
         return [[k, fixed_b, M] for k in (1, 2, 4, 8) if k <= M]
-    model = memory_model(shape, layers, stages, global_batch, halves)
-    out = pt.scenario({"op": "enumerate", "model": model, "k_max": k_max,
-                       "cluster": {"device_memory_limit": int(mem_cap_bytes), "devices": stages}})
-    return [e[:3] for e in out["entries"]]
+
+    def frontier(pairs_b_max):
+        model = memory_model(shape, layers, stages, global_batch, halves, pairs_b_max)
+        out = pt.scenario({"op": "enumerate", "model": model, "k_max": k_max,
+                           "cluster": {"device_memory_limit": int(mem_cap_bytes), "devices": stages}})
+        return [e[:3] for e in out["entries"]]
+
+    cands = frontier(0)
+    if not wgrad_pairs:
+        return cands
+    b_max = max(c[1] for c in cands)
+    for _ in range(16):
+        cands = frontier(b_max)
+        nb = max(c[1] for c in cands)
+        if nb >= b_max:
+            break
+        b_max = nb
+    return cands

@@ -32,7 +32,8 @@ def main():
     only = sys.argv[1] if len(sys.argv) > 1 else None
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 50
     for name, b, s, H, d, causal in [("gpt-1.3b", 2, 1024, 32, 64, 1), ("bert-large", 4, 512, 16, 64, 0),
-                                     ("bert-large b16", 16, 512, 16, 64, 0), ("gpt-6.7b", 2, 1024, 32, 128, 1)]:
+                                     ("bert-large b16", 16, 512, 16, 64, 0), ("gpt-6.7b", 2, 1024, 32, 128, 1),
+                                     ("gpt-1.3b b4", 4, 1024, 32, 64, 1), ("gpt-1.3b b1", 1, 1024, 32, 64, 1)]:
         h = H * d
         qkv = (torch.randn(b * s, 3 * h, device=dev) * 0.5).bfloat16()
         o = torch.empty(b * s, h, device=dev, dtype=torch.bfloat16)
