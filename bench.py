@@ -28,6 +28,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "samples/sec under emulated preemption: Ada-Grouper kFkB vs 1F1B, 2/4/8 B200"
 GLOBAL_BATCH, MICRO_B = 64, 2
+JSON_OUT = sys.stdout  # rank 0's JSON line (main() points it at the original stdout)
 
 
 def parse():
@@ -208,12 +209,16 @@ def main():
 
     # rank 0 prints exactly one JSON line on stdout: NCCL's communicator-init lines (which name
     # nRanks) go to stderr, nothing else of NCCL's is printed
-    nccl_log = None
-    if "NCCL_DEBUG" not in os.environ:
-        nccl_log = f"/tmp/ptk_nccl_{os.getpid()}.log"
+    # Native libraries (NCCL's version banner and INIT lines, which name nRanks) print on fd 1; rank
+    # 0 owes exactly one JSON line on stdout.  So fd 1 of this process is pointed at stderr and the
+    # JSON line goes to a saved copy of the original stdout.
+    global JSON_OUT
+    sys.stdout.flush()
+    JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION", "WARN"):
         os.environ["NCCL_DEBUG"] = "INFO"
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ["NCCL_DEBUG_FILE"] = nccl_log
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
     import torch
     import torch.distributed as dist
 
@@ -237,12 +242,8 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-            # create the NCCL communicator now, then copy NCCL's INIT lines (they name nRanks) to stderr
-            dist.all_reduce(torch.ones(1, device="cuda"))
+            dist.all_reduce(torch.ones(1, device="cuda"))  # creates the communicator now
             torch.cuda.synchronize()
-            if nccl_log and os.path.exists(nccl_log):
-                sys.stderr.write(Path(nccl_log).read_text())
-                sys.stderr.flush()
         group = dist.new_group(backend="gloo")
     log = lambda msg: print(f"[bench rank {rank}] {msg}", file=sys.stderr, flush=True)  # noqa: E731
     log(f"world {world}, device {local}")
@@ -352,7 +353,9 @@ def main():
                 tr0 = time.perf_counter()
                 if step > 0 and args.passive_profile:
                     tuner.observe_iteration(ex.timeline(), clock=step)
-                d = tuner.round(None if step == 0 else list(chosen), clock=step)
+                # the incumbent is the plan the executor ran last (the warm-up plan before the first
+                # round), so the first round is already a switch decision
+                d = tuner.round(list(chosen), clock=step)
                 decisions.append(d)
                 chosen = d["chosen"]
                 barrier()
@@ -504,7 +507,8 @@ def main():
         out["reference_planner_cpu"] = {"error": str(e)[:200]}
     if args.timeline:
         Path(args.timeline).write_text(json.dumps(tl))
-    print(json.dumps(out), flush=True)
+    JSON_OUT.write(json.dumps(out) + "\n")
+    JSON_OUT.flush()
     if world > 1:
         dist.destroy_process_group()
 

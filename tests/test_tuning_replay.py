@@ -2,9 +2,13 @@
 bit-for-bit on the CPU — by the spec oracle and by the C++ decision function —
 from the int64-ns compute/link samples the GPU run recorded.
 
-Fixture: tests/golden/gpu_tuner_log_*.json, written by
-  torchrun --nproc-per-node 2 bench.py --gpus 2 --trace two-regime --retune 2 --tuner-log ...
-on 2x B200 (round 1).
+Fixtures: tests/golden/gpu_tuner_log_*.json, written by bench.py --tuner-log on B200s:
+  * n2_bursty (round 1): 2 stages, bursty ON/OFF trace, 5 rounds, no switch;
+  * n4_square (round 2): 4 stages, square-wave trace (1.2 s preempted to 10 % of 400 Gb/s / 1.2 s
+    free), re-tuned every 2 steps with passive link samples, 15 rounds; its first round switches
+    from the warm-up incumbent k=1 to k=4 on the measured samples;
+  * n4_square_cap16 (round 2): the same trace under a 16 GB cap ((k, b) frontier
+    (1,4) (2,2) (3,1) (4,1)), 15 rounds.
 """
 import copy
 import json
@@ -32,3 +36,9 @@ def test_gpu_decisions_replay_bit_exact(path):
         assert pt.scenario(req)["decision"] == got
         ks.append(got["chosen"][0])
     assert all(k >= 1 for k in ks)
+
+
+def test_a_gpu_fixture_contains_a_switch():
+    """At least one recorded GPU decision is a switch, so the replay covers switching, not only
+    staying."""
+    assert any(r["decision"]["switched"] for p in LOGS for r in json.loads(p.read_text())["rounds"])
