@@ -219,6 +219,11 @@ def main():
     if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION", "WARN"):
         os.environ["NCCL_DEBUG"] = "INFO"
         os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:  # every link is paced (trace "none" = the base rate)
+        # leave SMs free for the emulator's trace gates (and contender CTAs): persistent GEMM / attention
+        # grids would otherwise hold every SM and delay each gate by a whole kernel (runtime/sm_budget.h)
+        os.environ.setdefault("PTK_SM_RESERVE", str(1 + (int(os.environ.get("PTK_CONTENDER_CTAS", "4"))
+                                                         if args.contender else 0)))
     import torch
     import torch.distributed as dist
 
@@ -453,6 +458,7 @@ def main():
                    "half_layer_ranges": [list(x) for x in halves],
                    "parallelism": f"pp{S}" if S > 1 else "single stage (no pipeline)",
                    "wgrad_pairs": wgrad_pairs,
+                   "sm_reserved_for_emulator": int(os.environ.get("PTK_SM_RESERVE", "0")),
                    "schedule": (f"Ada-Grouper adaptive kFkB ((k, b) per step {plans_run})" if S > 1 else "1F1B (S=1)"),
                    "emulated_preemption": trace_desc, "l2": "working set (weights + activations) >> 126 MB L2"},
         "schedules": {"ada_grouper": {"kb_per_step": plans_run, "samples_per_s": round(value, 3),

@@ -32,6 +32,7 @@
 #include "attention_sm100.h"
 #include "launch.cuh"
 #include "sm100_ptx.cuh"
+#include "../runtime/sm_budget.h"
 
 namespace ptk {
 
@@ -48,16 +49,7 @@ constexpr float kLazyRescaleLog2 = 8.f;
 #endif
 constexpr int kBwPoly = PTK_BW_POLY;  // backward: exponentials per 32 on the FMA pipe (0, 1, 2, 4 or 8)  // forward: move the running max only when it grows by > 2^8
 
-int sm_count() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+int sm_count() { return sm_budget(); }  // runtime/sm_budget.h
 
 template <int D>
 struct FaCfg {

@@ -36,6 +36,7 @@
 #include "gemm_sm100.h"
 #include "launch.cuh"
 #include "sm100_ptx.cuh"
+#include "../runtime/sm_budget.h"
 
 namespace ptk {
 
@@ -806,15 +807,7 @@ GemmPlan::Launcher pick(bool a_mn, bool b_mn) {
     return &launch_impl<BN, true, true, MC>;
 }
 
-int num_sms() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-    }
-    return n;
-}
+int num_sms() { return sm_budget(); }  // runtime/sm_budget.h: PTK_SM_RESERVE leaves SMs to the emulator
 
 }  // namespace
 

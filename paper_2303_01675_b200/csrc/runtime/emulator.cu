@@ -3,6 +3,7 @@
 #include "emulator.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <stdexcept>
 
@@ -63,15 +64,17 @@ __device__ double avail_at(const DevTrace* tr, int64_t now) {
 }
 
 // mode 0: record the transfer start; 1: hold until `done` bytes are due;
-// 2: hold until the whole transfer (+latency) is due.
+// 2: hold until the whole transfer (+latency) is due; 3: record the start now and hold until
+// `done` bytes (+latency) are due from it (the single gate paced_copy uses).
 __global__ void gate_kernel(const DevTrace* tr, int64_t* state, int64_t done, int mode) {
     const int64_t now = gtimer();
     if (mode == 0) {
         state[0] = now;
         return;
     }
-    const int64_t target = deliver_time(tr, state[0], done) + (mode == 2 ? tr->latency : 0);
-    while (gtimer() < target) __nanosleep(1000);
+    const int64_t t0 = mode == 3 ? now : state[0];
+    const int64_t target = deliver_time(tr, t0, done) + (mode >= 2 ? tr->latency : 0);
+    while (gtimer() < target) __nanosleep(500);
 }
 
 __global__ void timer_kernel(int64_t* out) { *out = gtimer(); }
@@ -81,7 +84,8 @@ __global__ void timer_kernel(int64_t* out) { *out = gtimer(); }
 // Only thread 0 of each CTA polls the host-mapped stop flag and the trace
 // (once per burst) and broadcasts through shared memory, so the contender does
 // not flood PCIe with uncached reads.
-__global__ void contender_kernel(const DevTrace* tr, uint4* peer, size_t n16, const volatile int* stop) {
+__global__ void contender_kernel(const DevTrace* tr, uint4* peer, size_t n16, const volatile int* stop,
+                                 float duty_override) {
     __shared__ int s_state;  // 0 off, 1 on, 2 stop
     const int64_t period = 50000;
     size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
@@ -95,7 +99,8 @@ __global__ void contender_kernel(const DevTrace* tr, uint4* peer, size_t n16, co
             } else {
                 const int64_t now = gtimer();
                 const double a = avail_at(tr, now);
-                st = (a < 1.0 && static_cast<double>(now % period) < (1.0 - a) * period) ? 1 : 0;
+                const double duty = duty_override >= 0.f ? duty_override : 1.0 - a;
+                st = (a < 1.0 && static_cast<double>(now % period) < duty * period) ? 1 : 0;
             }
             s_state = st;
         }
@@ -178,19 +183,21 @@ void Emulator::set_trace(int slot, const EmuTrace& t) {
 }
 
 cudaError_t Emulator::paced_copy(int slot, void* dst, const void* src, int64_t bytes, cudaStream_t st) {
-    if (!active(slot)) return cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice, st);
+    // PTK_EMU_NO_GATE=1 (calibration only): copies unpaced even on a traced link, so the contender's
+    // effect on a plain NVLink copy can be measured (scripts/contender_calibration.py)
+    static const bool no_gate = std::getenv("PTK_EMU_NO_GATE") != nullptr;
+    if (!active(slot) || no_gate)
+        return cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice, st);
+    // One gate per transfer: it records the start when the stream reaches the transfer and holds the
+    // stream until the trace has delivered every byte (+ latency); the copy engine then moves the
+    // payload at NVLink speed (tens of us), and the arrival flag written after it marks completion.
+    // (Per-chunk gates cost one kernel launch each; each launch waited for a free SM slot behind
+    // the compute kernels, adding 0.2-0.8 ms per transfer; profiles/r2_contender_calibration.md.)
     int64_t* state = state_ + slot * 8;
-    gate_kernel<<<1, 1, 0, st>>>(dev_[slot], state, 0, 0);
-    const int64_t chunk = ((bytes + kChunks - 1) / kChunks + 15) / 16 * 16;
-    for (int64_t off = 0; off < bytes; off += chunk) {
-        if (off > 0) gate_kernel<<<1, 1, 0, st>>>(dev_[slot], state, off, 1);
-        const int64_t len = std::min(chunk, bytes - off);
-        cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
-                                        static_cast<size_t>(len), cudaMemcpyDeviceToDevice, st);
-        if (e != cudaSuccess) return e;
-    }
-    gate_kernel<<<1, 1, 0, st>>>(dev_[slot], state, bytes, 2);
-    return cudaPeekAtLastError();
+    gate_kernel<<<1, 1, 0, st>>>(dev_[slot], state, bytes, 3);
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice, st);
 }
 
 cudaError_t Emulator::start_contender(int slot, void* peer_scratch, size_t bytes, cudaStream_t st) {
@@ -203,7 +210,18 @@ cudaError_t Emulator::start_contender(int slot, void* peer_scratch, size_t bytes
     }
     *stop_host_ = 0;
     std::atomic_thread_fence(std::memory_order_seq_cst);
-    contender_kernel<<<4, 128, 0, st>>>(dev_[slot], static_cast<uint4*>(peer_scratch), bytes / 16, stop_dev_);
+    // PTK_CONTENDER_CTAS (default 4) CTAs of peer stores; PTK_CONTENDER_DUTY overrides the duty
+    // cycle 1 - availability (calibration runs: scripts/contender_calibration.py)
+    static const int ctas = [] {
+        const char* v = std::getenv("PTK_CONTENDER_CTAS");
+        return v ? std::max(1, std::atoi(v)) : 4;
+    }();
+    static const float duty = [] {
+        const char* v = std::getenv("PTK_CONTENDER_DUTY");
+        return v ? static_cast<float>(std::atof(v)) : -1.f;
+    }();
+    contender_kernel<<<ctas, 128, 0, st>>>(dev_[slot], static_cast<uint4*>(peer_scratch), bytes / 16, stop_dev_,
+                                           duty);
     return cudaPeekAtLastError();
 }
 

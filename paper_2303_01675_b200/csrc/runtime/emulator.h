@@ -2,14 +2,16 @@
 //
 // A LinkTrace (base bandwidth, latency, piecewise-constant
 // availability) is uploaded to the device.  Every transfer on that link is
-// split into chunks; before chunk i a one-thread gate kernel spins on
-// %globaltimer until the trace says i*chunk bytes may have been delivered,
-// and a final gate holds the transfer until the trace's completion time
-// (+latency).  The copy engine moves each chunk at NVLink speed, so the
-// delivered-bytes curve follows  transfer_duration(trace, bytes, start)  of
-// the spec (network.cpp) whenever the emulated bandwidth is below the link's.
-// A contender kernel (optional) adds real competing NVLink stores to the same
-// peer while the trace is in a preempted segment.
+// preceded by one one-thread gate kernel on the send stream: it records the
+// transfer's start (%globaltimer) and spins until the trace has delivered all
+// its bytes (+latency) — the device twin of transfer_duration(trace, bytes,
+// start) of the spec (network.cpp); the copy engine then moves the payload at
+// NVLink speed and the arrival flag marks completion.  Send streams run at the
+// highest priority so a gate never waits behind pending compute CTAs, and
+// bench.py leaves one SM free of persistent kernels (runtime/sm_budget.h).
+// A contender kernel (optional, PTK_CONTENDER_CTAS CTAs) adds real competing
+// NVLink stores to the same peer while the trace is in a preempted segment;
+// its calibration is profiles/r2_contender_calibration.md.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -36,7 +38,6 @@ struct DevTrace;  // device-side copy
 class Emulator {
   public:
     static constexpr int kMaxLinks = 2;  // a stage sends on at most two links
-    static constexpr int kChunks = 8;
 
     Emulator() = default;
     ~Emulator();

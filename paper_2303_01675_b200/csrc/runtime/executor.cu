@@ -79,8 +79,10 @@ Executor::Executor(const ptk_exec_config& c) : cfg_(c) {
     ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priorities");
     if (std::getenv("PTK_FLAT_PRIORITY") != nullptr) hi = lo;  // diagnostics: all streams at one priority
     ck(cudaStreamCreateWithPriority(&comp_, cudaStreamNonBlocking, hi), "stream");
-    ck(cudaStreamCreateWithPriority(&sendst_, cudaStreamNonBlocking, lo), "stream");
-    ck(cudaStreamCreateWithPriority(&sendst_bwd_, cudaStreamNonBlocking, lo), "stream");
+    // send streams at the highest priority: their only kernels are the emulator's one-thread trace
+    // gates, which would otherwise wait behind every pending compute CTA for an SM slot
+    ck(cudaStreamCreateWithPriority(&sendst_, cudaStreamNonBlocking, hi), "stream");
+    ck(cudaStreamCreateWithPriority(&sendst_bwd_, cudaStreamNonBlocking, hi), "stream");
     if (const char* v = std::getenv("PTK_DEADLOCK_TIMEOUT_S")) deadlock_timeout_s_ = std::atof(v);
     if (const char* v = std::getenv("PTK_SEND_STREAMS")) per_link_send_ = std::string(v) == "per_link";
     ck(cudaStreamCreateWithPriority(&contend_[0], cudaStreamNonBlocking, lo), "stream");
@@ -323,7 +325,7 @@ void Executor::send(bool fwd, int mb, const __nv_bfloat16* src, int64_t bytes, c
     XferRecord r{fwd ? 2 * cfg_.stage : 2 * cfg_.stage - 1, mb, bytes, ev(), ev()};
     ck(cudaEventRecord(r.start, st), "event");
     ck(emu_.paced_copy(fwd ? 0 : 1, dst_block + off, src, bytes, st), "peer copy");
-    if (emu_.active(fwd ? 0 : 1)) emu_launches_ += Emulator::kChunks + 1;
+    if (emu_.active(fwd ? 0 : 1)) emu_launches_ += 1;
     write_flag(st, flag + mb, epoch_);
     ck(cudaEventRecord(r.end, st), "event");
     xrec_.push_back(r);

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../paper_2303_01675_b200/csrc/kernels/attention_sm100.cu"
+#include "../paper_2303_01675_b200/csrc/runtime/sm_budget.cpp"
 
 namespace ptk {  // the library's eager-load hook is not needed in this standalone tool
 void preload_module_of(const void*) {}
