@@ -982,15 +982,23 @@ namespace {
 
 template <int D, bool KV>
 struct BwCfg {
+    // d = 64: the elementwise results Pᵀ / dS(ᵀ) go to TMEM (bf16 pairs) and feed the accumulating
+    // products as their A operand (tcgen05.mma A-from-TMEM): no smem round trip, which halves the
+    // smem traffic per step (smem bandwidth bounded the step: scores 64 KiB + P/dS writes 64 KiB +
+    // their MMA reads 64 KiB + accumulating B 32 KiB + TMA 32 KiB per 128x128 step).  d = 128 has
+    // no TMEM room for them (X, Y and the 2d-column accumulator fill 512 columns).
+    static constexpr bool kTs = D == 64;
     static constexpr int kTile = kBlk * D * 2;  // one [128][D] tile
     static constexpr int kStages = D == 64 ? 2 : 1;
     static constexpr int kFixBuf = D == 64 ? 2 : 1;
-    static constexpr int kAccBuf = (KV && D == 128) ? 1 : 2;
+    static constexpr int kAccBuf = (KV && (D == 128 || kTs)) ? 1 : 2;
     static constexpr int kAccCols = KV ? 2 * D : D;  // per accumulator buffer
-    static constexpr int kPd = kBlk * kBlk * 2;      // one [128][128] bf16 A-operand buffer
+    static constexpr int kPd = kBlk * kBlk * 2;      // one [128][128] bf16 A-operand buffer (smem path)
     static constexpr int kSmem =
-        kFixBuf * 2 * kTile + kStages * 2 * kTile + 2 * kPd + 2 * 2 * kBlk * 4 + 1024 + 256;
+        kFixBuf * 2 * kTile + kStages * 2 * kTile + (kTs ? 0 : 2 * kPd) + 2 * 2 * kBlk * 4 + 1024 + 256;
     static constexpr uint32_t kX = 0, kY = 128, kAcc = 256;
+    static constexpr uint32_t kP = kAcc + kAccBuf * kAccCols, kDS = kP + 64;  // TMEM A operands (kTs)
+    static_assert(!kTs || kDS + 64 <= 512, "TMEM budget");
 };
 
 struct BwArgs {
@@ -1120,9 +1128,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sFix = smem;                           // [FB][2 tiles]: (K_j, V_j) (KV) | (Q_i, dO_i) (Q)
     uint8_t* sStep = sFix + FB * 2 * C::kTile;      // [S][2 tiles]: (Q_i, dO_i) (KV) | (K_j, V_j) (Q)
-    uint8_t* sP = sStep + S * 2 * C::kTile;         // Pᵀ (KV only)
-    uint8_t* sDS = sP + C::kPd;                     // dSᵀ (KV) | dS (Q)
-    float* sRow = reinterpret_cast<float*>(sDS + C::kPd);  // [2][lse[128], D[128]] (KV only)
+    uint8_t* sP = sStep + S * 2 * C::kTile;         // Pᵀ (KV only; smem path)
+    uint8_t* sDS = sP + (C::kTs ? 0 : C::kPd);      // dSᵀ (KV) | dS (Q) (smem path)
+    float* sRow = reinterpret_cast<float*>(sDS + (C::kTs ? 0 : C::kPd));  // [2][lse[128], D[128]] (KV only)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sRow + 2 * 2 * kBlk);
     uint64_t* fix_full = bars + 0;   // [2]
     uint64_t* fix_empty = bars + 2;  // [2]
@@ -1253,7 +1261,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t aoff = (k / 4) * kBlk * 128 + (k % 4) * 32;  // K-major A, k over 128 columns
                     const uint32_t boff = k * 2048;                            // MN-major B, k over 128 rows
                     const uint32_t acc = (ca.j > 0 || k > 0) ? 1u : 0u;
-                    if (KV) {
+                    if (C::kTs) {  // A operands from TMEM: 16 columns of k = 8 TMEM columns per step
+                        if (KV) {
+                            mma_bf16_ts(acc0, tmem + C::kP + k * 8, make_sw128_desc(s1 + boff, kBlk * 128, 1024),
+                                        kIdescAcc, acc);
+                            mma_bf16_ts(acc0 + D, tmem + C::kDS + k * 8,
+                                        make_sw128_desc(s0 + boff, kBlk * 128, 1024), kIdescAcc, acc);
+                        } else {
+                            mma_bf16_ts(acc0, tmem + C::kDS + k * 8, make_sw128_desc(s0 + boff, kBlk * 128, 1024),
+                                        kIdescAcc, acc);
+                        }
+                    } else if (KV) {
                         // dV += Pᵀ dO_i ; dK += dSᵀ Q_i
                         mma_bf16_ss(acc0, make_sw128_desc(pb + aoff, 16, 1024),
                                     make_sw128_desc(s1 + boff, kBlk * 128, 1024), kIdescAcc, acc);
@@ -1353,16 +1371,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(pd_free, (n - 1) & 1);  // previous step's MMAs done reading sP / sDS
                 }
                 if (warp == 4 && lane == 0) ATRACE(0, n, 3);
-                // columns [64*half, +64) are swizzle atom `half` of each [128][128] operand
-                const uint32_t prow = pbuf + half * (kBlk * 128) + r * 128;
-                const uint32_t drow = dbuf + half * (kBlk * 128) + r * 128;
+                if (C::kTs) {
+                    // this thread's 64 columns = 32 TMEM columns (bf16 pairs) of its row's A operand
+                    if (KV) tmem_st_32x32b_x32_u_nw(tmem + lane_base + C::kP + half * 32, pk_p);
+                    tmem_st_32x32b_x32_u_nw(tmem + lane_base + C::kDS + half * 32, pk_d);
+                    tmem_st_wait();
+                } else {
+                    // columns [64*half, +64) are swizzle atom `half` of each [128][128] operand
+                    const uint32_t prow = pbuf + half * (kBlk * 128) + r * 128;
+                    const uint32_t drow = dbuf + half * (kBlk * 128) + r * 128;
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    const uint32_t sw = (g ^ (r & 7)) * 16;
-                    if (KV) sts128(prow + sw, make_uint4(pk_p[g * 4], pk_p[g * 4 + 1], pk_p[g * 4 + 2], pk_p[g * 4 + 3]));
-                    sts128(drow + sw, make_uint4(pk_d[g * 4], pk_d[g * 4 + 1], pk_d[g * 4 + 2], pk_d[g * 4 + 3]));
+                    for (int g = 0; g < 8; ++g) {
+                        const uint32_t sw = (g ^ (r & 7)) * 16;
+                        if (KV)
+                            sts128(prow + sw, make_uint4(pk_p[g * 4], pk_p[g * 4 + 1], pk_p[g * 4 + 2], pk_p[g * 4 + 3]));
+                        sts128(drow + sw, make_uint4(pk_d[g * 4], pk_d[g * 4 + 1], pk_d[g * 4 + 2], pk_d[g * 4 + 3]));
+                    }
+                    fence_proxy_async_smem();
                 }
-                fence_proxy_async_smem();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(pd_full);
