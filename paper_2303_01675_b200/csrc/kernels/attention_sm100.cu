@@ -989,7 +989,10 @@ struct BwCfg {
     // no TMEM room for them (X, Y and the 2d-column accumulator fill 512 columns).
     static constexpr bool kTs = D == 64;
     static constexpr int kTile = kBlk * D * 2;  // one [128][D] tile
-    static constexpr int kStages = D == 64 ? 2 : 1;
+#ifndef PTK_BW_STAGES
+#define PTK_BW_STAGES 2
+#endif
+    static constexpr int kStages = D == 64 ? PTK_BW_STAGES : 1;
     static constexpr int kFixBuf = D == 64 ? 2 : 1;
     static constexpr int kAccBuf = (KV && (D == 128 || kTs)) ? 1 : 2;
     static constexpr int kAccCols = KV ? 2 * D : D;  // per accumulator buffer
@@ -1172,6 +1175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_begin();  // previous kernel complete: its outputs (qkv, lse, dO, ...) are visible
 
     if (warp == 0) {
+        if (C::kTs) reg_dealloc<72>();
         if (lane == 0) {  // ---------------- TMA producer
             // tile loader: rows [row0, row0+128) of a {d, s, heads, b} map, head coordinate hc
             auto load_tile = [&](const CUtensorMap* m, uint64_t* bar, uint8_t* dst, int row0, int hc, int bi) {
@@ -1209,6 +1213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
+        if (C::kTs) reg_dealloc<72>();
         if (lane == 0) {  // ---------------- MMA issuer
             auto issue_xy = [&](const BwCursor& c, int n) {
                 ATRACE(1, n, 0);
@@ -1299,7 +1304,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ++na;
             }
         }
-    } else if (warp >= 4) {  // ---------------- elementwise warps: thread = (row of the fixed block, column half)
+    } else if (warp < 4) {
+        if (C::kTs) reg_dealloc<72>();
+    } else {  // ---------------- elementwise warps: thread = (row of the fixed block, column half)
+        if (C::kTs) reg_alloc<208>();
         const int quad = warp & 3;
         const int half = (warp - 4) >> 2;  // columns [64*half, 64*half + 64) of X/Y
         const int r = quad * 32 + static_cast<int>(lane);
@@ -1348,23 +1356,51 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // dS = P (τ dP - τ D) are packed to bf16 pairs in registers, before waiting
                 // for the previous step's accumulating products to release the smem operands
                 uint32_t pk_p[32], pk_d[32];
+                if (C::kTs) {
+                    // all 64 columns of X and Y loaded before any compute: the score accumulators are
+                    // released one TMEM round trip after xy_full, so the next step's X/Y products start
+                    // while this step's elementwise work runs (208 registers: setmaxnreg below)
+                    float x[2][32], y[2][32];
 #pragma unroll
-                for (int pass = 0; pass < 2; ++pass) {
-                    float x[32], y[32];
-                    tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kX + half * 64 + pass * 32, x);
-                    tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kY + half * 64 + pass * 32, y);
-                    tmem_ld_wait();
-                    if (pass == 1) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(xy_free);
-                        if (warp == 4 && lane == 0) ATRACE(0, n, 1);
+                    for (int pass = 0; pass < 2; ++pass) {
+                        tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kX + half * 64 + pass * 32, x[pass]);
+                        tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kY + half * 64 + pass * 32, y[pass]);
                     }
-                    const int cb0 = half * 64 + pass * 32;
-                    if (diag)
-                        bw_pass<KV, true>(x, y, rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16, pk_d + pass * 16);
-                    else
-                        bw_pass<KV, false>(x, y, rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16, pk_d + pass * 16);
+                    tmem_ld_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(xy_free);
+                    if (warp == 4 && lane == 0) ATRACE(0, n, 1);
+#pragma unroll
+                    for (int pass = 0; pass < 2; ++pass) {
+                        const int cb0 = half * 64 + pass * 32;
+                        if (diag)
+                            bw_pass<KV, true>(x[pass], y[pass], rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16,
+                                              pk_d + pass * 16);
+                        else
+                            bw_pass<KV, false>(x[pass], y[pass], rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16,
+                                               pk_d + pass * 16);
+                    }
+                } else {
+#pragma unroll
+                    for (int pass = 0; pass < 2; ++pass) {
+                        float x[32], y[32];
+                        tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kX + half * 64 + pass * 32, x);
+                        tmem_ld_32x32b_x32_nw(tmem + lane_base + C::kY + half * 64 + pass * 32, y);
+                        tmem_ld_wait();
+                        if (pass == 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(xy_free);
+                            if (warp == 4 && lane == 0) ATRACE(0, n, 1);
+                        }
+                        const int cb0 = half * 64 + pass * 32;
+                        if (diag)
+                            bw_pass<KV, true>(x, y, rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16, pk_d + pass * 16);
+                        else
+                            bw_pass<KV, false>(x, y, rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16,
+                                               pk_d + pass * 16);
+                    }
                 }
                 if (warp == 4 && lane == 0) ATRACE(0, n, 2);
                 if (n > 0) {

@@ -49,6 +49,24 @@ int main(int argc, char** argv) {
         printf("error %s\n", cudaGetErrorString(e));
         return 1;
     }
+    if (kv == 9) {  // timing only: forward and backward, 20 launches each
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float fms = 0.f, bms = 0.f;
+        cudaEventRecord(e0);
+        for (int i = 0; i < 20; ++i) ptk::flash_forward(fp, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&fms, e0, e1);
+        cudaEventRecord(e0);
+        for (int i = 0; i < 20; ++i) ptk::flash_backward(bp, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&bms, e0, e1);
+        printf("fwd %.1f us  bwd %.1f us\n", fms * 50.f, bms * 50.f);
+        return 0;
+    }
     if (kv == 3) {  // ping-pong forward kernel timeline
         unsigned long long pt[3][64][8];
         cudaMemcpyFromSymbol(pt, ptk::g_pp_trace, sizeof pt);
