@@ -348,7 +348,7 @@ def main():
     arm_reset()
     with ClockSampler(local) as clk:
         if os.environ.get("PTK_BENCH_GEMM_TIMING", "1") != "0":  # 0: diagnostics, no per-GEMM events
-            # one micro-batch in 32 per stage and step (micro-batch 0 always): event records between GEMMs
+            # one micro-batch in 32 per stage and step, rotating with the step: event records between GEMMs
             # break the PDL overlap of the sampled micro-batches (1 in 8 cost BERT-large 4.5 % of a step)
             ex.gemm_timing(int(os.environ.get("PTK_BENCH_GEMM_STRIDE", "32")))
         t0 = time.perf_counter()
