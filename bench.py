@@ -227,7 +227,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2303_01675_b200.executor import StageExecutor, max_inflight, partition_halves
+    from paper_2303_01675_b200.executor import StageExecutor, partition_halves, stage_slots
     from paper_2303_01675_b200.stage import BERT_LARGE, GPT_1_3B, GPT_6_7B
     from paper_2303_01675_b200.tuning import OnlineTuner, candidate_set, outgoing_links
 
@@ -269,10 +269,8 @@ def main():
     wgrad_pairs = not args.no_wgrad_pairs
     cands = candidate_set(shape, halves, S, GB, cap, fixed_b=args.micro_batch, halves=True,
                           wgrad_pairs=wgrad_pairs) if S > 1 else [[1, args.micro_batch, GB // args.micro_batch]]
-    b_max = max(c[1] for c in cands)
     # physical slots are b_max samples wide: enough of them for every candidate's in-flight samples
-    slots = -(-max(max_inflight(rank, S, c[2], c[0]) * c[1] for c in cands) // b_max)
-    slots = max(slots, max(max_inflight(rank, S, c[2], c[0]) for c in cands if c[1] == b_max))
+    slots, b_max = stage_slots(rank, S, cands)
     ex = StageExecutor(shape, rank, S, GB, b_max=b_max, slots=slots, halves=halves[rank], wgrad_pairs=wgrad_pairs)
     ks = [c[0] for c in cands]
     b = cands[0][1]  # plan micro-batch size before tuning (the k=1 candidate)

@@ -120,6 +120,16 @@ def max_inflight(stage: int, stages: int, micro_batches: int, k: int) -> int:
     return min(micro_batches, min(stages - stage, math.ceil(micro_batches / k)) * k)
 
 
+def stage_slots(stage: int, stages: int, candidates) -> tuple[int, int]:
+    """(slots, b_max) the executor of `stage` needs to run every (k, b, M) candidate: physical stash
+    slots are b_max samples wide and hold b_max / b micro-batches each (sample-granular stash), so the
+    count covers the largest in-flight sample count over the candidates (SURVEY §4 closed form)."""
+    b_max = max(c[1] for c in candidates)
+    slots = -(-max(max_inflight(stage, stages, c[2], c[0]) * c[1] for c in candidates) // b_max)
+    slots = max(slots, max(max_inflight(stage, stages, c[2], c[0]) for c in candidates if c[1] == b_max))
+    return slots, b_max
+
+
 class StageExecutor:
     def __init__(self, shape: ModelShape, stage: int, stages: int, global_batch: int, b_max: int, slots: int,
                  layers: tuple[int, int] | None = None, seed: int = 42, data_seed: int = 1234, lr: float = 1e-4,
