@@ -1,0 +1,75 @@
+// Debug tool: LayerNorm forward / fused backward timing at the GPT-1.3B and BERT shapes, inputs
+// rotated over 16 buffer sets (> L2) so every launch reads from HBM.  Not part of the library.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr \
+//        -Iinclude -Ipaper_2303_01675_b200/csrc -o /tmp/ln_bench scripts/ln_bench.cu [-DPTK_LN_RB=4]
+#include <cstdio>
+#include <vector>
+
+#include "../paper_2303_01675_b200/csrc/kernels/gpt_kernels.cu"
+#include "../paper_2303_01675_b200/csrc/runtime/sm_budget.cpp"
+
+namespace ptk {
+void preload_module_of(const void*) {}
+}  // namespace ptk
+
+int main() {
+    for (int h : {2048, 1024}) {
+        for (int T : {2048, 4096}) {
+            const int sets = 16;
+            const size_t n = static_cast<size_t>(T) * h;
+            std::vector<__nv_bfloat16*> x(sets), dy(sets), r(sets), y(sets), dx(sets);
+            std::vector<float*> mean(sets), rstd(sets);
+            for (int s = 0; s < sets; ++s) {
+                cudaMalloc(&x[s], n * 2);
+                cudaMalloc(&dy[s], n * 2);
+                cudaMalloc(&r[s], n * 2);
+                cudaMalloc(&y[s], n * 2);
+                cudaMalloc(&dx[s], n * 2);
+                cudaMalloc(&mean[s], T * 4);
+                cudaMalloc(&rstd[s], T * 4);
+                cudaMemset(x[s], 0x3c, n * 2);
+                cudaMemset(dy[s], 0x3c, n * 2);
+                cudaMemset(r[s], 0, n * 2);
+            }
+            __nv_bfloat16 *g, *b;
+            float *pg, *pb, *po;
+            cudaMalloc(&g, h * 2);
+            cudaMalloc(&b, h * 2);
+            cudaMemset(g, 0x3c, h * 2);
+            cudaMemset(b, 0, h * 2);
+            cudaMalloc(&pg, 256 * h * 4);
+            cudaMalloc(&pb, 256 * h * 4);
+            cudaMalloc(&po, 256 * h * 4);
+            cudaMemset(pg, 0, 256 * h * 4);
+            cudaMemset(pb, 0, 256 * h * 4);
+            cudaMemset(po, 0, 256 * h * 4);
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            for (int i = 0; i < sets; ++i) ptk::layernorm_fwd(x[i], g, b, y[i], mean[i], rstd[i], T, h, 1e-5f, 0);
+            const int it = 64;
+            float fms = 0, bms = 0;
+            cudaEventRecord(e0);
+            for (int i = 0; i < it; ++i) ptk::layernorm_fwd(x[i % sets], g, b, y[i % sets], mean[i % sets], rstd[i % sets], T, h, 1e-5f, 0);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&fms, e0, e1);
+            cudaEventRecord(e0);
+            for (int i = 0; i < it; ++i)
+                ptk::layernorm_bwd(dy[i % sets], x[i % sets], mean[i % sets], rstd[i % sets], g, r[i % sets], dx[i % sets], pg, pb, po, T, h, 0);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&bms, e0, e1);
+            const double fb = 2.0 * n * 2, bb = 4.0 * n * 2;
+            printf("h=%d T=%d  fwd %.2f us (%.0f GB/s)  bwd %.2f us (%.0f GB/s, algorithmic dy+x+resid+dx)  err=%s\n", h, T,
+                   fms * 1e3 / it, fb / (fms * 1e-3 / it) / 1e9, bms * 1e3 / it, bb / (bms * 1e-3 / it) / 1e9,
+                   cudaGetErrorString(cudaGetLastError()));
+            for (int s = 0; s < sets; ++s) {
+                cudaFree(x[s]); cudaFree(dy[s]); cudaFree(r[s]); cudaFree(y[s]); cudaFree(dx[s]);
+                cudaFree(mean[s]); cudaFree(rstd[s]);
+            }
+            cudaFree(g); cudaFree(b); cudaFree(pg); cudaFree(pb); cudaFree(po);
+        }
+    }
+    return 0;
+}
