@@ -344,6 +344,14 @@ void Executor::begin_iteration(int iter, const int32_t* host_tokens) {
     const int S = cfg_.stages, s = cfg_.stage;
     const bool first = s == 0, last = s == S - 1;
     const int64_t toks = static_cast<int64_t>(cfg_.global_batch) * g.seq;
+    if (host_tokens) {
+        // ids index the embedding / LM-head rows on the device: an out-of-range one is a
+        // ConfigError here (before any state changes) instead of a faulting kernel
+        for (int64_t i = 0; i < 2 * toks; ++i)
+            if (static_cast<uint32_t>(host_tokens[i]) >= static_cast<uint32_t>(g.vocab))
+                throw pipetune::ConfigError("run_iteration: token/label id " + std::to_string(host_tokens[i]) +
+                                            " at " + std::to_string(i) + " outside [0, vocab)");
+    }
     iter_ = iter;
     ++epoch_;
     cursor_ = 0;

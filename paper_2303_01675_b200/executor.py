@@ -203,7 +203,11 @@ class StageExecutor:
             self._dp_view = self.stage_view()
         stream = torch.cuda.ExternalStream(self.compute_stream())
         with torch.cuda.stream(stream):
-            dist.all_reduce(self._dp_view.grads, op=dist.ReduceOp.AVG, group=dp_group)
+            if dist.get_backend(dp_group) == "nccl":
+                dist.all_reduce(self._dp_view.grads, op=dist.ReduceOp.AVG, group=dp_group)
+            else:  # gloo (tests on one GPU): no AVG reduction; sum, then scale on the compute stream
+                dist.all_reduce(self._dp_view.grads, op=dist.ReduceOp.SUM, group=dp_group)
+                self._dp_view.grads.mul_(1.0 / dist.get_world_size(dp_group))
         if step:
             L.check(self.lib.ptk_stage_optimizer_step(self.lib.ptk_exec_stage(self.h), self.cfg.lr,
                                                       self.cfg.weight_decay, C.c_void_p(stream.cuda_stream)))

@@ -60,7 +60,8 @@ def run_from(ex, replica, replicas, dp_group, first, last):
     n = GB // replicas
     st = ex.stage_view()
     for it in range(first, last):
-        ex.run_iteration(it, host_batch(it, replica * n, (replica + 1) * n).ctypes.data)
+        toks = host_batch(it, replica * n, (replica + 1) * n)  # keep the array alive across the call
+        ex.run_iteration(it, toks.ctypes.data)
         ex.data_parallel_step(dp_group)
         ex.finish_iteration()
     torch.cuda.synchronize()
@@ -70,15 +71,22 @@ def run_from(ex, replica, replicas, dp_group, first, last):
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--stages", type=int, default=1)
+    p.add_argument("--one-gpu", action="store_true",
+                   help="every rank on cuda:0 with gloo gradient all-reduce (tests/test_dp_gpu.py)")
     a = p.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
-    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank))))
+    dev = 0 if a.one_gpu else int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(dev)
+    if a.one_gpu:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     S = a.stages
     R = world // S
     replica, stage = rank // S, rank % S
     pipe_groups = [dist.new_group([r * S + s for s in range(S)], backend="gloo") for r in range(R)]
-    dp_groups = [dist.new_group([r * S + s for r in range(R)], backend="nccl") for s in range(S)]
+    dp_groups = [dist.new_group([r * S + s for r in range(R)], backend="gloo" if a.one_gpu else "nccl")
+                 for s in range(S)]
     layers = partition_layers(SHAPE.n_layer, S)
     M = (GB // R) // B
     slots = max(max_inflight(stage, S, M, k) for k in (1, 2))
@@ -106,7 +114,8 @@ def main():
         ref.set_defer_optimizer(True)
         n = GB
         st = ref.stage_view()
-        ref.run_iteration(0, host_batch(0, 0, n).ctypes.data)
+        toks = host_batch(0, 0, n)
+        ref.run_iteration(0, toks.ctypes.data)
         ref.finish_iteration()
         torch.cuda.synchronize()
         gref = {name: st.param(name, "grads").cpu().clone() for name in st.params}
