@@ -427,7 +427,8 @@ void Executor::enqueue_node(int id) {
     GemmTiming& tm = stage_->gemm_timing();
     // one micro-batch in `stride`, rotating with the iteration so paired and unpaired weight-gradient
     // micro-batches (and PDL-overlapped ones) are all sampled over a run
-    tm.enabled = tm.armed && m >= 0 && m % tm.stride == static_cast<int>(epoch_ % static_cast<uint32_t>(tm.stride));
+    const int period = std::max(1, std::min(tm.stride, M_));
+    tm.enabled = tm.armed && m >= 0 && m % tm.stride == static_cast<int>(epoch_ % static_cast<uint32_t>(period));
     if (n.kind == pipetune::TaskKind::ForwardCompute) {
         if (!first) wait_flag(comp_, act_flag_ + m, epoch_);
         __nv_bfloat16* out = last ? nullptr : act_send_[static_cast<size_t>(slot / split)] + sub;
