@@ -6,10 +6,11 @@
 // contiguous); the operand layout is folded into the TMA box and the UMMA
 // smem descriptor, so the dense-layer forward (X·Wᵀ), dgrad (dY·W) and wgrad
 // (dYᵀ·X) and every attention product are the same kernel without a
-// transpose pass.  One CTA per SM, 6 warps:
+// transpose pass.  One CTA per SM, 10 warps (kThreads = 320):
 //   warp 0      TMA producer (one elected lane)
 //   warp 1      TMEM allocator + tcgen05.mma issuer (one elected lane)
-//   warps 2..5  epilogue: tcgen05.ld → fused epilogue → st.global
+//   warps 2..9  epilogue, two per TMEM lane quarter: tcgen05.ld → fused epilogue →
+//               swizzled smem staging → TMA store / reduce-add
 // The accumulator is double-buffered in TMEM (2 x BN fp32 columns) so the
 // epilogue of tile i overlaps the main loop of tile i+1.
 //

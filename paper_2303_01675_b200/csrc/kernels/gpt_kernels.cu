@@ -1,5 +1,5 @@
-// Memory-bound GPT stage kernels for sm_100a: LayerNorm fwd/bwd, causal
-// softmax fwd/bwd, fused softmax-cross-entropy (loss + dlogits), embedding
+// Memory-bound GPT stage kernels for sm_100a: LayerNorm fwd/bwd,
+// fused softmax-cross-entropy (loss + dlogits), embedding
 // fwd/bwd, deterministic column reductions (bias / LN-affine grads), AdamW,
 // parameter init.  All reductions use fixed orders (no float atomics), so
 // gradients are bit-reproducible and independent of the schedule's k.
@@ -340,93 +340,6 @@ __global__ void __launch_bounds__(256) vec_finalize_kernel(const VecGradSeg* __r
     }
 }
 
-// --------------------------------------------------------------- softmax (causal)
-// S: fp32 [rows][n] (row r of a head covers query q = r % n); P: bf16.
-// Writes P for columns < round_up(q+1, 128): exp for k <= q, exact 0 above.
-__global__ void __launch_bounds__(128) softmax_causal_fwd_kernel(const float* __restrict__ S,
-                                                                 __nv_bfloat16* __restrict__ P, int rows, int n,
-                                                                 float scale_log2) {
-    pdl_begin();
-    const int row = blockIdx.x * 4 + threadIdx.x / 32;
-    const int lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    const int q = row % n;
-    const int tile_end = min(n, (q / 128 + 1) * 128);
-    const float* s = S + static_cast<int64_t>(row) * n;
-    __nv_bfloat16* p = P + static_cast<int64_t>(row) * n;
-    float mx = -INFINITY;
-    for (int c = lane * 4; c <= q; c += 128) {
-        const float4 v = *reinterpret_cast<const float4*>(s + c);
-        mx = fmaxf(mx, v.x);
-        if (c + 1 <= q) mx = fmaxf(mx, v.y);
-        if (c + 2 <= q) mx = fmaxf(mx, v.z);
-        if (c + 3 <= q) mx = fmaxf(mx, v.w);
-    }
-    mx = warp_max(mx) * scale_log2;
-    float sum = 0.f;
-    for (int c = lane * 4; c <= q; c += 128) {
-        const float4 v = *reinterpret_cast<const float4*>(s + c);
-        sum += exp2f(v.x * scale_log2 - mx);
-        if (c + 1 <= q) sum += exp2f(v.y * scale_log2 - mx);
-        if (c + 2 <= q) sum += exp2f(v.z * scale_log2 - mx);
-        if (c + 3 <= q) sum += exp2f(v.w * scale_log2 - mx);
-    }
-    const float inv = 1.f / warp_sum(sum);
-    for (int c = lane * 4; c < tile_end; c += 128) {
-        const float4 v = *reinterpret_cast<const float4*>(s + c);
-        const float e0 = c <= q ? exp2f(v.x * scale_log2 - mx) * inv : 0.f;
-        const float e1 = c + 1 <= q ? exp2f(v.y * scale_log2 - mx) * inv : 0.f;
-        const float e2 = c + 2 <= q ? exp2f(v.z * scale_log2 - mx) * inv : 0.f;
-        const float e3 = c + 3 <= q ? exp2f(v.w * scale_log2 - mx) * inv : 0.f;
-        __nv_bfloat162 a = __floats2bfloat162_rn(e0, e1), b = __floats2bfloat162_rn(e2, e3);
-        uint2 u;
-        u.x = *reinterpret_cast<uint32_t*>(&a);
-        u.y = *reinterpret_cast<uint32_t*>(&b);
-        *reinterpret_cast<uint2*>(p + c) = u;
-    }
-}
-
-// dS = scale * P * (dP - sum_k P dP), written like P (zeros above the diagonal).
-__global__ void __launch_bounds__(128) softmax_causal_bwd_kernel(const __nv_bfloat16* __restrict__ P,
-                                                                 const float* __restrict__ dP,
-                                                                 __nv_bfloat16* __restrict__ dS, int rows, int n,
-                                                                 float scale) {
-    pdl_begin();
-    const int row = blockIdx.x * 4 + threadIdx.x / 32;
-    const int lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    const int q = row % n;
-    const int tile_end = min(n, (q / 128 + 1) * 128);
-    const __nv_bfloat16* p = P + static_cast<int64_t>(row) * n;
-    const float* d = dP + static_cast<int64_t>(row) * n;
-    float dot = 0.f;
-    for (int c = lane * 4; c <= q; c += 128) {
-        const uint2 u = *reinterpret_cast<const uint2*>(p + c);
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-        const float4 v = *reinterpret_cast<const float4*>(d + c);
-        dot += a.x * v.x + (c + 1 <= q ? a.y * v.y : 0.f) + (c + 2 <= q ? b.x * v.z : 0.f) +
-               (c + 3 <= q ? b.y * v.w : 0.f);
-    }
-    dot = warp_sum(dot);
-    __nv_bfloat16* o = dS + static_cast<int64_t>(row) * n;
-    for (int c = lane * 4; c < tile_end; c += 128) {
-        const uint2 u = *reinterpret_cast<const uint2*>(p + c);
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-        const float4 v = *reinterpret_cast<const float4*>(d + c);
-        const float e0 = c <= q ? scale * a.x * (v.x - dot) : 0.f;
-        const float e1 = c + 1 <= q ? scale * a.y * (v.y - dot) : 0.f;
-        const float e2 = c + 2 <= q ? scale * b.x * (v.z - dot) : 0.f;
-        const float e3 = c + 3 <= q ? scale * b.y * (v.w - dot) : 0.f;
-        __nv_bfloat162 x = __floats2bfloat162_rn(e0, e1), y = __floats2bfloat162_rn(e2, e3);
-        uint2 w;
-        w.x = *reinterpret_cast<uint32_t*>(&x);
-        w.y = *reinterpret_cast<uint32_t*>(&y);
-        *reinterpret_cast<uint2*>(o + c) = w;
-    }
-}
-
 // --------------------------------------------------------------- cross-entropy
 // One 512-thread block per row of bf16 logits [rows][V]: loss[row] and, in
 // place, dlogits = (softmax - onehot(label)) * grad_scale.
@@ -756,19 +669,6 @@ cudaError_t vec_grad_finalize(const VecGradSeg* segs_dev, int nseg, int max_cols
     if (nseg > 65535) return cudaErrorInvalidValue;
     const int gx = (max_cols + 255) / 256;
     launch_kernel(vec_finalize_kernel, dim3(gx, nseg), 256, 0, st, 1, segs_dev);
-    return cudaPeekAtLastError();
-}
-
-cudaError_t softmax_causal_fwd(const float* S, __nv_bfloat16* P, int rows, int n, float scale, cudaStream_t st) {
-    if (n % 128) return cudaErrorInvalidValue;
-    launch_kernel(softmax_causal_fwd_kernel, (rows + 3) / 4, 128, 0, st, 1, S, P, rows, n, scale * 1.4426950408889634f);
-    return cudaPeekAtLastError();
-}
-
-cudaError_t softmax_causal_bwd(const __nv_bfloat16* P, const float* dP, __nv_bfloat16* dS, int rows, int n,
-                               float scale, cudaStream_t st) {
-    if (n % 128) return cudaErrorInvalidValue;
-    launch_kernel(softmax_causal_bwd_kernel, (rows + 3) / 4, 128, 0, st, 1, P, dP, dS, rows, n, scale);
     return cudaPeekAtLastError();
 }
 

@@ -30,9 +30,6 @@ cudaError_t layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const
 cudaError_t colsum_partial(const __nv_bfloat16* m, float* part, int rows, int cols, cudaStream_t st);
 // segs_dev: device array of nseg segments; max_cols: the widest segment.
 cudaError_t vec_grad_finalize(const VecGradSeg* segs_dev, int nseg, int max_cols, cudaStream_t st);
-cudaError_t softmax_causal_fwd(const float* S, __nv_bfloat16* P, int rows, int n, float scale, cudaStream_t st);
-cudaError_t softmax_causal_bwd(const __nv_bfloat16* P, const float* dP, __nv_bfloat16* dS, int rows, int n,
-                               float scale, cudaStream_t st);
 // logits overwritten by dlogits * grad_scale; loss_out[0] += sum(row losses) * loss_scale.
 cudaError_t cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss_rows, float* loss_out, int rows,
                           int vocab, float grad_scale, float loss_scale, cudaStream_t st);

@@ -73,11 +73,75 @@ void run(const char* name) {
     cudaFree(d);
 }
 
+int main_ld();
+
 int main() {
+    main_ld();
     run<128, false>("SS M128 N128 K16");
     run<64, false>("SS M128 N64 K16 (B MN-major)");
     run<64, true>("TS M128 N64 K16 (B MN-major)");
     run<128, true>("TS M128 N128 K16");
     run<256, false>("SS M128 N256 K16");
+    return 0;
+}
+
+// TMEM load bandwidth: W warps each read 32 lanes x 32 fp32 columns (4 KiB) per tcgen05.ld,
+// `iters` times (cycling over 128 columns), waiting after every `batch` loads.
+template <int W, int BATCH>
+__global__ void __launch_bounds__(32 * W, 1) ldtm_rate(unsigned long long* cycles, int iters) {
+    __shared__ uint32_t tmem_slot;
+    const int warp = threadIdx.x / 32;
+    if (warp == 0) tmem_alloc<512>(&tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    float acc = 0.f;
+    __syncthreads();
+    const unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; i += BATCH) {
+        float v[BATCH][32];
+#pragma unroll
+        for (int b = 0; b < BATCH; ++b) tmem_ld_32x32b_x32_nw(tmem + ((i + b) & 3) * 32 + (warp >> 2) * 128, v[b]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int b = 0; b < BATCH; ++b) acc += v[b][b];
+    }
+    __syncthreads();
+    const unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+    if (acc == 12345.f) cycles[0] = 0;
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_slot);
+    }
+}
+
+template <int W, int BATCH>
+void run_ld() {
+    unsigned long long* d;
+    cudaMalloc(&d, 148 * 8);
+    const int iters = 1024;
+    ldtm_rate<W, BATCH><<<148, 32 * W>>>(d, iters);
+    ldtm_rate<W, BATCH><<<148, 32 * W>>>(d, iters);
+    unsigned long long h[148];
+    cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    double c = 0;
+    for (int i = 0; i < 148; ++i) c += h[i];
+    c /= 148;
+    const double bytes = static_cast<double>(W) * iters * 32 * 32 * 4;
+    printf("LDTM 32x32b.x32: %2d warps, %d in flight per warp: %.1f bytes/clk/SM (%s)\n", W, BATCH, bytes / c,
+           cudaGetErrorString(cudaGetLastError()));
+    cudaFree(d);
+}
+
+int main_ld() {
+    run_ld<4, 1>();
+    run_ld<4, 4>();
+    run_ld<8, 1>();
+    run_ld<8, 4>();
+    run_ld<16, 4>();
     return 0;
 }
