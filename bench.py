@@ -301,9 +301,12 @@ def main():
 
     it = 0
 
-    def run(n, cfg):
+    def run(n, cfg, groups=None):
         nonlocal it
-        ex.set_plan(cfg[0], cfg[1])
+        if groups:  # a mixed-k plan chosen by the tuner (remainder group first)
+            ex.set_plan_groups(cfg[1], groups)
+        else:
+            ex.set_plan(cfg[0], cfg[1])
         ms = []
         for _ in range(n):
             ex.run_iteration(it)
@@ -342,7 +345,7 @@ def main():
                         group=group, repeats=args.tuner_repeats, passive=args.passive_profile) if S > 1 else None
     if tuner is not None:
         tuner.profile_compute()  # once, before the timed region
-    chosen, decisions, tune_s = cands[0], [], 0.0
+    chosen, chosen_groups, decisions, tune_s = cands[0], [], [], 0.0
     arm_reset()
     with ClockSampler(local) as clk:
         if os.environ.get("PTK_BENCH_GEMM_TIMING", "1") != "0":  # 0: diagnostics, no per-GEMM events
@@ -358,13 +361,14 @@ def main():
                     tuner.observe_iteration(ex.timeline(), clock=step)
                 # the incumbent is the plan the executor ran last (the warm-up plan before the first
                 # round), so the first round is already a switch decision
-                d = tuner.round(list(chosen), clock=step)
+                d = tuner.round(list(chosen), clock=step, current_groups=chosen_groups)
                 decisions.append(d)
                 chosen = d["chosen"]
+                chosen_groups = d.get("chosen_groups", [])
                 barrier()
                 tune_s += time.perf_counter() - tr0
-            ms += run(1, chosen)
-            plans_run.append([chosen[0], chosen[1]])
+            ms += run(1, chosen, chosen_groups)
+            plans_run.append([chosen[0], chosen[1]] + ([chosen_groups] if chosen_groups else []))
         barrier()
         wall = time.perf_counter() - t0
         gemm_flops, gemm_ms, gemm_n = ex.gemm_timing(0)
@@ -385,7 +389,10 @@ def main():
     import numpy as np
     rng = np.random.default_rng(7)
     host = rng.integers(0, shape.vocab, size=(2, GB * shape.seq), dtype=np.int32)
-    ex.set_plan(chosen[0], chosen[1])
+    if chosen_groups:
+        ex.set_plan_groups(chosen[1], chosen_groups)
+    else:
+        ex.set_plan(chosen[0], chosen[1])
     arm_reset()  # the same trace window as the timed arm (time-varying traces replay from t=0)
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -468,7 +475,7 @@ def main():
                       "speedup_vs_1f1b": round(value / v1f1b, 4)},
         **({"kfkb_sweep": {str(k): {"kbM": by_k[k], "samples_per_s": round(GB * args.steps / (max(v) / 1e3), 3)}
                             for k, v in all_sweep.items()}} if all_sweep else {}),
-        "tuner_decisions": [{"chosen": d["chosen"], "switched": d["switched"],
+        "tuner_decisions": [{"chosen": d["chosen"], "chosen_groups": d.get("chosen_groups"), "switched": d["switched"],
                              "estimates_ns": [e[3] for e in d["estimates"]]} for d in decisions],
         "pipeline_roofline": {"ideal_samples_per_s": round(ideal, 2), "frac": round(value / ideal, 4),
                               "peak_tflops": peak_sus, "peak_kind": f"sustained bf16, {pk_kind}"},

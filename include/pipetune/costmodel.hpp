@@ -32,6 +32,7 @@ struct PlanEstimate {
     PlanConfig config;
     Tick estimated_length = 0;
     std::string inputs_digest;  // the profile values used, rendered
+    std::vector<int> groups;    // explicit group sizes (plan_groups); empty = uniform kFkB at config.k
 };
 
 PlanEstimate estimate_length(const SchedulePlan& plan, const ModelSpec& model, const ComputeProfile& compute,
@@ -40,6 +41,21 @@ PlanEstimate estimate_length(const SchedulePlan& plan, const ModelSpec& model, c
 // Ascending estimate; ties: smaller k, then larger b.
 std::vector<PlanEstimate> rank_candidates(const CandidateSet& candidates, const ModelSpec& model,
                                           const ComputeProfile& compute, const ProfileStore& comm);
+
+// A mixed-k candidate: kFkB over explicit consecutive group sizes at micro-batch size b
+// (plan_groups; the reference planner's make_plan walks any group list, plan.cpp:20-21, 61-66).
+// Under constant profiled durations the one that pays off is "remainder group first": when k
+// does not divide M, a short FIRST group shortens the warm-up that uniform kFkB's short LAST
+// group does not.
+struct GroupCandidate {
+    int micro_batch_size = 1;
+    std::vector<int> groups;
+};
+
+// rank_candidates over uniform candidates and mixed-k plans together.  Ascending estimate;
+// ties: smaller (max) k, larger b, then group list (uniform first).
+std::vector<PlanEstimate> rank_plans(const CandidateSet& candidates, const std::vector<GroupCandidate>& mixed,
+                                     const ModelSpec& model, const ComputeProfile& compute, const ProfileStore& comm);
 
 // Builds the kFkB plan of a candidate config.
 SchedulePlan plan_for(const ModelSpec& model, const PlanConfig& config);

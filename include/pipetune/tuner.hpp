@@ -27,6 +27,7 @@ struct TuningDecision {
     Tick round_time = 0;
     std::vector<PlanEstimate> estimates;  // ranked
     PlanConfig chosen;
+    std::vector<int> chosen_groups;  // non-empty when a mixed-k plan (GroupCandidate) is chosen
     bool switched = false;
 };
 
@@ -54,6 +55,12 @@ TuningDecision tuning_round(const CandidateSet& candidates, const ModelSpec& mod
 
 // UnknownCandidate unless `next` is in the set; returns the switch overhead to
 // charge (0 for a no-op switch to the current config).
+// tuning_round over uniform and mixed-k candidates; `current_groups` identifies a mixed incumbent.
+TuningDecision tuning_round_plans(const CandidateSet& candidates, const std::vector<GroupCandidate>& mixed,
+                                  const ModelSpec& model, const ComputeProfile& compute, const ProfileStore& comm,
+                                  const PlanConfig& current, const std::vector<int>& current_groups, double hysteresis,
+                                  Tick round_time);
+
 Tick switch_plan(const CandidateSet& candidates, const PlanConfig& current, const PlanConfig& next,
                  const TuningPolicy& policy);
 

@@ -387,29 +387,47 @@ def simulate_true(stages, g, orders, traces, start=0):
 
 
 # ------------------------------------------------------------------ cost model / tuner
-def rank(model, cands, comp, store):
+def rank(model, cands, comp, store, mixed=()):
+    """Uniform candidates [k, b, M, _] and mixed-k ones (b, [group sizes]) ranked by the simulated
+    length over constant profiled durations; ties: smaller (max) k, larger b, group list (uniform
+    first).  Mixed entries carry their sizes as a 5th element."""
     stages = stage_list(model)
     out = []
+
+    def length(g, orders):
+        return simulate(stages, g, orders, lambda s, bb, f: comp[(s, bb, 0 if f else 1)],
+                        lambda link, nb, t: store.estimate(link, nb), 0)["pipeline_length"]
+
     for k, b, M, _ in cands:
         g = Graph(stages, b, M)
-        orders = kfkb_orders(g, k)
-        r = simulate(stages, g, orders, lambda s, bb, f: comp[(s, bb, 0 if f else 1)],
-                     lambda link, nb, t: store.estimate(link, nb), 0)
-        out.append([k, b, M, r["pipeline_length"]])
-    out.sort(key=lambda e: (e[3], e[0], -e[1]))
+        out.append([k, b, M, length(g, kfkb_orders(g, k))])
+    for b, sizes in mixed:
+        M = model["global_batch"] // b
+        g = Graph(stages, b, M)
+        ranges, first = [], 0
+        for n in sizes:
+            ranges.append((first, first + n - 1))
+            first += n
+        if first != M:
+            raise SpecError("PlanError", "groups do not tile [0, M)")
+        out.append([max(sizes), b, M, length(g, kfkb_orders(g, max(sizes), ranges)), list(sizes)])
+    out.sort(key=lambda e: (e[3], e[0], -e[1], e[4] if len(e) > 4 else []))
     return out
 
 
-def decide(ranked, current, h):
+def decide(ranked, current, h, current_groups=None):
+    """Returns (chosen [k, b, M], chosen groups or [], switched)."""
     best = ranked[0]
+    groups = lambda e: e[4] if len(e) > 4 else []  # noqa: E731
     if current is None:
-        return best[:3], False
-    cur = [e for e in ranked if e[:3] == list(current)]
+        return best[:3], groups(best), False
+    cg = list(current_groups or [])
+    cur = [e for e in ranked if e[:3] == list(current) and groups(e) == cg]
     if not cur:
         raise SpecError("UnknownCandidate", "current")
     better = float(best[3]) < float(cur[0][3]) * (1.0 - h)
-    switched = better and best[:3] != list(current)
-    return (best[:3] if switched else list(current)), switched
+    switched = better and not (best[:3] == list(current) and groups(best) == cg)
+    return (best[:3] if switched else list(current)), (groups(best) if switched else cg), switched
 
 
 def candidate_buckets(model, cands):
@@ -450,7 +468,7 @@ def run_adaptive(model, limit, traces, pol, horizon):
     t0 = clock
     clock = profile(buckets, traces, clock, reps, store)
     ranked = rank(model, cands, comp, store)
-    cur, _ = decide(ranked, None, h)
+    cur, _, _ = decide(ranked, None, h)
     rounds.append({"time": t0, "estimates": ranked, "chosen": cur, "switched": False})
     while clock < end:
         rs = clock
@@ -469,7 +487,7 @@ def run_adaptive(model, limit, traces, pol, horizon):
         t = clock
         clock = profile(buckets, traces, clock, reps, store)
         ranked = rank(model, cands, comp, store)
-        nxt, switched = decide(ranked, cur, h)
+        nxt, _, switched = decide(ranked, cur, h)
         if nxt != cur:
             clock += overhead
         cur = nxt
@@ -526,11 +544,15 @@ def run(req: dict) -> dict:
         for link, nb, _, dur in req["samples"]:
             st.record(link, nb, dur)
         cands = [(k, b, M, []) for k, b, M in req["candidates"]]
-        ranked = rank(model, cands, comp, st)
+        mixed = [(b, list(sizes)) for b, sizes in req.get("group_candidates", [])]
+        ranked = rank(model, cands, comp, st, mixed)
         cur = req.get("current")
-        chosen, switched = decide(ranked, cur, req.get("hysteresis", 0.02))
-        return {"decision": {"time": req.get("clock", 0), "estimates": ranked, "chosen": chosen,
-                             "switched": switched}}
+        chosen, groups, switched = decide(ranked, cur, req.get("hysteresis", 0.02), req.get("current_groups"))
+        out = {"time": req.get("clock", 0), "estimates": ranked, "chosen": chosen}
+        if groups:
+            out["chosen_groups"] = groups
+        out["switched"] = switched
+        return {"decision": out}
     if op == "tune":
         return run_adaptive(model, req["cluster"]["device_memory_limit"], traces_by_link(req, S),
                             req.get("policy", {}), req["horizon"])

@@ -55,18 +55,43 @@ PlanEstimate estimate_length(const SchedulePlan& plan, const ModelSpec& model, c
     return {plan.config, r.pipeline_length, digest};
 }
 
-std::vector<PlanEstimate> rank_candidates(const CandidateSet& candidates, const ModelSpec& model,
-                                          const ComputeProfile& compute, const ProfileStore& comm) {
+std::vector<PlanEstimate> rank_plans(const CandidateSet& candidates, const std::vector<GroupCandidate>& mixed,
+                                     const ModelSpec& model, const ComputeProfile& compute, const ProfileStore& comm) {
     std::vector<PlanEstimate> out;
-    out.reserve(candidates.entries.size());
+    out.reserve(candidates.entries.size() + mixed.size());
     for (const CandidateEntry& e : candidates.entries)
         out.push_back(estimate_length(plan_for(model, e.config), model, compute, comm));
+    for (const GroupCandidate& g : mixed) {
+        if (g.micro_batch_size < 1 || model.global_batch % g.micro_batch_size)
+            throw ConfigError("rank_plans: group candidate b must divide the global batch");
+        PlanConfig cfg{1, g.micro_batch_size, model.global_batch / g.micro_batch_size};
+        auto graph = std::make_shared<const TaskGraph>(build_task_graph(model, cfg));
+        std::vector<MicroBatchGroup> groups;
+        int first = 0, kmax = 0;
+        for (int n : g.groups) {
+            if (n < 1) throw ConfigError("rank_plans: group sizes must be >= 1");
+            groups.push_back({first, first + n - 1});
+            first += n;
+            kmax = std::max(kmax, n);
+        }
+        PlanEstimate e = estimate_length(plan_groups(graph, kmax, groups), model, compute, comm);
+        e.config = PlanConfig{kmax, g.micro_batch_size, cfg.micro_batch_count};
+        e.groups = g.groups;
+        out.push_back(std::move(e));
+    }
     std::stable_sort(out.begin(), out.end(), [](const PlanEstimate& a, const PlanEstimate& b) {
         if (a.estimated_length != b.estimated_length) return a.estimated_length < b.estimated_length;
         if (a.config.k != b.config.k) return a.config.k < b.config.k;
-        return a.config.micro_batch_size > b.config.micro_batch_size;
+        if (a.config.micro_batch_size != b.config.micro_batch_size)
+            return a.config.micro_batch_size > b.config.micro_batch_size;
+        return a.groups < b.groups;  // uniform (empty) first
     });
     return out;
+}
+
+std::vector<PlanEstimate> rank_candidates(const CandidateSet& candidates, const ModelSpec& model,
+                                          const ComputeProfile& compute, const ProfileStore& comm) {
+    return rank_plans(candidates, {}, model, compute, comm);
 }
 
 }  // namespace pipetune

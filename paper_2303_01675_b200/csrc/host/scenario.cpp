@@ -206,11 +206,15 @@ void write_decision(json::Writer& w, const TuningDecision& d) {
     w.begin_obj();
     w.key("time").num(d.round_time);
     w.key("estimates").begin_arr();
-    for (const PlanEstimate& e : d.estimates)
-        w.begin_arr().v(e.config.k).v(e.config.micro_batch_size).v(e.config.micro_batch_count).v(e.estimated_length).end_arr();
+    for (const PlanEstimate& e : d.estimates) {
+        w.begin_arr().v(e.config.k).v(e.config.micro_batch_size).v(e.config.micro_batch_count).v(e.estimated_length);
+        if (!e.groups.empty()) w.ints(e.groups);  // mixed-k candidates carry their group sizes
+        w.end_arr();
+    }
     w.end_arr();
     w.key("chosen");
     write_config(w, d.chosen);
+    if (!d.chosen_groups.empty()) w.key("chosen_groups").ints(d.chosen_groups);
     w.key("switched").raw(d.switched ? "true" : "false");
     w.end_obj();
 }
@@ -240,7 +244,8 @@ std::string run_scenario(const std::string& request) {
     json::require_keys(req, "scenario",
                        {"schema_version", "op", "model", "cluster", "traces", "plan", "policy", "horizon", "start",
                         "bytes", "trace", "buckets", "clock", "repeats", "window", "samples", "query", "k_max",
-                        "compute_profile", "current", "hysteresis", "candidates", "records"});
+                        "compute_profile", "current", "hysteresis", "candidates", "records",
+                        "group_candidates", "current_groups"});
     if (const Value* sv = req.get("schema_version"))
         if (sv->as_int("schema_version") != 1) throw ConfigError("unsupported schema_version");
     const Value* opv = req.get("op");
@@ -355,8 +360,26 @@ std::string run_scenario(const std::string& request) {
                        static_cast<int>(entry(*c, 2, "current").as_int("M"))};
             const double h = req.get("hysteresis") ? req.get("hysteresis")->as_double("hysteresis") : 0.02;
             const Tick t = req.get("clock") ? req.get("clock")->as_int("clock") : 0;
+            // mixed-k candidates: [[b, [group sizes]], ...]; a mixed incumbent: current_groups
+            std::vector<GroupCandidate> mixed;
+            if (const Value* gc = req.get("group_candidates")) {
+                if (gc->kind != Value::Array) throw ConfigError("group_candidates must be an array");
+                for (const Value& c : gc->arr) {
+                    GroupCandidate g;
+                    g.micro_batch_size = static_cast<int>(entry(c, 0, "group candidate").as_int("b"));
+                    const Value& sizes = entry(c, 1, "group candidate");
+                    if (sizes.kind != Value::Array) throw ConfigError("group candidate sizes must be an array");
+                    for (const Value& n : sizes.arr) g.groups.push_back(static_cast<int>(n.as_int("group size")));
+                    mixed.push_back(std::move(g));
+                }
+            }
+            std::vector<int> cur_groups;
+            if (const Value* cg = req.get("current_groups")) {
+                if (cg->kind != Value::Array) throw ConfigError("current_groups must be an array");
+                for (const Value& n : cg->arr) cur_groups.push_back(static_cast<int>(n.as_int("group size")));
+            }
             w.key("decision");
-            write_decision(w, tuning_round(set, model, comp, store, cur, h, t));
+            write_decision(w, tuning_round_plans(set, mixed, model, comp, store, cur, cur_groups, h, t));
         } else if (op == "tune") {
             const ClusterSpec cluster = parse_cluster(need(req, "cluster"));
             const LinkTraces traces = parse_traces(req.get("traces"), model.stage_count());

@@ -33,26 +33,36 @@ std::vector<std::pair<LinkId, Bytes>> candidate_buckets(const CandidateSet& cand
     return {all.begin(), all.end()};
 }
 
-TuningDecision tuning_round(const CandidateSet& candidates, const ModelSpec& model, const ComputeProfile& compute,
-                            const ProfileStore& comm, const PlanConfig& current, double hysteresis, Tick round_time) {
+TuningDecision tuning_round_plans(const CandidateSet& candidates, const std::vector<GroupCandidate>& mixed,
+                                  const ModelSpec& model, const ComputeProfile& compute, const ProfileStore& comm,
+                                  const PlanConfig& current, const std::vector<int>& current_groups, double hysteresis,
+                                  Tick round_time) {
     TuningDecision d;
     d.round_time = round_time;
-    d.estimates = rank_candidates(candidates, model, compute, comm);
+    d.estimates = rank_plans(candidates, mixed, model, compute, comm);
     if (d.estimates.empty()) throw InfeasibleModel("tuning_round: empty candidate set");
     const PlanEstimate& best = d.estimates.front();
     if (current.k == 0) {  // initial selection: nothing to switch away from
         d.chosen = best.config;
+        d.chosen_groups = best.groups;
         d.switched = false;
         return d;
     }
-    auto cur = std::find_if(d.estimates.begin(), d.estimates.end(),
-                            [&](const PlanEstimate& e) { return e.config == current; });
+    auto cur = std::find_if(d.estimates.begin(), d.estimates.end(), [&](const PlanEstimate& e) {
+        return e.config == current && e.groups == current_groups;
+    });
     if (cur == d.estimates.end()) throw UnknownCandidate("tuning_round: current plan is not a candidate");
     const bool better = static_cast<double>(best.estimated_length) <
                         static_cast<double>(cur->estimated_length) * (1.0 - hysteresis);
-    d.switched = better && !(best.config == current);
+    d.switched = better && !(best.config == current && best.groups == current_groups);
     d.chosen = d.switched ? best.config : current;
+    d.chosen_groups = d.switched ? best.groups : current_groups;
     return d;
+}
+
+TuningDecision tuning_round(const CandidateSet& candidates, const ModelSpec& model, const ComputeProfile& compute,
+                            const ProfileStore& comm, const PlanConfig& current, double hysteresis, Tick round_time) {
+    return tuning_round_plans(candidates, {}, model, compute, comm, current, {}, hysteresis, round_time);
 }
 
 Tick switch_plan(const CandidateSet& candidates, const PlanConfig& current, const PlanConfig& next,

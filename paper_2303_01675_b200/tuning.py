@@ -46,13 +46,16 @@ def all_gather(obj, group=None, world: int = 1):
 class OnlineTuner:
     def __init__(self, ex, rank: int, stages: int, global_batch: int, candidates: list[tuple[int, int]],
                  act_bytes_per_sample: int, hysteresis: float = 0.02, repeats: int = 3, window: int = 8,
-                 group=None, passive: bool = False):
+                 group=None, passive: bool = False, mixed: bool = True):
         self.ex, self.rank, self.S = ex, rank, stages
         self.gb = global_batch
         self.cands = [[k, b, global_batch // b] for k, b in candidates]
         self.act = act_bytes_per_sample
         self.h, self.repeats, self.window, self.group = hysteresis, repeats, window, group
         self.passive = passive  # use observe_iteration() samples for the current payload
+        # mixed-k candidates: for every k that does not divide M, the remainder group first
+        # (shorter warm-up than uniform kFkB's short last group; tests/test_mixed_plans.py)
+        self.mixed = [[b, [M % k] + [k] * (M // k)] for k, b, M in self.cands if M % k] if mixed else []
         self.compute = None
         self.samples: list[list[int]] = []
         self.log: list[dict] = []
@@ -101,21 +104,25 @@ class OnlineTuner:
                     mine.append([link, nbytes, clock, d])
         self._add_samples(sorted(x for r in all_gather(mine, self.group, self.S) for x in r))
 
-    def decide(self, current, clock: int = 0) -> dict:
+    def decide(self, current, clock: int = 0, current_groups=None) -> dict:
         req = {"op": "decide", "model": self.model, "candidates": self.cands, "compute_profile": self.compute,
                "samples": [list(x) for x in self.samples], "hysteresis": self.h, "window": self.window,
                "clock": clock}
+        if self.mixed:
+            req["group_candidates"] = self.mixed
         if current is not None:
-            req["current"] = list(current)
+            req["current"] = list(current)[:3]
+        if current_groups:
+            req["current_groups"] = list(current_groups)
         d = pt.scenario(req)["decision"]
         self.log.append({"request": req, "decision": d})
         return d
 
-    def round(self, current, clock: int = 0) -> dict:
+    def round(self, current, clock: int = 0, current_groups=None) -> dict:
         if self.compute is None:
             self.profile_compute()
         self.profile_links(clock)
-        return self.decide(current, clock)
+        return self.decide(current, clock, current_groups)
 
 
 def pair_bytes_per_sample(shape, hb: int, he: int, has_head: bool) -> int:
