@@ -8,7 +8,9 @@ Fixtures: tests/golden/gpu_tuner_log_*.json, written by bench.py --tuner-log on 
     free), re-tuned every 2 steps with passive link samples, 15 rounds; its first round switches
     from the warm-up incumbent k=1 to k=4 on the measured samples;
   * n4_square_cap16 (round 2): the same trace under a 16 GB cap ((k, b) frontier
-    (1,4) (2,2) (3,1) (4,1)), 15 rounds.
+    (1,4) (2,2) (3,1) (4,1)), 15 rounds;
+  * n4_mixed (round 2): global batch 60 (M=30 at b=2) with the remainder-first mixed-k candidates;
+    its first round switches to groups [2, 4×7] (chosen_groups), which the bench then ran.
 """
 import copy
 import json
@@ -36,6 +38,12 @@ def test_gpu_decisions_replay_bit_exact(path):
         assert pt.scenario(req)["decision"] == got
         ks.append(got["chosen"][0])
     assert all(k >= 1 for k in ks)
+
+
+def test_a_gpu_fixture_switches_to_a_mixed_plan():
+    """A recorded GPU decision chose a mixed-k plan (group sizes) from group_candidates."""
+    assert any(r["decision"].get("chosen_groups") and r["decision"]["switched"]
+               for p in LOGS for r in json.loads(p.read_text())["rounds"])
 
 
 def test_a_gpu_fixture_contains_a_switch():
