@@ -344,14 +344,7 @@ void Executor::begin_iteration(int iter, const int32_t* host_tokens) {
     const int S = cfg_.stages, s = cfg_.stage;
     const bool first = s == 0, last = s == S - 1;
     const int64_t toks = static_cast<int64_t>(cfg_.global_batch) * g.seq;
-    if (host_tokens) {
-        // ids index the embedding / LM-head rows on the device: an out-of-range one is a
-        // ConfigError here (before any state changes) instead of a faulting kernel
-        for (int64_t i = 0; i < 2 * toks; ++i)
-            if (static_cast<uint32_t>(host_tokens[i]) >= static_cast<uint32_t>(g.vocab))
-                throw pipetune::ConfigError("run_iteration: token/label id " + std::to_string(host_tokens[i]) +
-                                            " at " + std::to_string(i) + " outside [0, vocab)");
-    }
+    validate_tokens(host_tokens);  // before any state changes
     iter_ = iter;
     ++epoch_;
     cursor_ = 0;
@@ -388,6 +381,18 @@ void Executor::begin_iteration(int iter, const int32_t* host_tokens) {
         if (peer_scratch_bwd_) ck(emu_.start_contender(1, peer_scratch_bwd_, kScratch, contend_[1]), "contender");
     }
     emu_launches_ = 0;
+}
+
+void Executor::validate_tokens(const int32_t* host_tokens) const {
+    // ids index the embedding / LM-head rows on the device: an out-of-range one is a ConfigError
+    // here instead of a faulting kernel
+    if (!host_tokens) return;
+    const ptk_gpt_config& g = cfg_.gpt;
+    const int64_t n = 2 * static_cast<int64_t>(cfg_.global_batch) * g.seq;
+    for (int64_t i = 0; i < n; ++i)
+        if (static_cast<uint32_t>(host_tokens[i]) >= static_cast<uint32_t>(g.vocab))
+            throw pipetune::ConfigError("run_iteration: token/label id " + std::to_string(host_tokens[i]) + " at " +
+                                        std::to_string(i) + " outside [0, vocab)");
 }
 
 void Executor::peek_next(int* kind, int* mb) const {
@@ -473,6 +478,7 @@ void run_local_pipeline(const std::vector<Executor*>& st, int iter, const int32_
     for (int s = 0; s < S; ++s)
         if (!st[s] || st[s]->cfg().stage != s || st[s]->cfg().stages != S)
             throw std::invalid_argument("run_local_pipeline: stages[s] must be stage s of an S-stage pipeline");
+    for (Executor* e : st) e->validate_tokens(host_tokens);  // all or none of the stages begin
     for (Executor* e : st) e->begin_iteration(iter, host_tokens);
     // enqueued forwards / backwards per stage (both ascending in every plan)
     std::vector<int> nf(static_cast<size_t>(S), 0), nb(static_cast<size_t>(S), 0);

@@ -86,6 +86,8 @@ class Executor {
     // returns false once the iteration is fully enqueued.  Used to interleave
     // several same-process stages in a dependency-respecting global order.
     void begin_iteration(int iter, const int32_t* host_tokens);
+    // ConfigError unless every token / label id of host_tokens is in [0, vocab).
+    void validate_tokens(const int32_t* host_tokens) const;
     bool enqueue_next();
     // Next node of this stage's order (kind 0 F / 1 B / 2 GA, micro-batch), or
     // kind -1 once the iteration is fully enqueued.
