@@ -130,6 +130,17 @@ def stage_slots(stage: int, stages: int, candidates) -> tuple[int, int]:
     return slots, b_max
 
 
+def _tokens_ptr(host_tokens):
+    """host_tokens: None, a raw pointer (int), or an int32 array of 2 * global_batch * seq ids
+    (tokens then labels) — an array stays referenced by the caller's frame for the whole call."""
+    if host_tokens is None or isinstance(host_tokens, int):
+        return host_tokens
+    import numpy as np
+    if not (isinstance(host_tokens, np.ndarray) and host_tokens.dtype == np.int32 and host_tokens.flags.c_contiguous):
+        raise TypeError("host_tokens must be a C-contiguous int32 numpy array or a pointer")
+    return host_tokens.ctypes.data
+
+
 class StageExecutor:
     def __init__(self, shape: ModelShape, stage: int, stages: int, global_batch: int, b_max: int, slots: int,
                  layers: tuple[int, int] | None = None, seed: int = 42, data_seed: int = 1234, lr: float = 1e-4,
@@ -239,10 +250,10 @@ class StageExecutor:
 
     # ---- iterations
     def run_iteration(self, it: int, host_tokens=None):
-        L.check(self.lib.ptk_exec_run_iteration(self.h, it, host_tokens if host_tokens is not None else None))
+        L.check(self.lib.ptk_exec_run_iteration(self.h, it, _tokens_ptr(host_tokens)))
 
     def begin_iteration(self, it: int, host_tokens=None):
-        L.check(self.lib.ptk_exec_begin_iteration(self.h, it, host_tokens if host_tokens is not None else None))
+        L.check(self.lib.ptk_exec_begin_iteration(self.h, it, _tokens_ptr(host_tokens)))
 
     def enqueue_next(self) -> bool:
         more = C.c_int()
@@ -297,7 +308,7 @@ class StageExecutor:
         stage; returns each stage's device ms."""
         lib = stages[0].lib
         arr = (C.c_void_p * len(stages))(*[e.h.value for e in stages])
-        L.check(lib.ptk_exec_run_local(arr, len(stages), it, host_tokens if host_tokens is not None else None))
+        L.check(lib.ptk_exec_run_local(arr, len(stages), it, _tokens_ptr(host_tokens)))
         return [e.finish_iteration() for e in stages]
 
     def close(self):
