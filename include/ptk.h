@@ -252,7 +252,10 @@ int ptk_exec_set_send_streams(ptk_exec* ex, int per_link);
 int ptk_exec_read_loss(ptk_exec* ex, float* loss);
 /* Records of the last finished iteration, ns from its start:
  * {"compute": [[node, kind(0F/1B/2GA), mb, start, end]...], "xfer": [[link, mb, bytes, start, end]...],
- *  "launches": n, "h2d_bytes": n} */
+ *  "launches": n, "h2d_bytes": n, "k": k, "b": b, "groups": [plan group sizes...],
+ *  "t0_globaltimer": the iteration start on the GPU's %globaltimer (ns), "stage": s}.
+ * Scenario op "hardware_report" turns several stages' records into a SimResult
+ * (bubble_report / queue_analysis). */
 int ptk_exec_timeline_json(ptk_exec* ex, char* buf, size_t cap, size_t* written);
 int ptk_exec_probe_link(ptk_exec* ex, int link, int64_t bytes, int repeats, int64_t* out_ns);
 int ptk_exec_profile_compute(ptk_exec* ex, int micro_batch_size, int repeats, int64_t* fwd_ns, int64_t* bwd_ns);
