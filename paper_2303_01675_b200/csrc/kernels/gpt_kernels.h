@@ -14,7 +14,10 @@ cudaError_t layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const 
 // per-parameter partials float[kVecParts][cols] over the micro-batches of an
 // iteration; vec_grad_finalize adds them into the gradient (fixed order) and
 // clears them.  rows % kVecParts == 0.
-constexpr int kVecParts = 256;
+#ifndef PTK_VEC_PARTS
+#define PTK_VEC_PARTS 256
+#endif
+constexpr int kVecParts = PTK_VEC_PARTS;
 struct VecGradSeg {
     float* grad;
     float* part;

@@ -37,12 +37,12 @@ int main() {
             cudaMalloc(&b, h * 2);
             cudaMemset(g, 0x3c, h * 2);
             cudaMemset(b, 0, h * 2);
-            cudaMalloc(&pg, 256 * h * 4);
-            cudaMalloc(&pb, 256 * h * 4);
-            cudaMalloc(&po, 256 * h * 4);
-            cudaMemset(pg, 0, 256 * h * 4);
-            cudaMemset(pb, 0, 256 * h * 4);
-            cudaMemset(po, 0, 256 * h * 4);
+            cudaMalloc(&pg, ptk::kVecParts * h * 4);
+            cudaMalloc(&pb, ptk::kVecParts * h * 4);
+            cudaMalloc(&po, ptk::kVecParts * h * 4);
+            cudaMemset(pg, 0, ptk::kVecParts * h * 4);
+            cudaMemset(pb, 0, ptk::kVecParts * h * 4);
+            cudaMemset(po, 0, ptk::kVecParts * h * 4);
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
