@@ -989,10 +989,7 @@ struct BwCfg {
     // no TMEM room for them (X, Y and the 2d-column accumulator fill 512 columns).
     static constexpr bool kTs = D == 64;
     static constexpr int kTile = kBlk * D * 2;  // one [128][D] tile
-#ifndef PTK_BW_STAGES
-#define PTK_BW_STAGES 2
-#endif
-    static constexpr int kStages = D == 64 ? PTK_BW_STAGES : 1;
+    static constexpr int kStages = D == 64 ? 2 : 1;  // the ld_full / ld_empty barrier pairs hold two stages
     static constexpr int kFixBuf = D == 64 ? 2 : 1;
     static constexpr int kAccBuf = (KV && (D == 128 || kTs)) ? 1 : 2;
     static constexpr int kAccCols = KV ? 2 * D : D;  // per accumulator buffer
