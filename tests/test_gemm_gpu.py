@@ -5,7 +5,6 @@ operands (the attention head layout), all epilogues and the causal modes.
 Tolerance: bf16 output rounding (rel 1e-2 of the row scale) on top of fp32
 accumulation order differences.
 """
-import math
 
 import pytest
 import torch
