@@ -1169,7 +1169,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    pdl_begin();  // previous kernel complete: its outputs (qkv, lse, dO, ...) are visible
+    if (KV) {
+        pdl_begin();  // previous kernel complete: its outputs (qkv, lse, dO, D, ...) are visible
+    } else {
+        // The dQ pass reads only what the dK/dV pass read (qkv, dO, lse, D: complete before that
+        // pass started, and this grid launches only after it passed its own wait) and writes
+        // disjoint dqkv columns, so it need not wait for the dK/dV pass: its CTAs take the SMs the
+        // dK/dV pass frees in its tail.  It waits at the end instead, so kernels after it still see
+        // both passes complete.
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
 
     if (warp == 0) {
         if (C::kTs) reg_dealloc<72>();
@@ -1487,6 +1496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         tmem_dealloc<512>(tmem);
     }
+    if (!KV) asm volatile("griddepcontrol.wait;" ::: "memory");  // see the prologue
 }
 
 // D[b][H][q] = sum_dd dO[q][hh*d+dd] * O[q][hh*d+dd]: one warp per token row,
