@@ -26,7 +26,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
           f"-I{ROOT / 'include'}", f"-I{CSRC}"]
-CUDA_FLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"] + COMMON
+# PTK_EXTRA_NVCC_FLAGS: extra -D switches for experiments (part of the object cache key)
+CUDA_FLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"] + COMMON + \
+    os.environ.get("PTK_EXTRA_NVCC_FLAGS", "").split()
 CXX_FLAGS = COMMON + ["-x", "c++"]
 
 

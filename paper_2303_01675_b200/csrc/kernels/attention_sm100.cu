@@ -989,23 +989,31 @@ struct BwCfg {
     // no TMEM room for them (X, Y and the 2d-column accumulator fill 512 columns).
     static constexpr bool kTs = D == 64;
     static constexpr int kTile = kBlk * D * 2;  // one [128][D] tile
-    static constexpr int kStages = D == 64 ? 2 : 1;  // the ld_full / ld_empty barrier pairs hold two stages
+    // step operand stages: with three, the load of step n+2 does not wait for step n's accumulating
+    // products to release its stage (a TMA round trip that sat on the critical path with two)
+    static constexpr int kStages = D == 64 ? 3 : 1;
     static constexpr int kFixBuf = D == 64 ? 2 : 1;
     static constexpr int kAccBuf = (KV && (D == 128 || kTs)) ? 1 : 2;
     static constexpr int kAccCols = KV ? 2 * D : D;  // per accumulator buffer
     static constexpr int kPd = kBlk * kBlk * 2;      // one [128][128] bf16 A-operand buffer (smem path)
-    static constexpr int kSmem =
-        kFixBuf * 2 * kTile + kStages * 2 * kTile + (kTs ? 0 : 2 * kPd) + 2 * 2 * kBlk * 4 + 1024 + 256;
+    // epilogue staging for the TMA stores of a tile's outputs (KV: dV and dK, Q: dQ; 128B-swizzled
+    // [128 rows][64 cols] atoms); the smem path (d = 128) stages in the P / dS buffers instead
+    static constexpr int kOutBytes = kTs ? (KV ? 2 : 1) * kTile : 0;
+    static constexpr int kRowBytes = 2 * kBlk * 4;  // per stage: the stepped block's lse[128], τD[128] (KV)
+    static constexpr int kSmem = kFixBuf * 2 * kTile + kStages * 2 * kTile + (kTs ? 0 : 2 * kPd) + kOutBytes +
+                                 kStages * kRowBytes + 1024 + 256;
     static constexpr uint32_t kX = 0, kY = 128, kAcc = 256;
     static constexpr uint32_t kP = kAcc + kAccBuf * kAccCols, kDS = kP + 64;  // TMEM A operands (kTs)
     static_assert(!kTs || kDS + 64 <= 512, "TMEM budget");
+    static_assert(kStages <= 4, "ld_full / ld_empty hold four stages");
+    static_assert(kSmem <= 232448, "backward smem");
 };
 
 struct BwArgs {
     __nv_bfloat16* dqkv;  // [b*s][3h]
     float* col_part;      // optional [b*s/32][3h] += column sums of dqkv per 32 rows
     const float* lse;     // [b][H][s]
-    const float* dsum;    // [b][H][s]
+    const float* dsum;    // [b][H][s]: τ·D
     int s, H, h, b;
     float scale_log2, tau;
     int causal;
@@ -1017,7 +1025,7 @@ __device__ unsigned long long g_attn_trace[2][64][8];
 __device__ int g_attn_trace_kv = 1;  // which backward kernel records (1: KV, 0: Q)
 #define ATRACE(role, step, ev)                                                                        \
     do {                                                                                              \
-        if (blockIdx.x == 0 && (step) < 64 && g_attn_trace_kv == (KV ? 1 : 0))                       \
+        if (atrace_on && (step) < 64)                                                                 \
             g_attn_trace[role][step][ev] = clock64();                                                 \
     } while (0)
 #else
@@ -1118,7 +1126,7 @@ __device__ __forceinline__ void bw_pass(const float (&x)[32], const float (&y)[3
 template <int D, bool KV>
 __global__ void __launch_bounds__(kThreads, 1)
     flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
-                     const __grid_constant__ BwArgs a) {
+                     const __grid_constant__ CUtensorMap tmDQKV, const __grid_constant__ BwArgs a) {
     using C = BwCfg<D, KV>;
     constexpr int S = C::kStages, FB = C::kFixBuf, AB = C::kAccBuf;
     constexpr uint32_t kIdescXY = make_idesc_bf16(kBlk, kBlk, false, false);
@@ -1130,33 +1138,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sStep = sFix + FB * 2 * C::kTile;      // [S][2 tiles]: (Q_i, dO_i) (KV) | (K_j, V_j) (Q)
     uint8_t* sP = sStep + S * 2 * C::kTile;         // Pᵀ (KV only; smem path)
     uint8_t* sDS = sP + (C::kTs ? 0 : C::kPd);      // dSᵀ (KV) | dS (Q) (smem path)
-    float* sRow = reinterpret_cast<float*>(sDS + (C::kTs ? 0 : C::kPd));  // [2][lse[128], D[128]] (KV only)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sRow + 2 * 2 * kBlk);
-    uint64_t* fix_full = bars + 0;   // [2]
-    uint64_t* fix_empty = bars + 2;  // [2]
-    uint64_t* ld_full = bars + 4;    // [2]
-    uint64_t* ld_empty = bars + 6;   // [2]
+    uint8_t* sOut = C::kTs ? sDS + 0 : sP;          // epilogue staging (dedicated for d = 64)
+    // [S][lse[128], τD[128]] of the stepped query block (KV), bulk-loaded with the stage's tiles
+    float* sRow = reinterpret_cast<float*>(sDS + (C::kTs ? C::kOutBytes : C::kPd));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sRow) + S * C::kRowBytes);
+    uint64_t* fix_full = bars + 0;    // [2]
+    uint64_t* fix_empty = bars + 2;   // [2]
+    uint64_t* ld_full = bars + 16;    // [4]
+    uint64_t* ld_empty = bars + 20;   // [4]
     uint64_t* xy_full = bars + 8;
     uint64_t* xy_free = bars + 9;
     uint64_t* pd_full = bars + 10;
     uint64_t* pd_free = bars + 11;
     uint64_t* acc_full = bars + 12;   // [2]
     uint64_t* acc_empty = bars + 14;  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
+#ifdef PTK_ATTN_TRACE
+    // read once: a global load inside every trace point would add its latency to the timeline
+    const bool atrace_on = blockIdx.x == 0 && *static_cast<volatile int*>(&g_attn_trace_kv) == (KV ? 1 : 0);
+#endif
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmQKV);
         tma_prefetch_desc(&tmDO);
+        tma_prefetch_desc(&tmDQKV);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&fix_full[i], 1);
             mbar_init(&fix_empty[i], 1);
-            mbar_init(&ld_full[i], 1);
-            mbar_init(&ld_empty[i], 1);
             mbar_init(&acc_full[i], 1);
             mbar_init(&acc_empty[i], 8);
+        }
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&ld_full[i], 1);
+            mbar_init(&ld_empty[i], 1);
         }
         mbar_init(xy_full, 1);
         mbar_init(xy_free, 8);
@@ -1205,12 +1222,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int t = 0; t < c.nsteps; ++t, ++n) {
                     const int st = n % S;
                     mbar_wait(&ld_empty[st], ((n / S) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&ld_full[st], 2 * C::kTile);
+                    mbar_arrive_expect_tx(&ld_full[st], 2 * C::kTile + (KV ? C::kRowBytes : 0));
                     uint8_t* t0 = sStep + st * 2 * C::kTile;
                     const int row0 = (c.first + t) * kBlk;
                     if (KV) {
                         load_tile(&tmQKV, &ld_full[st], t0, row0, c.head, c.bi);            // Q_i
                         load_tile(&tmDO, &ld_full[st], t0 + C::kTile, row0, c.head, c.bi);  // dO_i
+                        // the per-query softmax statistics every elementwise thread reads (no exchange)
+                        const int64_t rb = (static_cast<int64_t>(c.bi) * a.H + c.head) * a.s + row0;
+                        float* rows = sRow + st * (C::kRowBytes / 4);
+                        bulk_load(rows, a.lse + rb, kBlk * 4, &ld_full[st]);
+                        bulk_load(rows + kBlk, a.dsum + rb, kBlk * 4, &ld_full[st]);
                     } else {
                         load_tile(&tmQKV, &ld_full[st], t0, row0, a.H + c.head, c.bi);                  // K_j
                         load_tile(&tmQKV, &ld_full[st], t0 + C::kTile, row0, 2 * a.H + c.head, c.bi);  // V_j
@@ -1325,14 +1347,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         //   KV: the stepped query block's lse (half 0) / D (half 1) at row r of that block
         //   Q:  this tile's own lse and D at row r
         auto stats = [&](const BwCursor& q, float& s0, float& s1) {
+            if (KV) return;  // KV: the stepped block's statistics arrive in smem with its tiles
             const int64_t rb = (static_cast<int64_t>(q.bi) * a.H + q.head) * a.s;
-            if (KV) {
-                s0 = (half == 0 ? a.lse : a.dsum)[rb + (q.first + q.j) * kBlk + r];
-                s1 = 0.f;
-            } else {
-                s0 = a.lse[rb + q.blk * kBlk + r];
-                s1 = a.dsum[rb + q.blk * kBlk + r];
-            }
+            s0 = a.lse[rb + q.blk * kBlk + r];
+            s1 = a.dsum[rb + q.blk * kBlk + r];
         };
         int n = 0;  // steps processed so far (all tiles)
         BwCursor c, cn;
@@ -1347,13 +1365,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             {
                 const int t = c.j;
                 const int other = c.first + t;  // index of the stepped block
-                const float my_lse = cur0, my_d = cur1 * a.tau;
-                const uint32_t rowv = rowv0 + (n & 1) * 2 * kBlk * 4;
-                if (KV) {  // this step's per-query lse (half 0) / τ·D (half 1) -> smem, barrier over the 8 warps
-                    sts32f(rowv + (half * kBlk + r) * 4, half == 0 ? cur0 : cur0 * a.tau);
-                    asm volatile("bar.sync 1, 256;" ::: "memory");
-                }
+                const float my_lse = cur0, my_d = cur1;
+                const uint32_t rowv = rowv0 + (n % S) * C::kRowBytes;
+                if (warp == 4 && lane == 0) ATRACE(0, n, 5);
                 mbar_wait(xy_full, n & 1);
+                if (KV) mbar_wait(&ld_full[n % S], (n / S) & 1);  // the stage's lse / τD landed (long done)
                 if (warp == 4 && lane == 0) ATRACE(0, n, 0);
                 tc_fence_after();
                 const bool diag = a.causal && other == c.blk;
@@ -1377,6 +1393,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(xy_free);
                     if (warp == 4 && lane == 0) ATRACE(0, n, 1);
+                    // each 32-column pass goes to TMEM as soon as it is packed: the wait for the previous
+                    // step's accumulating products and the first store overlap the second pass
 #pragma unroll
                     for (int pass = 0; pass < 2; ++pass) {
                         const int cb0 = half * 64 + pass * 32;
@@ -1386,7 +1404,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else
                             bw_pass<KV, false>(x[pass], y[pass], rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16,
                                                pk_d + pass * 16);
+                        if (pass == 0) {
+                            if (n > 0) mbar_wait(pd_free, (n - 1) & 1);  // previous step's MMAs done reading P / dS
+                            tc_fence_after();
+                            if (warp == 4 && lane == 0) ATRACE(0, n, 3);
+                        }
+                        if (KV) tmem_st_32x32b_x16_u_nw(tmem + lane_base + C::kP + half * 32 + pass * 16, pk_p + pass * 16);
+                        tmem_st_32x32b_x16_u_nw(tmem + lane_base + C::kDS + half * 32 + pass * 16, pk_d + pass * 16);
                     }
+                    tmem_st_wait();
                 } else {
 #pragma unroll
                     for (int pass = 0; pass < 2; ++pass) {
@@ -1409,17 +1435,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 if (warp == 4 && lane == 0) ATRACE(0, n, 2);
-                if (n > 0) {
-                    mbar_wait(pd_free, (n - 1) & 1);  // previous step's MMAs done reading sP / sDS
-                }
-                if (warp == 4 && lane == 0) ATRACE(0, n, 3);
-                if (C::kTs) {
-                    // this thread's 64 columns = 32 TMEM columns (bf16 pairs) of its row's A operand
-                    if (KV) tmem_st_32x32b_x32_u_nw(tmem + lane_base + C::kP + half * 32, pk_p);
-                    tmem_st_32x32b_x32_u_nw(tmem + lane_base + C::kDS + half * 32, pk_d);
-                    tmem_st_wait();
-                } else {
-                    // columns [64*half, +64) are swizzle atom `half` of each [128][128] operand
+                if (!C::kTs) {
+                    if (n > 0) mbar_wait(pd_free, (n - 1) & 1);  // previous step's MMAs done reading sP / sDS
+                    if (warp == 4 && lane == 0) ATRACE(0, n, 3);
+                    // this thread's 64 columns are swizzle atom `half` of each [128][128] operand
                     const uint32_t prow = pbuf + half * (kBlk * 128) + r * 128;
                     const uint32_t drow = dbuf + half * (kBlk * 128) + r * 128;
 #pragma unroll
@@ -1435,33 +1454,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(pd_full);
                 if (warp == 4 && lane == 0) ATRACE(0, n, 4);
+                if (warp == 11 && lane == 0) ATRACE(0, n, 6);
             }
             if (c.j < c.nsteps - 1) {
                 bw_next<KV>(a, c);
                 continue;
             }
             const int ab = AB == 1 ? 0 : (c.k & 1);
+            // epilogue: accumulators -> bf16 -> swizzled smem staging -> TMA stores into dqkv.  KV:
+            // half 0 holds dV (section 2), half 1 dK (section 1); Q: dQ, half h columns [h*D/2, +D/2).
+            // (Direct row-per-thread global stores cost ~2000 cycles per tile: every warp store
+            // touched 32 rows.)
+            constexpr int kCols = KV ? D : D / 2;
+            const int sec = KV ? (half == 0 ? 2 : 1) : 0;
+            const int64_t colbase = static_cast<int64_t>(sec) * a.h + c.head * D + (KV ? 0 : half * (D / 2));
+            const int64_t prow = (static_cast<int64_t>(c.bi) * a.s + c.blk * kBlk + (r & ~31)) / 32;
+            float cp_old[kCols / 32];
+            if (a.col_part != nullptr) {  // this thread's own bias partials, fetched off the critical path
+#pragma unroll
+                for (int cc = 0; cc < kCols / 32; ++cc) cp_old[cc] = a.col_part[prow * (3 * a.h) + colbase + cc * 32 + lane];
+            }
+            if (warp == 4 && lane == 0) tma_store_wait_read();  // the previous tile's stores left the staging
+            asm volatile("bar.sync 1, 256;" ::: "memory");
             mbar_wait(&acc_full[ab], (c.k / AB) & 1);
             tc_fence_after();
-            // epilogue: accumulators -> dqkv (bf16).  KV: half 0 writes dV (section 2),
-            // half 1 writes dK (section 1).  Q: dQ, half h writes columns [h*D/2, +D/2).
-            const int row = c.blk * kBlk + r;
-            __nv_bfloat16* base = a.dqkv + (static_cast<int64_t>(c.bi) * a.s + row) * (3 * a.h) + c.head * D;
-            __nv_bfloat16* dst = KV ? base + (half == 0 ? 2 * a.h : a.h) : base + half * (D / 2);
             const uint32_t col0 = C::kAcc + ab * C::kAccCols + (KV ? half * D : half * (D / 2));
-            constexpr int kCols = KV ? D : D / 2;
+            const uint32_t stage = smem_u32(sOut) + (KV ? half * C::kTile : 0);
 #pragma unroll
             for (int cc = 0; cc < kCols / 32; ++cc) {
                 float v[32];
                 tmem_ld_32x32b_x32(tmem + lane_base + col0 + cc * 32, v);
+                const int cs = (KV ? 0 : half * (D / 2)) + cc * 32;  // column within the section's head
+                const uint32_t row_addr = stage + (cs / 64) * (kBlk * 128) + r * 128;
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    uint4 u;
-                    u.x = pack_bf16(v[g * 8 + 0], v[g * 8 + 1]);
-                    u.y = pack_bf16(v[g * 8 + 2], v[g * 8 + 3]);
-                    u.z = pack_bf16(v[g * 8 + 4], v[g * 8 + 5]);
-                    u.w = pack_bf16(v[g * 8 + 6], v[g * 8 + 7]);
-                    *reinterpret_cast<uint4*>(dst + cc * 32 + g * 8) = u;
+                    const uint4 u = make_uint4(pack_bf16(v[g * 8 + 0], v[g * 8 + 1]), pack_bf16(v[g * 8 + 2], v[g * 8 + 3]),
+                                               pack_bf16(v[g * 8 + 4], v[g * 8 + 5]), pack_bf16(v[g * 8 + 6], v[g * 8 + 7]));
+                    sts128(row_addr + ((((cs % 64) / 8 + g) ^ (r & 7)) * 16), u);
                 }
                 if (a.col_part != nullptr) {
                     // QKV bias gradient: column sums of the warp's 32 rows of dqkv as stored.  A
@@ -1479,16 +1508,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                             x[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
                         }
                     }
-                    const int64_t prow = (static_cast<int64_t>(c.bi) * a.s + c.blk * kBlk + (r & ~31)) / 32;
-                    const int64_t col = (dst - base) + c.head * D + cc * 32 + lane;
-                    a.col_part[prow * (3 * a.h) + col] += x[0];
+                    cp_old[cc] += x[0];
                 }
             }
             tc_fence_before();
-            __syncwarp();
+            fence_proxy_async_smem();
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // staging complete, accumulators read
             if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            if (warp == 4 && lane == 0) {
+                const int row0 = c.blk * kBlk;
+#pragma unroll
+                for (int h2 = 0; h2 < (KV ? 2 : 1); ++h2) {
+                    const int sec2 = KV ? (h2 == 0 ? 2 : 1) : 0;
+#pragma unroll
+                    for (int kb = 0; kb < D / 64; ++kb)
+                        tma_store_4d(&tmDQKV, sOut + h2 * C::kTile + kb * (kBlk * 128), kb * 64, row0, sec2 * a.H + c.head,
+                                     c.bi);
+                }
+                tma_store_commit();
+                if (!C::kTs) tma_store_wait_read();  // the staging is the P / dS buffers of the next step
+            }
+            if (!C::kTs) asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (a.col_part != nullptr) {
+#pragma unroll
+                for (int cc = 0; cc < kCols / 32; ++cc) a.col_part[prow * (3 * a.h) + colbase + cc * 32 + lane] = cp_old[cc];
+            }
             bw_next<KV>(a, c);
         }
+        if (warp == 4 && lane == 0) tma_store_wait_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -1499,13 +1546,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!KV) asm volatile("griddepcontrol.wait;" ::: "memory");  // see the prologue
 }
 
-// D[b][H][q] = sum_dd dO[q][hh*d+dd] * O[q][hh*d+dd]: one warp per token row,
+// D[b][H][q] = τ · sum_dd dO[q][hh*d+dd] * O[q][hh*d+dd] (τ = 1/sqrt(d), the score scale the
+// backward's dS = τ P (dP - D) needs, applied once here): one warp per token row,
 // coalesced 16-byte loads over the whole row, per-head sums reduced across the
 // d/8 lanes that hold a head (fixed shuffle order: deterministic).
 template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ dO,
                                                            const __nv_bfloat16* __restrict__ O,
-                                                           float* __restrict__ dsum, int rows, int s, int H) {
+                                                           float* __restrict__ dsum, int rows, int s, int H,
+                                                           float tau) {
     pdl_begin();
     constexpr int kLanesPerHead = D / 8;
     const int row = blockIdx.x * 8 + threadIdx.x / 32;
@@ -1543,7 +1592,7 @@ __global__ void __launch_bounds__(256) attn_bwd_dot_kernel(const __nv_bfloat16* 
             for (int o = 1; o < kLanesPerHead; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (ci < chunks && (lane % kLanesPerHead) == 0) {
                 const int head = ci / kLanesPerHead;
-                dsum[(static_cast<int64_t>(bi) * H + head) * s + q] = acc;
+                dsum[(static_cast<int64_t>(bi) * H + head) * s + q] = acc * tau;
             }
         }
     }
@@ -1580,7 +1629,7 @@ cudaError_t launch_bwd(const FlashBwdPlan& p, cudaStream_t st) {
              p.causal};
     const int tiles = p.s / kBlk * p.H * p.b;
     const int grid = tiles < sm_count() ? tiles : sm_count();
-    return launch_kernel(flash_bwd_kernel<D, KV>, grid, kThreads, C::kSmem, st, 1, p.tmQKV, p.tmDO, a);
+    return launch_kernel(flash_bwd_kernel<D, KV>, grid, kThreads, C::kSmem, st, 1, p.tmQKV, p.tmDO, p.tmDQKV, a);
 }
 
 }  // namespace
@@ -1591,6 +1640,8 @@ cudaError_t flash_bwd_prepare(const void* qkv, const void* o, const void* dO, co
     cudaError_t e = qkv_map(&p->tmQKV, qkv, b, s, H, d, kBlk);
     if (e != cudaSuccess) return e;
     e = do_map(&p->tmDO, dO, b, s, H, d);
+    if (e != cudaSuccess) return e;
+    e = qkv_map(&p->tmDQKV, dqkv, b, s, H, d, kBlk);
     if (e != cudaSuccess) return e;
     p->o = static_cast<const __nv_bfloat16*>(o);
     p->dO = static_cast<const __nv_bfloat16*>(dO);
@@ -1610,9 +1661,11 @@ cudaError_t flash_backward(const FlashBwdPlan& p, cudaStream_t st) {
     const int rows = p.b * p.s;
     cudaError_t e;
     if (p.d == 64)
-        e = launch_kernel(attn_bwd_dot_kernel<64>, (rows + 7) / 8, 256, 0, st, 1, p.dO, p.o, p.dsum, rows, p.s, p.H);
+        e = launch_kernel(attn_bwd_dot_kernel<64>, (rows + 7) / 8, 256, 0, st, 1, p.dO, p.o, p.dsum, rows, p.s, p.H,
+                          1.f / sqrtf(64.f));
     else
-        e = launch_kernel(attn_bwd_dot_kernel<128>, (rows + 7) / 8, 256, 0, st, 1, p.dO, p.o, p.dsum, rows, p.s, p.H);
+        e = launch_kernel(attn_bwd_dot_kernel<128>, (rows + 7) / 8, 256, 0, st, 1, p.dO, p.o, p.dsum, rows, p.s, p.H,
+                          1.f / sqrtf(128.f));
     if (e != cudaSuccess) return e;
     e = p.d == 64 ? launch_bwd<64, true>(p, st) : launch_bwd<128, true>(p, st);
     if (e != cudaSuccess) return e;

@@ -25,6 +25,7 @@ cudaError_t flash_forward(const FlashPlan& p, cudaStream_t st);
 struct FlashBwdPlan {
     alignas(64) CUtensorMap tmQKV;  // qkv as {d, s, 3H, b}, box {64, 128}
     alignas(64) CUtensorMap tmDO;   // dO [b*s][H*d] as {d, s, H, b}, box {64, 128}
+    alignas(64) CUtensorMap tmDQKV;  // dqkv as {d, s, 3H, b}, box {64, 128}: the epilogue's TMA stores
     const __nv_bfloat16* o = nullptr;
     const __nv_bfloat16* dO = nullptr;
     const float* lse = nullptr;

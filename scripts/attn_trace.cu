@@ -111,11 +111,12 @@ int main(int argc, char** argv) {
     cudaMemcpyFromSymbol(tr, ptk::g_attn_trace, sizeof tr);
     const unsigned long long t0 = tr[1][0][0];
     printf("%s kernel, CTA 0, cycles since the first XY issue\n", kv ? "KV" : "Q");
-    printf("step | mma: xy_issue_begin xy_issued pd_full_seen acc_issued acc_done(MMA build only) | ew: xy_full xy_free computed pd_free stored\n");
+    printf("step | mma: xy_issue_begin xy_issued pd_full_seen acc_issued acc_done(MMA build only) | ew: row_barrier "
+           "xy_full xy_free computed pd_free stored stored(warp 11)\n");
     for (int n = 0; n < 20; ++n) {
         auto f = [&](int r, int ev) { return static_cast<long long>(tr[r][n][ev] - t0); };
-        printf("%3d | %8lld %8lld %8lld %8lld %8lld | %8lld %8lld %8lld %8lld %8lld\n", n, f(1, 0), f(1, 1), f(1, 2),
-               f(1, 3), f(1, 4), f(0, 0), f(0, 1), f(0, 2), f(0, 3), f(0, 4));
+        printf("%3d | %8lld %8lld %8lld %8lld %8lld | %8lld %8lld %8lld %8lld %8lld %8lld %8lld\n", n, f(1, 0), f(1, 1),
+               f(1, 2), f(1, 3), f(1, 4), f(0, 5), f(0, 0), f(0, 1), f(0, 2), f(0, 3), f(0, 4), f(0, 6));
     }
     return 0;
 }
