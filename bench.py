@@ -323,13 +323,26 @@ def main():
         for c in cands[1:]:
             run(1, c)  # every candidate plan warmed (GEMM / attention plans cached)
 
+    gemm_stride = int(os.environ.get("PTK_BENCH_GEMM_STRIDE", "32"))
+    gemm_sampling = os.environ.get("PTK_BENCH_GEMM_TIMING", "1") != "0"  # 0: diagnostics, no per-GEMM events
+
+    def run_arm(n, cfg):
+        """A fixed-plan arm under the same GEMM event sampling as the timed Ada-Grouper arm (the events
+        break the PDL overlap of the sampled micro-batch), so the arms compare like for like."""
+        if gemm_sampling:
+            ex.gemm_timing(gemm_stride)
+        out = run(n, cfg)
+        if gemm_sampling:
+            ex.gemm_timing(0)  # discarded: the roofline is the Ada-Grouper arm's
+        return out
+
     # ---- fixed-plan arms (same kernels, same trace from t=0)
     fixed = {}
     if S > 1:
         for k in (sorted(by_k) if args.k_sweep else (1, 2)):
             if k in by_k:
                 arm_reset()
-                fixed[k] = run(args.steps, by_k[k])
+                fixed[k] = run_arm(args.steps, by_k[k])
                 log(f"fixed arm k={k}: {sum(fixed[k]):.1f} ms")
         if wgrad_pairs and 1 in by_k:
             # 1F1B also with one weight-gradient GEMM per micro-batch: pairing alternates short and
@@ -337,7 +350,7 @@ def main():
             # faster of the two (decided on the max-over-ranks times below)
             ex.set_wgrad_pairs(False)
             arm_reset()
-            fixed["1_unpaired"] = run(args.steps, by_k[1])
+            fixed["1_unpaired"] = run_arm(args.steps, by_k[1])
             ex.set_wgrad_pairs(True)
 
     # ---- timed region: Ada-Grouper (tuning round at start, re-tune every `retune` steps)
@@ -348,10 +361,10 @@ def main():
     chosen, chosen_groups, decisions, tune_s = cands[0], [], [], 0.0
     arm_reset()
     with ClockSampler(local) as clk:
-        if os.environ.get("PTK_BENCH_GEMM_TIMING", "1") != "0":  # 0: diagnostics, no per-GEMM events
+        if gemm_sampling:
             # one micro-batch in 32 per stage and step, rotating with the step: event records between GEMMs
             # break the PDL overlap of the sampled micro-batches (1 in 8 cost BERT-large 4.5 % of a step)
-            ex.gemm_timing(int(os.environ.get("PTK_BENCH_GEMM_STRIDE", "32")))
+            ex.gemm_timing(gemm_stride)
         t0 = time.perf_counter()
         ms, plans_run = [], []
         for step in range(args.steps):
