@@ -367,8 +367,21 @@ def main():
             ex.gemm_timing(gemm_stride)
         t0 = time.perf_counter()
         ms, plans_run = [], []
+        # A re-tuning round whose candidates all share the running plan's micro-batch size needs no
+        # probe (the passive samples of the last iteration cover every candidate payload on every
+        # rank), so it runs on the host WHILE the GPU executes the step before the boundary, on the
+        # timeline of the step before that; the decision applies from the boundary on.  Only the host
+        # time the step did not cover is charged.  Rounds that must probe stay at the boundary with
+        # the pipeline suspended.
+        overlap_ok = tuner is not None and args.passive_profile and args.retune > 0 and \
+            os.environ.get("PTK_BENCH_OVERLAP_TUNING", "1") != "0"
+        pending, last_tl = None, None
         for step in range(args.steps):
-            if tuner is not None and (step == 0 or (args.retune > 0 and step % args.retune == 0)):
+            due = tuner is not None and (step == 0 or (args.retune > 0 and step % args.retune == 0))
+            if pending is not None:  # decided during the previous step
+                chosen, chosen_groups = pending
+                pending = None
+            elif due:
                 tr0 = time.perf_counter()
                 if step > 0 and args.passive_profile:
                     tuner.observe_iteration(ex.timeline(), clock=step)
@@ -380,8 +393,28 @@ def main():
                 chosen_groups = d.get("chosen_groups", [])
                 barrier()
                 tune_s += time.perf_counter() - tr0
-            ms += run(1, chosen, chosen_groups)
+            if chosen_groups:
+                ex.set_plan_groups(chosen[1], chosen_groups)
+            else:
+                ex.set_plan(chosen[0], chosen[1])
+            ex.run_iteration(it)
+            nxt, host_s = step + 1, None
+            if (overlap_ok and last_tl is not None and nxt < args.steps and nxt % args.retune == 0
+                    and all(c[1] == chosen[1] for c in cands)):
+                tr0 = time.perf_counter()
+                tuner.observe_iteration(last_tl, clock=nxt)
+                d = tuner.round(list(chosen), clock=nxt, current_groups=chosen_groups)
+                decisions.append(d)
+                pending = (d["chosen"], d.get("chosen_groups", []))
+                barrier()
+                host_s = time.perf_counter() - tr0
+            dev_ms = ex.finish_iteration()
+            it += 1
+            ms.append(dev_ms)
+            if host_s is not None:
+                tune_s += max(0.0, host_s - dev_ms * 1e-3)
             plans_run.append([chosen[0], chosen[1]] + ([chosen_groups] if chosen_groups else []))
+            last_tl = ex.timeline() if overlap_ok and (step + 2) % args.retune == 0 else None
         barrier()
         wall = time.perf_counter() - t0
         gemm_flops, gemm_ms, gemm_n = ex.gemm_timing(0)
