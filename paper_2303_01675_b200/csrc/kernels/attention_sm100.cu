@@ -1000,8 +1000,14 @@ struct BwCfg {
     // [128 rows][64 cols] atoms); the smem path (d = 128) stages in the P / dS buffers instead
     static constexpr int kOutBytes = kTs ? (KV ? 2 : 1) * kTile : 0;
     static constexpr int kRowBytes = 2 * kBlk * 4;  // per stage: the stepped block's lse[128], τD[128] (KV)
+    // KV: the per-query softmax statistics enter the score products as extra K columns: per stage a
+    // [128 queries][16] bf16 "stats" operand (−lse/c and −D, each as three bf16 terms) and, fixed, two
+    // [128 keys][16] "ones" operands selecting them (X' = S − lse/c, Y' = dPᵀ − D); K-major, no swizzle
+    static constexpr bool kFold = KV && D == 64;  // d = 128 (one stage) keeps the smem row reads
+    static constexpr int kStatBytes = kBlk * 16 * 2;  // 4 KiB
+    static constexpr int kStatSmem = kFold ? (kStages + 2) * kStatBytes : 0;
     static constexpr int kSmem = kFixBuf * 2 * kTile + kStages * 2 * kTile + (kTs ? 0 : 2 * kPd) + kOutBytes +
-                                 kStages * kRowBytes + 1024 + 256;
+                                 kStatSmem + kStages * kRowBytes + 1024 + 256;
     static constexpr uint32_t kX = 0, kY = 128, kAcc = 256;
     static constexpr uint32_t kP = kAcc + kAccBuf * kAccCols, kDS = kP + 64;  // TMEM A operands (kTs)
     static_assert(!kTs || kDS + 64 <= 512, "TMEM budget");
@@ -1073,7 +1079,7 @@ __device__ __forceinline__ float4 lds128f(uint32_t addr) {
 // 32 columns [cb0, cb0+32) of one row: P = 2^(X c - lse) and dS = P (τ Y - τ D),
 // packed to bf16 pairs.  KV: the per-column (query) lse / τD come from smem
 // (rowv); Q: the row's own my_lse / my_d.  MASK only on diagonal blocks.
-template <bool KV, bool MASK>
+template <bool KV, bool MASK, bool FOLD>
 __device__ __forceinline__ void bw_pass(const float (&x)[32], const float (&y)[32], uint32_t rowv, int cb0, int r,
                                         float sc, float tau, float my_lse, float my_d, uint32_t* pk_p,
                                         uint32_t* pk_d) {
@@ -1081,7 +1087,7 @@ __device__ __forceinline__ void bw_pass(const float (&x)[32], const float (&y)[3
     for (int e4 = 0; e4 < 8; ++e4) {
         const int cb = cb0 + e4 * 4;
         float l2[4], dd[4];
-        if (KV) {
+        if (KV && !FOLD) {
             const float4 lv = lds128f(rowv + cb * 4);
             const float4 dv = lds128f(rowv + (kBlk + cb) * 4);
             l2[0] = lv.x, l2[1] = lv.y, l2[2] = lv.z, l2[3] = lv.w;
@@ -1092,34 +1098,59 @@ __device__ __forceinline__ void bw_pass(const float (&x)[32], const float (&y)[3
         }
         float pv[4], dv4[4];
         float xs[4];
+        if constexpr (FOLD) {
+            // X' = S − lse/c and Y' = dPᵀ − D come out of the score products: P = 2^(c X'),
+            // dS/τ = P Y' (τ is applied to the dK accumulator in the epilogue)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            xs[u] = x[e4 * 4 + u];
-            if (MASK) {
-                // KV: row = key, col = query -> valid iff query >= key ; Q: row = query, col = key
-                const int col = cb + u;
-                if (KV ? col < r : col > r) xs[u] = -INFINITY;  // exp2(-inf) = 0
+            for (int u = 0; u < 4; ++u) {
+                xs[u] = x[e4 * 4 + u];
+                if (MASK && cb + u < r) xs[u] = -INFINITY;  // row = key, col = query: valid iff query >= key
             }
-        }
-        // packed fp32x2 (FFMA2 / FMUL2): the same per-lane operations as the scalar form
-        const float2 sc2 = make_float2(sc, sc), tau2 = make_float2(tau, tau);
+            const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
-        for (int u = 0; u < 4; u += 2) {
-            const float2 t = __ffma2_rn(make_float2(xs[u], xs[u + 1]), sc2, make_float2(-l2[u], -l2[u + 1]));
-            // a share of the exponentials on the FMA pipe (the pass is MUFU-bound; kBwPoly of 8)
-            const bool poly = !MASK && kBwPoly > 0 && (e4 % (8 / kBwPoly)) == 0;
-            pv[u] = ex2(t.x);
-            pv[u + 1] = (poly && u + 1 == 3) ? ex2_poly(t.y) : ex2(t.y);
-            const float2 g = __ffma2_rn(tau2, make_float2(y[e4 * 4 + u], y[e4 * 4 + u + 1]),
-                                        make_float2(-dd[u], -dd[u + 1]));
-            const float2 ds = __fmul2_rn(make_float2(pv[u], pv[u + 1]), g);
-            dv4[u] = ds.x;
-            dv4[u + 1] = ds.y;
+            for (int u = 0; u < 4; u += 2) {
+                const float2 t = __fmul2_rn(make_float2(xs[u], xs[u + 1]), sc2);
+                const bool poly = !MASK && kBwPoly > 0 && (e4 % (8 / kBwPoly)) == 0;
+                pv[u] = ex2(t.x);
+                pv[u + 1] = (poly && u + 1 == 3) ? ex2_poly(t.y) : ex2(t.y);
+                const float2 ds = __fmul2_rn(make_float2(pv[u], pv[u + 1]), make_float2(y[e4 * 4 + u], y[e4 * 4 + u + 1]));
+                dv4[u] = ds.x;
+                dv4[u + 1] = ds.y;
+            }
+            pk_p[e4 * 2] = pack_bf16(pv[0], pv[1]);
+            pk_p[e4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
+            pk_d[e4 * 2] = pack_bf16(dv4[0], dv4[1]);
+            pk_d[e4 * 2 + 1] = pack_bf16(dv4[2], dv4[3]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                xs[u] = x[e4 * 4 + u];
+                if (MASK) {
+                    // KV: row = key, col = query -> valid iff query >= key ; Q: row = query, col = key
+                    const int col = cb + u;
+                    if (KV ? col < r : col > r) xs[u] = -INFINITY;  // exp2(-inf) = 0
+                }
+            }
+            // packed fp32x2 (FFMA2 / FMUL2): the same per-lane operations as the scalar form
+            const float2 sc2 = make_float2(sc, sc), tau2 = make_float2(tau, tau);
+#pragma unroll
+            for (int u = 0; u < 4; u += 2) {
+                const float2 t = __ffma2_rn(make_float2(xs[u], xs[u + 1]), sc2, make_float2(-l2[u], -l2[u + 1]));
+                // a share of the exponentials on the FMA pipe (the pass is MUFU-bound; kBwPoly of 8)
+                const bool poly = !MASK && kBwPoly > 0 && (e4 % (8 / kBwPoly)) == 0;
+                pv[u] = ex2(t.x);
+                pv[u + 1] = (poly && u + 1 == 3) ? ex2_poly(t.y) : ex2(t.y);
+                const float2 g = __ffma2_rn(tau2, make_float2(y[e4 * 4 + u], y[e4 * 4 + u + 1]),
+                                            make_float2(-dd[u], -dd[u + 1]));
+                const float2 ds = __fmul2_rn(make_float2(pv[u], pv[u + 1]), g);
+                dv4[u] = ds.x;
+                dv4[u + 1] = ds.y;
+            }
+            pk_p[e4 * 2] = pack_bf16(pv[0], pv[1]);
+            pk_p[e4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
+            pk_d[e4 * 2] = pack_bf16(dv4[0], dv4[1]);
+            pk_d[e4 * 2 + 1] = pack_bf16(dv4[2], dv4[3]);
         }
-        pk_p[e4 * 2] = pack_bf16(pv[0], pv[1]);
-        pk_p[e4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
-        pk_d[e4 * 2] = pack_bf16(dv4[0], dv4[1]);
-        pk_d[e4 * 2 + 1] = pack_bf16(dv4[2], dv4[3]);
     }
 }
 
@@ -1140,7 +1171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sDS = sP + (C::kTs ? 0 : C::kPd);      // dSᵀ (KV) | dS (Q) (smem path)
     uint8_t* sOut = C::kTs ? sDS + 0 : sP;          // epilogue staging (dedicated for d = 64)
     // [S][lse[128], τD[128]] of the stepped query block (KV), bulk-loaded with the stage's tiles
-    float* sRow = reinterpret_cast<float*>(sDS + (C::kTs ? C::kOutBytes : C::kPd));
+    uint8_t* sStat = sDS + (C::kTs ? C::kOutBytes : C::kPd);  // KV: [S] stats, then ones_x, ones_y
+    float* sRow = reinterpret_cast<float*>(sStat + C::kStatSmem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sRow) + S * C::kRowBytes);
     uint64_t* fix_full = bars + 0;    // [2]
     uint64_t* fix_empty = bars + 2;   // [2]
@@ -1152,7 +1184,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* pd_free = bars + 11;
     uint64_t* acc_full = bars + 12;   // [2]
     uint64_t* acc_empty = bars + 14;  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+    uint64_t* stat_full = bars + 24;  // [4] KV: the stage's stats operand is built
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
@@ -1174,6 +1207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < S; ++i) {
             mbar_init(&ld_full[i], 1);
             mbar_init(&ld_empty[i], 1);
+            mbar_init(&stat_full[i], 2);  // warps 2 and 3
         }
         mbar_init(xy_full, 1);
         mbar_init(xy_free, 8);
@@ -1182,6 +1216,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
+    if (C::kFold) {
+        // stats buffers zeroed (their second K chunk stays zero), ones operands: row k of ones_x is
+        // [1,1,1,0..], of ones_y [0,0,0,1,1,1,0..]; layout [8-row group][k chunk][8 rows][8 bf16]
+        uint32_t* z = reinterpret_cast<uint32_t*>(sStat);
+        for (int i = threadIdx.x; i < (S + 2) * C::kStatBytes / 4; i += blockDim.x) {
+            const int off = i * 4 - S * C::kStatBytes;  // byte offset into the ones tiles
+            uint32_t v = 0;
+            if (off >= 0) {
+                const int tile = off / C::kStatBytes, o = off % C::kStatBytes;
+                const int chunk = (o / 128) % 2, e = (o % 16) / 2;  // bf16 pair index e, e+1
+                if (chunk == 0) {
+                    const bool lo = tile == 0 ? e < 3 : (e >= 3 && e < 6), hi = tile == 0 ? e + 1 < 3 : (e + 1 >= 3 && e + 1 < 6);
+                    v = (lo ? 0x3F80u : 0u) | (hi ? 0x3F80u << 16 : 0u);
+                }
+            }
+            z[i] = v;
+        }
+        fence_proxy_async_smem();
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1261,6 +1314,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_bf16_ss(tmem + C::kY, make_sw128_desc(f1 + off, 16, 1024), make_sw128_desc(s1 + off, 16, 1024),
                                 kIdescXY, k > 0 ? 1u : 0u);
                 }
+                if (C::kFold) {  // X' = X − lse/c, Y' = Y − D: the stats columns against the ones operands
+                    mbar_wait(&stat_full[st], (n / S) & 1);
+                    tc_fence_after();
+                    const uint32_t sb = smem_u32(sStat + st * C::kStatBytes);
+                    const uint32_t ox = smem_u32(sStat + S * C::kStatBytes), oy = ox + C::kStatBytes;
+                    mma_bf16_ss(tmem + C::kX, make_interleave_desc(ox, 128, 256), make_interleave_desc(sb, 128, 256),
+                                kIdescXY, 1u);
+                    mma_bf16_ss(tmem + C::kY, make_interleave_desc(oy, 128, 256), make_interleave_desc(sb, 128, 256),
+                                kIdescXY, 1u);
+                }
                 mma_commit(xy_full);
                 ATRACE(1, n, 1);
                 if (c.j == c.nsteps - 1) mma_commit(&fix_empty[fb]);
@@ -1334,6 +1397,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp < 4) {
         if (C::kTs) reg_dealloc<72>();
+        if (C::kFold) {  // ---------------- stats operand builders: per step, from the stage's lse / τD rows
+            const int tid = threadIdx.x - 64;  // 0..63: rows tid and tid + 64 of the stepped block
+            const float inv_c = 1.f / a.scale_log2, inv_tau = 1.f / a.tau;
+            auto split3 = [](float v, uint32_t& p01, uint32_t& p2) {  // v ≈ b0 + b1 + b2 (bf16 terms)
+                const __nv_bfloat16 b0 = __float2bfloat16(v);
+                const float r1 = v - __bfloat162float(b0);
+                const __nv_bfloat16 b1 = __float2bfloat16(r1);
+                const __nv_bfloat16 b2 = __float2bfloat16(r1 - __bfloat162float(b1));
+                p01 = static_cast<uint32_t>(__bfloat16_as_ushort(b0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(b1)) << 16);
+                p2 = __bfloat16_as_ushort(b2);
+            };
+            int n = 0;
+            BwCursor c;
+            for (bw_tile<KV>(a, 0, c); c.valid; bw_next<KV>(a, c), ++n) {
+                const int st = n % S;
+                mbar_wait(&ld_full[st], (n / S) & 1);  // the rows landed; the stage's previous stats consumed
+                const float* rows = sRow + st * (C::kRowBytes / 4);
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const int q = tid + 64 * h2;
+                    uint32_t l01, l2, d01, d2;
+                    split3(-rows[q] * inv_c, l01, l2);
+                    split3(-rows[kBlk + q] * inv_tau, d01, d2);
+                    // chunk 0 of row q: [l0, l1, l2, d0, d1, d2, 0, 0]
+                    sts128(smem_u32(sStat + st * C::kStatBytes + (q / 8) * 256 + (q % 8) * 16),
+                           make_uint4(l01, l2 | (d01 << 16), (d01 >> 16) | (d2 << 16), 0u));
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&stat_full[st]);
+            }
+        }
     } else {  // ---------------- elementwise warps: thread = (row of the fixed block, column half)
         if (C::kTs) reg_alloc<208>();
         const int quad = warp & 3;
@@ -1369,7 +1464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t rowv = rowv0 + (n % S) * C::kRowBytes;
                 if (warp == 4 && lane == 0) ATRACE(0, n, 5);
                 mbar_wait(xy_full, n & 1);
-                if (KV) mbar_wait(&ld_full[n % S], (n / S) & 1);  // the stage's lse / τD landed (long done)
+                if (KV && !C::kFold) mbar_wait(&ld_full[n % S], (n / S) & 1);  // the stage's lse / τD landed
                 if (warp == 4 && lane == 0) ATRACE(0, n, 0);
                 tc_fence_after();
                 const bool diag = a.causal && other == c.blk;
@@ -1399,10 +1494,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int pass = 0; pass < 2; ++pass) {
                         const int cb0 = half * 64 + pass * 32;
                         if (diag)
-                            bw_pass<KV, true>(x[pass], y[pass], rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16,
+                            bw_pass<KV, true, C::kFold>(x[pass], y[pass], rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16,
                                               pk_d + pass * 16);
                         else
-                            bw_pass<KV, false>(x[pass], y[pass], rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16,
+                            bw_pass<KV, false, C::kFold>(x[pass], y[pass], rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16,
                                                pk_d + pass * 16);
                         if (pass == 0) {
                             if (n > 0) mbar_wait(pd_free, (n - 1) & 1);  // previous step's MMAs done reading P / dS
@@ -1428,9 +1523,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         const int cb0 = half * 64 + pass * 32;
                         if (diag)
-                            bw_pass<KV, true>(x, y, rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16, pk_d + pass * 16);
+                            bw_pass<KV, true, C::kFold>(x, y, rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16, pk_d + pass * 16);
                         else
-                            bw_pass<KV, false>(x, y, rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16,
+                            bw_pass<KV, false, C::kFold>(x, y, rowv, cb0, r, sc, tau, my_lse, my_d, pk_p + pass * 16,
                                                pk_d + pass * 16);
                     }
                 }
@@ -1484,6 +1579,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int cc = 0; cc < kCols / 32; ++cc) {
                 float v[32];
                 tmem_ld_32x32b_x32(tmem + lane_base + col0 + cc * 32, v);
+                if (C::kFold && half == 1) {  // dK accumulated dS/τ (the folded Y' carries no τ)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] *= a.tau;
+                }
                 const int cs = (KV ? 0 : half * (D / 2)) + cc * 32;  // column within the section's head
                 const uint32_t row_addr = stage + (cs / 64) * (kBlk * 128) + r * 128;
 #pragma unroll

@@ -199,6 +199,18 @@ __device__ __forceinline__ uint64_t make_sw128_desc(uint32_t start, uint32_t lbo
     return d;
 }
 
+// Shared-memory matrix descriptor, no swizzle (layout type 0, "interleaved"): K-major core matrices
+// of 8 rows x 16 bytes (rows contiguous); lbo = byte distance between the two K-adjacent core matrices
+// of a K=16 step, sbo = byte distance between 8-row groups.
+__device__ __forceinline__ uint64_t make_interleave_desc(uint32_t start, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((start >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // descriptor version for tcgen05
+    return d;
+}
+
 // Instruction descriptor for kind::f16 with bf16 A/B and fp32 D.
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int m, int n, bool a_mn_major, bool b_mn_major) {
     return (1u << 4)                                   // D format f32
