@@ -104,9 +104,10 @@ __device__ unsigned long long g_fwd_trace[2][64][8];
 // ping-pong forward: [0 lane A softmax, 1 lane B softmax, 2 MMA][lane block][event]
 __device__ unsigned long long g_pp_trace[3][64][8];
 __device__ unsigned long long g_pp_cta[160][4];  // per CTA: globaltimer at entry, first S issue, MMA done, exit
+__device__ int g_pp_trace_cta = 0;              // the CTA whose timeline is recorded
 #define PTRACE(role, step, ev)                                                  \
     do {                                                                        \
-        if (blockIdx.x == 0 && (step) < 64) g_pp_trace[role][step][ev] = clock64(); \
+        if (ptrace_on && (step) < 64) g_pp_trace[role][step][ev] = clock64();   \
     } while (0)
 #else
 #define FTRACE(role, step, ev) \
@@ -448,7 +449,8 @@ struct Fa2Cfg {
     static constexpr int kQBytes = kBlk * D * 2;     // 16 KiB, K-major sw128
     static constexpr int kKVBytes = 2 * kBlk * D * 2;  // K then V
     static constexpr int kStages = 4;
-    static constexpr int kSmem = 4 * kQBytes + kStages * kKVBytes + 1024 + 768;
+    static constexpr int kOBytes = kBlk * D * 2;  // per lane: the O tile staged for its TMA store
+    static constexpr int kSmem = 4 * kQBytes + kStages * kKVBytes + 2 * kOBytes + 1024 + 768;
     // TMEM: S_L at 128 L (fp32 128x128); P_L at 256 + 64 L (bf16x2-packed 128x128, the A operand of
     // P·V read straight from TMEM); O_L at 384 + 64 L (fp32 128x64)
     static constexpr uint32_t kTmemS = 0, kTmemP = 256, kTmemO = 384;
@@ -486,7 +488,7 @@ __device__ __forceinline__ int fa2_nkv(const FaArgs& a, int p, int lane) {
 template <int kFwdPoly>
 __global__ void __launch_bounds__(384, 1)
     flash_fwd_pp_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
-                        const __grid_constant__ FaArgs a) {
+                        const __grid_constant__ CUtensorMap tmO, const __grid_constant__ FaArgs a) {
     using C = Fa2Cfg;
     constexpr int D = C::D, NS = C::kStages;
     constexpr uint32_t kIdescS = make_idesc_bf16(kBlk, kBlk, false, false);
@@ -496,7 +498,8 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                        // [lane][qbuf] 16 KiB each
     uint8_t* sKV = sQ + 4 * C::kQBytes;        // [stage] K 16 KiB, V 16 KiB
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NS * C::kKVBytes);
+    uint8_t* sO = sKV + NS * C::kKVBytes;      // [lane] O staging, 128B-swizzled [128 rows][64 cols]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 2 * C::kOBytes);
     uint64_t* q_full = bars + 0;     // [lane][qbuf]
     uint64_t* q_empty = bars + 4;    // [lane][qbuf]
     uint64_t* kv_full = bars + 8;    // [NS]
@@ -516,6 +519,7 @@ __global__ void __launch_bounds__(384, 1)
     const int warp = threadIdx.x / 32;
     const uint32_t lane_id_ = lane_id();
 #ifdef PTK_ATTN_TRACE
+    const bool ptrace_on = static_cast<int>(blockIdx.x) == *static_cast<volatile int*>(&g_pp_trace_cta);
     auto gt = [] {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -803,26 +807,36 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_after();
             const float inv = 1.f / l;
             const int q = qb * kBlk + r;
-            __nv_bfloat16* orow = a.o + (static_cast<int64_t>(it.bi) * a.s + q) * a.h + it.head * D;
+            // O -> registers (the accumulator is released at once) -> bf16 into this lane's 128B-swizzled
+            // staging -> one TMA store of the [128][64] tile.  Row-per-thread global stores cost about
+            // 1500 cycles per item: every warp store touched 32 rows.
+            float v[D];
 #pragma unroll
-            for (int cc = 0; cc < D; cc += 16) {
-                float v[16];
-                tmem_ld_32x32b_x16(o_cols + cc, v);
-#pragma unroll
-                for (int g = 0; g < 2; ++g) {
-                    uint4 u;
-                    u.x = pack_bf16(v[g * 8 + 0] * inv, v[g * 8 + 1] * inv);
-                    u.y = pack_bf16(v[g * 8 + 2] * inv, v[g * 8 + 3] * inv);
-                    u.z = pack_bf16(v[g * 8 + 4] * inv, v[g * 8 + 5] * inv);
-                    u.w = pack_bf16(v[g * 8 + 6] * inv, v[g * 8 + 7] * inv);
-                    *reinterpret_cast<uint4*>(orow + cc + g * 8) = u;
-                }
-            }
+            for (int cc = 0; cc < D; cc += 32) tmem_ld_32x32b_x32_nw(o_cols + cc, v + cc);
+            tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
             if (lane_id_ == 0) mbar_arrive(&o_empty[L]);
+            const uint32_t bar_id = 1 + L, issuer = (warp & 3) == 0 && lane_id_ == 0;
+            if (issuer) tma_store_wait_read();  // the lane's previous item left the staging
+            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+            const uint32_t row_addr = smem_u32(sO + L * C::kOBytes) + r * 128;
+#pragma unroll
+            for (int g = 0; g < D / 8; ++g) {
+                const float* f = v + 8 * g;
+                const uint4 u = make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
+                                           pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
+                sts128(row_addr + ((g ^ (r & 7)) * 16), u);
+            }
+            fence_proxy_async_smem();
+            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+            if (issuer) {
+                tma_store_4d(&tmO, sO + L * C::kOBytes, 0, qb * kBlk, it.head, it.bi);
+                tma_store_commit();
+            }
             a.lse[(static_cast<int64_t>(it.bi) * a.H + it.head) * a.s + q] = m + __log2f(l);
         }
+        if ((warp & 3) == 0 && lane_id_ == 0) tma_store_wait_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -869,6 +883,23 @@ cudaError_t qkv_map(CUtensorMap* m, const void* qkv, int b, int s, int H, int d,
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// o [b*s][H*d] viewed as dims {d, s, H, b}, box {64, 128} (the ping-pong forward's TMA stores).
+cudaError_t o_map(CUtensorMap* m, const void* o, int b, int s, int H, int d) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    const int64_t h = static_cast<int64_t>(H) * d;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(s), static_cast<cuuint64_t>(H),
+                          static_cast<cuuint64_t>(b)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(h * 2), static_cast<cuuint64_t>(d * 2),
+                             static_cast<cuuint64_t>(s * h * 2)};
+    cuuint32_t box[4] = {64, static_cast<cuuint32_t>(kBlk), 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(o), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 bool fwd_pp_enabled() {
     static const bool on = [] {
         const char* v = std::getenv("PTK_FWD_PP");
@@ -901,7 +932,7 @@ cudaError_t launch_fwd_pp_t(const FlashPlan& p, cudaStream_t st) {
     const int items = p.s / (2 * kBlk) * p.H * p.b;
     const int grid = items < sm_count() ? items : sm_count();
     if ((items + grid - 1) / grid > kFa2MaxItems) return launch_fwd_single<64>(p, st);
-    return launch_kernel(flash_fwd_pp_kernel<POLY>, grid, 384, Fa2Cfg::kSmem, st, 1, p.tmQK, p.tmV, a);
+    return launch_kernel(flash_fwd_pp_kernel<POLY>, grid, 384, Fa2Cfg::kSmem, st, 1, p.tmQK, p.tmV, p.tmO, a);
 }
 
 cudaError_t launch_fwd_pp(const FlashPlan& p, cudaStream_t st) {
@@ -943,6 +974,8 @@ cudaError_t flash_prepare(const void* qkv, void* o, float* lse, int b, int s, in
     cudaError_t e = qkv_map(&p->tmQK, qkv, b, s, H, d, kBlk);
     if (e != cudaSuccess) return e;
     e = qkv_map(&p->tmV, qkv, b, s, H, d, 64);
+    if (e != cudaSuccess) return e;
+    e = o_map(&p->tmO, o, b, s, H, d);
     if (e != cudaSuccess) return e;
     p->o = static_cast<__nv_bfloat16*>(o);
     p->lse = lse;

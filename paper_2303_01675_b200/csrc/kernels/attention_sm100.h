@@ -10,6 +10,7 @@ namespace ptk {
 struct FlashPlan {
     alignas(64) CUtensorMap tmQK;  // qkv viewed as {d, s, 3H, b}, box {64, 128}
     alignas(64) CUtensorMap tmV;   // same view, box {64, 64} (V as the MN-major B operand)
+    alignas(64) CUtensorMap tmO;   // o viewed as {d, s, H, b}, box {64, 128}: the epilogue's TMA stores
     __nv_bfloat16* o = nullptr;    // [b*s][H*d]
     float* lse = nullptr;          // [b][H][s] (log2 units of scaled scores)
     int b = 0, s = 0, H = 0, d = 0;

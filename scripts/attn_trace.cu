@@ -2,7 +2,7 @@
 // attention backward kernels at the GPT-1.3B shape.  Not part of the library.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr -DPTK_ATTN_TRACE \
 //        -Iinclude -Ipaper_2303_01675_b200/csrc -o scripts/attn_trace scripts/attn_trace.cu -lcuda
-//   scripts/attn_trace 3    (ping-pong forward; 2 single-tile forward; 1 / 0 backward KV / Q)
+//   scripts/attn_trace 3 [cta]  (ping-pong forward of CTA cta; 2 single-tile forward; 1 / 0 backward KV / Q)
 #include <cstdio>
 #include <vector>
 
@@ -38,6 +38,8 @@ int main(int argc, char** argv) {
     fill<<<512, 256>>>(qkv, T * 3 * h, 1);
     fill<<<512, 256>>>(dO, T * h, 2);
     cudaMemcpyToSymbol(ptk::g_attn_trace_kv, &kv, sizeof kv);
+    const int trace_cta = argc > 2 ? atoi(argv[2]) : 0;  // mode 3: the CTA whose timeline is recorded
+    cudaMemcpyToSymbol(ptk::g_pp_trace_cta, &trace_cta, sizeof trace_cta);
     ptk::FlashPlan fp;
     ptk::FlashBwdPlan bp;
     if (ptk::flash_prepare(qkv, o, lse, b, s, H, d, &fp, 1) != cudaSuccess) return 1;
@@ -71,9 +73,9 @@ int main(int argc, char** argv) {
         unsigned long long pt[3][64][8];
         cudaMemcpyFromSymbol(pt, ptk::g_pp_trace, sizeof pt);
         const unsigned long long p0 = pt[2][0][0];
-        printf("ping-pong forward, CTA 0, cycles since S_A(0) was issued; per lane block n\n");
+        printf("ping-pong forward, CTA %d, cycles since S_A(0) was issued; per lane block n\n", trace_cta);
         printf("  n | lane A: s_full loaded exps pv_ok p_full | lane B: same | mma: S_A pA_seen PV_A S_B pB_seen PV_B\n");
-        for (int n = 0; n < 20; ++n) {
+        for (int n = 0; n < 24; ++n) {
             auto f = [&](int r, int ev) { return static_cast<long long>(pt[r][n][ev] - p0); };
             printf("%3d | %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld %7lld\n",
                    n, f(0, 0), f(0, 1), f(0, 2), f(0, 3), f(0, 4), f(1, 0), f(1, 1), f(1, 2), f(1, 3), f(1, 4),
