@@ -177,11 +177,24 @@ def candidate_set(shape, layers, stages: int, global_batch: int, mem_cap_bytes: 
     cands = frontier(0)
     if not wgrad_pairs:
         return cands
-    b_max = max(c[1] for c in cands)
-    for _ in range(16):
-        cands = frontier(b_max)
-        nb = max(c[1] for c in cands)
-        if nb >= b_max:
-            break
-        b_max = nb
-    return cands
+    # The pairing buffers are a fixed cost sized by the largest candidate b.  Take the largest b_max
+    # (a divisor of the global batch, from the unpaired frontier's largest b down) that is
+    # self-consistent: with the buffers budgeted at b_max the frontier still reaches b_max.  Budgets
+    # that leave no frontier at all are skipped (they used to raise InfeasibleModel).
+    divisors = [d for d in range(global_batch, 0, -1) if global_batch % d == 0]
+    for b_max in [d for d in divisors if d <= max(c[1] for c in cands)]:
+        try:
+            paired = frontier(b_max)
+        except pt.PipetuneError as e:
+            if e.kind != "InfeasibleModel":
+                raise
+            continue
+        if max(c[1] for c in paired) < b_max:
+            continue
+        out = []
+        for k, b, _ in paired:  # a candidate above the budget runs at the largest divisor within it
+            b = max(d for d in divisors if d <= min(b, b_max))
+            if all(o[0] != k for o in out):
+                out.append([k, b, global_batch // b])
+        return out
+    raise pt.PipetuneError("InfeasibleModel", "no (k, b) fits the memory cap with the paired weight-gradient buffers")

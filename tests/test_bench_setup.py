@@ -49,3 +49,29 @@ def test_every_candidate_fits_every_rank(S, shape, gb, b, cap):
             plan = pt.plan_kfkb(model, cb, k)
             vslots = slots * (b_max // cb if b_max % cb == 0 else 1)
             assert _peak_inflight(plan, rank) + 1 <= vslots, (S, rank, k, cb)
+
+
+@pytest.mark.parametrize("S", [2, 4, 8])
+@pytest.mark.parametrize("shape,b,cap", [(GPT_1_3B, 2, 16e9), (GPT_1_3B, 2, 40e9), (GPT_1_3B, 2, 80e9),
+                                         (BERT_LARGE, 4, 8e9), (BERT_LARGE, 4, 12e9), (GPT_6_7B, 1, 60e9),
+                                         (GPT_6_7B, 1, 80e9)], ids=lambda x: getattr(x, "hidden", x))
+def test_paired_candidates_fit_their_own_budget(S, shape, b, cap):
+    """With paired weight gradients the pairing buffers are a fixed per-stage cost sized by the largest
+    candidate b.  Every candidate (k, b) must fit the cap with those buffers charged at that b_max
+    (the memory frontier under that budget reaches b for the same k), and budgets that leave no
+    frontier are skipped instead of raising (round 2: 10/12 GB BERT and 40 GB GPT-1.3B raised)."""
+    from paper_2303_01675_b200.tuning import memory_model
+    halves = partition_halves(shape.n_layer, S, head_weight=2.3 if shape.arch == "bert" else 1.6,
+                              attn_weight=0.42 if shape.arch == "bert" else 0.47)
+    try:
+        cands = candidate_set(shape, halves, S, 64, cap, fixed_b=b, halves=True, wgrad_pairs=True)
+    except pt.PipetuneError as e:
+        assert e.kind == "InfeasibleModel"
+        return
+    b_max = max(c[1] for c in cands)
+    out = pt.scenario({"op": "enumerate", "model": memory_model(shape, halves, S, 64, True, b_max), "k_max": 8,
+                       "cluster": {"device_memory_limit": int(cap), "devices": S}})
+    best = {e[0]: e[1] for e in out["entries"]}
+    for k, cb, M in cands:
+        assert M * cb == 64
+        assert k in best and best[k] >= cb, (k, cb, best)
