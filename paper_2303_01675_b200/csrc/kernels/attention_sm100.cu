@@ -998,20 +998,23 @@ cudaError_t flash_forward(const FlashPlan& p, cudaStream_t st) {
 // Backward.  Deterministic two-kernel form (no atomics), both persistent:
 //   mode KV: tile = (key block j, head, sample), steps over query blocks i >= j:
 //     Sᵀ = K_j Q_iᵀ, dPᵀ = V_j dO_iᵀ            (TMEM, thread = key row)
-//     Pᵀ = 2^(Sᵀ c - lse2[q]),  dSᵀ = τ Pᵀ (dPᵀ - D[q])   -> smem (bf16)
+//     Pᵀ = 2^(Sᵀ c - lse2[q]),  dSᵀ = τ Pᵀ (dPᵀ - D[q])
 //     dV_j += Pᵀ dO_i,  dK_j += dSᵀ Q_i           (TMEM accumulators)
 //   mode Q:  tile = (query block i, head, sample), steps over key blocks j <= i:
 //     S = Q_i K_jᵀ, dP = dO_i V_jᵀ  (thread = query row)
-//     dS = τ P (dP - D[q])  -> smem;  dQ_i += dS K_j
+//     dS = τ P (dP - D[q]);  dQ_i += dS K_j
 // A [rows][64-col] 128B-swizzled tile is simultaneously the K-major operand
 // for the score products and the MN-major operand (LBO = 16 KiB between
 // 64-wide column atoms) for the accumulating products, so every operand is
-// loaded once per step.  D = rowsum(dO ∘ O) comes from attn_bwd_dot_kernel.
+// loaded once per step.  τ·D = τ rowsum(dO ∘ O) comes from attn_bwd_dot_kernel.
+// d = 64: P/dS go to TMEM as the A operand of the accumulating products, three
+// operand stages, and in the KV pass −lse/c and −D enter the score products as
+// extra K columns (a per-stage stats operand against a fixed ones operand) so
+// the elementwise pass reads no per-column statistics; d = 128: P/dS through
+// smem, one stage, the statistics from the stage's smem rows.
 // One CTA per SM walks its tiles (heaviest first, boustrophedon); the fixed
-// tiles and the accumulators are double-buffered across tiles (d = 64) so a
-// tile's epilogue and the next tile's loads/score products overlap.  The
-// elementwise warps compute P/dS of step t in registers while the
-// accumulating products of step t-1 still read the smem operands.
+// tiles are double-buffered across tiles (d = 64).  Epilogues stage the bf16
+// outputs in 128B-swizzled smem and leave with TMA stores.
 // ============================================================================
 namespace {
 
