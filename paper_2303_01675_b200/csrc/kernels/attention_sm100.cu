@@ -435,14 +435,16 @@ __global__ void __launch_bounds__(32 * (4 + 4 * NQ), 1)
 // the non-exponential work of the same warps, all phase-locked on one S
 // buffer and one P buffer).  Here a CTA works on a PAIR of 128-query tiles of
 // one (head, sample) — lane A = query block 2p, lane B = 2p+1 — which share
-// every K/V block.  Each lane has its own S (TMEM), P (smem), O (TMEM,
-// double-buffered across pairs) and four softmax warps with ONE THREAD PER
-// QUERY ROW (all 128 columns of the row in registers: the row max needs no
-// cross-warp exchange and no named barrier).  The MMA warp keeps each lane one
-// score product ahead (S_L(j+1) is issued as soon as lane L has read S_L(j)
-// into registers) and issues PV_L(j) when lane L's P is in smem, so while one
-// lane's warps do their non-exponential work (TMEM loads, max, P stores, O
-// rescale) the other lane's exponentials keep the MUFU busy.
+// every K/V block.  Each lane has its own S, P (bf16, the TMEM A operand of
+// P·V) and O in TMEM, and four softmax warps with ONE THREAD PER QUERY ROW (all
+// 128 columns of the row in registers: the row max needs no cross-warp
+// exchange).  The MMA warp keeps each lane one score product ahead (S_L(j+1)
+// is issued as soon as lane L has read S_L(j) into registers) and issues
+// PV_L(j) when lane L's P is in TMEM, lanes in a fixed A-then-B order so their
+// exponential passes stay offset: while one lane's warps do their
+// non-exponential work (TMEM loads, max, P stores, O rescale) the other lane's
+// exponentials keep the MUFU busy.  O leaves through per-lane smem staging and
+// a TMA store.
 // ============================================================================
 struct Fa2Cfg {
     static constexpr int D = 64;
