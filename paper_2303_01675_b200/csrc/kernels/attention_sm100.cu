@@ -765,8 +765,9 @@ __global__ void __launch_bounds__(384, 1)
                     for (int e = 0; e < kBlk; e += 2) {
                         const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, mm2);
                         if (kFwdPoly > 0 && ((e >> 1) & 7) < kFwdPoly / 2) {  // first kFwdPoly of every 16
-                            x[e] = ex2_poly(t.x);
-                            x[e + 1] = ex2_poly(t.y);
+                            const float2 pp = ex2_poly2(t);
+                            x[e] = pp.x;
+                            x[e + 1] = pp.y;
                         } else {
                             x[e] = ex2(t.x);
                             x[e + 1] = ex2(t.y);

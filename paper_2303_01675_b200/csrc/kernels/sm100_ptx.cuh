@@ -342,6 +342,21 @@ __device__ __forceinline__ float ex2_poly(float x) {
     return __int_as_float(__float_as_int(p) + (__float_as_int(y) << 23));
 }
 
+// ex2_poly on a pair with packed fp32x2 arithmetic (FADD2 / FFMA2): about half the FMA-pipe issue
+// slots of two scalar calls, the same operations per lane.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -125.f);
+    x.y = fmaxf(x.y, -125.f);
+    const float2 c = make_float2(12582912.f, 12582912.f);
+    const float2 y = __fadd2_rn(x, c);
+    const float2 f = __fadd2_rn(x, __fadd2_rn(c, make_float2(-y.x, -y.y)));  // x - (y - c)
+    float2 p = __ffma2_rn(f, make_float2(0.054848004f, 0.054848004f), make_float2(0.24180661f, 0.24180661f));
+    p = __ffma2_rn(p, f, make_float2(0.69324821f, 0.69324821f));
+    p = __ffma2_rn(p, f, make_float2(0.99998868f, 0.99998868f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(y.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(y.y) << 23)));
+}
+
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
