@@ -93,7 +93,9 @@ int ptk_gemm_plan_info(const ptk_gemm_desc* desc, int* info);
  * lse fp32 [b][H][s] = log2(sum_k 2^(S_qk * log2(e)/sqrt(d))) (row max included). */
 int ptk_flash_forward(const void* qkv, void* o, float* lse, int b, int s, int H, int d, int causal, void* stream);
 /* Its backward: dqkv bf16 [b*s][3*H*d] (dQ | dK | dV sections) from qkv, o, dO = d(o),
- * lse; dsum: fp32 scratch [b][H][s].  Deterministic (no atomics). */
+ * lse; dsum: fp32 scratch [b][H][s] (holds tau*rowsum(dO*o)).  Deterministic (no atomics).
+ * All pointers 16-byte aligned: the tensors are read / written by TMA and the per-block lse and
+ * dsum rows (512 B) by bulk copies. */
 int ptk_flash_backward(const void* qkv, const void* o, const void* dO, const float* lse, float* dsum, void* dqkv,
                        int b, int s, int H, int d, int causal, void* stream);
 
