@@ -527,7 +527,8 @@ def main():
                               "peak_tflops": peak_sus, "peak_kind": f"sustained bf16, {pk_kind}"},
         "roofline": {"bound": "tensor", "kernel": "gemm_bf16_kernel (tcgen05 + TMA, all stage GEMMs)",
                      "achieved": round(achieved, 1), "peak": peak_sus, "unit": "TFLOP/s",
-                     "frac": round(achieved / peak_sus, 4), "traffic": gemm_traffic(),
+                     "frac": round(achieved / peak_sus, 4),
+                     "traffic": (gemm_traffic() or {}).get("bytes_per_launch"), "traffic_detail": gemm_traffic(),
                      "launches": sum(g[2] for g in all_gemm),
                      "note": f"algorithmic GEMM FLOPs / summed CUDA-event GEMM durations over the timed steps; "
                              f"peak = sustained bf16 of {pk_kind} MEASURED_PEAKS.json"},
