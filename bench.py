@@ -59,6 +59,9 @@ def parse():
                    help="one weight-gradient GEMM per micro-batch (default: two-K-segment pairs, whose "
                         "buffers the --mem-cap-gb frontier budgets)")
     p.add_argument("--tuner-repeats", type=int, default=3, help="active link probes per payload (SPEC default 3)")
+    p.add_argument("--probe-every", type=int, default=1,
+                   help="with --passive-profile: re-probe other candidates' payloads every N tuning rounds "
+                        "(1: every round, SPEC.md:294)")
     p.add_argument("--passive-profile", action="store_true",
                    help="feed every re-tuning round the last iteration's own transfers as link samples and probe "
                         "only the other candidates' payloads")
@@ -288,7 +291,8 @@ def main():
                       "period_ms": args.period_ms if args.trace == "square" else None,
                       "bursty_mean_on_off_ms": [args.on_ms, args.off_ms] if args.trace == "bursty" else None,
                       "seed": args.trace_seed, "retune_every": args.retune, "contender_kernels": args.contender,
-                      "tuner_repeats": args.tuner_repeats, "passive_profile": args.passive_profile}
+                      "tuner_repeats": args.tuner_repeats, "passive_profile": args.passive_profile,
+                      "probe_every": args.probe_every}
 
     sync_gt = [0]
 
@@ -355,7 +359,8 @@ def main():
 
     # ---- timed region: Ada-Grouper (tuning round at start, re-tune every `retune` steps)
     tuner = OnlineTuner(ex, rank, S, GB, [(c[0], c[1]) for c in cands], shape.seq * shape.hidden * 2,
-                        group=group, repeats=args.tuner_repeats, passive=args.passive_profile) if S > 1 else None
+                        group=group, repeats=args.tuner_repeats, passive=args.passive_profile,
+                        probe_every=args.probe_every) if S > 1 else None
     if tuner is not None:
         tuner.profile_compute()  # once, before the timed region
     chosen, chosen_groups, decisions, tune_s = cands[0], [], [], 0.0
@@ -400,7 +405,7 @@ def main():
             ex.run_iteration(it)
             nxt, host_s = step + 1, None
             if (overlap_ok and last_tl is not None and nxt < args.steps and nxt % args.retune == 0
-                    and all(c[1] == chosen[1] for c in cands)):
+                    and not tuner.needs_probes(chosen[1])):
                 tr0 = time.perf_counter()
                 tuner.observe_iteration(last_tl, clock=nxt)
                 d = tuner.round(list(chosen), clock=nxt, current_groups=chosen_groups)

@@ -46,8 +46,13 @@ def all_gather(obj, group=None, world: int = 1):
 class OnlineTuner:
     def __init__(self, ex, rank: int, stages: int, global_batch: int, candidates: list[tuple[int, int]],
                  act_bytes_per_sample: int, hysteresis: float = 0.02, repeats: int = 3, window: int = 8,
-                 group=None, passive: bool = False, mixed: bool = True):
+                 group=None, passive: bool = False, mixed: bool = True, probe_every: int = 1):
         self.ex, self.rank, self.S = ex, rank, stages
+        # with passive samples, re-probe the other candidates' payloads only every `probe_every`
+        # rounds (1: every round); in between, their ProfileStore buckets keep serving
+        # the last `window` samples
+        self.probe_every = max(1, probe_every)
+        self.rounds = 0
         self.gb = global_batch
         self.cands = [[k, b, global_batch // b] for k, b in candidates]
         self.act = act_bytes_per_sample
@@ -90,11 +95,24 @@ class OnlineTuner:
         self._add_samples(sorted(x for r in all_gather(mine, self.group, self.S) for x in r))
         self.passive_bytes = {x[1] for x in mine}
 
+    def needs_probes(self, current_b: int) -> bool:
+        """Whether the next round, observing an iteration that ran at micro-batch `current_b`, will
+        probe any payload.  Computed from state every rank shares (candidates, gathered samples,
+        round count), so all ranks agree without a collective."""
+        payloads = {c[1] * self.act for c in self.cands}
+        skip = {current_b * self.act} if self.passive else set()
+        if self.passive and self.rounds % self.probe_every != 0:
+            skip |= {x[1] for x in self.samples}
+        return bool(payloads - skip)
+
     def profile_links(self, clock: int = 0):
         """Active probes (pipeline suspended): every candidate payload not already
-        measured passively in the last iteration, `repeats` times per outgoing link."""
+        measured passively in the last iteration, `repeats` times per outgoing link (rounds between
+        `probe_every` boundaries probe only payloads the store has never seen)."""
         mine = []
         skip = getattr(self, "passive_bytes", set()) if self.passive else set()
+        if self.passive and self.rounds % self.probe_every != 0:
+            skip = skip | {x[1] for x in self.samples}
         for b in sorted({c[1] for c in self.cands}):
             nbytes = b * self.act
             if nbytes in skip:
@@ -122,6 +140,7 @@ class OnlineTuner:
         if self.compute is None:
             self.profile_compute()
         self.profile_links(clock)
+        self.rounds += 1
         return self.decide(current, clock, current_groups)
 
 

@@ -75,3 +75,48 @@ def test_partition_and_inflight():
     assert [max_inflight(s, 4, 16, 1) for s in range(4)] == [4, 3, 2, 1]
     assert max_inflight(0, 8, 32, 2) == 16  # 16 warm-up forwards
     assert outgoing_links(0, 4) == [0] and outgoing_links(3, 4) == [5] and outgoing_links(1, 4) == [2, 1]
+
+
+class CountingExec(FakeExec):
+    def __init__(self, rank):
+        super().__init__(rank, slow_links=set())
+        self.probes = []
+
+    def probe_link(self, link, nbytes, repeats):
+        self.probes.append(nbytes)
+        return super().probe_link(link, nbytes, repeats)
+
+
+def test_probe_every_skips_known_payloads_between_boundaries():
+    """--probe-every N with passive samples: a boundary round probes every candidate payload the last
+    iteration did not carry; the N-1 rounds after it skip payloads the store has already seen, and
+    needs_probes() predicts exactly that (bench.py overlaps such rounds with the running step)."""
+    ex = CountingExec(1)
+    act = 4096
+    # stage 1 of 2: one outgoing link (the gradient link back to stage 0)
+    t = OnlineTuner(ex, 1, 2, 16, [(1, 4), (2, 2), (4, 1)], act_bytes_per_sample=act, passive=True, probe_every=3)
+    t.compute = []  # compute profiles and the C++ decision are not under test here
+    t.decide = lambda current, clock=0, current_groups=None: {"chosen": list(current)}
+    import paper_2303_01675_b200.tuning as T
+    real = T.all_gather
+    T.all_gather = lambda obj, group=None, world=1: [obj]  # one rank's view is enough for this logic
+    try:
+        def observe(b):
+            t.observe_iteration({"xfer": [[1, 0, b * act, 0, 1000]]})
+
+        observe(4)
+        assert t.needs_probes(4)  # boundary: b = 2 and b = 1 payloads were never carried
+        t.round([1, 4, 4])
+        assert sorted(set(ex.probes)) == [1 * act, 2 * act] and t.rounds == 1
+        for _ in range(2):  # off-boundary rounds: every payload is in the store now
+            observe(4)
+            assert not t.needs_probes(4)
+            n = len(ex.probes)
+            t.round([1, 4, 4])
+            assert len(ex.probes) == n  # nothing probed
+        observe(4)
+        assert t.rounds == 3 and t.needs_probes(4)  # the next boundary re-probes
+        t.round([1, 4, 4])
+        assert len(ex.probes) > n
+    finally:
+        T.all_gather = real
