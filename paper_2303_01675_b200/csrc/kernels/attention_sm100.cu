@@ -1691,13 +1691,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // coalesced 16-byte loads over the whole row, per-head sums reduced across the
 // d/8 lanes that hold a head (fixed shuffle order: deterministic).
 template <int D>
-__global__ void __launch_bounds__(256) attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ dO,
+__global__ void __launch_bounds__(128) attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ dO,
                                                            const __nv_bfloat16* __restrict__ O,
                                                            float* __restrict__ dsum, int rows, int s, int H,
                                                            float tau) {
     pdl_begin();
     constexpr int kLanesPerHead = D / 8;
-    const int row = blockIdx.x * 8 + threadIdx.x / 32;
+    const int row = blockIdx.x * 4 + threadIdx.x / 32;  // 4 rows per block: fine-grained SM balance
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
     const int chunks = H * kLanesPerHead;  // 16-byte chunks per row
@@ -1801,10 +1801,10 @@ cudaError_t flash_backward(const FlashBwdPlan& p, cudaStream_t st) {
     const int rows = p.b * p.s;
     cudaError_t e;
     if (p.d == 64)
-        e = launch_kernel(attn_bwd_dot_kernel<64>, (rows + 7) / 8, 256, 0, st, 1, p.dO, p.o, p.dsum, rows, p.s, p.H,
+        e = launch_kernel(attn_bwd_dot_kernel<64>, (rows + 3) / 4, 128, 0, st, 1, p.dO, p.o, p.dsum, rows, p.s, p.H,
                           1.f / sqrtf(64.f));
     else
-        e = launch_kernel(attn_bwd_dot_kernel<128>, (rows + 7) / 8, 256, 0, st, 1, p.dO, p.o, p.dsum, rows, p.s, p.H,
+        e = launch_kernel(attn_bwd_dot_kernel<128>, (rows + 3) / 4, 128, 0, st, 1, p.dO, p.o, p.dsum, rows, p.s, p.H,
                           1.f / sqrtf(128.f));
     if (e != cudaSuccess) return e;
     e = p.d == 64 ? launch_bwd<64, true>(p, st) : launch_bwd<128, true>(p, st);
