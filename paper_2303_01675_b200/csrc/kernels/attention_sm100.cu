@@ -1497,7 +1497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (; c.valid; ++n) {
             const float cur0 = pre0, cur1 = pre1;
             bw_next<KV>(a, cn);
-            if (cn.valid) stats(cn, pre0, pre1);
+            if (cn.valid && cn.j == 0) stats(cn, pre0, pre1);  // Q: per-tile values, fetched at a tile's first step
             {
                 const int t = c.j;
                 const int other = c.first + t;  // index of the stepped block
