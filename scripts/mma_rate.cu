@@ -52,6 +52,67 @@ __global__ void __launch_bounds__(128, 1) mma_rate(unsigned long long* cycles, i
     }
 }
 
+// Both operands MN-major (the weight-gradient layout), descriptors as gemm_sm100.cu builds them:
+// 64-element MN atoms 8 KiB apart (LBO), 8-row K groups 1 KiB apart, K16 steps 2 KiB apart.
+template <int N>
+__global__ void __launch_bounds__(128, 1) mma_rate_mn(unsigned long long* cycles, int iters) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint32_t tmem_slot;
+    __shared__ uint64_t done;
+    const int warp = threadIdx.x / 32;
+    for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    if (threadIdx.x == 0) {
+        mbar_init(&done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem_alloc<512>(&tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (threadIdx.x == 0) {
+        constexpr uint32_t idesc = make_idesc_bf16(128, N, true, true);
+        const uint32_t a = smem_u32(smem), b = smem_u32(smem + 16384);
+        const unsigned long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const uint32_t k = i & 3;
+            mma_bf16_ss(tmem, make_sw128_desc(a + k * 2048, 8192, 1024), make_sw128_desc(b + k * 2048, 8192, 1024),
+                        idesc, 1);
+        }
+        const unsigned long long t1 = clock64();
+        mma_commit(&done);
+        mbar_wait(&done, 0);
+        const unsigned long long t2 = clock64();
+        cycles[blockIdx.x * 2] = t1 - t0;
+        cycles[blockIdx.x * 2 + 1] = t2 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int N>
+void run_mn(const char* name) {
+    unsigned long long* d;
+    cudaMalloc(&d, 148 * 2 * 8);
+    cudaFuncSetAttribute(mma_rate_mn<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024);
+    const int iters = 2048;
+    mma_rate_mn<N><<<148, 128, 70 * 1024>>>(d, iters);
+    mma_rate_mn<N><<<148, 128, 70 * 1024>>>(d, iters);
+    unsigned long long h[296];
+    cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    double total = 0;
+    for (int i = 0; i < 148; ++i) total += h[2 * i + 1];
+    const double per = total / 148 / iters;
+    printf("%-28s complete %.1f cycles/MMA  -> %.0f FLOP/clk/SM (%s)\n", name, per, 2.0 * 128 * N * 16 / per,
+           cudaGetErrorString(cudaGetLastError()));
+    cudaFree(d);
+}
+
 template <int N, bool TS>
 void run(const char* name) {
     unsigned long long* d;
@@ -82,6 +143,8 @@ int main() {
     run<64, true>("TS M128 N64 K16 (B MN-major)");
     run<128, true>("TS M128 N128 K16");
     run<256, false>("SS M128 N256 K16");
+    run_mn<256>("SS M128 N256 K16 (A,B MN)");
+    run_mn<128>("SS M128 N128 K16 (A,B MN)");
     return 0;
 }
 
