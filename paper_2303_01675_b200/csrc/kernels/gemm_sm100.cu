@@ -30,6 +30,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "../runtime/preload.h"
@@ -599,6 +600,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const CUtensorMap* mb = seg2 ? &tmB2s : &tmB;
                     if (!A_MN) {
                         tma_load_4d_2sm(ma, &full[stage], sa, k0, tc.m0, tc.z1, tc.z2);
+                    } else if (args.mn5_a) {  // both 64-wide M atoms in one box
+                        tma_load_5d_2sm(ma, &full[stage], sa, 0, k0, tc.m0 / 64, tc.z1, tc.z2);
                     } else {
 #pragma unroll
                         for (int j = 0; j < 2; ++j)
@@ -606,6 +609,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (!B_MN) {
                         tma_load_4d_2sm(full_w ? mb : &tmB2, &full[stage], sb, k0, nrow, tc.z1, tc.z2);
+                    } else if (args.mn5_b) {  // one box: two atoms (tmB / tmB2s), one for a tail half (tmB2)
+                        tma_load_5d_2sm(full_w ? mb : &tmB2, &full[stage], sb, 0, k0, nrow / 64, tc.z1, tc.z2);
                     } else {
                         for (int j = 0; j < (full_w ? 2 : 1); ++j)
                             tma_load_4d_2sm(mb, &full[stage], sb + j * 64 * kBK * 2, nrow + 64 * j, k0, tc.z1, tc.z2);
@@ -716,6 +721,31 @@ EncodeTiledFn encode_fn() {
 }
 
 // Operand map: dims = {contiguous, strided, batch1, batch2}; box = {64, rows}.
+// MN-major operand as a 5-D view {64, strided, contig/64, batch1, batch2}: one box of `blocks`
+// 64-wide atoms lands them back to back in smem, exactly as `blocks` separate 4-D boxes would.
+int encode_operand_mn5(CUtensorMap* map, const ptk_matrix& m, int contig_extent, int strided_extent, int box_rows,
+                       int blocks, int batch1, int batch2) {
+    EncodeTiledFn enc = encode_fn();
+    if (enc == nullptr) return PTK_ERR_CUDA;
+    if ((reinterpret_cast<uintptr_t>(m.ptr) & 15) != 0 || (m.ld * 2) % 16 != 0 || contig_extent % 64 != 0)
+        return PTK_ERR_ALIGN;
+    const int64_t row_bytes = m.ld * 2;
+    int64_t s1 = m.batch_stride[0] * 2, s2 = m.batch_stride[1] * 2;
+    if (batch1 <= 1) s1 = row_bytes * strided_extent;
+    if (batch2 <= 1) s2 = s1 * (batch1 > 0 ? batch1 : 1);
+    if (s1 % 16 != 0 || s2 % 16 != 0 || s1 <= 0 || s2 <= 0) return PTK_ERR_ALIGN;
+    cuuint64_t dims[5] = {64, static_cast<cuuint64_t>(strided_extent), static_cast<cuuint64_t>(contig_extent / 64),
+                          static_cast<cuuint64_t>(batch1), static_cast<cuuint64_t>(batch2)};
+    cuuint64_t strides[4] = {static_cast<cuuint64_t>(row_bytes), 128, static_cast<cuuint64_t>(s1),
+                             static_cast<cuuint64_t>(s2)};
+    cuuint32_t box[5] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(blocks), 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, m.ptr, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? PTK_OK : PTK_ERR_CUDA;
+}
+
 int encode_operand(CUtensorMap* map, const ptk_matrix& m, int contig_extent, int strided_extent, int box_rows,
                    int batch1, int batch2) {
     EncodeTiledFn enc = encode_fn();
@@ -894,7 +924,39 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
         if (rc != PTK_OK) return rc;
     }
 
+    // CTA-pair kernel with MN-major operands: one 5-D box per operand and stage instead of two
+    // 64-wide boxes (the both-MN weight-gradient layout issued twice the TMA loads for the same bytes)
+    static const bool mn5_on = [] {
+        const char* e = std::getenv("PTK_GEMM_MN5");
+        return e == nullptr || e[0] != '0';
+    }();
+    int mn5_a = 0, mn5_b = 0;
+    if (pair && mn5_on && d.a.mn_major && d.m % 64 == 0 && (d.k2 <= 0 || d.a2.mn_major)) {
+        CUtensorMap ta = p.tmA, ta2 = p.tmA2;
+        rc = encode_operand_mn5(&ta, d.a, d.m, d.k, kBK, 2, b1, b2);
+        if (rc == PTK_OK && d.k2 > 0) rc = encode_operand_mn5(&ta2, d.a2, d.m, d.k2, kBK, 2, 1, 1);
+        if (rc == PTK_OK) {
+            p.tmA = ta;
+            p.tmA2 = d.k2 > 0 ? ta2 : ta;
+            mn5_a = 1;
+        }
+    }
+    if (pair && mn5_on && d.b.mn_major && d.n % 64 == 0 && (d.k2 <= 0 || (d.b2.mn_major && d.n % 256 == 0))) {
+        CUtensorMap tb = p.tmB, tb2 = p.tmB2, tbs = p.tmB2s;
+        rc = encode_operand_mn5(&tb, d.b, d.n, d.k, kBK, 2, b1, b2);
+        if (rc == PTK_OK) rc = encode_operand_mn5(&tb2, d.b, d.n, d.k, kBK, 1, b1, b2);  // tail halves
+        if (rc == PTK_OK && d.k2 > 0) rc = encode_operand_mn5(&tbs, d.b2, d.n, d.k2, kBK, 2, 1, 1);
+        if (rc == PTK_OK) {
+            p.tmB = tb;
+            p.tmB2 = tb2;
+            p.tmB2s = d.k2 > 0 ? tbs : tb;
+            mn5_b = 1;
+        }
+    }
+
     GemmArgs& a = p.args;
+    a.mn5_a = mn5_a;
+    a.mn5_b = mn5_b;
     a.M = d.m;
     a.N = d.n;
     a.K = d.k + (d.k2 > 0 ? d.k2 : 0);

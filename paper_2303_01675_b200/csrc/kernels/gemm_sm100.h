@@ -24,6 +24,7 @@ struct GemmArgs {
     float* col_part;  // optional [ceil(M/32)][N] += column sums of C per 32-row block
     int full_tiles;  // CTA-pair kernel: work items >= full_tiles are 256 x 128 halves of the tail tiles
     int n_fast;
+    int mn5_a, mn5_b;  // CTA-pair kernel: MN-major A / B maps are 5-D (both 64-wide atoms in one box)
     int kb_split;    // CTA-pair kernel: k-blocks >= kb_split come from the second K segment (tmA2 / tmB2s)      // tile raster: 0 = m-tiles fastest (B tile shared), 1 = n-tiles fastest (A tile shared)
 };
 
