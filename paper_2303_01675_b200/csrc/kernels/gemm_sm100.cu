@@ -376,6 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int k0 = kb * kBK;
                     if (!A_MN) {
                         tma_load_4d(&tmA, &full[stage], sa, k0, tc.m0, tc.z1, tc.z2);
+                    } else if (args.mn5_a) {  // both 64-wide M atoms in one 5-D box
+                        tma_load_5d(&tmA, &full[stage], sa, 0, k0, tc.m0 / 64, tc.z1, tc.z2);
                     } else {
 #pragma unroll
                         for (int j = 0; j < kBM / 64; ++j)
@@ -394,6 +396,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     } else if (!B_MN) {
                         tma_load_4d(&tmB, &full[stage], sb, k0, tc.n0, tc.z1, tc.z2);
+                    } else if (args.mn5_b) {  // the BN/64 atoms in one 5-D box
+                        tma_load_5d(&tmB, &full[stage], sb, 0, k0, tc.n0 / 64, tc.z1, tc.z2);
                     } else {
 #pragma unroll
                         for (int j = 0; j < BN / 64; ++j)
@@ -951,6 +955,24 @@ int gemm_prepare(const ptk_gemm_desc& d, GemmPlan* out) {
             p.tmB2 = tb2;
             p.tmB2s = d.k2 > 0 ? tbs : tb;
             mn5_b = 1;
+        }
+    }
+
+    // the same for the 1-CTA kernels (A: two atoms; B: BN/64 atoms; the multicast kernel's B is K-major)
+    if (!pair && mn5_on && d.causal == PTK_CAUSAL_NONE && d.k2 <= 0) {
+        if (d.a.mn_major && d.m % 64 == 0) {
+            CUtensorMap ta = p.tmA;
+            if (encode_operand_mn5(&ta, d.a, d.m, d.k, kBK, kBM / 64, b1, b2) == PTK_OK) {
+                p.tmA = p.tmA2 = ta;
+                mn5_a = 1;
+            }
+        }
+        if (d.b.mn_major && !mc_pre && d.n % 64 == 0) {
+            CUtensorMap tb = p.tmB;
+            if (encode_operand_mn5(&tb, d.b, d.n, d.k, kBK, bn / 64, b1, b2) == PTK_OK) {
+                p.tmB = p.tmB2 = p.tmB2s = tb;
+                mn5_b = 1;
+            }
         }
     }
 

@@ -71,6 +71,16 @@ __device__ __forceinline__ void bulk_load(void* smem, const void* src, uint32_t 
                  : "memory");
 }
 
+// 5-D tiled tensor load (an MN-major operand's 64-wide atoms in one box), completion on `bar`.
+__device__ __forceinline__ void tma_load_5d(const CUtensorMap* map, uint64_t* bar, void* smem, int c0, int c1,
+                                            int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
