@@ -622,25 +622,33 @@ void Executor::profile_compute(int b, int repeats, int64_t* fwd_ns, int64_t* bwd
     ck(cudaEventCreate(&e1), "event");
     ck(cudaEventCreate(&e2), "event");
     double f = 0, bw = 0;
-    // one micro-batch at a time in one slot: profile with per-micro-batch weight gradients
+    // With paired weight gradients (as the pipeline runs them) a profile round is two micro-batches
+    // in slots 0 and 1: the first backward defers its weight gradients, the second runs both as one
+    // two-K-segment GEMM; the per-micro-batch figures are the pair's means.  (Profiling unpaired
+    // weight gradients made small-b plans look cheaper than they run.)  Otherwise one micro-batch
+    // in slot 0.
     const bool pairs = stage_->wgrad_pairs_on();
     stage_->flush_wgrads(comp_);
-    stage_->set_wgrad_pairs(false);
+    const int per_round = pairs && g.slots >= 2 ? 2 : 1;
+    if (per_round == 1) stage_->set_wgrad_pairs(false);
     for (int r = 0; r < repeats + 1; ++r) {  // first round is warm-up
-        ck(cudaEventRecord(e0, comp_), "event");
-        stage_->forward(0, tok_dev_, xin, lab_dev_, xout, comp_);
-        ck(cudaEventRecord(e1, comp_), "event");
-        stage_->backward(0, tok_dev_, dy, dx, comp_);
-        ck(cudaEventRecord(e2, comp_), "event");
-        ck(cudaEventSynchronize(e2), "sync");
-        float a = 0, c = 0;
-        ck(cudaEventElapsedTime(&a, e0, e1), "elapsed");
-        ck(cudaEventElapsedTime(&c, e1, e2), "elapsed");
-        if (r > 0) {
-            f += a;
-            bw += c;
+        for (int m = 0; m < per_round; ++m) {
+            ck(cudaEventRecord(e0, comp_), "event");
+            stage_->forward(m, tok_dev_, xin, lab_dev_, xout, comp_);
+            ck(cudaEventRecord(e1, comp_), "event");
+            stage_->backward(m, tok_dev_, dy, dx, comp_);
+            ck(cudaEventRecord(e2, comp_), "event");
+            ck(cudaEventSynchronize(e2), "sync");
+            float a = 0, c = 0;
+            ck(cudaEventElapsedTime(&a, e0, e1), "elapsed");
+            ck(cudaEventElapsedTime(&c, e1, e2), "elapsed");
+            if (r > 0) {
+                f += a / per_round;
+                bw += c / per_round;
+            }
         }
     }
+    stage_->flush_wgrads(comp_);
     (void)T;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
