@@ -591,8 +591,8 @@ __global__ void __launch_bounds__(384, 1)
                     uint8_t* kk = sKV + st * C::kKVBytes;
                     uint8_t* vv = kk + kBlk * D * 2;
                     tma_load_4d(&tmQK, &kv_full[st], kk, 0, j * kBlk, a.H + it.head, it.bi);
-                    tma_load_4d(&tmV, &kv_full[st], vv, 0, j * kBlk, 2 * a.H + it.head, it.bi);
-                    tma_load_4d(&tmV, &kv_full[st], vv + 8192, 0, j * kBlk + 64, 2 * a.H + it.head, it.bi);
+                    // V [128 keys][64] in one box: the same rows two 64-row boxes would place
+                    tma_load_4d(&tmQK, &kv_full[st], vv, 0, j * kBlk, 2 * a.H + it.head, it.bi);
                 }
             }
         }
